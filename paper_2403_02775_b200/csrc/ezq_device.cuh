@@ -1,0 +1,113 @@
+// Device-side numeric primitives shared by every kernel family, so the tensor
+// path, the channel-scale path and the packer cannot diverge.
+//
+// Reference semantics restated here (file:line into /root/reference/proj):
+//   level_of / eval_dense level   src/rtn.cpp:27-32, src/optimize.cpp:37-45
+//   initial_scale                 src/rtn.cpp:81-86
+//   snap                          src/optimize.cpp:79-82
+//   adam_step                     src/optimize.cpp:86-94
+//   outlier predicate             src/outliers.cpp:23,40
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ezq {
+
+constexpr int64_t kStatsChunk = 8192;  // stats.cpp:18
+constexpr double kScaleFloor = 1e-12;  // optimize.cpp:20
+
+// Adam state for one scalar (optimize.hpp:12-16) with host-precomputed bias
+// corrections bc1[t] = 1 - pow(b1, t), bc2[t] = 1 - pow(b2, t) (glibc pow on
+// the host, exactly as optimize.cpp:90-91 evaluates them). No contraction.
+struct AdamConsts {
+    double b1, b2, c1, c2, lr, eps;  // c1 = 1-b1, c2 = 1-b2
+};
+
+__host__ __device__ __forceinline__ float level_guard(int lmax) {
+    return 0.5f - static_cast<float>(lmax + 1) * 2.384185791015625e-07f;  // 2^-22
+}
+
+#ifdef __CUDACC__
+
+// ---- exact (reference-identical) level ------------------------------------
+// u = x * inv in fp64; clamp before rounding; llround = half away from zero.
+// trunc/sub are exact for |u| < 2^52, so this is bit-identical to libm llround.
+__device__ __forceinline__ double level_exact(double x, double inv, double dmin, double dmax) {
+    const double u = __dmul_rn(x, inv);
+    if (u >= dmax) return dmax;
+    if (u <= dmin) return dmin;
+    const double t = trunc(u);
+    const double f = __dsub_rn(u, t);
+    return fabs(f) >= 0.5 ? __dadd_rn(t, copysign(1.0, u)) : t;
+}
+
+// ---- fast level in fp32 with a certified guard band ------------------------
+// With invf = float(inv): |u32 - u64| <= |u|*2^-23*(1+eps) <= (lmax+1)*2^-23
+// for every unclamped u. Rounding boundaries sit only at half-integers inside
+// (lmin, lmax) (clamping is continuous with rounding there), so whenever
+// |u32 - rint(u32)| < 0.5 - guard with guard = (lmax+1)*2^-22 the fp32 level
+// equals the exact level. Callers track the max |r| and take the exact path
+// when it crosses the band.
+struct FastLevel {
+    float invf, fmin, fmax;
+};
+
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: FADD rounds to integer
+
+__device__ __forceinline__ float level_fast(float x, const FastLevel& fl, float& rmax) {
+    float u = __fmul_rn(x, fl.invf);
+    u = fminf(fmaxf(u, fl.fmin), fl.fmax);
+    const float t = __fadd_rn(u, kMagic);
+    const float q = __fsub_rn(t, kMagic);
+    rmax = fmaxf(rmax, fabsf(__fsub_rn(u, q)));
+    return q;
+}
+
+// ---- scale handling ----------------------------------------------------------
+__device__ __forceinline__ double snap(double s) {
+    const double snapped = static_cast<double>(__double2float_rn(s));
+    return snapped < kScaleFloor ? kScaleFloor : snapped;  // std::max(snapped, floor)
+}
+
+// initial_scale(x) with max|x| already known (division by 2^(k-1) is exact).
+__device__ __forceinline__ double initial_scale_from_max(double max_abs, int lmax) {
+    if (max_abs == 0.0) return 1.0;
+    return __ddiv_rn(max_abs, static_cast<double>(lmax));
+}
+
+__device__ __forceinline__ double adam_update(double& m, double& v, double s, double g,
+                                              double bc1, double bc2, const AdamConsts& a) {
+    m = __dadd_rn(__dmul_rn(a.b1, m), __dmul_rn(a.c1, g));
+    v = __dadd_rn(__dmul_rn(a.b2, v), __dmul_rn(__dmul_rn(a.c2, g), g));
+    const double mh = __ddiv_rn(m, bc1);
+    const double vh = __ddiv_rn(v, bc2);
+    const double upd = __ddiv_rn(__dmul_rn(a.lr, mh), __dadd_rn(__dsqrt_rn(vh), a.eps));
+    const double updated = __dsub_rn(s, upd);
+    return updated < kScaleFloor ? kScaleFloor : updated;  // std::max(updated, floor)
+}
+
+// ---- outlier predicate (outliers.cpp:23): |double(v) - mean| >= thr ---------
+__device__ __forceinline__ bool is_outlier(float v, double mean, double thr) {
+    return fabs(__dsub_rn(static_cast<double>(v), mean)) >= thr;
+}
+
+// ---- exact sequential accumulation of one element (optimize.cpp:36-49) -----
+// err += d*d and grad += d*q with separate roundings (the reference is built
+// without FMA contraction); d = s*q - x is exact since s*q is.
+__device__ __forceinline__ void seq_accumulate(double x, double q, double s, double& err,
+                                               double& grad) {
+    const double d = __dsub_rn(__dmul_rn(s, q), x);
+    err = __dadd_rn(err, __dmul_rn(d, d));
+    grad = __dadd_rn(grad, __dmul_rn(d, q));
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+#endif  // __CUDACC__
+
+}  // namespace ezq

@@ -1,0 +1,220 @@
+// K4 (final levels + packing) and K5 (dense restore + outlier scatter).
+//
+// K4 restates quantize_channel (rtn.cpp:88-99) at the stored float scale,
+// the outlier-slot convention (level 0, pipeline.cpp:86) and pack_levels
+// (rtn.cpp:123-149): k = 4 packs (level - lmin) nibbles with the even FLAT
+// index in the low nibble (pairs straddle rows when cols is odd); any other
+// k stores one offset byte per level. One thread owns 16 consecutive flat
+// elements -> one 8-byte (k=4) or 16-byte store. HBM-bound: 4N bytes read,
+// N/2 (or N) written.
+//
+// K5 restates dequantize_impl (pipeline.cpp:117-142): What_ij =
+// float(double(s_j) * l_ij), which equals the correctly rounded fp32 product
+// s_j * l_ij (the fp64 product is exact), then the stored outlier values are
+// scattered back bit-exactly (outliers.cpp:106-114).
+#include "ezq_kernels.cuh"
+
+namespace ezq {
+
+namespace {
+
+__device__ __forceinline__ int find_tensor(const int64_t* base, int ntens, int64_t g) {
+    int lo = 0, hi = ntens - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (base[mid] <= g)
+            lo = mid;
+        else
+            hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kPackThreads) k_pack(const TDesc* __restrict__ td,
+                                                       const int64_t* __restrict__ pblk_base,
+                                                       int ntens, int64_t total, Scratch sc,
+                                                       CfgDev cfg) {
+    const int64_t g = blockIdx.x;
+    if (g >= total) return;
+    const int t = find_tensor(pblk_base, ntens, g);
+    const TDesc& d = td[t];
+    const int64_t e0 = ((g - d.pblk_base) * kPackThreads + threadIdx.x) * kPackPerThread;
+    if (e0 >= d.n) return;
+    const TStats* st = d.st;
+    const double mean = st->mean, thr = st->thr;
+    const int mask = st->mask;
+    const int64_t C = d.cols;
+    int64_t col = e0 % C;
+    const double dmin = cfg.lmin, dmax = cfg.lmax;
+    const float fmin = static_cast<float>(cfg.lmin), fmax = static_cast<float>(cfg.lmax);
+    const float guard = cfg.guard;
+    const int64_t cnt = min(static_cast<int64_t>(kPackPerThread), d.n - e0);
+
+    float x[kPackPerThread];
+    if (cnt == kPackPerThread && (reinterpret_cast<uintptr_t>(d.W + e0) & 15) == 0) {
+        const float4* p4 = reinterpret_cast<const float4*>(d.W + e0);
+#pragma unroll
+        for (int k = 0; k < kPackPerThread / 4; ++k) {
+            const float4 v = __ldg(p4 + k);
+            x[4 * k] = v.x;
+            x[4 * k + 1] = v.y;
+            x[4 * k + 2] = v.z;
+            x[4 * k + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kPackPerThread; ++k) x[k] = (k < cnt) ? d.W[e0 + k] : 0.f;
+    }
+
+    uint8_t off[kPackPerThread];
+#pragma unroll
+    for (int k = 0; k < kPackPerThread; ++k) {
+        int lvl = 0;
+        if (k < cnt && !(mask && is_outlier(x[k], mean, thr))) {
+            const double inv = sc.inv[d.col_base + col];
+            const FastLevel fl{__double2float_rn(inv), fmin, fmax};
+            float rm = 0.f;
+            float q = level_fast(x[k], fl, rm);
+            if (rm >= guard) q = static_cast<float>(level_exact(x[k], inv, dmin, dmax));
+            lvl = static_cast<int>(q);
+        }
+        off[k] = (k < cnt) ? static_cast<uint8_t>(lvl - cfg.lmin) : 0;
+        if (++col == C) col = 0;
+    }
+
+    if (cfg.bits == 4) {
+        uint8_t b[kPackPerThread / 2];
+#pragma unroll
+        for (int k = 0; k < kPackPerThread / 2; ++k)
+            b[k] = static_cast<uint8_t>(off[2 * k] | (off[2 * k + 1] << 4));
+        uint8_t* dst = d.packed + e0 / 2;
+        if (cnt == kPackPerThread) {
+            uint2 w;
+            w.x = b[0] | (b[1] << 8) | (b[2] << 16) | (static_cast<uint32_t>(b[3]) << 24);
+            w.y = b[4] | (b[5] << 8) | (b[6] << 16) | (static_cast<uint32_t>(b[7]) << 24);
+            *reinterpret_cast<uint2*>(dst) = w;
+        } else {
+            const int64_t nb = (cnt + 1) / 2;
+            for (int64_t k = 0; k < nb; ++k) dst[k] = b[k];
+        }
+    } else {
+        uint8_t* dst = d.packed + e0;
+        if (cnt == kPackPerThread) {
+            uint4 w;
+            w.x = off[0] | (off[1] << 8) | (off[2] << 16) | (static_cast<uint32_t>(off[3]) << 24);
+            w.y = off[4] | (off[5] << 8) | (off[6] << 16) | (static_cast<uint32_t>(off[7]) << 24);
+            w.z = off[8] | (off[9] << 8) | (off[10] << 16) | (static_cast<uint32_t>(off[11]) << 24);
+            w.w = off[12] | (off[13] << 8) | (off[14] << 16) |
+                  (static_cast<uint32_t>(off[15]) << 24);
+            *reinterpret_cast<uint4*>(dst) = w;
+        } else {
+            for (int64_t k = 0; k < cnt; ++k) dst[k] = off[k];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kPackThreads) k_dequant(int64_t rows, int64_t cols, int bits,
+                                                          const uint8_t* __restrict__ packed,
+                                                          const float* __restrict__ scales,
+                                                          float* __restrict__ out,
+                                                          unsigned long long* bad_byte) {
+    const int64_t n = rows * cols;
+    const int64_t e0 = (static_cast<int64_t>(blockIdx.x) * kPackThreads + threadIdx.x) *
+                       kPackPerThread;
+    if (e0 >= n) return;
+    const int64_t cnt = min(static_cast<int64_t>(kPackPerThread), n - e0);
+    const int lmin = -(1 << (bits - 1)) + 1;
+    const int span = (1 << (bits - 1)) - lmin;
+    uint8_t off[kPackPerThread];
+    if (bits == 4) {
+        uint8_t b[kPackPerThread / 2];
+        if (cnt == kPackPerThread) {
+            const uint2 w = *reinterpret_cast<const uint2*>(packed + e0 / 2);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                b[k] = (w.x >> (8 * k)) & 0xff;
+                b[4 + k] = (w.y >> (8 * k)) & 0xff;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kPackPerThread / 2; ++k)
+                b[k] = (2 * k < cnt) ? packed[e0 / 2 + k] : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < kPackPerThread / 2; ++k) {
+            off[2 * k] = b[k] & 0x0f;
+            off[2 * k + 1] = b[k] >> 4;
+        }
+    } else {
+        if (cnt == kPackPerThread) {
+            const uint4 w = *reinterpret_cast<const uint4*>(packed + e0);
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int k = 0; k < kPackPerThread; ++k) off[k] = (ws[k / 4] >> (8 * (k % 4))) & 0xff;
+        } else {
+#pragma unroll
+            for (int k = 0; k < kPackPerThread; ++k) off[k] = (k < cnt) ? packed[e0 + k] : 0;
+        }
+        // unpack_levels rejects offsets beyond the level span (rtn.cpp:173-178).
+#pragma unroll
+        for (int k = 0; k < kPackPerThread; ++k)
+            if (k < cnt && off[k] > span) atomicMin(bad_byte, static_cast<unsigned long long>(e0 + k));
+    }
+    int64_t col = e0 % cols;
+    float v[kPackPerThread];
+#pragma unroll
+    for (int k = 0; k < kPackPerThread; ++k) {
+        v[k] = __fmul_rn(scales[col], static_cast<float>(lmin + off[k]));
+        if (++col == cols) col = 0;
+    }
+    if (cnt == kPackPerThread && (reinterpret_cast<uintptr_t>(out + e0) & 15) == 0) {
+        float4* o4 = reinterpret_cast<float4*>(out + e0);
+#pragma unroll
+        for (int k = 0; k < kPackPerThread / 4; ++k)
+            o4[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+    } else {
+        for (int64_t k = 0; k < cnt; ++k) out[e0 + k] = v[k];
+    }
+}
+
+__global__ void k_scatter(int64_t rows, int64_t cols, const ezq_outlier* __restrict__ e,
+                          int64_t n, float* __restrict__ out, unsigned long long* bad_entry) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const ezq_outlier o = e[i];
+    if (o.row >= static_cast<uint64_t>(rows) || o.col >= static_cast<uint64_t>(cols)) {
+        atomicMin(bad_entry, static_cast<unsigned long long>(i));
+        return;
+    }
+    out[static_cast<int64_t>(o.row) * cols + o.col] = o.value;
+}
+
+}  // namespace
+
+void launch_pack(const TDesc* td, const int64_t* pblk_base, int ntens, int64_t total_blocks,
+                 Scratch sc, CfgDev cfg, cudaStream_t st) {
+    if (total_blocks == 0) return;
+    k_pack<<<(unsigned)total_blocks, kPackThreads, 0, st>>>(td, pblk_base, ntens, total_blocks,
+                                                            sc, cfg);
+    count_launch();
+}
+
+void launch_dequant(int64_t rows, int64_t cols, int bits, const uint8_t* packed,
+                    const float* scales, float* out, unsigned long long* bad_byte,
+                    cudaStream_t st) {
+    const int64_t n = rows * cols;
+    const int64_t blocks = (n + kPackBlock - 1) / kPackBlock;
+    if (blocks == 0) return;
+    k_dequant<<<(unsigned)blocks, kPackThreads, 0, st>>>(rows, cols, bits, packed, scales, out,
+                                                         bad_byte);
+    count_launch();
+}
+
+void launch_scatter(int64_t rows, int64_t cols, const ezq_outlier* e, int64_t n, float* out,
+                    unsigned long long* bad_entry, cudaStream_t st) {
+    if (n == 0) return;
+    k_scatter<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(rows, cols, e, n, out, bad_entry);
+    count_launch();
+}
+
+}  // namespace ezq

@@ -1,0 +1,734 @@
+// Tensor-scale C-ABI: the batched quantize pipeline (pipeline.cpp:65-115 of
+// the reference, applied to a batch of independent tensors the way
+// model.cpp:154-192 applies it to a model), tensor statistics, outlier
+// detection, dequantisation and reconstruction error.
+//
+// Phase 1 (all tensors, grouped launches): K1 pass 1 -> merge -> pass 2 ->
+// merge -> K2 count -> scan; one D2H of the per-tensor stats (sizes the COO
+// buffers, reports non-finite inputs). Phase 2: K2 write, K3 per row-class,
+// K3b, column finalize, column-ordered totals, K4. One more sync publishes
+// the errors / invariant.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <vector>
+
+#include "runtime.hpp"
+
+namespace ezq {
+
+namespace {
+
+constexpr unsigned long long kNoBad = ~0ull;
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+TStats fresh_stats() {
+    TStats s;
+    std::memset(&s, 0, sizeof(s));
+    s.bad_index = kNoBad;
+    return s;
+}
+
+// Uploads `h` into arena memory `d` (async; host vector must outlive the copy
+// -> callers keep it alive until the next sync).
+template <class T>
+int upload(T* d, const std::vector<T>& h, cudaStream_t st) {
+    if (h.empty()) return EZQ_OK;
+    EZQ_CK(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+    return EZQ_OK;
+}
+
+void free_qweight_arrays(ezq_qweight* q) {
+    if (!q || !q->owned) return;
+    if (q->mem == EZQ_MEM_DEVICE) {
+        cudaFree(q->packed);
+        cudaFree(q->scales);
+        cudaFree(q->outliers);
+    } else {
+        std::free(q->packed);
+        std::free(q->scales);
+        std::free(q->outliers);
+    }
+    q->packed = nullptr;
+    q->scales = nullptr;
+    q->outliers = nullptr;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* cols, int n,
+                   const ezq_config* cfg, int mode, int in_mem, int out_mem, void* user_stream,
+                   ezq_qweight** outs, int* failed) {
+    if (failed) *failed = -1;
+    if (n <= 0) return clear_error();
+    for (int i = 0; i < n; ++i) outs[i] = nullptr;
+    if (mode < EZQ_MODE_EASYQUANT || mode > EZQ_MODE_OUTLIERS_ONLY)
+        return set_error(EZQ_ERR_INVALID_ARGUMENT, "unknown quant mode " + std::to_string(mode));
+    // DenseMatrix::validate shape check first (types.cpp:10-12).
+    for (int i = 0; i < n; ++i) {
+        if (rows[i] <= 0 || cols[i] <= 0) {
+            if (failed) *failed = i;
+            return set_error(EZQ_ERR_INVALID_ARGUMENT,
+                             "matrix shape must be positive, got " + std::to_string(rows[i]) +
+                                 "x" + std::to_string(cols[i]));
+        }
+    }
+    std::string cfg_msg;
+    const int cfg_status = validate_config(cfg, &cfg_msg);
+
+    int dev;
+    if (int s = bind_device(&dev)) return s;
+    const DeviceInfo& di = device_info(dev);
+    cudaStream_t st = pick_stream(user_stream, dev);
+
+    // ---- sizes & host descriptors ----
+    std::vector<TDesc> hd(n);
+    std::vector<int64_t> chunk_base(n + 1), dblk_base(n + 1), pblk_base(n + 1);
+    int64_t tot_chunks = 0, tot_dblk = 0, tot_pblk = 0, tot_cols = 0, tot_in = 0;
+    for (int i = 0; i < n; ++i) {
+        const int64_t N = rows[i] * cols[i];
+        TDesc& d = hd[i];
+        std::memset(&d, 0, sizeof(d));
+        d.rows = rows[i];
+        d.cols = cols[i];
+        d.n = N;
+        d.chunk_base = chunk_base[i] = tot_chunks;
+        d.n_chunks = ceil_div(N, kStatsChunk);
+        tot_chunks += d.n_chunks;
+        d.dblk_base = dblk_base[i] = tot_dblk;
+        d.n_dblk = ceil_div(N, kDetectBlock);
+        tot_dblk += d.n_dblk;
+        d.pblk_base = pblk_base[i] = tot_pblk;
+        tot_pblk += ceil_div(N, kPackBlock);
+        d.col_base = tot_cols;
+        tot_cols += cols[i];
+        if (in_mem == EZQ_MEM_HOST) tot_in += N;
+    }
+    chunk_base[n] = tot_chunks;
+    dblk_base[n] = tot_dblk;
+    pblk_base[n] = tot_pblk;
+
+    // ---- K3 plans: one launch per distinct row count ----
+    const bool eq = mode == EZQ_MODE_EASYQUANT;
+    std::map<int64_t, std::vector<int>> by_rows;
+    for (int i = 0; i < n; ++i) by_rows[rows[i]].push_back(i);
+    struct Plan {
+        K3Launch kl;
+        std::vector<K3Group> groups;
+        size_t goff = 0;
+        int grid = 0;
+    };
+    std::vector<Plan> plans;
+    size_t tot_groups = 0, gstrip_floats = 0;
+    if (cfg_status == EZQ_OK) {
+        for (auto& kv : by_rows) {
+            Plan p;
+            p.kl = plan_k3(kv.first, 0, di.sms, di.max_smem_optin);
+            // Shrink the strip width (columns per CTA) when that evens out
+            // the last wave: cost ~ waves * width / warp-efficiency.
+            const int unit = (p.kl.W == 1) ? 32 / p.kl.L : 1;
+            int best_cb = p.kl.teams;
+            double best_cost = 1e300;
+            for (int cb = p.kl.teams; cb >= std::max(unit, p.kl.teams / 2); cb -= unit) {
+                int64_t groups = 0;
+                for (int i : kv.second) groups += ceil_div(cols[i], cb);
+                const double waves = std::ceil(static_cast<double>(groups) / di.sms);
+                const double warps = (p.kl.W == 1) ? cb * p.kl.L / 32.0 : cb * p.kl.W;
+                const double eff = std::min(1.0, warps / 12.0);
+                const double cost = waves * cb / eff;
+                if (cost < best_cost - 1e-9) {
+                    best_cost = cost;
+                    best_cb = cb;
+                }
+            }
+            p.kl.teams = best_cb;
+            p.kl.threads = (p.kl.W == 1) ? ((best_cb * p.kl.L + 31) / 32) * 32 : best_cb * p.kl.W * 32;
+            if (!p.kl.global_strip)
+                p.kl.smem = static_cast<size_t>(best_cb) * p.kl.rstride * sizeof(float) +
+                            static_cast<size_t>(2) * best_cb * p.kl.W * 2 * sizeof(double);
+            for (int i : kv.second)
+                for (int64_t c0 = 0; c0 < cols[i]; c0 += best_cb)
+                    p.groups.push_back({i, static_cast<int32_t>(c0),
+                                        static_cast<int32_t>(std::min<int64_t>(best_cb, cols[i] - c0)),
+                                        0});
+            p.goff = tot_groups;
+            tot_groups += p.groups.size();
+            p.grid = static_cast<int>(p.groups.size());
+            if (p.kl.global_strip) {
+                p.grid = std::min<int>(p.grid, di.sms * 2);
+                gstrip_floats = std::max(gstrip_floats, static_cast<size_t>(p.grid) *
+                                                            p.kl.teams * p.kl.rstride);
+            }
+            plans.push_back(std::move(p));
+        }
+    }
+    // 32-column tiles for K3b / finalize.
+    std::vector<int2> tiles;
+    for (int i = 0; i < n; ++i)
+        for (int64_t c0 = 0; c0 < cols[i]; c0 += 32) tiles.push_back(make_int2(i, (int)c0));
+    std::vector<double> bc;
+    bias_tables(cfg, bc);
+
+    // ---- arena ----
+    Arena ar;
+    ar.reserve(sizeof(TStats) * n);
+    ar.reserve(sizeof(TDesc) * n);
+    for (int k = 0; k < 3; ++k) ar.reserve_n<int64_t>(n + 1);
+    for (int k = 0; k < 3; ++k) ar.reserve_n<double>(tot_chunks);
+    for (int k = 0; k < 2; ++k) ar.reserve_n<float>(tot_chunks);
+    for (int k = 0; k < 2; ++k) ar.reserve_n<long long>(tot_dblk);
+    for (int k = 0; k < 5; ++k) ar.reserve_n<double>(tot_cols);
+    ar.reserve(sizeof(double) * bc.size());
+    ar.reserve(sizeof(K3Group) * tot_groups);
+    ar.reserve(sizeof(int2) * tiles.size());
+    ar.reserve(sizeof(float) * tot_in);
+    ar.reserve(sizeof(float) * gstrip_floats);
+    if (int s = ar.allocate(st)) return s;
+    TStats* d_stats = ar.take<TStats>(n);
+    TDesc* d_desc = ar.take<TDesc>(n);
+    int64_t* d_chunk_base = ar.take<int64_t>(n + 1);
+    int64_t* d_dblk_base = ar.take<int64_t>(n + 1);
+    int64_t* d_pblk_base = ar.take<int64_t>(n + 1);
+    Scratch sc;
+    sc.p_sum = ar.take<double>(tot_chunks);
+    sc.p_max = ar.take<double>(tot_chunks);
+    sc.p_dev = ar.take<double>(tot_chunks);
+    sc.p_mn = ar.take<float>(tot_chunks);
+    sc.p_mx = ar.take<float>(tot_chunks);
+    sc.blk_count = ar.take<long long>(tot_dblk);
+    sc.blk_offset = ar.take<long long>(tot_dblk);
+    sc.s0 = ar.take<double>(tot_cols);
+    sc.s_opt = ar.take<double>(tot_cols);
+    sc.err_rtn = ar.take<double>(tot_cols);
+    sc.err_fin = ar.take<double>(tot_cols);
+    sc.inv = ar.take<double>(tot_cols);
+    double* d_bc = ar.take<double>(bc.size());
+    K3Group* d_groups = ar.take<K3Group>(tot_groups);
+    int2* d_tiles = ar.take<int2>(tiles.size());
+    float* d_in = ar.take<float>(tot_in);
+    float* d_gstrip = ar.take<float>(gstrip_floats);
+    if (!ar.ok()) return set_error(EZQ_ERR_CUDA, "internal: arena overflow (quantize_batch)");
+
+    // ---- inputs ----
+    int64_t in_off = 0;
+    for (int i = 0; i < n; ++i) {
+        hd[i].st = d_stats + i;
+        if (in_mem == EZQ_MEM_HOST) {
+            float* dst = d_in + in_off;
+            EZQ_CK(cudaMemcpyAsync(dst, Ws[i], sizeof(float) * hd[i].n, cudaMemcpyHostToDevice, st));
+            hd[i].W = dst;
+            in_off += hd[i].n;
+        } else {
+            hd[i].W = Ws[i];
+        }
+    }
+    std::vector<TStats> hs(n, fresh_stats());
+    if (int s = upload(d_stats, hs, st)) return s;
+    if (int s = upload(d_desc, hd, st)) return s;
+    if (int s = upload(d_chunk_base, chunk_base, st)) return s;
+    if (int s = upload(d_dblk_base, dblk_base, st)) return s;
+    if (int s = upload(d_pblk_base, pblk_base, st)) return s;
+    if (int s = upload(d_bc, bc, st)) return s;
+    if (int s = upload(d_tiles, tiles, st)) return s;
+    for (auto& p : plans) {
+        if (p.groups.empty()) continue;
+        EZQ_CK(cudaMemcpyAsync(d_groups + p.goff, p.groups.data(), sizeof(K3Group) * p.groups.size(),
+                               cudaMemcpyHostToDevice, st));
+    }
+
+    // ---- phase 1 ----
+    launch_stats_pass1(d_desc, d_chunk_base, n, tot_chunks, sc, st);
+    launch_stats_fin1(d_desc, n, sc, st);
+    if (cfg_status == EZQ_OK) {
+        launch_stats_pass2(d_desc, d_chunk_base, n, tot_chunks, sc, st);
+        launch_stats_fin2(d_desc, n, sc, cfg->sigma_n, mode != EZQ_MODE_RTN, st);
+        if (mode != EZQ_MODE_RTN) {
+            launch_detect_count(d_desc, d_dblk_base, n, tot_dblk, sc, st);
+            launch_detect_scan(d_desc, n, sc, st);
+        }
+    }
+    EZQ_CK(cudaGetLastError());
+    EZQ_CK(cudaMemcpyAsync(hs.data(), d_stats, sizeof(TStats) * n, cudaMemcpyDeviceToHost, st));
+    EZQ_CK(cudaStreamSynchronize(st));
+    for (int i = 0; i < n; ++i) {
+        if (hs[i].bad_index != kNoBad) {  // types.cpp:17-20
+            if (failed) *failed = i;
+            return set_error(EZQ_ERR_INVALID_ARGUMENT,
+                             "non-finite element at flat index " + std::to_string(hs[i].bad_index),
+                             static_cast<int64_t>(hs[i].bad_index));
+        }
+    }
+    if (cfg_status != EZQ_OK) return set_error(cfg_status, cfg_msg);
+    if (mode != EZQ_MODE_RTN) {
+        for (int i = 0; i < n; ++i)
+            if (rows[i] > UINT32_MAX || cols[i] > UINT32_MAX) {  // outliers.cpp:30-31
+                if (failed) *failed = i;
+                return set_error(EZQ_ERR_INVALID_ARGUMENT,
+                                 "matrix dimensions exceed 32-bit coordinate range");
+            }
+    }
+
+    // ---- outputs (device) ----
+    struct Out {
+        uint8_t* packed = nullptr;
+        float* scales = nullptr;
+        ezq_outlier* outl = nullptr;
+    };
+    std::vector<Out> dout(n);
+    auto free_dout = [&]() {
+        for (auto& o : dout) {
+            cudaFree(o.packed);
+            cudaFree(o.scales);
+            cudaFree(o.outl);
+            o = Out{};
+        }
+    };
+    for (int i = 0; i < n; ++i) {
+        const int64_t pb = ezq_packed_size(hd[i].n, cfg->bits);
+        cudaError_t e1 = cudaMalloc(&dout[i].packed, std::max<int64_t>(pb, 1));
+        cudaError_t e2 = cudaMalloc(&dout[i].scales, sizeof(float) * cols[i]);
+        cudaError_t e3 = cudaSuccess;
+        if (hs[i].n_out > 0) e3 = cudaMalloc(&dout[i].outl, sizeof(ezq_outlier) * hs[i].n_out);
+        if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
+            free_dout();
+            return cuda_error(cudaErrorMemoryAllocation, "output allocation");
+        }
+        hd[i].packed = dout[i].packed;
+        hd[i].scales = dout[i].scales;
+        hd[i].outliers = dout[i].outl;
+    }
+    if (int s = upload(d_desc, hd, st)) {
+        free_dout();
+        return s;
+    }
+
+    // ---- phase 2 ----
+    const CfgDev cd = make_cfg(cfg, mode, d_bc);
+    if (mode != EZQ_MODE_RTN) launch_detect_write(d_desc, d_dblk_base, n, tot_dblk, sc, st);
+    for (auto& p : plans)
+        launch_k3(p.kl, d_desc, d_groups + p.goff, static_cast<int>(p.groups.size()), sc, cd,
+                  d_gstrip, p.grid, st);
+    launch_seq_errors(d_desc, d_tiles, static_cast<int>(tiles.size()), sc, cd, st);
+    launch_col_finalize(d_desc, d_tiles, static_cast<int>(tiles.size()), sc, cd, st);
+    launch_tensor_totals(d_desc, n, sc, st);
+    launch_pack(d_desc, d_pblk_base, n, tot_pblk, sc, cd, st);
+    {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) {
+            free_dout();
+            return cuda_error(e, "phase-2 launch");
+        }
+    }
+    EZQ_CK(cudaMemcpyAsync(hs.data(), d_stats, sizeof(TStats) * n, cudaMemcpyDeviceToHost, st));
+
+    // ---- results ----
+    std::vector<std::unique_ptr<ezq_qweight>> res(n);
+    for (int i = 0; i < n; ++i) {
+        res[i].reset(static_cast<ezq_qweight*>(std::calloc(1, sizeof(ezq_qweight))));
+        ezq_qweight* q = res[i].get();
+        q->rows = rows[i];
+        q->cols = cols[i];
+        q->bits = cfg->bits;
+        q->mem = out_mem;
+        q->owned = 1;
+        q->packed_bytes = ezq_packed_size(hd[i].n, cfg->bits);
+        if (out_mem == EZQ_MEM_HOST) {
+            q->packed = static_cast<uint8_t*>(std::malloc(std::max<int64_t>(q->packed_bytes, 1)));
+            q->scales = static_cast<float*>(std::malloc(sizeof(float) * cols[i]));
+            q->outliers = hs[i].n_out > 0 ? static_cast<ezq_outlier*>(
+                                                std::malloc(sizeof(ezq_outlier) * hs[i].n_out))
+                                          : nullptr;
+            cudaMemcpyAsync(q->packed, dout[i].packed, q->packed_bytes, cudaMemcpyDeviceToHost, st);
+            cudaMemcpyAsync(q->scales, dout[i].scales, sizeof(float) * cols[i],
+                            cudaMemcpyDeviceToHost, st);
+            if (hs[i].n_out > 0)
+                cudaMemcpyAsync(q->outliers, dout[i].outl, sizeof(ezq_outlier) * hs[i].n_out,
+                                cudaMemcpyDeviceToHost, st);
+        } else {
+            q->packed = dout[i].packed;
+            q->scales = dout[i].scales;
+            q->outliers = dout[i].outl;
+        }
+    }
+    cudaError_t se = cudaStreamSynchronize(st);
+    if (out_mem == EZQ_MEM_HOST) free_dout();
+    if (se != cudaSuccess) {
+        for (auto& q : res) free_qweight_arrays(q.get()), std::free(q.release());
+        return cuda_error(se, "phase-2 sync");
+    }
+    for (int i = 0; i < n; ++i) {
+        ezq_qweight* q = res[i].get();
+        q->n_outliers = hs[i].n_out;
+        q->mean = hs[i].mean;
+        q->stddev = hs[i].stddev;
+        q->sigma_n = cfg->sigma_n;
+        q->has_errors = 1;
+        q->rtn_error = hs[i].rtn_error;
+        q->final_error = hs[i].final_error;
+    }
+    for (int i = 0; i < n; ++i) {
+        int code = 0;
+        std::string msg;
+        if (hs[i].scale_zero) {
+            code = EZQ_ERR_INVALID_ARGUMENT;
+            msg = "scale must be finite and > 0, got " + fmt_double(0.0);
+        } else if (hs[i].final_error > hs[i].rtn_error) {  // pipeline.cpp:107-108
+            code = EZQ_ERR_INVARIANT;
+            msg = "optimized error exceeds round-to-nearest error";
+        }
+        if (code) {
+            for (auto& q : res) {
+                free_qweight_arrays(q.get());
+                std::free(q.release());
+            }
+            if (failed) *failed = i;
+            return set_error(code, msg);
+        }
+    }
+    for (int i = 0; i < n; ++i) outs[i] = res[i].release();
+    (void)eq;
+    return clear_error();
+}
+
+}  // namespace ezq
+
+using namespace ezq;
+
+extern "C" {
+
+int ezq_quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* cols, int n,
+                       const ezq_config* cfg, int mode, int in_mem, int out_mem, void* stream,
+                       ezq_qweight** outs, int* failed_index) {
+    return quantize_batch(Ws, rows, cols, n, cfg, mode, in_mem, out_mem, stream, outs,
+                          failed_index);
+}
+
+int ezq_quantize_tensor(const float* W, int64_t rows, int64_t cols, const ezq_config* cfg,
+                        int mode, int in_mem, int out_mem, void* stream, ezq_qweight** out) {
+    const float* ws[1] = {W};
+    return quantize_batch(ws, &rows, &cols, 1, cfg, mode, in_mem, out_mem, stream, out, nullptr);
+}
+
+void ezq_qweight_free(ezq_qweight* q) {
+    if (!q) return;
+    free_qweight_arrays(q);
+    std::free(q);
+}
+
+int ezq_qweight_wrap(int64_t rows, int64_t cols, int bits, const uint8_t* packed,
+                     int64_t packed_bytes, const float* scales, int64_t n_scales,
+                     const ezq_outlier* outliers, int64_t n_outliers, double mean, double stddev,
+                     float sigma_n, int mem, ezq_qweight** out) {
+    ezq_qweight* q = static_cast<ezq_qweight*>(std::calloc(1, sizeof(ezq_qweight)));
+    q->rows = rows;
+    q->cols = cols;
+    q->bits = bits;
+    q->mem = mem;
+    q->owned = 0;
+    q->packed = const_cast<uint8_t*>(packed);
+    q->packed_bytes = packed_bytes;
+    q->scales = const_cast<float*>(scales);
+    q->reserved = static_cast<int32_t>(n_scales == cols ? 0 : 1);  // scale-count mismatch flag
+    q->outliers = const_cast<ezq_outlier*>(outliers);
+    q->n_outliers = n_outliers;
+    q->mean = mean;
+    q->stddev = stddev;
+    q->sigma_n = sigma_n;
+    *out = q;
+    return clear_error();
+}
+
+// ---- tensor_stats (stats.cpp:27-108) ---------------------------------------
+int ezq_tensor_stats(const float* W, int64_t rows, int64_t cols, int mem, void* stream,
+                     ezq_stats* out) {
+    std::memset(out, 0, sizeof(*out));
+    const int64_t N = rows * cols;
+    if (rows <= 0 || cols <= 0 || N <= 0) return clear_error();  // stats.cpp:51
+    int dev;
+    if (int s = bind_device(&dev)) return s;
+    cudaStream_t st = pick_stream(stream, dev);
+    TDesc hd;
+    std::memset(&hd, 0, sizeof(hd));
+    hd.rows = rows;
+    hd.cols = cols;
+    hd.n = N;
+    hd.n_chunks = ceil_div(N, kStatsChunk);
+    Arena ar;
+    ar.reserve(sizeof(TStats));
+    ar.reserve(sizeof(TDesc));
+    ar.reserve(2 * sizeof(int64_t));
+    for (int k = 0; k < 3; ++k) ar.reserve_n<double>(hd.n_chunks);
+    for (int k = 0; k < 2; ++k) ar.reserve_n<float>(hd.n_chunks);
+    if (mem == EZQ_MEM_HOST) ar.reserve(sizeof(float) * N);
+    if (int s = ar.allocate(st)) return s;
+    TStats* d_st = ar.take<TStats>(1);
+    TDesc* d_td = ar.take<TDesc>(1);
+    int64_t* d_cb = ar.take<int64_t>(2);
+    Scratch sc{};
+    sc.p_sum = ar.take<double>(hd.n_chunks);
+    sc.p_max = ar.take<double>(hd.n_chunks);
+    sc.p_dev = ar.take<double>(hd.n_chunks);
+    sc.p_mn = ar.take<float>(hd.n_chunks);
+    sc.p_mx = ar.take<float>(hd.n_chunks);
+    if (mem == EZQ_MEM_HOST) {
+        float* dW = ar.take<float>(N);
+        EZQ_CK(cudaMemcpyAsync(dW, W, sizeof(float) * N, cudaMemcpyHostToDevice, st));
+        hd.W = dW;
+    } else {
+        hd.W = W;
+    }
+    hd.st = d_st;
+    std::vector<TStats> hs(1, fresh_stats());
+    std::vector<TDesc> hdv(1, hd);
+    std::vector<int64_t> cb = {0, hd.n_chunks};
+    if (int s = upload(d_st, hs, st)) return s;
+    if (int s = upload(d_td, hdv, st)) return s;
+    if (int s = upload(d_cb, cb, st)) return s;
+    launch_stats_pass1(d_td, d_cb, 1, hd.n_chunks, sc, st);
+    launch_stats_fin1(d_td, 1, sc, st);
+    launch_stats_pass2(d_td, d_cb, 1, hd.n_chunks, sc, st);
+    launch_stats_fin2(d_td, 1, sc, 0.f, 0, st);
+    EZQ_CK(cudaGetLastError());
+    EZQ_CK(cudaMemcpyAsync(hs.data(), d_st, sizeof(TStats), cudaMemcpyDeviceToHost, st));
+    EZQ_CK(cudaStreamSynchronize(st));
+    out->mean = hs[0].mean;
+    out->stddev = hs[0].stddev;
+    out->max_abs = hs[0].max_abs;
+    out->count = N;
+    return clear_error();
+}
+
+// ---- detect_outliers (outliers.cpp:29-73) ----------------------------------
+int ezq_detect_outliers(const float* W, int64_t rows, int64_t cols, const ezq_config* cfg,
+                        int mem, void* stream, ezq_outlier** entries, int64_t* n, double* mean,
+                        double* stddev) {
+    *entries = nullptr;
+    *n = 0;
+    if (rows > UINT32_MAX || cols > UINT32_MAX)
+        return set_error(EZQ_ERR_INVALID_ARGUMENT, "matrix dimensions exceed 32-bit coordinate range");
+    const int64_t N = rows * cols;
+    if (rows <= 0 || cols <= 0 || N <= 0) {
+        *mean = 0.0;
+        *stddev = 0.0;
+        return clear_error();
+    }
+    int dev;
+    if (int s = bind_device(&dev)) return s;
+    cudaStream_t st = pick_stream(stream, dev);
+    TDesc hd;
+    std::memset(&hd, 0, sizeof(hd));
+    hd.rows = rows;
+    hd.cols = cols;
+    hd.n = N;
+    hd.n_chunks = ceil_div(N, kStatsChunk);
+    hd.n_dblk = ceil_div(N, kDetectBlock);
+    Arena ar;
+    ar.reserve(sizeof(TStats));
+    ar.reserve(sizeof(TDesc));
+    ar.reserve(2 * sizeof(int64_t));
+    ar.reserve(2 * sizeof(int64_t));
+    for (int k = 0; k < 3; ++k) ar.reserve_n<double>(hd.n_chunks);
+    for (int k = 0; k < 2; ++k) ar.reserve_n<float>(hd.n_chunks);
+    for (int k = 0; k < 2; ++k) ar.reserve_n<long long>(hd.n_dblk);
+    if (mem == EZQ_MEM_HOST) ar.reserve(sizeof(float) * N);
+    if (int s = ar.allocate(st)) return s;
+    TStats* d_st = ar.take<TStats>(1);
+    TDesc* d_td = ar.take<TDesc>(1);
+    int64_t* d_cb = ar.take<int64_t>(2);
+    int64_t* d_db = ar.take<int64_t>(2);
+    Scratch sc{};
+    sc.p_sum = ar.take<double>(hd.n_chunks);
+    sc.p_max = ar.take<double>(hd.n_chunks);
+    sc.p_dev = ar.take<double>(hd.n_chunks);
+    sc.p_mn = ar.take<float>(hd.n_chunks);
+    sc.p_mx = ar.take<float>(hd.n_chunks);
+    sc.blk_count = ar.take<long long>(hd.n_dblk);
+    sc.blk_offset = ar.take<long long>(hd.n_dblk);
+    if (mem == EZQ_MEM_HOST) {
+        float* dW = ar.take<float>(N);
+        EZQ_CK(cudaMemcpyAsync(dW, W, sizeof(float) * N, cudaMemcpyHostToDevice, st));
+        hd.W = dW;
+    } else {
+        hd.W = W;
+    }
+    hd.st = d_st;
+    std::vector<TStats> hs(1, fresh_stats());
+    std::vector<TDesc> hdv(1, hd);
+    std::vector<int64_t> cb = {0, hd.n_chunks}, db = {0, hd.n_dblk};
+    if (int s = upload(d_st, hs, st)) return s;
+    if (int s = upload(d_td, hdv, st)) return s;
+    if (int s = upload(d_cb, cb, st)) return s;
+    if (int s = upload(d_db, db, st)) return s;
+    launch_stats_pass1(d_td, d_cb, 1, hd.n_chunks, sc, st);
+    launch_stats_fin1(d_td, 1, sc, st);
+    launch_stats_pass2(d_td, d_cb, 1, hd.n_chunks, sc, st);
+    launch_stats_fin2(d_td, 1, sc, cfg->sigma_n, 1, st);
+    launch_detect_count(d_td, d_db, 1, hd.n_dblk, sc, st);
+    launch_detect_scan(d_td, 1, sc, st);
+    EZQ_CK(cudaGetLastError());
+    EZQ_CK(cudaMemcpyAsync(hs.data(), d_st, sizeof(TStats), cudaMemcpyDeviceToHost, st));
+    EZQ_CK(cudaStreamSynchronize(st));
+    *mean = hs[0].mean;
+    *stddev = hs[0].stddev;
+    const int64_t cnt = hs[0].n_out;
+    if (cnt > 0) {
+        ezq_outlier* d_e = nullptr;
+        EZQ_CK(cudaMallocAsync(&d_e, sizeof(ezq_outlier) * cnt, st));
+        hdv[0].outliers = d_e;
+        if (int s = upload(d_td, hdv, st)) return s;
+        launch_detect_write(d_td, d_db, 1, hd.n_dblk, sc, st);
+        ezq_outlier* h = static_cast<ezq_outlier*>(std::malloc(sizeof(ezq_outlier) * cnt));
+        EZQ_CK(cudaMemcpyAsync(h, d_e, sizeof(ezq_outlier) * cnt, cudaMemcpyDeviceToHost, st));
+        cudaFreeAsync(d_e, st);
+        EZQ_CK(cudaStreamSynchronize(st));
+        *entries = h;
+    }
+    *n = cnt;
+    return clear_error();
+}
+
+// ---- dequantize_tensor (pipeline.cpp:117-142) -------------------------------
+int ezq_dequantize_tensor(const ezq_qweight* q, float* out, int out_mem, void* stream) {
+    if (q->rows <= 0 || q->cols <= 0)
+        return set_error(EZQ_ERR_IO_FORMAT, "quantized tensor has empty shape");
+    if (q->reserved)  // wrap() saw n_scales != cols
+        return set_error(EZQ_ERR_IO_FORMAT, "scale count does not match columns");
+    const int64_t N = q->rows * q->cols;
+    const int64_t need = ezq_packed_size(N, q->bits);
+    if (q->packed_bytes < need)
+        return set_error(EZQ_ERR_INVALID_ARGUMENT,
+                         "packed buffer holds " + std::to_string(q->packed_bytes) + " bytes, need " +
+                             std::to_string(need) + " for " + std::to_string(N) + " levels");
+    int dev;
+    if (int s = bind_device(&dev)) return s;
+    cudaStream_t st = pick_stream(stream, dev);
+    Arena ar;
+    ar.reserve(2 * sizeof(unsigned long long));
+    const bool hin = q->mem == EZQ_MEM_HOST;  // take() order below mirrors reserve()
+    if (hin) {
+        ar.reserve(need);
+        ar.reserve(sizeof(float) * q->cols);
+        ar.reserve(sizeof(ezq_outlier) * q->n_outliers);
+    }
+    if (out_mem == EZQ_MEM_HOST) ar.reserve(sizeof(float) * N);
+    if (int s = ar.allocate(st)) return s;
+    unsigned long long* d_bad = ar.take<unsigned long long>(2);
+    const uint8_t* pk = q->packed;
+    const float* sc = q->scales;
+    const ezq_outlier* oe = q->outliers;
+    if (hin) {
+        uint8_t* a = ar.take<uint8_t>(need);
+        float* b = ar.take<float>(q->cols);
+        ezq_outlier* c = ar.take<ezq_outlier>(q->n_outliers);
+        EZQ_CK(cudaMemcpyAsync(a, q->packed, need, cudaMemcpyHostToDevice, st));
+        EZQ_CK(cudaMemcpyAsync(b, q->scales, sizeof(float) * q->cols, cudaMemcpyHostToDevice, st));
+        if (q->n_outliers)
+            EZQ_CK(cudaMemcpyAsync(c, q->outliers, sizeof(ezq_outlier) * q->n_outliers,
+                                   cudaMemcpyHostToDevice, st));
+        pk = a;
+        sc = b;
+        oe = c;
+    }
+    float* dst = out_mem == EZQ_MEM_HOST ? ar.take<float>(N) : out;
+    EZQ_CK(cudaMemsetAsync(d_bad, 0xff, 2 * sizeof(unsigned long long), st));
+    launch_dequant(q->rows, q->cols, q->bits, pk, sc, dst, d_bad, st);
+    launch_scatter(q->rows, q->cols, oe, q->n_outliers, dst, d_bad + 1, st);
+    EZQ_CK(cudaGetLastError());
+    unsigned long long hb[2];
+    EZQ_CK(cudaMemcpyAsync(hb, d_bad, sizeof(hb), cudaMemcpyDeviceToHost, st));
+    EZQ_CK(cudaStreamSynchronize(st));
+    if (hb[0] != kNoBad) {
+        uint8_t byte = 0;
+        EZQ_CK(cudaMemcpy(&byte, pk + hb[0], 1, cudaMemcpyDeviceToHost));
+        const int lmin = -(1 << (q->bits - 1)) + 1;
+        const int span = (1 << (q->bits - 1)) - lmin;
+        return set_error(EZQ_ERR_INVALID_ARGUMENT,
+                         "packed byte " + std::to_string(byte) + " exceeds level span " +
+                             std::to_string(span),
+                         static_cast<int64_t>(hb[0]));
+    }
+    if (hb[1] != kNoBad) {
+        ezq_outlier e;
+        EZQ_CK(cudaMemcpy(&e, oe + hb[1], sizeof(e), cudaMemcpyDeviceToHost));
+        return set_error(EZQ_ERR_INVALID_ARGUMENT,
+                         "outlier coordinate (" + std::to_string(e.row) + ", " +
+                             std::to_string(e.col) + ") outside " + std::to_string(q->rows) + "x" +
+                             std::to_string(q->cols),
+                         static_cast<int64_t>(hb[1]));
+    }
+    if (out_mem == EZQ_MEM_HOST) {
+        EZQ_CK(cudaMemcpyAsync(out, dst, sizeof(float) * N, cudaMemcpyDeviceToHost, st));
+        EZQ_CK(cudaStreamSynchronize(st));
+    }
+    return clear_error();
+}
+
+// ---- reconstruction_error (rtn.cpp:34-77) -----------------------------------
+int ezq_reconstruction_error(const float* a, const float* b, int64_t rows, int64_t cols,
+                             const uint32_t* skip_rows, const uint32_t* skip_cols, int64_t n_skip,
+                             int mem, void* stream, double* out) {
+    *out = 0.0;
+    // Column lists in entry order (outlier_rows_by_column, outliers.cpp:75-87).
+    std::vector<int64_t> off;
+    std::vector<uint32_t> srows;
+    if (skip_rows && n_skip > 0) {
+        std::vector<int64_t> cnt(static_cast<size_t>(cols) + 1, 0);
+        for (int64_t i = 0; i < n_skip; ++i) {
+            if (skip_cols[i] >= static_cast<uint64_t>(cols))
+                return set_error(EZQ_ERR_INVALID_ARGUMENT,
+                                 "outlier column " + std::to_string(skip_cols[i]) +
+                                     " out of range for " + std::to_string(cols) + " columns");
+            ++cnt[skip_cols[i] + 1];
+        }
+        for (int64_t c = 0; c < cols; ++c) cnt[c + 1] += cnt[c];
+        off = cnt;
+        srows.resize(n_skip);
+        std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+        for (int64_t i = 0; i < n_skip; ++i) srows[pos[skip_cols[i]]++] = skip_rows[i];
+    }
+    if (rows <= 0 || cols <= 0) return clear_error();
+    int dev;
+    if (int s = bind_device(&dev)) return s;
+    cudaStream_t st = pick_stream(stream, dev);
+    const int64_t N = rows * cols;
+    Arena ar;
+    ar.reserve(sizeof(double) * cols);
+    ar.reserve(sizeof(int64_t) * off.size());
+    ar.reserve(sizeof(uint32_t) * srows.size());
+    if (mem == EZQ_MEM_HOST) {
+        ar.reserve(sizeof(float) * N);
+        ar.reserve(sizeof(float) * N);
+    }
+    if (int s = ar.allocate(st)) return s;
+    double* d_col = ar.take<double>(cols);
+    int64_t* d_off = off.empty() ? nullptr : ar.take<int64_t>(off.size());
+    uint32_t* d_rows = srows.empty() ? nullptr : ar.take<uint32_t>(srows.size());
+    const float *da = a, *db = b;
+    if (mem == EZQ_MEM_HOST) {
+        float* x = ar.take<float>(N);
+        float* y = ar.take<float>(N);
+        EZQ_CK(cudaMemcpyAsync(x, a, sizeof(float) * N, cudaMemcpyHostToDevice, st));
+        EZQ_CK(cudaMemcpyAsync(y, b, sizeof(float) * N, cudaMemcpyHostToDevice, st));
+        da = x;
+        db = y;
+    }
+    if (d_off) {
+        if (int s = upload(d_off, off, st)) return s;
+        if (int s = upload(d_rows, srows, st)) return s;
+    }
+    launch_recon_error(da, db, rows, cols, d_off, d_rows, d_col, st);
+    EZQ_CK(cudaGetLastError());
+    std::vector<double> col(cols);
+    EZQ_CK(cudaMemcpyAsync(col.data(), d_col, sizeof(double) * cols, cudaMemcpyDeviceToHost, st));
+    EZQ_CK(cudaStreamSynchronize(st));
+    double total = 0.0;
+    for (double v : col) total += v;  // column-ordered merge (rtn.cpp:74-75)
+    *out = total;
+    return clear_error();
+}
+
+}  // extern "C"

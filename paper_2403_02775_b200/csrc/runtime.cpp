@@ -1,0 +1,350 @@
+// Host runtime: error slots, streams, device info, config validation and the
+// small C-ABI utilities. No compute happens here.
+#include "runtime.hpp"
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
+namespace ezq {
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+namespace {
+
+struct ErrState {
+    int code = 0;
+    std::string msg;
+    int64_t index = -1;
+};
+thread_local ErrState t_err;
+thread_local int t_device = -1;
+thread_local std::unordered_map<int, cudaStream_t> t_streams;
+
+std::mutex g_mu;
+std::unordered_map<int, DeviceInfo> g_info;
+std::unordered_map<int, bool> g_pool_ready;
+
+}  // namespace
+
+int set_error(int code, const std::string& msg, int64_t index) {
+    t_err.code = code;
+    t_err.msg = msg;
+    t_err.index = index;
+    return code;
+}
+
+int clear_error() {
+    t_err.code = 0;
+    t_err.msg.clear();
+    t_err.index = -1;
+    return EZQ_OK;
+}
+
+int cuda_error(cudaError_t e, const char* where) {
+    const int code = (e == cudaErrorMemoryAllocation) ? EZQ_ERR_OOM : EZQ_ERR_CUDA;
+    return set_error(code, std::string("CUDA error ") + cudaGetErrorString(e) + " at " + where);
+}
+
+int bind_device(int* dev) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return set_error(EZQ_ERR_NO_DEVICE,
+                         "no CUDA device available (the B200 engine has no CPU fallback)");
+    }
+    int d = t_device;
+    if (d < 0) {
+        EZQ_CK(cudaGetDevice(&d));
+    } else {
+        EZQ_CK(cudaSetDevice(d));
+    }
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (!g_pool_ready[d]) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+            g_pool_ready[d] = true;
+        }
+    }
+    *dev = d;
+    return EZQ_OK;
+}
+
+cudaStream_t thread_stream(int dev) {
+    auto it = t_streams.find(dev);
+    if (it != t_streams.end()) return it->second;
+    cudaStream_t s = nullptr;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    t_streams[dev] = s;
+    return s;
+}
+
+const DeviceInfo& device_info(int dev) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_info.find(dev);
+    if (it != g_info.end()) return it->second;
+    DeviceInfo di;
+    cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&di.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return g_info[dev] = di;
+}
+
+std::string fmt_double(double v) { return std::to_string(v); }
+
+int validate_config(const ezq_config* c, std::string* msg) {
+    if (c->bits < 2 || c->bits > 8) {
+        *msg = "bits must be in [2, 8], got " + std::to_string(c->bits);
+        return EZQ_ERR_INVALID_ARGUMENT;
+    }
+    if (!(c->sigma_n >= 0.0f) || !std::isfinite(c->sigma_n)) {
+        *msg = "sigma_n must be finite and >= 0";
+        return EZQ_ERR_INVALID_ARGUMENT;
+    }
+    if (!(c->lr > 0.0) || !std::isfinite(c->lr)) {
+        *msg = "lr must be finite and > 0";
+        return EZQ_ERR_INVALID_ARGUMENT;
+    }
+    if (!(c->beta1 >= 0.0 && c->beta1 < 1.0)) {
+        *msg = "adam_beta1 must be in [0, 1)";
+        return EZQ_ERR_INVALID_ARGUMENT;
+    }
+    if (!(c->beta2 >= 0.0 && c->beta2 < 1.0)) {
+        *msg = "adam_beta2 must be in [0, 1)";
+        return EZQ_ERR_INVALID_ARGUMENT;
+    }
+    if (!(c->eps > 0.0)) {
+        *msg = "adam_eps must be > 0";
+        return EZQ_ERR_INVALID_ARGUMENT;
+    }
+    if (c->steps < 0) {
+        *msg = "steps must be >= 0";
+        return EZQ_ERR_INVALID_ARGUMENT;
+    }
+    if (c->select_step < 0) {
+        *msg = "select_step must be >= 0";
+        return EZQ_ERR_INVALID_ARGUMENT;
+    }
+    return EZQ_OK;
+}
+
+void bias_tables(const ezq_config* c, std::vector<double>& h) {
+    const int n = (c->steps > 0 ? c->steps : 0) + 1;
+    h.assign(2 * static_cast<size_t>(n), 1.0);
+    for (int t = 1; t < n; ++t) {
+        // optimize.cpp:90-91 evaluates exactly these with glibc pow.
+        h[t] = 1.0 - std::pow(c->beta1, static_cast<double>(t));
+        h[n + t] = 1.0 - std::pow(c->beta2, static_cast<double>(t));
+    }
+}
+
+CfgDev make_cfg(const ezq_config* c, int mode, const double* bc_dev) {
+    CfgDev d{};
+    d.bits = c->bits;
+    d.lmin = -(1 << (c->bits - 1)) + 1;
+    d.lmax = 1 << (c->bits - 1);
+    d.mode = mode;
+    d.steps = c->steps;
+    d.select = c->select;
+    d.fixed_at = c->select_step < c->steps ? c->select_step : c->steps;
+    d.sigma_n = c->sigma_n;
+    d.guard = level_guard(d.lmax);
+    d.adam.b1 = c->beta1;
+    d.adam.b2 = c->beta2;
+    d.adam.c1 = 1.0 - c->beta1;
+    d.adam.c2 = 1.0 - c->beta2;
+    d.adam.lr = c->lr;
+    d.adam.eps = c->eps;
+    const int n = (c->steps > 0 ? c->steps : 0) + 1;
+    d.bc1 = bc_dev;
+    d.bc2 = bc_dev ? bc_dev + n : nullptr;
+    return d;
+}
+
+int Arena::allocate(cudaStream_t st) {
+    owner_ = st;
+    off_ = 0;
+    if (need_ == 0) return EZQ_OK;
+    EZQ_CK(cudaMallocAsync(reinterpret_cast<void**>(&base_), need_, st));
+    return EZQ_OK;
+}
+
+void Arena::release(cudaStream_t st) {
+    if (base_) cudaFreeAsync(base_, st);
+    base_ = nullptr;
+}
+
+Arena::~Arena() {
+    if (base_) cudaFreeAsync(base_, owner_);
+}
+
+}  // namespace ezq
+
+using namespace ezq;
+
+extern "C" {
+
+void ezq_config_default(ezq_config* c) {
+    std::memset(c, 0, sizeof(*c));
+    c->bits = 4;
+    c->sigma_n = 3.0f;
+    c->lr = 1e-3;
+    c->beta1 = 0.9;
+    c->beta2 = 0.999;
+    c->eps = 1e-8;
+    c->steps = 200;
+    c->select = EZQ_SELECT_BEST;
+    c->select_step = 100;
+    c->seed = 0;
+}
+
+int ezq_config_validate(const ezq_config* cfg) {
+    std::string msg;
+    const int s = validate_config(cfg, &msg);
+    return s ? set_error(s, msg) : clear_error();
+}
+
+int ezq_last_error(char* msg, size_t cap, int64_t* index) {
+    if (msg && cap) {
+        std::strncpy(msg, t_err.msg.c_str(), cap - 1);
+        msg[cap - 1] = 0;
+    }
+    if (index) *index = t_err.index;
+    return t_err.code;
+}
+
+int ezq_device_count(int* n) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+        cudaGetLastError();
+        c = 0;
+    }
+    *n = c;
+    return clear_error();
+}
+
+int ezq_set_device(int device) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess || device < 0 || device >= c) {
+        cudaGetLastError();
+        return set_error(EZQ_ERR_NO_DEVICE, "invalid device " + std::to_string(device));
+    }
+    t_device = device;
+    EZQ_CK(cudaSetDevice(device));
+    return clear_error();
+}
+
+int ezq_synchronize(void) {
+    int dev;
+    if (int s = bind_device(&dev)) return s;
+    EZQ_CK(cudaStreamSynchronize(thread_stream(dev)));
+    return clear_error();
+}
+
+const char* ezq_version(void) { return "ezquant-b200 0.1.0 (sm_100a)"; }
+
+int64_t ezq_kernel_launches(void) { return g_launches.load(); }
+
+void ezq_free(void* p) { std::free(p); }
+
+// ---- host scalar utilities (bookkeeping; identical arithmetic) -----------
+double ezq_initial_scale(const float* x, int64_t n, const ezq_config* cfg) {
+    double max_abs = 0.0;  // rtn.cpp:81-86
+    for (int64_t i = 0; i < n; ++i) {
+        const double a = std::fabs(static_cast<double>(x[i]));
+        max_abs = (max_abs < a) ? a : max_abs;
+    }
+    if (max_abs == 0.0) return 1.0;
+    return max_abs / static_cast<double>(1 << (cfg->bits - 1));
+}
+
+int ezq_adam_step(double* m, double* v, int64_t* t, double scale, double grad,
+                  const ezq_config* c, double* out) {
+    // optimize.cpp:86-94; volatile temporaries keep the host compiler from
+    // contracting into FMAs so the result matches the device update.
+    *t += 1;
+    volatile double a = c->beta1 * *m;
+    volatile double b = (1.0 - c->beta1) * grad;
+    *m = a + b;
+    volatile double p = (1.0 - c->beta2) * grad;
+    volatile double q = p * grad;
+    volatile double r = c->beta2 * *v;
+    *v = r + q;
+    const double mh = *m / (1.0 - std::pow(c->beta1, static_cast<double>(*t)));
+    const double vh = *v / (1.0 - std::pow(c->beta2, static_cast<double>(*t)));
+    volatile double num = c->lr * mh;
+    const double upd = num / (std::sqrt(vh) + c->eps);
+    const double updated = scale - upd;
+    *out = updated < 1e-12 ? 1e-12 : updated;
+    return clear_error();
+}
+
+int64_t ezq_packed_size(int64_t count, int bits) { return bits == 4 ? (count + 1) / 2 : count; }
+
+int ezq_pack_levels(const int16_t* lv, int64_t n, int bits, uint8_t* out) {
+    const int lmin = -(1 << (bits - 1)) + 1, lmax = 1 << (bits - 1);
+    for (int64_t i = 0; i < n; ++i)  // rtn.cpp:127-131
+        if (lv[i] < lmin || lv[i] > lmax)
+            return set_error(EZQ_ERR_INVALID_ARGUMENT,
+                             "level " + std::to_string(lv[i]) + " outside [" +
+                                 std::to_string(lmin) + ", " + std::to_string(lmax) + "]");
+    const int64_t nb = ezq_packed_size(n, bits);
+    std::memset(out, 0, static_cast<size_t>(nb));
+    if (bits == 4) {
+        for (int64_t i = 0; i < n; ++i) {
+            const uint8_t nib = static_cast<uint8_t>(lv[i] - lmin);
+            if (i % 2 == 0)
+                out[i / 2] = nib;
+            else
+                out[i / 2] |= static_cast<uint8_t>(nib << 4);
+        }
+    } else {
+        for (int64_t i = 0; i < n; ++i) out[i] = static_cast<uint8_t>(lv[i] - lmin);
+    }
+    return clear_error();
+}
+
+int ezq_unpack_levels(const uint8_t* b, int64_t nbytes, int64_t count, int bits, int16_t* out) {
+    if (count < 0) return set_error(EZQ_ERR_INVALID_ARGUMENT, "negative level count");
+    const int64_t need = ezq_packed_size(count, bits);
+    if (nbytes < need)  // rtn.cpp:153-157
+        return set_error(EZQ_ERR_INVALID_ARGUMENT,
+                         "packed buffer holds " + std::to_string(nbytes) + " bytes, need " +
+                             std::to_string(need) + " for " + std::to_string(count) + " levels");
+    const int lmin = -(1 << (bits - 1)) + 1;
+    const int span = (1 << (bits - 1)) - lmin;
+    if (bits == 4) {
+        for (int64_t i = 0; i < count; ++i) {
+            const uint8_t v = b[i / 2];
+            out[i] = static_cast<int16_t>(lmin + ((i % 2 == 0) ? (v & 0x0f) : (v >> 4)));
+        }
+    } else {
+        for (int64_t i = 0; i < count; ++i) {
+            if (b[i] > span)
+                return set_error(EZQ_ERR_INVALID_ARGUMENT,
+                                 "packed byte " + std::to_string(b[i]) + " exceeds level span " +
+                                     std::to_string(span),
+                                 i);
+            out[i] = static_cast<int16_t>(lmin + b[i]);
+        }
+    }
+    return clear_error();
+}
+
+int ezq_dequantize_channel(const int16_t* lv, int64_t n, double scale, float* out) {
+    if (!(scale > 0.0) || !std::isfinite(scale))
+        return set_error(EZQ_ERR_INVALID_ARGUMENT,
+                         "scale must be finite and > 0, got " + fmt_double(scale));
+    for (int64_t i = 0; i < n; ++i)
+        out[i] = static_cast<float>(scale * static_cast<double>(lv[i]));  // rtn.cpp:101-107
+    return clear_error();
+}
+
+}  // extern "C"

@@ -1,0 +1,452 @@
+"""ctypes binding of the B200 engine's C-ABI (include/ezquant_c.h).
+
+This is the Python face of the drop-in boundary: the same entry points a
+reference integrator would bind. Arrays are numpy (host) or
+torch CUDA tensors (device, passed by data_ptr()). There is no CPU fallback:
+if libezq_b200.so is missing or no CUDA device exists, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_DIR = os.path.join(_HERE, "_lib")
+LIB_PATH = os.path.join(LIB_DIR, "libezq_b200.so")
+
+OK, INVALID_ARGUMENT, INVARIANT, IO_FAILURE, IO_FORMAT, IO_VERSION = 0, 1, 2, 3, 4, 5
+CUDA_ERROR, NO_DEVICE, OOM = 10, 11, 12
+MEM_HOST, MEM_DEVICE = 0, 1
+MODES = {"easyquant": 0, "rtn": 1, "outliers-only": 2}
+SELECT_BEST, SELECT_FIXED = 0, 1
+
+
+class EzqError(RuntimeError):
+    def __init__(self, code: int, msg: str, index: int):
+        super().__init__(f"[ezq {code}] {msg}")
+        self.code, self.msg, self.index = code, msg, index
+
+
+class InvalidArgument(EzqError, ValueError):
+    pass
+
+
+class InvariantError(EzqError):
+    pass
+
+
+class IoError(EzqError):
+    pass
+
+
+class CConfig(C.Structure):
+    _fields_ = [("bits", C.c_int32), ("sigma_n", C.c_float), ("lr", C.c_double),
+                ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("steps", C.c_int32), ("select", C.c_int32), ("select_step", C.c_int32),
+                ("reserved", C.c_int32), ("seed", C.c_uint64)]
+
+
+class CStats(C.Structure):
+    _fields_ = [("mean", C.c_double), ("stddev", C.c_double), ("max_abs", C.c_double),
+                ("count", C.c_int64)]
+
+
+class COutlier(C.Structure):
+    _fields_ = [("row", C.c_uint32), ("col", C.c_uint32), ("value", C.c_float)]
+
+
+OUTLIER_DTYPE = np.dtype([("row", "<u4"), ("col", "<u4"), ("value", "<f4")])
+
+
+class CQWeight(C.Structure):
+    _fields_ = [("rows", C.c_int64), ("cols", C.c_int64), ("bits", C.c_int32), ("mem", C.c_int32),
+                ("packed_bytes", C.c_int64), ("packed", C.POINTER(C.c_uint8)),
+                ("scales", C.POINTER(C.c_float)), ("n_outliers", C.c_int64),
+                ("outliers", C.POINTER(COutlier)), ("mean", C.c_double), ("stddev", C.c_double),
+                ("sigma_n", C.c_float), ("has_errors", C.c_int32), ("rtn_error", C.c_double),
+                ("final_error", C.c_double), ("owned", C.c_int32), ("reserved", C.c_int32)]
+
+
+class COptResult(C.Structure):
+    _fields_ = [("scale", C.c_float), ("best_step", C.c_int32), ("initial_error", C.c_double),
+                ("final_error", C.c_double), ("best_scale", C.c_double),
+                ("best_error", C.c_double), ("n_trace", C.c_int32), ("reserved", C.c_int32)]
+
+
+@dataclass
+class Config:
+    """QuantConfig (types.hpp:37-54) with the reference defaults."""
+    bits: int = 4
+    sigma_n: float = 3.0
+    lr: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    steps: int = 200
+    select: str = "best"          # "best" | "fixed"
+    select_step: int = 100
+    seed: int = 0
+
+    def to_c(self) -> CConfig:
+        return CConfig(self.bits, self.sigma_n, self.lr, self.beta1, self.beta2, self.eps,
+                       self.steps, SELECT_FIXED if self.select == "fixed" else SELECT_BEST,
+                       self.select_step, 0, self.seed)
+
+    @property
+    def level_min(self) -> int:
+        return -(1 << (self.bits - 1)) + 1
+
+    @property
+    def level_max(self) -> int:
+        return 1 << (self.bits - 1)
+
+
+@dataclass
+class QuantizedWeight:
+    """Host copy of QuantizedWeight (types.hpp:103-113)."""
+    rows: int
+    cols: int
+    bits: int
+    packed: np.ndarray                  # uint8
+    scales: np.ndarray                  # float32 [cols]
+    outliers: np.ndarray                # OUTLIER_DTYPE, sorted by (row, col)
+    mean: float = 0.0
+    stddev: float = 0.0
+    sigma_n: float = 0.0
+    rtn_error: Optional[float] = None
+    final_error: Optional[float] = None
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"B200 engine not built: {LIB_PATH} missing (run __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        P, I64, I32, D = C.c_void_p, C.c_int64, C.c_int, C.c_double
+        L.ezq_last_error.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(C.c_int64)]
+        L.ezq_config_validate.argtypes = [C.POINTER(CConfig)]
+        L.ezq_device_count.argtypes = [C.POINTER(C.c_int)]
+        L.ezq_set_device.argtypes = [I32]
+        L.ezq_version.restype = C.c_char_p
+        L.ezq_kernel_launches.restype = I64
+        L.ezq_tensor_stats.argtypes = [P, I64, I64, I32, P, C.POINTER(CStats)]
+        L.ezq_detect_outliers.argtypes = [P, I64, I64, C.POINTER(CConfig), I32, P,
+                                          C.POINTER(C.POINTER(COutlier)), C.POINTER(I64),
+                                          C.POINTER(D), C.POINTER(D)]
+        L.ezq_quantize_tensor.argtypes = [P, I64, I64, C.POINTER(CConfig), I32, I32, I32, P,
+                                          C.POINTER(C.POINTER(CQWeight))]
+        L.ezq_quantize_batch.argtypes = [C.POINTER(P), C.POINTER(I64), C.POINTER(I64), I32,
+                                         C.POINTER(CConfig), I32, I32, I32, P,
+                                         C.POINTER(C.POINTER(CQWeight)), C.POINTER(C.c_int)]
+        L.ezq_dequantize_tensor.argtypes = [C.POINTER(CQWeight), P, I32, P]
+        L.ezq_qweight_wrap.argtypes = [I64, I64, I32, P, I64, P, I64, P, I64, D, D, C.c_float,
+                                       I32, C.POINTER(C.POINTER(CQWeight))]
+        L.ezq_qweight_free.argtypes = [C.POINTER(CQWeight)]
+        L.ezq_free.argtypes = [P]
+        L.ezq_reconstruction_error.argtypes = [P, P, I64, I64, P, P, I64, I32, P, C.POINTER(D)]
+        L.ezq_channel_eval.argtypes = [P, I64, P, I64, D, C.POINTER(CConfig), C.POINTER(D),
+                                       C.POINTER(D)]
+        L.ezq_optimize_channel.argtypes = [P, I64, P, I64, C.POINTER(CConfig), I32,
+                                           C.POINTER(COptResult), P, P, P]
+        L.ezq_brute_force_scale.argtypes = [P, I64, P, I64, C.POINTER(CConfig), I32,
+                                            C.POINTER(D), C.POINTER(D)]
+        L.ezq_quantize_channel.argtypes = [P, I64, D, C.POINTER(CConfig), P]
+        L.ezq_initial_scale.argtypes = [P, I64, C.POINTER(CConfig)]
+        L.ezq_initial_scale.restype = D
+        L.ezq_adam_step.argtypes = [C.POINTER(D), C.POINTER(D), C.POINTER(I64), D, D,
+                                    C.POINTER(CConfig), C.POINTER(D)]
+        L.ezq_packed_size.argtypes = [I64, I32]
+        L.ezq_packed_size.restype = I64
+        L.ezq_pack_levels.argtypes = [P, I64, I32, P]
+        L.ezq_unpack_levels.argtypes = [P, I64, I64, I32, P]
+        L.ezq_dequantize_channel.argtypes = [P, I64, D, P]
+        L.ezq_gemv_prepare.argtypes = [C.POINTER(CQWeight), P, C.POINTER(P)]
+        L.ezq_gemv.argtypes = [P, P, I32, I32, P, P]
+        L.ezq_gemv_plan_free.argtypes = [P]
+        _lib = L
+    return _lib
+
+
+def _raise(code: int):
+    buf = C.create_string_buffer(2048)
+    idx = C.c_int64(-1)
+    lib().ezq_last_error(buf, 2048, C.byref(idx))
+    msg = buf.value.decode()
+    cls = {INVALID_ARGUMENT: InvalidArgument, INVARIANT: InvariantError, IO_FAILURE: IoError,
+           IO_FORMAT: IoError, IO_VERSION: IoError}.get(code, EzqError)
+    raise cls(code, msg, idx.value)
+
+
+def check(code: int):
+    if code != OK:
+        _raise(code)
+
+
+def _ptr(a) -> Optional[int]:
+    """Address of a numpy array or torch tensor (None for None)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()
+
+
+def _mem(a) -> int:
+    return MEM_HOST if isinstance(a, np.ndarray) else (MEM_DEVICE if a.is_cuda else MEM_HOST)
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        return None
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    lib().ezq_device_count(C.byref(n))
+    return n.value
+
+
+def set_device(d: int):
+    check(lib().ezq_set_device(d))
+
+
+def kernel_launches() -> int:
+    return int(lib().ezq_kernel_launches())
+
+
+def config_validate(cfg: Config):
+    c = cfg.to_c()
+    check(lib().ezq_config_validate(C.byref(c)))
+
+
+# ---- tensor-scale ---------------------------------------------------------
+def tensor_stats(W, stream=None) -> dict:
+    """stats.hpp:14 -> {mean, stddev, max_abs, count}."""
+    rows, cols = W.shape
+    st = CStats()
+    check(lib().ezq_tensor_stats(_ptr(W), rows, cols, _mem(W), _stream(stream), C.byref(st)))
+    return {"mean": st.mean, "stddev": st.stddev, "max_abs": st.max_abs, "count": st.count}
+
+
+def detect_outliers(W, cfg: Config, stream=None):
+    """outliers.hpp:15 -> (entries[OUTLIER_DTYPE], mean, stddev)."""
+    rows, cols = W.shape
+    c = cfg.to_c()
+    e = C.POINTER(COutlier)()
+    n = C.c_int64(0)
+    mean, std = C.c_double(0), C.c_double(0)
+    check(lib().ezq_detect_outliers(_ptr(W), rows, cols, C.byref(c), _mem(W), _stream(stream),
+                                    C.byref(e), C.byref(n), C.byref(mean), C.byref(std)))
+    out = np.zeros(n.value, dtype=OUTLIER_DTYPE)
+    if n.value:
+        C.memmove(out.ctypes.data, e, n.value * 12)
+        lib().ezq_free(e)
+    return out, mean.value, std.value
+
+
+def _from_c(q: CQWeight) -> QuantizedWeight:
+    assert q.mem == MEM_HOST
+    packed = np.ctypeslib.as_array(q.packed, shape=(q.packed_bytes,)).copy() if q.packed_bytes else np.zeros(0, np.uint8)
+    scales = np.ctypeslib.as_array(q.scales, shape=(q.cols,)).copy()
+    outl = np.zeros(q.n_outliers, dtype=OUTLIER_DTYPE)
+    if q.n_outliers:
+        C.memmove(outl.ctypes.data, q.outliers, q.n_outliers * 12)
+    return QuantizedWeight(q.rows, q.cols, q.bits, packed, scales, outl, q.mean, q.stddev,
+                           q.sigma_n, q.rtn_error if q.has_errors else None,
+                           q.final_error if q.has_errors else None)
+
+
+def quantize_tensor(W, cfg: Config, mode: str = "easyquant", stream=None) -> QuantizedWeight:
+    """pipeline.hpp:33 -- host copy of the artifact (device work inside)."""
+    rows, cols = W.shape
+    c = cfg.to_c()
+    q = C.POINTER(CQWeight)()
+    check(lib().ezq_quantize_tensor(_ptr(W), rows, cols, C.byref(c), MODES[mode], _mem(W),
+                                    MEM_HOST, _stream(stream), C.byref(q)))
+    try:
+        return _from_c(q.contents)
+    finally:
+        lib().ezq_qweight_free(q)
+
+
+class DeviceBatch:
+    """Device-resident outputs of ezq_quantize_batch (freed on close())."""
+
+    def __init__(self, ptrs):
+        self.ptrs = ptrs
+
+    def __len__(self):
+        return len(self.ptrs)
+
+    def __getitem__(self, i) -> CQWeight:
+        return self.ptrs[i].contents
+
+    def close(self):
+        for p in self.ptrs:
+            if p:
+                lib().ezq_qweight_free(p)
+        self.ptrs = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def quantize_batch(Ws: Sequence, cfg: Config, mode: str = "easyquant", out_mem: int = MEM_HOST,
+                   stream=None):
+    """ezq_quantize_batch: list of QuantizedWeight (host) or a DeviceBatch."""
+    n = len(Ws)
+    ptrs = (C.c_void_p * n)(*[_ptr(w) for w in Ws])
+    rows = (C.c_int64 * n)(*[w.shape[0] for w in Ws])
+    cols = (C.c_int64 * n)(*[w.shape[1] for w in Ws])
+    outs = (C.POINTER(CQWeight) * n)()
+    failed = C.c_int(-1)
+    c = cfg.to_c()
+    check(lib().ezq_quantize_batch(ptrs, rows, cols, n, C.byref(c), MODES[mode], _mem(Ws[0]),
+                                   out_mem, _stream(stream), outs, C.byref(failed)))
+    if out_mem == MEM_DEVICE:
+        return DeviceBatch(list(outs))
+    res = []
+    for p in outs:
+        res.append(_from_c(p.contents))
+        lib().ezq_qweight_free(p)
+    return res
+
+
+def dequantize(q: QuantizedWeight, out=None, stream=None) -> np.ndarray:
+    """pipeline.hpp:41 dequantize_tensor for a host artifact."""
+    outl = np.ascontiguousarray(q.outliers, dtype=OUTLIER_DTYPE)
+    w = C.POINTER(CQWeight)()
+    packed = np.ascontiguousarray(q.packed, dtype=np.uint8)
+    scales = np.ascontiguousarray(q.scales, dtype=np.float32)
+    check(lib().ezq_qweight_wrap(q.rows, q.cols, q.bits, _ptr(packed), packed.size, _ptr(scales),
+                                 scales.size, _ptr(outl), outl.size, q.mean, q.stddev, q.sigma_n,
+                                 MEM_HOST, C.byref(w)))
+    if out is None:
+        out = np.zeros((max(q.rows, 0), max(q.cols, 0)), dtype=np.float32)
+    try:
+        check(lib().ezq_dequantize_tensor(w, _ptr(out), _mem(out), _stream(stream)))
+    finally:
+        lib().ezq_qweight_free(w)
+    return out
+
+
+def reconstruction_error(a, b, skip: Optional[np.ndarray] = None) -> float:
+    rows, cols = a.shape
+    r = c = None
+    n = 0
+    if skip is not None and len(skip):
+        r = np.ascontiguousarray(skip["row"]).astype(np.uint32)
+        c = np.ascontiguousarray(skip["col"]).astype(np.uint32)
+        n = len(skip)
+    out = C.c_double(0)
+    check(lib().ezq_reconstruction_error(_ptr(a), _ptr(b), rows, cols, _ptr(r), _ptr(c), n,
+                                         _mem(a), None, C.byref(out)))
+    return out.value
+
+
+# ---- channel-scale ----------------------------------------------------------
+def _f32(x):
+    return np.ascontiguousarray(x, dtype=np.float32)
+
+
+def _mask(m):
+    if m is None:
+        return None, 0
+    m = np.ascontiguousarray(m, dtype=np.uint32)
+    return m, m.size
+
+
+def channel_eval(x, mask, s: float, cfg: Config):
+    x = _f32(x)
+    m, nm = _mask(mask)
+    e, g = C.c_double(0), C.c_double(0)
+    c = cfg.to_c()
+    check(lib().ezq_channel_eval(_ptr(x), x.size, _ptr(m), nm, s, C.byref(c), C.byref(e), C.byref(g)))
+    return e.value, g.value
+
+
+def optimize_channel(x, mask, cfg: Config, keep_trace: bool = False) -> dict:
+    x = _f32(x)
+    m, nm = _mask(mask)
+    c = cfg.to_c()
+    r = COptResult()
+    n = max(cfg.steps, 0) + 1
+    ts = np.zeros(n, np.int32)
+    sc = np.zeros(n, np.float64)
+    er = np.zeros(n, np.float64)
+    check(lib().ezq_optimize_channel(_ptr(x), x.size, _ptr(m), nm, C.byref(c), int(keep_trace),
+                                     C.byref(r), _ptr(ts), _ptr(sc), _ptr(er)))
+    k = r.n_trace
+    return {"scale": r.scale, "initial_error": r.initial_error, "final_error": r.final_error,
+            "best_step": r.best_step, "best_scale": r.best_scale, "best_error": r.best_error,
+            "trace_step": ts[:k], "trace_scale": sc[:k], "trace_error": er[:k]}
+
+
+def brute_force_scale(x, mask, cfg: Config, grid_points: int = 2000):
+    x = _f32(x)
+    m, nm = _mask(mask)
+    c = cfg.to_c()
+    s, e = C.c_double(0), C.c_double(0)
+    check(lib().ezq_brute_force_scale(_ptr(x), x.size, _ptr(m), nm, C.byref(c), grid_points,
+                                      C.byref(s), C.byref(e)))
+    return s.value, e.value
+
+
+def quantize_channel(x, scale: float, cfg: Config) -> np.ndarray:
+    x = _f32(x)
+    out = np.zeros(x.size, np.int16)
+    c = cfg.to_c()
+    check(lib().ezq_quantize_channel(_ptr(x), x.size, scale, C.byref(c), _ptr(out)))
+    return out
+
+
+def initial_scale(x, cfg: Config) -> float:
+    x = _f32(x)
+    c = cfg.to_c()
+    return lib().ezq_initial_scale(_ptr(x), x.size, C.byref(c))
+
+
+def adam_step(state: dict, scale: float, grad: float, cfg: Config) -> float:
+    m, v, t = C.c_double(state["m"]), C.c_double(state["v"]), C.c_int64(state["t"])
+    out = C.c_double(0)
+    c = cfg.to_c()
+    check(lib().ezq_adam_step(C.byref(m), C.byref(v), C.byref(t), scale, grad, C.byref(c), C.byref(out)))
+    state.update(m=m.value, v=v.value, t=t.value)
+    return out.value
+
+
+def packed_size(count: int, bits: int) -> int:
+    return int(lib().ezq_packed_size(count, bits))
+
+
+def pack_levels(levels, bits: int) -> np.ndarray:
+    lv = np.ascontiguousarray(levels, dtype=np.int16)
+    out = np.zeros(packed_size(lv.size, bits), np.uint8)
+    check(lib().ezq_pack_levels(_ptr(lv), lv.size, bits, _ptr(out)))
+    return out
+
+
+def unpack_levels(b, count: int, bits: int) -> np.ndarray:
+    b = np.ascontiguousarray(b, dtype=np.uint8)
+    out = np.zeros(max(count, 0), np.int16)
+    check(lib().ezq_unpack_levels(_ptr(b), b.size, count, bits, _ptr(out)))
+    return out
+
+
+def dequantize_channel(levels, scale: float) -> np.ndarray:
+    lv = np.ascontiguousarray(levels, dtype=np.int16)
+    out = np.zeros(lv.size, np.float32)
+    check(lib().ezq_dequantize_channel(_ptr(lv), lv.size, scale, _ptr(out)))
+    return out
