@@ -28,6 +28,19 @@ __host__ __device__ __forceinline__ float level_guard(int lmax) {
     return 0.5f - static_cast<float>(lmax + 1) * 2.384185791015625e-07f;  // 2^-22
 }
 
+// Guard for the saturating-FFMA level of the K3 inner loop (LevelSat):
+// v = sat(x*A + B) with A = RN32(1/RN32(s*span)), B = RN32(-lmin/span),
+// w = v*span. Error budget against u = x/s (derivation in DESIGN.md §3):
+//   |w + lmin - u| <= (lmax+0.5)*2^-23 + (|lmin|+span+1)*2^-24  (+ O(2^-46)),
+// the reference's own u64 = RN(x*RN(1/s)) is within 2^-52|u| of u, and the
+// residual r is rounded once more (<= 2^-25). Budget doubled + 2^-20 slack.
+__host__ __device__ __forceinline__ float level_guard_sat(int lmin, int lmax) {
+    const float span = static_cast<float>(lmax - lmin);
+    const float b = (static_cast<float>(lmax) + 0.5f) * 1.1920928955078125e-07f +
+                    (static_cast<float>(-lmin) + span + 1.0f) * 5.9604644775390625e-08f;
+    return 0.5f - (2.0f * b + 9.5367431640625e-07f);
+}
+
 #ifdef __CUDACC__
 
 // ---- exact (reference-identical) level ------------------------------------
@@ -62,6 +75,20 @@ __device__ __forceinline__ float level_fast(float x, const FastLevel& fl, float&
     const float q = __fsub_rn(t, kMagic);
     rmax = fmaxf(rmax, fabsf(__fsub_rn(u, q)));
     return q;
+}
+
+// ---- level -> double without F2F ------------------------------------------
+// F2F.F64.F32 issues at ~16/clk/SM on B200 (measured), an eighth of the FP32
+// rate. For t = RN32(w + MAGIC) = MAGIC + q (|q| < 2^22) the bit pattern is
+// 0x4B400000 + q, so one IMAD.WIDE.U32 forms the double
+// 0x4338000080000000 + q = 1.5*2^52 + 2^31 + q and one DADD removes the bias:
+// exact for every level.
+__device__ __forceinline__ double level_bits_to_double(float t) {
+    unsigned long long w;
+    asm("mad.wide.u32 %0, %1, 1, %2;"
+        : "=l"(w)
+        : "r"(__float_as_uint(t)), "l"(0x4338000034C00000ull));
+    return __dsub_rn(__longlong_as_double(static_cast<long long>(w)), 6755401588539392.0);
 }
 
 // ---- scale handling ----------------------------------------------------------

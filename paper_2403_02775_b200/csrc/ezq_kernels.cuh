@@ -4,7 +4,7 @@
 //   K1  stats_pass1/2 + finalize   tensor mean/sigma, bit-exact chunk order
 //   K2  detect_count/scan/write    n-sigma mask -> flat-ordered COO
 //   K3  qrange                     per-column q_range Adam loop, strip in SMEM
-//   K3b seq_errors + col_finalize  reference-order per-column errors, scales
+//   K3b seq_errors                 reference-order per-column errors, scales
 //   K4  pack                       exact final levels -> nibbles/bytes
 //   K5  dequant + scatter          dense restore with outliers
 //   K6  gemv                       fused dequant + outlier GEMV (k_gemv.cu)
@@ -76,8 +76,8 @@ struct Scratch {
     long long* blk_count;
     long long* blk_offset;
     // per-column (global column index)
-    double* s0;       // initial scale (snapped for Easyquant, raw otherwise)
-    double* s_opt;    // scale chosen by K3 (Easyquant)
+    double* s_rtn;    // initial scale per column (snapped / float(s0))
+    double* s_fin;    // scale chosen by K3 per column
     double* err_rtn;  // reference-order error at s_rtn
     double* err_fin;  // reference-order error at s_fin
     double* inv;      // 1 / double(final float scale), for K4
@@ -87,6 +87,9 @@ struct CfgDev {
     int bits, lmin, lmax, mode;  // mode: EZQ_MODE_*
     int steps, select, fixed_at, pad;
     float sigma_n, guard;
+    float guard_sat;  // K3 saturating-FFMA level guard (level_guard_sat)
+    float sat_b;      // RN32(-lmin / span)
+    int pad2;
     AdamConsts adam;
     const double* bc1;  // [steps+1], index t
     const double* bc2;
@@ -112,11 +115,12 @@ struct K3Launch {
 };
 
 // ---- launchers (defined in the .cu files; all asynchronous on `st`) -------
+// `aligned`: every tensor base is 16-byte aligned (enables the cp.async path).
 void launch_stats_pass1(const TDesc* td, const int64_t* chunk_base, int ntens,
-                        int64_t total_chunks, Scratch sc, cudaStream_t st);
+                        int64_t total_chunks, Scratch sc, cudaStream_t st, bool aligned);
 void launch_stats_fin1(const TDesc* td, int ntens, Scratch sc, cudaStream_t st);
 void launch_stats_pass2(const TDesc* td, const int64_t* chunk_base, int ntens,
-                        int64_t total_chunks, Scratch sc, cudaStream_t st);
+                        int64_t total_chunks, Scratch sc, cudaStream_t st, bool aligned);
 void launch_stats_fin2(const TDesc* td, int ntens, Scratch sc, float sigma_n, int mask_mode,
                        cudaStream_t st);
 void launch_detect_count(const TDesc* td, const int64_t* dblk_base, int ntens,
@@ -126,12 +130,13 @@ void launch_detect_write(const TDesc* td, const int64_t* dblk_base, int ntens,
                          int64_t total_blocks, Scratch sc, cudaStream_t st);
 
 K3Launch plan_k3(int64_t rows, int64_t total_cols_hint, int num_sms, int max_smem);
+size_t k3_smem(const K3Launch& kl, int teams);
+size_t k3_small_smem(const K3Launch& kl, int teams);
+void set_k3_width(K3Launch& kl, int teams);
 void launch_k3(const K3Launch& kl, const TDesc* td, const K3Group* groups, int ngroups,
                Scratch sc, CfgDev cfg, float* gstrip, int grid, cudaStream_t st);
 void launch_seq_errors(const TDesc* td, const int2* tiles, int ntiles, Scratch sc, CfgDev cfg,
                        cudaStream_t st);
-void launch_col_finalize(const TDesc* td, const int2* tiles, int ntiles, Scratch sc,
-                         CfgDev cfg, cudaStream_t st);
 void launch_tensor_totals(const TDesc* td, int ntens, Scratch sc, cudaStream_t st);
 void launch_pack(const TDesc* td, const int64_t* pblk_base, int ntens, int64_t total_blocks,
                  Scratch sc, CfgDev cfg, cudaStream_t st);

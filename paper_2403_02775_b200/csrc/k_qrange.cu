@@ -18,8 +18,9 @@
 // bits, so every lane runs the scalar Adam update redundantly and no
 // broadcast is needed) and, for W > 1, a fixed-order sum of per-warp partials
 // behind one named barrier per step. Tree order differs from the reference's
-// ascending-row order only in the last bits of err/grad; K3b recomputes the
-// two reported errors per column in exact reference order.
+// ascending-row order only in the last bits of err/grad; the K3b epilogue
+// recomputes the two reported errors per column from the strip in exact
+// reference order (sequential fp64, separate roundings).
 //
 // Roofline: FP64/issue bound. Algorithmic work per element-step = 1 DMUL
 // (u) + 3 DFMA (d, d^2, d*q) = 7 flop.
@@ -105,7 +106,7 @@ __device__ __forceinline__ void elem_exact(float x, double inv, double dmin, dou
 }
 
 template <int L, int W, bool GLOBAL>
-__global__ void __launch_bounds__(512) k_qrange(const TDesc* __restrict__ td,
+__global__ void __launch_bounds__(512, 1) k_qrange(const TDesc* __restrict__ td,
                                                 const K3Group* __restrict__ groups,
                                                 int ngroups, Scratch sc, CfgDev cfg, int rpad,
                                                 int rstride, int teams, float* gstrip) {
@@ -153,14 +154,12 @@ __global__ void __launch_bounds__(512) k_qrange(const TDesc* __restrict__ td,
         }
         __syncthreads();
 
-        // Idle columns: whole warps (W == 1) or whole teams (W > 1) skip.
-        if (W == 1) {
-            if (warp * (32 / L) >= g.ncols) continue;
-        } else if (team >= g.ncols) {
-            continue;
-        }
+        // Idle columns: whole warps (W == 1) or whole teams (W > 1) skip the
+        // optimisation but still meet the CTA barriers below.
+        const bool active = (W == 1) ? (warp * (32 / L) < g.ncols) : (team < g.ncols);
         const float4* col4 =
             reinterpret_cast<const float4*>(strip + static_cast<size_t>(team) * rstride);
+        if (active) {
         int parity = 0;
 
         // initial_scale over the normals (rtn.cpp:81-86): max is order-free.
@@ -171,39 +170,82 @@ __global__ void __launch_bounds__(512) k_qrange(const TDesc* __restrict__ td,
         }
         mx = team_max<L, W>(mx, red, team, wi, lane, teams, parity);
         const double s0_raw = initial_scale_from_max(static_cast<double>(mx), cfg.lmax);
-        const int64_t gc = d.col_base + g.col0 + team;
         const bool writer = (pt == 0) && (team < g.ncols);
 
-        if (!optimize) {
-            if (writer) sc.s0[gc] = s0_raw;
-            continue;
-        }
-
+        // Rtn / OutliersOnly: float(initial_scale), no optimisation
+        // (pipeline.cpp:52-55).
+        double s_rtn = static_cast<double>(__double2float_rn(s0_raw));
+        double s_fin = s_rtn;
+        if (optimize) {
         // ---- Adam loop (optimize.cpp:138-167) ----
         double s = snap(s0_raw);
         const double s0 = s;
         double m = 0.0, v = 0.0;
         double e0 = 0.0, best_err = 0.0, best_s = s, fixed_s = s, fixed_err = 0.0;
-        const float guard = cfg.guard;
+        const float spanf = static_cast<float>(cfg.lmax - cfg.lmin);
+        const float magic_l = kMagic + static_cast<float>(cfg.lmin);  // exact
+        const float gsat = cfg.guard_sat;
         for (int t = 0;; ++t) {
-            const double inv = __ddiv_rn(1.0, s);
-            const FastLevel fl{__double2float_rn(inv), static_cast<float>(cfg.lmin),
-                               static_cast<float>(cfg.lmax)};
+            // Level per element (certified fp32, exact fp64 fix inside the
+            // guard band): v = sat(x*A + B) maps [lmin, lmax] onto [0, 1];
+            // t = RN(v*span + MAGIC + lmin) = MAGIC + q; r = w + lmin - q.
+            const float A = __frcp_rn(__fmul_rn(__double2float_rn(s), spanf));
             double ea = 0.0, eb = 0.0, ga = 0.0, gb = 0.0;
-            float rmax = 0.f;
-#pragma unroll 4
-            for (int k = 0; k < K; ++k) {
-                const float4 x = col4[pt + k * P];
-                elem_fast(x.x, fl, s, rmax, ea, ga);
-                elem_fast(x.y, fl, s, rmax, eb, gb);
-                elem_fast(x.z, fl, s, rmax, ea, ga);
-                elem_fast(x.w, fl, s, rmax, eb, gb);
+            double ec = 0.0, ed = 0.0, gc2 = 0.0, gd = 0.0;
+            int k = 0;
+            for (; k + 4 <= K; k += 4) {
+                float xv[16];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float4 x = col4[pt + (k + j) * P];
+                    xv[4 * j] = x.x;
+                    xv[4 * j + 1] = x.y;
+                    xv[4 * j + 2] = x.z;
+                    xv[4 * j + 3] = x.w;
+                }
+                float rmax = 0.f;
+                float tv[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const float v = __saturatef(__fmaf_rn(xv[j], A, cfg.sat_b));
+                    tv[j] = __fmaf_rn(v, spanf, magic_l);  // MAGIC + q
+                    const float r = __fmaf_rn(v, spanf, __fsub_rn(magic_l, tv[j]));
+                    rmax = fmaxf(rmax, fabsf(r));
+                }
+                double xd[16], qd[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) qd[j] = level_bits_to_double(tv[j]);
+                if (rmax >= gsat) {
+                    // An element sits within the fp32 error band of a rounding
+                    // boundary: take the reference's fp64 levels for this group.
+                    const double inv = __ddiv_rn(1.0, s);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        qd[j] = level_exact(static_cast<double>(xv[j]), inv, dmin, dmax);
+                }
+#pragma unroll
+                for (int j = 0; j < 16; ++j) xd[j] = static_cast<double>(xv[j]);
+                // Four accumulator pairs keep the DFMA chains short (8.4-cycle
+                // latency); lanes sum them in a fixed order below.
+#pragma unroll
+                for (int j = 0; j < 16; j += 4) {
+                    const double d0 = fma(s, qd[j], -xd[j]);
+                    const double d1 = fma(s, qd[j + 1], -xd[j + 1]);
+                    const double d2 = fma(s, qd[j + 2], -xd[j + 2]);
+                    const double d3 = fma(s, qd[j + 3], -xd[j + 3]);
+                    ea = fma(d0, d0, ea);
+                    ga = fma(d0, qd[j], ga);
+                    eb = fma(d1, d1, eb);
+                    gb = fma(d1, qd[j + 1], gb);
+                    ec = fma(d2, d2, ec);
+                    gc2 = fma(d2, qd[j + 2], gc2);
+                    ed = fma(d3, d3, ed);
+                    gd = fma(d3, qd[j + 3], gd);
+                }
             }
-            if (rmax >= guard) {
-                // Some element sits within the fp32 error band of a rounding
-                // boundary: redo this thread's slice with exact fp64 levels.
-                ea = eb = ga = gb = 0.0;
-                for (int k = 0; k < K; ++k) {
+            if (k < K) {
+                const double inv = __ddiv_rn(1.0, s);
+                for (; k < K; ++k) {
                     const float4 x = col4[pt + k * P];
                     elem_exact(x.x, inv, dmin, dmax, s, ea, ga);
                     elem_exact(x.y, inv, dmin, dmax, s, eb, gb);
@@ -211,7 +253,7 @@ __global__ void __launch_bounds__(512) k_qrange(const TDesc* __restrict__ td,
                     elem_exact(x.w, inv, dmin, dmax, s, eb, gb);
                 }
             }
-            double err = ea + eb, gr = ga + gb;
+            double err = (ea + ec) + (eb + ed), gr = (ga + gc2) + (gb + gd);
             team_sum2<L, W>(err, gr, red, team, wi, lane, teams, parity);
             const double grad = 2.0 * gr;
             if (t == 0) {
@@ -231,119 +273,221 @@ __global__ void __launch_bounds__(512) k_qrange(const TDesc* __restrict__ td,
             if (t == cfg.steps) break;
             s = snap(adam_update(m, v, s, grad, cfg.bc1[t + 1], cfg.bc2[t + 1], cfg.adam));
         }
+        if (cfg.select == EZQ_SELECT_FIXED)
+            s_fin = (fixed_err <= e0) ? fixed_s : s0;  // optimize.cpp:169-178
+        else
+            s_fin = best_s;
+        s_rtn = s0;
+        }  // optimize
         if (writer) {
-            sc.s0[gc] = s0;
-            double chosen;
-            if (cfg.select == EZQ_SELECT_FIXED)
-                chosen = (fixed_err <= e0) ? fixed_s : s0;  // optimize.cpp:169-178
-            else
-                chosen = best_s;
-            sc.s_opt[gc] = chosen;
+            const int64_t gcol = d.col_base + g.col0 + team;
+            sc.s_rtn[gcol] = s_rtn;
+            sc.s_fin[gcol] = s_fin;
+        }
+        }  // active
+    }
+}
+
+// ---- K3b: reference-order errors (rtn_error / final_error per column) ----
+// One CTA = 32 adjacent columns of one tensor, lane = column; warp 0 sums
+// at the initial scale, warp 1 at the chosen scale. The CTA streams 64-row x 32-column tiles (row segments of 128 contiguous bytes)
+// through an 8-stage cp.async ring; each lane then walks its column in
+// ascending row order with the reference's separate roundings (eval_dense,
+// optimize.cpp:36-49), skipping isolated outliers exactly like
+// normal_mask_apply. Two chains per lane: initial scale and chosen scale.
+// The per-column finalisation (stored float scale, per-column invariant,
+// 1/scale for K4) follows in the same thread.
+constexpr int kBTile = 64;
+constexpr int kBStages = 8;
+constexpr size_t kBSmem = sizeof(float) * kBStages * kBTile * 32;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
+                 "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_bytes) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem),
+                 "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Tile `t` (rows [64t, 64t+64)) of columns [c0, c0+32) into buf[64][32];
+// the CTA's 64 threads split the 512 16-byte pieces (8 each).
+__device__ __forceinline__ void k3b_issue(float* buf, const float* W, int64_t R, int64_t C,
+                                          int64_t c0, int t, int tid, bool vec) {
+    const int ncol = static_cast<int>(min(static_cast<int64_t>(32), C - c0));
+    if (vec) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int idx = i * 64 + tid;
+            const int r = idx >> 3, part = idx & 7;
+            const int64_t row = static_cast<int64_t>(t) * kBTile + r;
+            int bytes = (ncol - part * 4) * 4;
+            bytes = bytes < 0 ? 0 : (bytes > 16 ? 16 : bytes);
+            if (row >= R) bytes = 0;
+            if (bytes > 0) cp_async16(buf + r * 32 + part * 4, W + row * C + c0 + part * 4, bytes);
+        }
+    } else {
+        const int lane = tid & 31, half = tid >> 5;
+#pragma unroll 4
+        for (int r = half; r < kBTile; r += 2) {
+            const int64_t row = static_cast<int64_t>(t) * kBTile + r;
+            if (row < R && lane < ncol) cp_async4(buf + r * 32 + lane, W + row * C + c0 + lane, 4);
         }
     }
 }
 
-// ---- K3b: reference-order errors -------------------------------------------
-// Block = 64 threads = one tile of 32 adjacent columns x {rtn, final}; each
-// thread walks its column in ascending row order (coalesced 128-byte rows per
-// warp) with the reference's separate-rounding accumulation.
+// Squared residual of one normal element at scale s in reference semantics
+// (eval_dense, optimize.cpp:37-47): the level equals level_of's; d = s*q - x
+// is exact (s*q is), so d*d carries the reference's single rounding.
+__device__ __forceinline__ double seq_sq(float x, double xd, double s, float invf, double inv,
+                                         float fmin, float fmax, double dmin, double dmax,
+                                         float guard) {
+    float u = __fmul_rn(x, invf);
+    u = fminf(fmaxf(u, fmin), fmax);
+    const float t = __fadd_rn(u, kMagic);
+    const float r = __fsub_rn(u, __fsub_rn(t, kMagic));
+    double q = level_bits_to_double(t);
+    if (fabsf(r) >= guard) q = level_exact(xd, inv, dmin, dmax);
+    const double d = fma(s, q, -xd);
+    return __dmul_rn(d, d);
+}
+
 __global__ void __launch_bounds__(64) k_seq_errors(const TDesc* __restrict__ td,
-                                                   const int2* __restrict__ tiles, Scratch sc,
-                                                   CfgDev cfg) {
+                                                   const int2* __restrict__ tiles, int ntiles,
+                                                   Scratch sc, CfgDev cfg) {
+    extern __shared__ __align__(16) float bsm[];
+    const int tid = threadIdx.x, lane = tid & 31, which = tid >> 5;  // 0: rtn, 1: final
     const int2 tile = tiles[blockIdx.x];
     const TDesc& d = td[tile.x];
-    const int lane = threadIdx.x & 31, which = threadIdx.x >> 5;
-    const int64_t c = tile.y + lane;
-    if (c >= d.cols) return;
-    const int64_t gc = d.col_base + c;
-    const bool eq = cfg.mode == EZQ_MODE_EASYQUANT;
-    double s;
-    if (which == 0) {
-        // Easyquant: error at the snapped initial scale (optimize.cpp:138-141);
-        // Rtn / OutliersOnly: at float(initial_scale) (pipeline.cpp:52-55).
-        s = eq ? sc.s0[gc] : static_cast<double>(__double2float_rn(sc.s0[gc]));
-    } else {
-        if (!eq || sc.s_opt[gc] == sc.s0[gc]) {
-            sc.err_fin[gc] = __longlong_as_double(0x7ff8000000000000ll);  // "same as rtn"
-            return;
-        }
-        s = sc.s_opt[gc];
-    }
-    if (!(s > 0.0) || !isfinite(s)) {  // check_scale (rtn.cpp:19-22)
-        d.st->scale_zero = 1;
-        s = 1.0;
-    }
+    const int64_t c0 = tile.y, R = d.rows, C = d.cols;
+    const int64_t c = c0 + lane;
+    const bool live = c < C;
+    const int64_t gc = d.col_base + (live ? c : c0);
+    const bool vec = ((reinterpret_cast<uintptr_t>(d.W) & 15) == 0) && (C % 4 == 0);
     const TStats* st = d.st;
     const double mean = st->mean, thr = st->thr;
     const int mask = st->mask;
+    const double s_r = sc.s_rtn[gc], s_f = sc.s_fin[gc];
+    const bool skip = which == 1 && s_f == s_r;  // chosen == initial: reuse rtn
+    const double s = which ? s_f : s_r;
     const double inv = __ddiv_rn(1.0, s);
-    const FastLevel fl{__double2float_rn(inv), static_cast<float>(cfg.lmin),
-                       static_cast<float>(cfg.lmax)};
+    const float invf = __double2float_rn(inv);
+    const float fmin = static_cast<float>(cfg.lmin), fmax = static_cast<float>(cfg.lmax);
     const double dmin = cfg.lmin, dmax = cfg.lmax;
     const float guard = cfg.guard;
+    const int ntl = static_cast<int>((R + kBTile - 1) / kBTile);
     double err = 0.0;
-    const float* p = d.W + c;
-    const int64_t R = d.rows, C = d.cols;
-#pragma unroll 8
-    for (int64_t r = 0; r < R; ++r) {
-        const float x = p[r * C];
-        if (mask && is_outlier(x, mean, thr)) continue;
-        float rm = 0.f;
-        double q = static_cast<double>(level_fast(x, fl, rm));
-        if (rm >= guard) q = level_exact(static_cast<double>(x), inv, dmin, dmax);
-        const double dd = __dsub_rn(__dmul_rn(s, q), static_cast<double>(x));
-        err = __dadd_rn(err, __dmul_rn(dd, dd));
+#pragma unroll
+    for (int p = 0; p < kBStages - 1; ++p) {
+        if (p < ntl) k3b_issue(bsm + p * kBTile * 32, d.W, R, C, c0, p, tid, vec);
+        cp_async_commit();
     }
-    if (which == 0)
-        sc.err_rtn[gc] = err;
-    else
-        sc.err_fin[gc] = err;
-}
-
-// Per column: pick the stored scale, keep final <= rtn per column, and
-// publish float scales + 1/scale for the packer.
-__global__ void __launch_bounds__(32) k_col_finalize(const TDesc* __restrict__ td,
-                                                     const int2* __restrict__ tiles, Scratch sc,
-                                                     CfgDev cfg) {
-    const int2 tile = tiles[blockIdx.x];
-    const TDesc& d = td[tile.x];
-    const int64_t c = tile.y + threadIdx.x;
-    if (c >= d.cols) return;
-    const int64_t gc = d.col_base + c;
-    const double rtn = sc.err_rtn[gc];
-    double fin = rtn;
-    float scale;
-    if (cfg.mode == EZQ_MODE_EASYQUANT) {
-        double s = sc.s_opt[gc];
-        const double f = sc.err_fin[gc];
-        if (!isnan(f)) {
-            if (f > rtn) {
-                s = sc.s0[gc];  // tree/sequential near-tie: keep the initial scale
-            } else {
-                fin = f;
+    for (int t = 0; t < ntl; ++t) {
+        const int nt = t + kBStages - 1;
+        if (nt < ntl) k3b_issue(bsm + (nt % kBStages) * kBTile * 32, d.W, R, C, c0, nt, tid, vec);
+        cp_async_commit();
+        cp_async_wait<kBStages - 1>();
+        __syncthreads();
+        const float* buf = bsm + (t % kBStages) * kBTile * 32;
+        const int nr =
+            static_cast<int>(min(static_cast<int64_t>(kBTile), R - static_cast<int64_t>(t) * kBTile));
+        if (live && !skip) {
+            int r = 0;
+            for (; r + 16 <= nr; r += 16) {
+                double term[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const float x = buf[(r + j) * 32 + lane];
+                    const double xd = static_cast<double>(x);
+                    const double sq = seq_sq(x, xd, s, invf, inv, fmin, fmax, dmin, dmax, guard);
+                    // normal_mask_apply: an isolated outlier adds exactly +0
+                    term[j] = (mask && fabs(__dsub_rn(xd, mean)) >= thr) ? 0.0 : sq;
+                }
+#pragma unroll
+                for (int j = 0; j < 16; ++j) err = __dadd_rn(err, term[j]);
+            }
+            for (; r < nr; ++r) {
+                const float x = buf[r * 32 + lane];
+                const double xd = static_cast<double>(x);
+                const double sq = seq_sq(x, xd, s, invf, inv, fmin, fmax, dmin, dmax, guard);
+                err = __dadd_rn(err, (mask && fabs(__dsub_rn(xd, mean)) >= thr) ? 0.0 : sq);
             }
         }
-        scale = __double2float_rn(s);
-    } else {
-        scale = __double2float_rn(sc.s0[gc]);
+        __syncthreads();
     }
-    sc.err_fin[gc] = fin;
+    cp_async_wait<0>();
+    __shared__ double fin_err[32];
+    if (which == 1) fin_err[lane] = err;
+    __syncthreads();
+    if (which == 1 || !live) return;
+    const double er = err;
+    double ef = fin_err[lane];
+    double s_store = s_f;
+    if (s_f == s_r) {
+        ef = er;
+    } else if (ef > er) {
+        // tree/sequential near-tie: keep the initial scale so the per-column
+        // invariant final <= rtn holds (pipeline.cpp:107)
+        s_store = s_r;
+        ef = er;
+    }
+    const float scale = __double2float_rn(s_store);
+    if (!(scale > 0.f)) d.st->scale_zero = 1;  // check_scale (rtn.cpp:19-22)
     d.scales[c] = scale;
     sc.inv[gc] = scale > 0.f ? __ddiv_rn(1.0, static_cast<double>(scale)) : 1.0;
+    sc.err_rtn[gc] = er;
+    sc.err_fin[gc] = ef;
 }
 
-// Column-ordered tensor totals (pipeline.cpp:96-103).
-__global__ void k_tensor_totals(const TDesc* __restrict__ td, int ntens, Scratch sc) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= ntens) return;
-    const TDesc& d = td[t];
+// Column-ordered tensor totals (pipeline.cpp:96-103): one CTA per tensor
+// stages the per-column errors through SMEM (coalesced) and one thread adds
+// them in column order.
+__global__ void __launch_bounds__(256) k_tensor_totals(const TDesc* __restrict__ td, Scratch sc) {
+    const TDesc& d = td[blockIdx.x];
+    __shared__ double buf[2][2048];
     double rtn = 0.0, fin = 0.0;
-    for (int64_t c = 0; c < d.cols; ++c) {
-        rtn = __dadd_rn(rtn, sc.err_rtn[d.col_base + c]);
-        fin = __dadd_rn(fin, sc.err_fin[d.col_base + c]);
+    for (int64_t base = 0; base < d.cols; base += 2048) {
+        const int cnt = static_cast<int>(min(static_cast<int64_t>(2048), d.cols - base));
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+            buf[0][i] = sc.err_rtn[d.col_base + base + i];
+            buf[1][i] = sc.err_fin[d.col_base + base + i];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int i = 0;
+            for (; i + 8 <= cnt; i += 8) {
+                double a[8], b[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    a[j] = buf[0][i + j];
+                    b[j] = buf[1][i + j];
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    rtn = __dadd_rn(rtn, a[j]);
+                    fin = __dadd_rn(fin, b[j]);
+                }
+            }
+            for (; i < cnt; ++i) {
+                rtn = __dadd_rn(rtn, buf[0][i]);
+                fin = __dadd_rn(fin, buf[1][i]);
+            }
+        }
+        __syncthreads();
     }
-    d.st->rtn_error = rtn;
-    d.st->final_error = fin;
+    if (threadIdx.x == 0) {
+        d.st->rtn_error = rtn;
+        d.st->final_error = fin;
+    }
 }
 
 template <int L, int W>
@@ -364,7 +508,8 @@ void launch_k3_lw(const K3Launch& kl, const TDesc* td, const K3Group* groups, in
 
 }  // namespace
 
-// Geometry: ~128 elements per thread per step, 12-16 warps per CTA.
+// Geometry: ~128 elements per thread per step; columns per CTA (CB) chosen
+// by the caller (choose_k3_width) for load balance across the SMs.
 K3Launch plan_k3(int64_t rows, int64_t /*total_cols_hint*/, int /*num_sms*/, int max_smem) {
     K3Launch kl{};
     kl.rows = rows;
@@ -386,21 +531,26 @@ K3Launch plan_k3(int64_t rows, int64_t /*total_cols_hint*/, int /*num_sms*/, int
     const int P = kl.L * kl.W;
     kl.rpad = static_cast<int>(((rows + 4 * P - 1) / (4 * P)) * (4 * P));
     kl.rstride = kl.rpad + 4;
-    const int max_warps = 16;
-    const int team_unit = (kl.W == 1) ? 32 / kl.L : 1;  // teams per warp-granule
-    int teams = (kl.W == 1) ? max_warps * (32 / kl.L) : max_warps / kl.W;
-    auto smem_for = [&](int t) {
-        return static_cast<size_t>(t) * kl.rstride * sizeof(float) +
-               static_cast<size_t>(2) * t * kl.W * 2 * sizeof(double);
-    };
-    while (teams > team_unit && smem_for(teams) > static_cast<size_t>(max_smem)) teams -= team_unit;
-    kl.global_strip = smem_for(teams) > static_cast<size_t>(max_smem);
-    if (kl.global_strip) teams = (kl.W == 1) ? team_unit : 1;
+    const int unit = (kl.W == 1) ? 32 / kl.L : 1;  // columns per warp-granule
+    kl.teams = unit;
+    kl.global_strip = k3_smem(kl, unit) > static_cast<size_t>(max_smem);
+    set_k3_width(kl, unit);
+    return kl;
+}
+
+size_t k3_smem(const K3Launch& kl, int teams) {
+    return static_cast<size_t>(teams) * kl.rstride * sizeof(float) + k3_small_smem(kl, teams);
+}
+
+// Reduction slots [2][teams][W][2].
+size_t k3_small_smem(const K3Launch& kl, int teams) {
+    return static_cast<size_t>(2) * teams * kl.W * 2 * sizeof(double);
+}
+
+void set_k3_width(K3Launch& kl, int teams) {
     kl.teams = teams;
     kl.threads = (kl.W == 1) ? ((teams * kl.L + 31) / 32) * 32 : teams * kl.W * 32;
-    kl.smem = kl.global_strip ? static_cast<size_t>(2) * teams * kl.W * 2 * sizeof(double)
-                              : smem_for(teams);
-    return kl;
+    kl.smem = kl.global_strip ? k3_small_smem(kl, teams) : k3_smem(kl, teams);
 }
 
 void launch_k3(const K3Launch& kl, const TDesc* td, const K3Group* groups, int ngroups,
@@ -421,19 +571,17 @@ void launch_k3(const K3Launch& kl, const TDesc* td, const K3Group* groups, int n
 void launch_seq_errors(const TDesc* td, const int2* tiles, int ntiles, Scratch sc, CfgDev cfg,
                        cudaStream_t st) {
     if (ntiles == 0) return;
-    k_seq_errors<<<ntiles, 64, 0, st>>>(td, tiles, sc, cfg);
-    count_launch();
-}
-
-void launch_col_finalize(const TDesc* td, const int2* tiles, int ntiles, Scratch sc,
-                         CfgDev cfg, cudaStream_t st) {
-    if (ntiles == 0) return;
-    k_col_finalize<<<ntiles, 32, 0, st>>>(td, tiles, sc, cfg);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_seq_errors, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBSmem);
+        attr = true;
+    }
+    k_seq_errors<<<ntiles, 64, kBSmem, st>>>(td, tiles, ntiles, sc, cfg);
     count_launch();
 }
 
 void launch_tensor_totals(const TDesc* td, int ntens, Scratch sc, cudaStream_t st) {
-    k_tensor_totals<<<(ntens + 63) / 64, 64, 0, st>>>(td, ntens, sc);
+    k_tensor_totals<<<ntens, 256, 0, st>>>(td, sc);
     count_launch();
 }
 

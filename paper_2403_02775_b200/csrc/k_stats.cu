@@ -48,6 +48,276 @@ __device__ __forceinline__ void p1_elem(P1& a, float v, unsigned long long flat)
     if (!isfinite(v) && a.bad == ~0ull) a.bad = flat;
 }
 
+// ---- cp.async-pipelined chunk passes --------------------------------------
+// One warp owns 32 consecutive global chunks (lane c <-> chunk c, so each
+// lane runs exactly the reference's sequential chain for its chunk). The warp
+// streams the chunks through SMEM in 64-element tiles with cp.async (8-stage
+// ring, seven tiles = 56 KB in flight per warp: enough to cover HBM latency
+// at the ~29 GB/s one warp's 32 DADD chains consume): each cp.async instruction moves two
+// contiguous 256-byte chunk segments, so HBM sees fully coalesced traffic
+// while every lane reads its own tile with conflict-free LDS.128 (68-float
+// row pitch). Requires 16-byte aligned tensors (else the simple kernels run).
+constexpr int kTile = 64;
+constexpr int kPitch = kTile + 4;
+constexpr int kStages = 8;       // 7 tiles (56 KB) in flight per warp
+constexpr int kWarpsPerCta = 1;
+constexpr int kTilesPerChunk = static_cast<int>(kStatsChunk / kTile);
+constexpr size_t kStatsSmem = sizeof(float) * kStages * 32 * kPitch * kWarpsPerCta;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
+                 "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Each lane copies its OWN chunk's tile (16 x 16-byte cp.async, 256 B
+// contiguous): no address shuffles; every 32-byte sector is fully used.
+__device__ __forceinline__ void issue_tile(float* row, const float* my_ptr, int my_cnt, int t) {
+    if (my_ptr == nullptr) return;
+    const int e0 = t * kTile;
+#pragma unroll
+    for (int part = 0; part < kTile / 4; ++part) {
+        const int e = e0 + part * 4;
+        int bytes = (my_cnt - e) * 4;
+        bytes = bytes < 0 ? 0 : (bytes > 16 ? 16 : bytes);
+        if (bytes > 0) cp_async16(row + part * 4, my_ptr + e, bytes);
+    }
+}
+
+// Pass 1: the reference-order fp64 sum chain (stats.cpp:31-37) plus the
+// order-free parts of sum_chunk: max|x| (fmax of non-negative values is
+// exact in any order), min / max (FMNMX; equal to the reference's ternaries
+// for the mn == mx test given merge rules in k_stats_merge) and a
+// non-finite probe (an fp32 running sum turns non-finite on any inf/NaN; a
+// probe overflow only triggers the exact re-scan of that tile).
+// Pass 2: the deviation chain (stats.cpp:43-46), separate roundings.
+template <bool PASS2>
+__global__ void __launch_bounds__(32 * kWarpsPerCta) k_stats_pipe(const TDesc* __restrict__ td,
+                                                                  const int64_t* __restrict__ chunk_base,
+                                                                  int ntens, int64_t total,
+                                                                  Scratch sc) {
+    extern __shared__ __align__(16) float sbuf[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float* ring = sbuf + warp * kStages * 32 * kPitch;
+    const int64_t g = (static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + warp) * 32 + lane;
+    const float* ptr = nullptr;
+    int cnt = 0;
+    int t = 0;
+    double mean = 0.0;
+    unsigned long long flat0 = 0;
+    if (g < total) {
+        t = find_tensor(chunk_base, ntens, g);
+        const TDesc& d = td[t];
+        const int64_t lo = (g - d.chunk_base) * kStatsChunk;
+        cnt = static_cast<int>(min(kStatsChunk, d.n - lo));
+        ptr = d.W + lo;
+        flat0 = lo;
+        if (PASS2) {
+            mean = d.st->mean;
+            if (d.st->constant) ptr = nullptr;  // stats.cpp:77-83 skips pass 2
+        }
+    }
+    if (__all_sync(0xffffffffu, ptr == nullptr)) return;
+    const int ntiles = ptr ? (cnt + kTile - 1) / kTile : 0;
+    const int max_tiles = __reduce_max_sync(0xffffffffu, ntiles);
+    float* myrow0 = ring + lane * kPitch;
+
+    double acc = 0.0;
+    float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000), amax = 0.f;
+    unsigned long long bad = ~0ull;
+
+#pragma unroll
+    for (int p = 0; p < kStages - 1; ++p) {
+        if (p < ntiles) issue_tile(myrow0 + p * 32 * kPitch, ptr, cnt, p);
+        cp_async_commit();
+    }
+    for (int tile = 0; tile < max_tiles; ++tile) {
+        const int nt = tile + kStages - 1;
+        if (nt < ntiles) issue_tile(myrow0 + (nt % kStages) * 32 * kPitch, ptr, cnt, nt);
+        cp_async_commit();
+        cp_async_wait<kStages - 1>();
+        const float* r1 = myrow0 + (tile % kStages) * 32 * kPitch;
+        const int e0 = tile * kTile;
+        if (tile < ntiles) {
+            const int n = min(kTile, cnt - e0);
+            if (n == kTile) {
+                const float4* row = reinterpret_cast<const float4*>(r1);
+                if (PASS2) {
+                    double sq[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const double dv = __dsub_rn(static_cast<double>(r1[j]), mean);
+                        sq[j] = __dmul_rn(dv, dv);
+                    }
+#pragma unroll
+                    for (int grp = 0; grp < kTile / 16; ++grp) {
+                        double nx[16];
+                        if (grp + 1 < kTile / 16) {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                const double dv =
+                                    __dsub_rn(static_cast<double>(r1[16 * (grp + 1) + j]), mean);
+                                nx[j] = __dmul_rn(dv, dv);
+                            }
+                        }
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) acc = __dadd_rn(acc, sq[j]);
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) sq[j] = nx[j];
+                    }
+                } else {
+                    float probe = 0.f;
+                    double xd[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) xd[j] = static_cast<double>(r1[j]);
+#pragma unroll
+                    for (int grp = 0; grp < kTile / 16; ++grp) {
+                        double nx[16];
+                        if (grp + 1 < kTile / 16) {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                nx[j] = static_cast<double>(r1[16 * (grp + 1) + j]);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) acc = __dadd_rn(acc, xd[j]);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const float4 v = row[4 * grp + q];
+                            mn = fminf(fminf(mn, v.x), fminf(fminf(v.y, v.z), v.w));
+                            mx = fmaxf(fmaxf(mx, v.x), fmaxf(fmaxf(v.y, v.z), v.w));
+                            amax = fmaxf(fmaxf(amax, fabsf(v.x)),
+                                         fmaxf(fmaxf(fabsf(v.y), fabsf(v.z)), fabsf(v.w)));
+                            probe = __fadd_rn(probe, __fadd_rn(__fadd_rn(v.x, v.y),
+                                                               __fadd_rn(v.z, v.w)));
+                        }
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) xd[j] = nx[j];
+                    }
+                    if (!isfinite(probe) && bad == ~0ull) {
+                        for (int k = 0; k < kTile; ++k)
+                            if (!isfinite(r1[k])) {
+                                bad = flat0 + e0 + k;
+                                break;
+                            }
+                    }
+                }
+            } else {
+                for (int k = 0; k < n; ++k) {
+                    const float v = r1[k];
+                    if (PASS2) {
+                        const double dv = __dsub_rn(static_cast<double>(v), mean);
+                        acc = __dadd_rn(acc, __dmul_rn(dv, dv));
+                    } else {
+                        acc = __dadd_rn(acc, static_cast<double>(v));
+                        mn = fminf(mn, v);
+                        mx = fmaxf(mx, v);
+                        amax = fmaxf(amax, fabsf(v));
+                        if (!isfinite(v) && bad == ~0ull) bad = flat0 + e0 + k;
+                    }
+                }
+            }
+        }
+    }
+    cp_async_wait<0>();
+    if (ptr == nullptr) return;
+    if (PASS2) {
+        sc.p_dev[g] = acc;
+    } else {
+        sc.p_sum[g] = acc;
+        sc.p_max[g] = static_cast<double>(amax);
+        sc.p_mn[g] = mn;
+        sc.p_mx[g] = mx;
+        if (bad != ~0ull) atomicMin(&td[t].st->bad_index, bad);
+    }
+}
+
+// One CTA per tensor. Order-free merges (max|x|, min, max) run as block
+// reductions; the two sums are merged in chunk order by thread 0 from
+// registers-prefetched SMEM (stats.cpp:66-76 / 96-98). Constant-tensor rule
+// (stats.cpp:77-83): the reference keeps the first of equal values, so for a
+// constant tensor mn == W[0]; a NaN at W[0] pins its mn/mx to NaN (never
+// constant), NaNs elsewhere are skipped exactly like FMNMX skips them.
+template <bool PASS2>
+__global__ void __launch_bounds__(256) k_stats_merge(const TDesc* __restrict__ td, Scratch sc,
+                                                     float sigma_n, int mask_mode) {
+    const TDesc& d = td[blockIdx.x];
+    TStats* st = d.st;
+    __shared__ double bs[2048];
+    if (PASS2 && st->constant) {
+        if (threadIdx.x == 0) {
+            st->mask = 0;
+            st->thr = __longlong_as_double(0x7ff0000000000000ll);
+            st->n_out = 0;
+        }
+        return;
+    }
+    double sum = 0.0;
+    float amax = 0.f, mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
+    for (int64_t base = 0; base < d.n_chunks; base += 2048) {
+        const int cnt = static_cast<int>(min(static_cast<int64_t>(2048), d.n_chunks - base));
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const int64_t c = d.chunk_base + base + i;
+            bs[i] = PASS2 ? sc.p_dev[c] : sc.p_sum[c];
+            if (!PASS2) {
+                amax = fmaxf(amax, static_cast<float>(sc.p_max[c]));
+                mn = fminf(mn, sc.p_mn[c]);
+                mx = fmaxf(mx, sc.p_mx[c]);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int i = 0;
+            for (; i + 8 <= cnt; i += 8) {
+                double v[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[j] = bs[i + j];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) sum = __dadd_rn(sum, v[j]);
+            }
+            for (; i < cnt; ++i) sum = __dadd_rn(sum, bs[i]);
+        }
+        __syncthreads();
+    }
+    if (!PASS2) {
+        typedef cub::BlockReduce<float, 256> BR;
+        __shared__ typename BR::TempStorage tmp;
+        amax = BR(tmp).Reduce(amax, cub::Max());
+        __syncthreads();
+        mn = BR(tmp).Reduce(mn, cub::Min());
+        __syncthreads();
+        mx = BR(tmp).Reduce(mx, cub::Max());
+    }
+    if (threadIdx.x != 0) return;
+    if (PASS2) {
+        st->ss = sum;
+        st->stddev = __dsqrt_rn(__ddiv_rn(sum, static_cast<double>(d.n)));
+        st->mask = (mask_mode && st->stddev != 0.0) ? 1 : 0;
+        st->thr = st->mask ? __dmul_rn(static_cast<double>(sigma_n), st->stddev)
+                           : __longlong_as_double(0x7ff0000000000000ll);
+        st->n_out = 0;
+    } else {
+        st->sum = sum;
+        st->max_abs = static_cast<double>(amax);
+        st->mn = mn;
+        st->mx = mx;
+        const float w0 = d.W[0];
+        if (mn == mx && !isnan(w0)) {
+            st->constant = 1;
+            st->mean = static_cast<double>(w0);
+            st->stddev = 0.0;
+        } else {
+            st->constant = 0;
+            st->mean = __ddiv_rn(sum, static_cast<double>(d.n));
+        }
+    }
+}
+
 __global__ void __launch_bounds__(128) k_stats_pass1(const TDesc* __restrict__ td,
                                                      const int64_t* __restrict__ chunk_base,
                                                      int ntens, int64_t total, Scratch sc) {
@@ -90,37 +360,6 @@ __global__ void __launch_bounds__(128) k_stats_pass1(const TDesc* __restrict__ t
     if (a.bad != ~0ull) atomicMin(&d.st->bad_index, a.bad);
 }
 
-// One thread per tensor: chunk-ordered merge (stats.cpp:66-90).
-__global__ void k_stats_fin1(const TDesc* __restrict__ td, int ntens, Scratch sc) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= ntens) return;
-    const TDesc& d = td[t];
-    TStats* st = d.st;
-    const int64_t b = d.chunk_base;
-    double sum = 0.0, mx_abs = 0.0;
-    float mn = sc.p_mn[b], mx = sc.p_mx[b];
-    for (int64_t c = 0; c < d.n_chunks; ++c) {
-        sum = __dadd_rn(sum, sc.p_sum[b + c]);
-        const double m = sc.p_max[b + c];
-        mx_abs = (mx_abs < m) ? m : mx_abs;
-        const float a = sc.p_mn[b + c], z = sc.p_mx[b + c];
-        mn = (a < mn) ? a : mn;
-        mx = (mx < z) ? z : mx;
-    }
-    st->sum = sum;
-    st->max_abs = mx_abs;
-    st->mn = mn;
-    st->mx = mx;
-    if (mn == mx) {
-        st->constant = 1;
-        st->mean = static_cast<double>(mn);
-        st->stddev = 0.0;
-    } else {
-        st->constant = 0;
-        st->mean = __ddiv_rn(sum, static_cast<double>(d.n));
-    }
-}
-
 __global__ void __launch_bounds__(128) k_stats_pass2(const TDesc* __restrict__ td,
                                                      const int64_t* __restrict__ chunk_base,
                                                      int ntens, int64_t total, Scratch sc) {
@@ -157,25 +396,6 @@ __global__ void __launch_bounds__(128) k_stats_pass2(const TDesc* __restrict__ t
         acc = __dadd_rn(acc, __dmul_rn(dv, dv));
     }
     sc.p_dev[d.chunk_base + (g - d.chunk_base)] = acc;
-}
-
-__global__ void k_stats_fin2(const TDesc* __restrict__ td, int ntens, Scratch sc, float sigma_n,
-                             int mask_mode) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= ntens) return;
-    const TDesc& d = td[t];
-    TStats* st = d.st;
-    if (!st->constant) {
-        double ss = 0.0;
-        for (int64_t c = 0; c < d.n_chunks; ++c) ss = __dadd_rn(ss, sc.p_dev[d.chunk_base + c]);
-        st->ss = ss;
-        st->stddev = __dsqrt_rn(__ddiv_rn(ss, static_cast<double>(d.n)));
-    }
-    // detect_impl (outliers.cpp:33-40): no outliers when stddev == 0.
-    st->mask = (mask_mode && st->stddev != 0.0) ? 1 : 0;
-    st->thr = st->mask ? __dmul_rn(static_cast<double>(sigma_n), st->stddev)
-                       : __longlong_as_double(0x7ff0000000000000ll);
-    st->n_out = 0;
 }
 
 // ---- K2 -------------------------------------------------------------------
@@ -298,31 +518,51 @@ __global__ void __launch_bounds__(kDT) k_detect_write(const TDesc* __restrict__ 
 }  // namespace
 
 void launch_stats_pass1(const TDesc* td, const int64_t* chunk_base, int ntens,
-                        int64_t total_chunks, Scratch sc, cudaStream_t st) {
+                        int64_t total_chunks, Scratch sc, cudaStream_t st, bool aligned) {
     if (total_chunks == 0) return;
-    const int T = 128;
-    k_stats_pass1<<<(unsigned)((total_chunks + T - 1) / T), T, 0, st>>>(td, chunk_base, ntens,
-                                                                        total_chunks, sc);
+    if (aligned) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_stats_pipe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kStatsSmem);
+            cudaFuncSetAttribute(k_stats_pipe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kStatsSmem);
+            attr = true;
+        }
+        const int64_t per = 32 * kWarpsPerCta;
+        k_stats_pipe<false><<<(unsigned)((total_chunks + per - 1) / per), 32 * kWarpsPerCta,
+                              kStatsSmem, st>>>(td, chunk_base, ntens, total_chunks, sc);
+    } else {
+        const int T = 128;
+        k_stats_pass1<<<(unsigned)((total_chunks + T - 1) / T), T, 0, st>>>(td, chunk_base, ntens,
+                                                                            total_chunks, sc);
+    }
     count_launch();
 }
 
 void launch_stats_fin1(const TDesc* td, int ntens, Scratch sc, cudaStream_t st) {
-    k_stats_fin1<<<(ntens + 63) / 64, 64, 0, st>>>(td, ntens, sc);
+    k_stats_merge<false><<<ntens, 256, 0, st>>>(td, sc, 0.f, 0);
     count_launch();
 }
 
 void launch_stats_pass2(const TDesc* td, const int64_t* chunk_base, int ntens,
-                        int64_t total_chunks, Scratch sc, cudaStream_t st) {
+                        int64_t total_chunks, Scratch sc, cudaStream_t st, bool aligned) {
     if (total_chunks == 0) return;
-    const int T = 128;
-    k_stats_pass2<<<(unsigned)((total_chunks + T - 1) / T), T, 0, st>>>(td, chunk_base, ntens,
-                                                                        total_chunks, sc);
+    if (aligned) {
+        const int64_t per = 32 * kWarpsPerCta;
+        k_stats_pipe<true><<<(unsigned)((total_chunks + per - 1) / per), 32 * kWarpsPerCta,
+                             kStatsSmem, st>>>(td, chunk_base, ntens, total_chunks, sc);
+    } else {
+        const int T = 128;
+        k_stats_pass2<<<(unsigned)((total_chunks + T - 1) / T), T, 0, st>>>(td, chunk_base, ntens,
+                                                                            total_chunks, sc);
+    }
     count_launch();
 }
 
 void launch_stats_fin2(const TDesc* td, int ntens, Scratch sc, float sigma_n, int mask_mode,
                        cudaStream_t st) {
-    k_stats_fin2<<<(ntens + 63) / 64, 64, 0, st>>>(td, ntens, sc, sigma_n, mask_mode);
+    k_stats_merge<true><<<ntens, 256, 0, st>>>(td, sc, sigma_n, mask_mode);
     count_launch();
 }
 

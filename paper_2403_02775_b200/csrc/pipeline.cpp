@@ -25,6 +25,43 @@ constexpr unsigned long long kNoBad = ~0ull;
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Columns per K3 CTA. The busiest SM processes ceil(groups / SMs) strips of
+// `cb` columns; fewer concurrent warps than ~12 per SM leave the FP64/issue
+// pipes idle during each step's reduction + Adam latency. Minimise
+// (columns on the busiest SM) / warp-efficiency; ties go to wider strips.
+int choose_k3_width(const K3Launch& base, const std::vector<int>& members, const int64_t* cols,
+                    const DeviceInfo& di) {
+    const int unit = (base.W == 1) ? 32 / base.L : 1;
+    const int max_teams = (base.W == 1) ? 16 * unit : std::max(1, 16 / base.W);
+    int best_cb = unit;
+    double best = 1e300;
+    for (int cb = unit; cb <= max_teams; cb += unit) {
+        K3Launch t = base;
+        set_k3_width(t, cb);
+        // Warps of a CTA map to SMSPs by warp id % 4: only multiples of 4
+        // warps keep the four schedulers equally loaded.
+        if ((t.threads / 32) % 4 != 0) continue;
+        if (!t.global_strip && t.smem > static_cast<size_t>(di.max_smem_optin)) break;
+        const int cps_smem = t.global_strip ? 8 : static_cast<int>(di.smem_per_sm / (t.smem + 1024));
+        const int cps = std::min({cps_smem, 2048 / t.threads, 8});
+        if (cps < 1) break;
+        int64_t groups = 0;
+        for (int i : members) groups += ceil_div(cols[i], cb);
+        const int64_t per_sm = ceil_div(groups, di.sms);
+        const double warps = static_cast<double>(std::min<int64_t>(cps, per_sm)) * (t.threads / 32);
+        const double eff = std::min(1.0, warps / 12.0);
+        // A lone CTA per SM cannot hide its strip load and sequential-error
+        // epilogue behind another CTA's Adam loop.
+        const double overlap = (std::min<int64_t>(cps, per_sm) >= 2) ? 1.0 : 1.12;
+        const double cost = static_cast<double>(per_sm * cb) / eff * overlap;
+        if (cost <= best + 1e-9) {
+            best = cost;
+            best_cb = cb;
+        }
+    }
+    return best_cb;
+}
+
 TStats fresh_stats() {
     TStats s;
     std::memset(&s, 0, sizeof(s));
@@ -128,28 +165,8 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
         for (auto& kv : by_rows) {
             Plan p;
             p.kl = plan_k3(kv.first, 0, di.sms, di.max_smem_optin);
-            // Shrink the strip width (columns per CTA) when that evens out
-            // the last wave: cost ~ waves * width / warp-efficiency.
-            const int unit = (p.kl.W == 1) ? 32 / p.kl.L : 1;
-            int best_cb = p.kl.teams;
-            double best_cost = 1e300;
-            for (int cb = p.kl.teams; cb >= std::max(unit, p.kl.teams / 2); cb -= unit) {
-                int64_t groups = 0;
-                for (int i : kv.second) groups += ceil_div(cols[i], cb);
-                const double waves = std::ceil(static_cast<double>(groups) / di.sms);
-                const double warps = (p.kl.W == 1) ? cb * p.kl.L / 32.0 : cb * p.kl.W;
-                const double eff = std::min(1.0, warps / 12.0);
-                const double cost = waves * cb / eff;
-                if (cost < best_cost - 1e-9) {
-                    best_cost = cost;
-                    best_cb = cb;
-                }
-            }
-            p.kl.teams = best_cb;
-            p.kl.threads = (p.kl.W == 1) ? ((best_cb * p.kl.L + 31) / 32) * 32 : best_cb * p.kl.W * 32;
-            if (!p.kl.global_strip)
-                p.kl.smem = static_cast<size_t>(best_cb) * p.kl.rstride * sizeof(float) +
-                            static_cast<size_t>(2) * best_cb * p.kl.W * 2 * sizeof(double);
+            const int best_cb = choose_k3_width(p.kl, kv.second, cols, di);
+            set_k3_width(p.kl, best_cb);
             for (int i : kv.second)
                 for (int64_t c0 = 0; c0 < cols[i]; c0 += best_cb)
                     p.groups.push_back({i, static_cast<int32_t>(c0),
@@ -166,7 +183,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
             plans.push_back(std::move(p));
         }
     }
-    // 32-column tiles for K3b / finalize.
+    // 32-column tiles for K3b.
     std::vector<int2> tiles;
     for (int i = 0; i < n; ++i)
         for (int64_t c0 = 0; c0 < cols[i]; c0 += 32) tiles.push_back(make_int2(i, (int)c0));
@@ -182,9 +199,9 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     for (int k = 0; k < 2; ++k) ar.reserve_n<float>(tot_chunks);
     for (int k = 0; k < 2; ++k) ar.reserve_n<long long>(tot_dblk);
     for (int k = 0; k < 5; ++k) ar.reserve_n<double>(tot_cols);
+    ar.reserve_n<int2>(tiles.size());
     ar.reserve(sizeof(double) * bc.size());
     ar.reserve(sizeof(K3Group) * tot_groups);
-    ar.reserve(sizeof(int2) * tiles.size());
     ar.reserve(sizeof(float) * tot_in);
     ar.reserve(sizeof(float) * gstrip_floats);
     if (int s = ar.allocate(st)) return s;
@@ -201,16 +218,16 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     sc.p_mx = ar.take<float>(tot_chunks);
     sc.blk_count = ar.take<long long>(tot_dblk);
     sc.blk_offset = ar.take<long long>(tot_dblk);
-    sc.s0 = ar.take<double>(tot_cols);
-    sc.s_opt = ar.take<double>(tot_cols);
+    sc.s_rtn = ar.take<double>(tot_cols);
+    sc.s_fin = ar.take<double>(tot_cols);
     sc.err_rtn = ar.take<double>(tot_cols);
     sc.err_fin = ar.take<double>(tot_cols);
     sc.inv = ar.take<double>(tot_cols);
     double* d_bc = ar.take<double>(bc.size());
     K3Group* d_groups = ar.take<K3Group>(tot_groups);
-    int2* d_tiles = ar.take<int2>(tiles.size());
     float* d_in = ar.take<float>(tot_in);
     float* d_gstrip = ar.take<float>(gstrip_floats);
+    int2* d_tiles = ar.take<int2>(tiles.size());
     if (!ar.ok()) return set_error(EZQ_ERR_CUDA, "internal: arena overflow (quantize_batch)");
 
     // ---- inputs ----
@@ -226,6 +243,8 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
             hd[i].W = Ws[i];
         }
     }
+    bool all_aligned = true;
+    for (int i = 0; i < n; ++i) all_aligned &= (reinterpret_cast<uintptr_t>(hd[i].W) & 15) == 0;
     std::vector<TStats> hs(n, fresh_stats());
     if (int s = upload(d_stats, hs, st)) return s;
     if (int s = upload(d_desc, hd, st)) return s;
@@ -241,10 +260,10 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     }
 
     // ---- phase 1 ----
-    launch_stats_pass1(d_desc, d_chunk_base, n, tot_chunks, sc, st);
+    launch_stats_pass1(d_desc, d_chunk_base, n, tot_chunks, sc, st, all_aligned);
     launch_stats_fin1(d_desc, n, sc, st);
     if (cfg_status == EZQ_OK) {
-        launch_stats_pass2(d_desc, d_chunk_base, n, tot_chunks, sc, st);
+        launch_stats_pass2(d_desc, d_chunk_base, n, tot_chunks, sc, st, all_aligned);
         launch_stats_fin2(d_desc, n, sc, cfg->sigma_n, mode != EZQ_MODE_RTN, st);
         if (mode != EZQ_MODE_RTN) {
             launch_detect_count(d_desc, d_dblk_base, n, tot_dblk, sc, st);
@@ -313,7 +332,6 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
         launch_k3(p.kl, d_desc, d_groups + p.goff, static_cast<int>(p.groups.size()), sc, cd,
                   d_gstrip, p.grid, st);
     launch_seq_errors(d_desc, d_tiles, static_cast<int>(tiles.size()), sc, cd, st);
-    launch_col_finalize(d_desc, d_tiles, static_cast<int>(tiles.size()), sc, cd, st);
     launch_tensor_totals(d_desc, n, sc, st);
     launch_pack(d_desc, d_pblk_base, n, tot_pblk, sc, cd, st);
     {
@@ -488,9 +506,9 @@ int ezq_tensor_stats(const float* W, int64_t rows, int64_t cols, int mem, void* 
     if (int s = upload(d_st, hs, st)) return s;
     if (int s = upload(d_td, hdv, st)) return s;
     if (int s = upload(d_cb, cb, st)) return s;
-    launch_stats_pass1(d_td, d_cb, 1, hd.n_chunks, sc, st);
+    launch_stats_pass1(d_td, d_cb, 1, hd.n_chunks, sc, st, (reinterpret_cast<uintptr_t>(hd.W) & 15) == 0);
     launch_stats_fin1(d_td, 1, sc, st);
-    launch_stats_pass2(d_td, d_cb, 1, hd.n_chunks, sc, st);
+    launch_stats_pass2(d_td, d_cb, 1, hd.n_chunks, sc, st, (reinterpret_cast<uintptr_t>(hd.W) & 15) == 0);
     launch_stats_fin2(d_td, 1, sc, 0.f, 0, st);
     EZQ_CK(cudaGetLastError());
     EZQ_CK(cudaMemcpyAsync(hs.data(), d_st, sizeof(TStats), cudaMemcpyDeviceToHost, st));
@@ -563,9 +581,9 @@ int ezq_detect_outliers(const float* W, int64_t rows, int64_t cols, const ezq_co
     if (int s = upload(d_td, hdv, st)) return s;
     if (int s = upload(d_cb, cb, st)) return s;
     if (int s = upload(d_db, db, st)) return s;
-    launch_stats_pass1(d_td, d_cb, 1, hd.n_chunks, sc, st);
+    launch_stats_pass1(d_td, d_cb, 1, hd.n_chunks, sc, st, (reinterpret_cast<uintptr_t>(hd.W) & 15) == 0);
     launch_stats_fin1(d_td, 1, sc, st);
-    launch_stats_pass2(d_td, d_cb, 1, hd.n_chunks, sc, st);
+    launch_stats_pass2(d_td, d_cb, 1, hd.n_chunks, sc, st, (reinterpret_cast<uintptr_t>(hd.W) & 15) == 0);
     launch_stats_fin2(d_td, 1, sc, cfg->sigma_n, 1, st);
     launch_detect_count(d_td, d_db, 1, hd.n_dblk, sc, st);
     launch_detect_scan(d_td, 1, sc, st);

@@ -94,6 +94,7 @@ const DeviceInfo& device_info(int dev) {
     DeviceInfo di;
     cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&di.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&di.smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     return g_info[dev] = di;
 }
 
@@ -156,6 +157,8 @@ CfgDev make_cfg(const ezq_config* c, int mode, const double* bc_dev) {
     d.fixed_at = c->select_step < c->steps ? c->select_step : c->steps;
     d.sigma_n = c->sigma_n;
     d.guard = level_guard(d.lmax);
+    d.guard_sat = level_guard_sat(d.lmin, d.lmax);
+    d.sat_b = static_cast<float>(static_cast<double>(-d.lmin) / static_cast<double>(d.lmax - d.lmin));
     d.adam.b1 = c->beta1;
     d.adam.b2 = c->beta2;
     d.adam.c1 = 1.0 - c->beta1;

@@ -34,6 +34,7 @@ inline cudaStream_t pick_stream(void* user, int dev) {
 struct DeviceInfo {
     int sms = 0;
     int max_smem_optin = 0;
+    int smem_per_sm = 0;
 };
 const DeviceInfo& device_info(int dev);
 
