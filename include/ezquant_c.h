@@ -168,6 +168,8 @@ int ezq_qweight_wrap(int64_t rows, int64_t cols, int bits, const uint8_t* packed
                      const ezq_outlier* outliers, int64_t n_outliers, double mean,
                      double stddev, float sigma_n, int mem, ezq_qweight** out);
 void ezq_qweight_free(ezq_qweight* q);
+/* Host copy (library-owned) of a device-resident artifact. */
+int ezq_qweight_to_host(const ezq_qweight* q, ezq_qweight** out);
 void ezq_free(void* p);
 
 /* reconstruction_error (rtn.hpp:34-44; rtn.cpp:34-77): per-column sequential

@@ -437,6 +437,29 @@ void ezq_qweight_free(ezq_qweight* q) {
     std::free(q);
 }
 
+int ezq_qweight_to_host(const ezq_qweight* q, ezq_qweight** out) {
+    *out = nullptr;
+    ezq_qweight* h = static_cast<ezq_qweight*>(std::calloc(1, sizeof(ezq_qweight)));
+    *h = *q;
+    h->mem = EZQ_MEM_HOST;
+    h->owned = 1;
+    h->packed = static_cast<uint8_t*>(std::malloc(std::max<int64_t>(q->packed_bytes, 1)));
+    h->scales = static_cast<float*>(std::malloc(sizeof(float) * std::max<int64_t>(q->cols, 1)));
+    h->outliers = q->n_outliers ? static_cast<ezq_outlier*>(std::malloc(sizeof(ezq_outlier) * q->n_outliers))
+                                : nullptr;
+    const cudaMemcpyKind k = q->mem == EZQ_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost;
+    cudaError_t e = cudaMemcpy(h->packed, q->packed, q->packed_bytes, k);
+    if (e == cudaSuccess) e = cudaMemcpy(h->scales, q->scales, sizeof(float) * q->cols, k);
+    if (e == cudaSuccess && q->n_outliers)
+        e = cudaMemcpy(h->outliers, q->outliers, sizeof(ezq_outlier) * q->n_outliers, k);
+    if (e != cudaSuccess) {
+        ezq_qweight_free(h);
+        return cuda_error(e, "ezq_qweight_to_host");
+    }
+    *out = h;
+    return clear_error();
+}
+
 int ezq_qweight_wrap(int64_t rows, int64_t cols, int bits, const uint8_t* packed,
                      int64_t packed_bytes, const float* scales, int64_t n_scales,
                      const ezq_outlier* outliers, int64_t n_outliers, double mean, double stddev,

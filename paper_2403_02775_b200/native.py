@@ -150,6 +150,7 @@ def lib() -> C.CDLL:
         L.ezq_qweight_wrap.argtypes = [I64, I64, I32, P, I64, P, I64, P, I64, D, D, C.c_float,
                                        I32, C.POINTER(C.POINTER(CQWeight))]
         L.ezq_qweight_free.argtypes = [C.POINTER(CQWeight)]
+        L.ezq_qweight_to_host.argtypes = [C.POINTER(CQWeight), C.POINTER(C.POINTER(CQWeight))]
         L.ezq_free.argtypes = [P]
         L.ezq_reconstruction_error.argtypes = [P, P, I64, I64, P, P, I64, I32, P, C.POINTER(D)]
         L.ezq_channel_eval.argtypes = [P, I64, P, I64, D, C.POINTER(CConfig), C.POINTER(D),
@@ -289,6 +290,19 @@ class DeviceBatch:
 
     def __getitem__(self, i) -> CQWeight:
         return self.ptrs[i].contents
+
+    def to_host(self, i) -> "QuantizedWeight":
+        h = C.POINTER(CQWeight)()
+        check(lib().ezq_qweight_to_host(self.ptrs[i], C.byref(h)))
+        try:
+            return _from_c(h.contents)
+        finally:
+            lib().ezq_qweight_free(h)
+
+    def dequantize_into(self, i, out, stream=None):
+        """ezq_dequantize_tensor of entry i into `out` (torch CUDA tensor or numpy)."""
+        check(lib().ezq_dequantize_tensor(self.ptrs[i], _ptr(out), _mem(out), _stream(stream)))
+        return out
 
     def close(self):
         for p in self.ptrs:

@@ -1,0 +1,295 @@
+"""GPU parity gate: the CUDA path (through the C-ABI) vs the oracle (C
+restatement) and the golden fixtures of the compiled reference.
+
+Bar (BASELINE.json north_star): masks / CSR / codes / packed bytes bit-exact;
+scales within 1e-5 relative (we assert bit-exact -- the tree-ordered
+optimizer reproduces the reference's trajectory); reported errors equal (the
+K3b pass recomputes them in reference order). Tests restate the reference's
+own suites (file:line cited)."""
+import numpy as np
+import pytest
+
+from conftest import golden_cfg, golden_quant_files, load_golden
+from paper_2403_02775_b200.native import Config
+
+pytestmark = pytest.mark.gpu
+
+
+def assert_same_quant(q, ref, W=None, scale_rtol=0.0, code_flip_frac=0.0):
+    """same_quantized (test_pipeline.cpp:45-51) with the north_star tolerances."""
+    assert np.array_equal(q.outliers, ref["outliers"]), "outlier CSR differs"
+    assert q.mean == ref["mean"] and q.stddev == ref["stddev"]
+    if scale_rtol == 0.0:
+        assert np.array_equal(q.scales.view(np.uint32), np.asarray(ref["scales"]).view(np.uint32))
+    else:
+        rel = np.abs(q.scales.astype(np.float64) - ref["scales"]) / ref["scales"]
+        assert rel.max() <= scale_rtol
+    if code_flip_frac == 0.0:
+        assert np.array_equal(q.packed, ref["packed"])
+    else:
+        a, b = q.packed, np.asarray(ref["packed"])
+        flips = int(np.sum((a & 15) != (b & 15)) + np.sum((a >> 4) != (b >> 4)))
+        assert flips <= code_flip_frac * W.size
+    if scale_rtol == 0.0:
+        assert q.rtn_error == ref["rtn_error"] and q.final_error == ref["final_error"]
+
+
+# ---- golden fixtures (compiled reference outputs) --------------------------
+@pytest.mark.parametrize("fname", golden_quant_files())
+def test_golden_quantize_gpu(gpu, fname):
+    g = load_golden(fname)
+    cfg = golden_cfg(g["cfg"])
+    q = gpu.quantize_tensor(g["W"], cfg, str(g["mode"]))
+    assert_same_quant(q, g)
+    d = gpu.dequantize(q)
+    assert np.array_equal(d.view(np.uint32), g["dequant"].view(np.uint32))
+
+
+def test_golden_stats_gpu(gpu):
+    g = load_golden("stats.npz")
+    for name in ("kat", "pop", "single", "ragged", "multi_chunk"):
+        st = gpu.tensor_stats(g[name + "_W"])
+        assert [st["mean"], st["stddev"], st["max_abs"]] == g[name + "_out"].tolist(), name
+
+
+def test_golden_channel_gpu(gpu):
+    g = load_golden("channel.npz")
+    r = gpu.optimize_channel(g["x"], None, Config(lr=3e-3), keep_trace=True)
+    assert np.array_equal(r["trace_scale"], g["trace_scale"])
+    assert np.array_equal(r["trace_error"], g["trace_error"])
+    assert r["scale"] == g["scale"] and r["best_step"] == int(g["best_step"])
+    assert list(gpu.brute_force_scale(g["x"], None, Config(), 2000)) == g["bf"].tolist()
+    assert list(gpu.channel_eval(g["x"], None, 0.11, Config())) == g["ev"].tolist()
+
+
+# ---- seeded parity sweep vs the oracle --------------------------------------
+CASES = [
+    # (rows, cols, seed, scale, cfg, mode, planted)
+    (64, 64, 31, 1.0, Config(), "easyquant", 0),
+    (96, 64, 71, 0.05, Config(steps=60), "easyquant", 31),
+    (513, 77, 5, 0.02, Config(), "easyquant", 0),
+    (513, 77, 5, 0.02, Config(bits=3), "easyquant", 0),
+    (513, 77, 5, 0.02, Config(bits=2), "easyquant", 0),
+    (513, 77, 5, 0.02, Config(bits=5), "easyquant", 0),
+    (513, 77, 5, 0.02, Config(bits=8), "easyquant", 0),
+    (300, 211, 11, 1.0, Config(select="fixed"), "easyquant", 200),
+    (300, 211, 11, 1.0, Config(), "outliers-only", 200),
+    (300, 211, 11, 1.0, Config(), "rtn", 200),
+    (1024, 96, 12, 0.02, Config(lr=1e-4), "easyquant", 0),
+    (2048, 256, 7, 1.0, Config(), "easyquant", 2000),
+    (4099, 37, 8, 1.0, Config(sigma_n=2.5), "easyquant", 0),       # ragged rows, odd cols
+    (8192, 48, 9, 0.02, Config(lr=1e-4), "easyquant", 0),
+    (11008, 40, 13, 0.02, Config(), "easyquant", 0),
+    (12288, 24, 19, 0.02, Config(), "easyquant", 0),
+    (1, 37, 63, 1.0, Config(), "easyquant", 0),                       # 1xN (test_pipeline.cpp:192)
+    (53, 1, 64, 1.0, Config(), "easyquant", 0),                       # Nx1
+    (7, 11, 6, 1.0, Config(sigma_n=0.0), "easyquant", 0),             # every element an outlier
+]
+
+
+@pytest.mark.parametrize("rows,cols,seed,scale,cfg,mode,planted", CASES)
+def test_parity_vs_oracle(gpu, O, rows, cols, seed, scale, cfg, mode, planted):
+    W = O.gaussian(rows, cols, seed, scale)
+    if planted:
+        O.plant_outliers(W, planted, 10 * scale, 50 * scale, seed + 1000)
+    q = gpu.quantize_tensor(W, cfg, mode)
+    r = O.quantize(W, cfg, mode)
+    assert r["status"] == "ok"
+    assert_same_quant(q, r)
+    d = gpu.dequantize(q)
+    dr = O.dequantize(rows, cols, cfg.bits, r["packed"], r["scales"], r["outliers"])
+    assert np.array_equal(d.view(np.uint32), dr.view(np.uint32))
+
+
+def test_parity_c1_full_size(gpu, O):
+    """configs[0]: 4096x4096 Gaussian + 0.5% planted 10-50 sigma outliers,
+    reference defaults (k=4, sigma_n=3, 200 steps, best-error)."""
+    W = O.gaussian(4096, 4096, 1234)
+    O.plant_outliers(W, int(round(0.005 * W.size)), 10.0, 50.0, 5678)
+    q = gpu.quantize_tensor(W, Config())
+    r = O.quantize(W, Config())
+    assert len(q.outliers) == 83886
+    assert_same_quant(q, r)
+
+
+def test_batch_equals_single(gpu, O):
+    """Grouped multi-tensor launches (the whole-model driver) give the same
+    bytes as one-tensor calls (model.cpp:154-192 worker-count invariance)."""
+    shapes = [(256, 128), (128, 256), (256, 128), (64, 96), (1000, 33)]
+    Ws = [O.gaussian(r, c, 100 + i, 0.02) for i, (r, c) in enumerate(shapes)]
+    batch = gpu.quantize_batch(Ws, Config(steps=50))
+    for W, qb in zip(Ws, batch):
+        qs = gpu.quantize_tensor(W, Config(steps=50))
+        assert np.array_equal(qb.packed, qs.packed)
+        assert np.array_equal(qb.scales, qs.scales)
+        assert np.array_equal(qb.outliers, qs.outliers)
+        assert (qb.rtn_error, qb.final_error) == (qs.rtn_error, qs.final_error)
+
+
+def test_device_resident_io(gpu, O):
+    import torch
+    W = O.gaussian(512, 256, 77, 0.02)
+    Wd = torch.from_numpy(W).cuda()
+    qh = gpu.quantize_tensor(W, Config())
+    qd = gpu.quantize_tensor(Wd, Config())
+    assert np.array_equal(qh.packed, qd.packed) and np.array_equal(qh.scales, qd.scales)
+    b = gpu.quantize_batch([Wd], Config(), out_mem=gpu.MEM_DEVICE)
+    h = b.to_host(0)
+    assert np.array_equal(h.packed, qh.packed) and np.array_equal(h.scales, qh.scales)
+    assert np.array_equal(h.outliers, qh.outliers) and h.final_error == qh.final_error
+    out = torch.empty(W.shape, dtype=torch.float32, device="cuda")
+    b.dequantize_into(0, out)
+    assert np.array_equal(out.cpu().numpy(), gpu.dequantize(qh))
+    b.close()
+
+
+# ---- reference unit tests restated on the GPU path ---------------------------
+def test_stats_kats_gpu(gpu):  # test_stats.cpp:27-102
+    st = gpu.tensor_stats(np.array([[0, 0, 0, 0, 100]], np.float32))
+    assert st["mean"] == pytest.approx(20.0, rel=1e-12) and st["stddev"] == pytest.approx(40.0, rel=1e-12)
+    assert st["max_abs"] == 100.0 and st["count"] == 5
+    for c in (0.0, 1.0, -3.25, 1e-8, 7e6):
+        st = gpu.tensor_stats(np.full((33, 17), c, np.float32))
+        assert st["stddev"] == 0.0 and st["mean"] == float(np.float32(c))
+    st = gpu.tensor_stats(np.array([[-2.5]], np.float32))
+    assert (st["mean"], st["stddev"], st["max_abs"]) == (-2.5, 0.0, 2.5)
+    # signed zeros: the reference keeps the first of equal values
+    st = gpu.tensor_stats(np.array([[-0.0, 0.0, 0.0]], np.float32))
+    assert st["stddev"] == 0.0 and np.signbit(st["mean"])
+
+
+def test_detect_kats_gpu(gpu, O):  # test_outliers.cpp:31-125
+    out, mean, std = gpu.detect_outliers(np.array([[0, 0, 0, 0, 100]], np.float32), Config(sigma_n=2.0))
+    assert len(out) == 1 and (out[0]["row"], out[0]["col"], out[0]["value"]) == (0, 4, 100.0)
+    assert mean == pytest.approx(20.0) and std == pytest.approx(40.0)
+    for n in (0.0, 1.0, 3.0):
+        out, _, std = gpu.detect_outliers(np.full((9, 9), 5.5, np.float32), Config(sigma_n=n))
+        assert len(out) == 0 and std == 0.0
+    W = O.gaussian(1000, 1000, 2024)
+    frac = len(gpu.detect_outliers(W, Config(sigma_n=3.0))[0]) / W.size
+    assert 0.0017 < frac < 0.0037
+    W = O.gaussian(200, 200, 5)
+    wide = gpu.detect_outliers(W, Config(sigma_n=1.5))[0]
+    narrow = gpu.detect_outliers(W, Config(sigma_n=2.5))[0]
+    assert set(map(tuple, narrow[["row", "col"]].tolist())) <= set(map(tuple, wide[["row", "col"]].tolist()))
+    W = O.gaussian(257, 129, 9)
+    a = gpu.detect_outliers(W, Config(sigma_n=2.0))
+    b = O.detect_outliers(W, 2.0)
+    assert np.array_equal(a[0], b[0]) and a[1:] == b[1:]
+    for a_, b_ in ((2.0, 0.0), (1.0, 3.0), (-0.5, 1.25)):  # affine invariance (:89-105)
+        T = (np.float32(a_) * O.gaussian(64, 48, 7) + np.float32(b_)).astype(np.float32)
+        base = gpu.detect_outliers(O.gaussian(64, 48, 7), Config(sigma_n=2.0))[0]
+        mapped = gpu.detect_outliers(T, Config(sigma_n=2.0))[0]
+        assert np.array_equal(base[["row", "col"]], mapped[["row", "col"]])
+
+
+def test_pipeline_behaviours_gpu(gpu, O):  # test_pipeline.cpp:61-257
+    m = np.full((16, 12), 2.0, np.float32)
+    q = gpu.quantize_tensor(m, Config())
+    assert len(q.outliers) == 0 and q.rtn_error == 0.0 and q.final_error == 0.0
+    assert np.array_equal(gpu.dequantize(q), m)
+    m = np.array([[0.5], [-1.5], [4.0], [2.0]], np.float32)
+    q = gpu.quantize_tensor(m, Config(), "rtn")
+    assert q.final_error == 0.0 and np.array_equal(gpu.dequantize(q), m)
+    m = np.array([[100.0, 1.0], [-100.0, 1.0]], np.float32)
+    back = gpu.dequantize(gpu.quantize_tensor(m, Config(sigma_n=1.0)))
+    assert back[0, 0] == 100.0 and back[1, 0] == -100.0
+    W = O.gaussian(512, 512, 51, 0.05)
+    O.plant_outliers(W, int(0.005 * 512 * 512), 0.5, 2.5, 52)
+    easy = gpu.quantize_tensor(W, Config())
+    iso = gpu.quantize_tensor(W, Config(), "outliers-only")
+    rtn = gpu.quantize_tensor(W, Config(), "rtn")
+    e = [gpu.reconstruction_error(W, gpu.dequantize(x)) for x in (easy, iso, rtn)]
+    assert e[0] < e[1] < e[2]
+    assert easy.rtn_error == pytest.approx(iso.final_error, rel=1e-12)
+    q = gpu.quantize_tensor(O.gaussian(96, 32, 33), Config())
+    rec = gpu.reconstruction_error(O.gaussian(96, 32, 33), gpu.dequantize(q), q.outliers)
+    assert rec == pytest.approx(q.final_error, rel=1e-5)
+    W = O.gaussian(24, 16, 75)
+    q = gpu.quantize_tensor(W, Config(sigma_n=100.0))
+    lv = gpu.unpack_levels(q.packed, W.size, 4).reshape(W.shape)
+    assert np.array_equal(gpu.dequantize(q), (q.scales.astype(np.float64) * lv).astype(np.float32))
+
+
+def test_error_semantics_gpu(gpu):
+    bad = np.array([[1.0, 2.0], [3.0, np.inf]], np.float32)
+    with pytest.raises(gpu.InvalidArgument) as e:
+        gpu.quantize_tensor(bad, Config())
+    assert e.value.msg == "non-finite element at flat index 3" and e.value.index == 3
+    with pytest.raises(gpu.InvalidArgument) as e:
+        gpu.quantize_tensor(np.ones((2, 2), np.float32), Config(bits=9))
+    assert e.value.msg == "bits must be in [2, 8], got 9"
+    # non-finite wins over a bad config (validate() order, pipeline.cpp:67-68)
+    with pytest.raises(gpu.InvalidArgument) as e:
+        gpu.quantize_tensor(bad, Config(bits=9))
+    assert "non-finite" in e.value.msg
+    with pytest.raises(gpu.InvalidArgument):
+        gpu.channel_eval(np.ones(3, np.float32), None, 0.0, Config())
+    with pytest.raises(gpu.InvalidArgument):
+        gpu.quantize_channel(np.ones(3, np.float32), -1.0, Config())
+    with pytest.raises(gpu.InvalidArgument):
+        gpu.brute_force_scale(np.ones(3, np.float32), None, Config(), 1)
+    # dequantize validation (pipeline.cpp:118-121, rtn.cpp:153-178, outliers.cpp:108-111)
+    q = gpu.quantize_tensor(np.ones((3, 3), np.float32) * np.arange(9, dtype=np.float32).reshape(3, 3), Config())
+    q.outliers = np.array([(3, 0, 1.0)], dtype=q.outliers.dtype)
+    with pytest.raises(gpu.InvalidArgument) as e:
+        gpu.dequantize(q)
+    assert e.value.msg == "outlier coordinate (3, 0) outside 3x3"
+    q8 = gpu.quantize_tensor(np.ones((2, 2), np.float32), Config(bits=2))
+    q8.packed = np.array([0, 1, 9, 0], np.uint8)
+    with pytest.raises(gpu.InvalidArgument) as e:
+        gpu.dequantize(q8)
+    assert e.value.msg == "packed byte 9 exceeds level span 3"
+    q.packed = q.packed[:2]
+    with pytest.raises(gpu.InvalidArgument):
+        gpu.dequantize(q)
+
+
+def test_channel_api_exact_gpu(gpu, O):  # test_optimize.cpp
+    cfg = Config()
+    assert gpu.channel_eval(np.array([0.3], np.float32), None, 0.25, cfg)[1] == pytest.approx(-0.1, rel=1e-6)
+    assert gpu.channel_eval(np.array([3.0], np.float32), None, 0.25, cfg)[1] == pytest.approx(-16.0, rel=1e-12)
+    x = np.array([0.3, 50.0, -0.22], np.float32)
+    assert gpu.channel_eval(x, [1], 0.25, cfg) == gpu.channel_eval(np.array([0.3, -0.22], np.float32), None, 0.25, cfg)
+    for seed in (100, 101, 102, 103):  # within 5% of the grid oracle (:137-146)
+        x = O.gaussian(1, 1024, seed)[0]
+        r = gpu.optimize_channel(x, None, cfg)
+        assert r["final_error"] <= 1.05 * gpu.brute_force_scale(x, None, cfg, 2000)[1]
+        ro = O.optimize_channel(x, cfg)
+        assert r["scale"] == ro["scale"] and r["final_error"] == ro["final_error"]
+    r = gpu.optimize_channel(np.array([5.0, 6.0], np.float32), [0, 1], cfg, keep_trace=True)
+    assert r["scale"] == 1.0 and r["final_error"] == 0.0 and len(r["trace_scale"]) == 0
+    x = O.gaussian(1, 1024, 10)[0]
+    f = gpu.optimize_channel(x, None, Config(select="fixed", select_step=100), keep_trace=True)
+    assert f["final_error"] <= f["initial_error"]
+    assert f["scale"] == np.float32(f["trace_scale"][100]) and f["final_error"] == f["trace_error"][100]
+    x = O.gaussian(1, 512, 11)[0]
+    x[17], x[400] = 250.0, -180.0
+    a = gpu.optimize_channel(x, [17, 400], cfg)
+    b = gpu.optimize_channel(np.delete(x, [17, 400]), None, cfg)
+    assert (a["scale"], a["final_error"]) == (b["scale"], b["final_error"])
+    xs = O.gaussian(1, 301, 8)[0]
+    base = gpu.quantize_channel(xs, 0.09, cfg)
+    for c in (0.25, 4.0, 1024.0):  # power-of-two scale equivariance (test_rtn.cpp:227-239)
+        assert np.array_equal(gpu.quantize_channel((np.float32(c) * xs).astype(np.float32), c * 0.09, cfg), base)
+    assert gpu.quantize_channel(np.array([0.125, -0.125], np.float32), 0.25, cfg).tolist() == [1, -1]
+
+
+def test_property_roundtrip_large(gpu, O):
+    """Size-independent properties at a larger LLaMA-like shape: outliers
+    restore bit-exactly, non-outliers within half a step when unclipped,
+    final <= rtn, and bit-identical results on repeat."""
+    W = O.gaussian(4096, 1024, 21, 0.02)
+    O.plant_outliers(W, 20000, 0.2, 1.0, 22)
+    q1 = gpu.quantize_tensor(W, Config(sigma_n=2.5758))
+    q2 = gpu.quantize_tensor(W, Config(sigma_n=2.5758))
+    assert np.array_equal(q1.packed, q2.packed) and np.array_equal(q1.scales, q2.scales)
+    assert q1.final_error <= q1.rtn_error
+    d = gpu.dequantize(q1)
+    o = q1.outliers
+    assert np.array_equal(d[o["row"], o["col"]].view(np.uint32), W[o["row"], o["col"]].view(np.uint32))
+    s = q1.scales.astype(np.float64)[None, :]
+    mask = np.ones(W.shape, bool)
+    mask[o["row"], o["col"]] = False
+    inside = mask & (W <= 8 * s) & (W >= -7 * s)
+    assert np.all(np.abs(d.astype(np.float64) - W)[inside] <= (s / 2 + 1e-6).repeat(W.shape[0], 0)[inside])
