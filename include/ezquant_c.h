@@ -131,6 +131,17 @@ const char* ezq_version(void);
 /* Number of kernels launched by this process (instrumentation for bench). */
 int64_t ezq_kernel_launches(void);
 
+/* ---- instrumentation (bench / profiling) ------------------------------------ */
+/* When enabled, every kernel launch of the named families is bracketed by
+ * CUDA events on its own stream; ezq_profile_read synchronizes them and
+ * returns the summed device time, launch count and algorithmic work (flop for
+ * "qrange", bytes for the HBM-bound families). Families: "stats", "detect",
+ * "qrange", "seqerr", "pack", "dequant", "gemv". */
+int ezq_profile_enable(int on);
+int ezq_profile_read(const char* family, double* ms, int64_t* launches, double* work);
+/* FP64 DFMA peak of the current device (TFLOP/s), measured by a microkernel. */
+int ezq_measure_fp64_peak(double* tflops);
+
 /* ---- tensor statistics (stats.hpp:14-20; stats.cpp:27-108) ----------------- */
 /* Bit-exact with the reference: 8192-element fp64 chunks, chunk-ordered merge.
  * `W` is host or device memory per `mem`. Also runs DenseMatrix::validate's

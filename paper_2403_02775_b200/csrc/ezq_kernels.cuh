@@ -162,5 +162,9 @@ void launch_quantize_channel(const float* x, int64_t n, double scale, CfgDev cfg
 
 // Instrumentation: kernels launched by this process.
 void count_launch(int n = 1);
+// Optional per-family device timing (ezq_profile_enable): returns a token to
+// pass to prof_end, or -1 when profiling is off.
+int prof_begin(const char* family, cudaStream_t st);
+void prof_end(int token, cudaStream_t st, double work);
 
 }  // namespace ezq

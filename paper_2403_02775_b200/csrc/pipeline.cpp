@@ -81,9 +81,13 @@ int upload(T* d, const std::vector<T>& h, cudaStream_t st) {
 void free_qweight_arrays(ezq_qweight* q) {
     if (!q || !q->owned) return;
     if (q->mem == EZQ_MEM_DEVICE) {
-        cudaFree(q->packed);
-        cudaFree(q->scales);
-        cudaFree(q->outliers);
+        // Stream-ordered pool memory: no device-wide synchronisation.
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaStream_t st = thread_stream(dev);
+        if (q->packed) cudaFreeAsync(q->packed, st);
+        if (q->scales) cudaFreeAsync(q->scales, st);
+        if (q->outliers) cudaFreeAsync(q->outliers, st);
     } else {
         std::free(q->packed);
         std::free(q->scales);
@@ -260,15 +264,23 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     }
 
     // ---- phase 1 ----
+    int64_t tot_elems = 0;
+    for (int i = 0; i < n; ++i) tot_elems += hd[i].n;
+    int pt = prof_begin("stats", st);
     launch_stats_pass1(d_desc, d_chunk_base, n, tot_chunks, sc, st, all_aligned);
     launch_stats_fin1(d_desc, n, sc, st);
     if (cfg_status == EZQ_OK) {
         launch_stats_pass2(d_desc, d_chunk_base, n, tot_chunks, sc, st, all_aligned);
         launch_stats_fin2(d_desc, n, sc, cfg->sigma_n, mode != EZQ_MODE_RTN, st);
+        prof_end(pt, st, 8.0 * tot_elems);  // two reads of W
         if (mode != EZQ_MODE_RTN) {
+            pt = prof_begin("detect", st);
             launch_detect_count(d_desc, d_dblk_base, n, tot_dblk, sc, st);
             launch_detect_scan(d_desc, n, sc, st);
+            prof_end(pt, st, 4.0 * tot_elems);
         }
+    } else {
+        prof_end(pt, st, 4.0 * tot_elems);
     }
     EZQ_CK(cudaGetLastError());
     EZQ_CK(cudaMemcpyAsync(hs.data(), d_stats, sizeof(TStats) * n, cudaMemcpyDeviceToHost, st));
@@ -300,18 +312,18 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     std::vector<Out> dout(n);
     auto free_dout = [&]() {
         for (auto& o : dout) {
-            cudaFree(o.packed);
-            cudaFree(o.scales);
-            cudaFree(o.outl);
+            if (o.packed) cudaFreeAsync(o.packed, st);
+            if (o.scales) cudaFreeAsync(o.scales, st);
+            if (o.outl) cudaFreeAsync(o.outl, st);
             o = Out{};
         }
     };
     for (int i = 0; i < n; ++i) {
         const int64_t pb = ezq_packed_size(hd[i].n, cfg->bits);
-        cudaError_t e1 = cudaMalloc(&dout[i].packed, std::max<int64_t>(pb, 1));
-        cudaError_t e2 = cudaMalloc(&dout[i].scales, sizeof(float) * cols[i]);
+        cudaError_t e1 = cudaMallocAsync(&dout[i].packed, std::max<int64_t>(pb, 1), st);
+        cudaError_t e2 = cudaMallocAsync(&dout[i].scales, sizeof(float) * cols[i], st);
         cudaError_t e3 = cudaSuccess;
-        if (hs[i].n_out > 0) e3 = cudaMalloc(&dout[i].outl, sizeof(ezq_outlier) * hs[i].n_out);
+        if (hs[i].n_out > 0) e3 = cudaMallocAsync(&dout[i].outl, sizeof(ezq_outlier) * hs[i].n_out, st);
         if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
             free_dout();
             return cuda_error(cudaErrorMemoryAllocation, "output allocation");
@@ -327,13 +339,34 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
 
     // ---- phase 2 ----
     const CfgDev cd = make_cfg(cfg, mode, d_bc);
-    if (mode != EZQ_MODE_RTN) launch_detect_write(d_desc, d_dblk_base, n, tot_dblk, sc, st);
-    for (auto& p : plans)
+    int64_t tot_out = 0;
+    for (int i = 0; i < n; ++i) tot_out += hs[i].n_out;
+    if (mode != EZQ_MODE_RTN) {
+        const int p2 = prof_begin("detect", st);
+        launch_detect_write(d_desc, d_dblk_base, n, tot_dblk, sc, st);
+        prof_end(p2, st, 4.0 * tot_elems + 12.0 * tot_out);
+    }
+    for (auto& p : plans) {
+        // Algorithmic work: 7 flop (1 DMUL + 3 DFMA) per normal element-step.
+        double normals = 0.0;
+        for (auto& g : p.groups) (void)g;
+        for (int i = 0; i < n; ++i)
+            if (rows[i] == p.kl.rows) normals += static_cast<double>(hd[i].n - hs[i].n_out);
+        const double steps1 = (mode == EZQ_MODE_EASYQUANT) ? cfg->steps + 1.0 : 0.0;
+        const int p3 = prof_begin("qrange", st);
         launch_k3(p.kl, d_desc, d_groups + p.goff, static_cast<int>(p.groups.size()), sc, cd,
                   d_gstrip, p.grid, st);
+        prof_end(p3, st, 7.0 * normals * steps1);
+    }
+    int p4 = prof_begin("seqerr", st);
     launch_seq_errors(d_desc, d_tiles, static_cast<int>(tiles.size()), sc, cd, st);
     launch_tensor_totals(d_desc, n, sc, st);
+    prof_end(p4, st, 4.0 * tot_elems);
+    int64_t tot_packed = 0;
+    for (int i = 0; i < n; ++i) tot_packed += ezq_packed_size(hd[i].n, cfg->bits);
+    p4 = prof_begin("pack", st);
     launch_pack(d_desc, d_pblk_base, n, tot_pblk, sc, cd, st);
+    prof_end(p4, st, 4.0 * tot_elems + static_cast<double>(tot_packed));
     {
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) {
@@ -676,8 +709,10 @@ int ezq_dequantize_tensor(const ezq_qweight* q, float* out, int out_mem, void* s
     }
     float* dst = out_mem == EZQ_MEM_HOST ? ar.take<float>(N) : out;
     EZQ_CK(cudaMemsetAsync(d_bad, 0xff, 2 * sizeof(unsigned long long), st));
+    const int pd = prof_begin("dequant", st);
     launch_dequant(q->rows, q->cols, q->bits, pk, sc, dst, d_bad, st);
     launch_scatter(q->rows, q->cols, oe, q->n_outliers, dst, d_bad + 1, st);
+    prof_end(pd, st, static_cast<double>(need) + 4.0 * q->cols + 4.0 * N + 16.0 * q->n_outliers);
     EZQ_CK(cudaGetLastError());
     unsigned long long hb[2];
     EZQ_CK(cudaMemcpyAsync(hb, d_bad, sizeof(hb), cudaMemcpyDeviceToHost, st));

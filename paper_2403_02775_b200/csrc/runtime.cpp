@@ -16,6 +16,15 @@ void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 namespace {
 
+struct ProfRec {
+    std::string family;
+    cudaEvent_t a, b;
+    double work;
+};
+std::mutex g_prof_mu;
+std::vector<ProfRec> g_prof;
+std::atomic<int> g_prof_on{0};
+
 struct ErrState {
     int code = 0;
     std::string msg;
@@ -30,6 +39,26 @@ std::unordered_map<int, DeviceInfo> g_info;
 std::unordered_map<int, bool> g_pool_ready;
 
 }  // namespace
+
+int prof_begin(const char* family, cudaStream_t st) {
+    if (!g_prof_on.load()) return -1;
+    ProfRec r;
+    r.family = family;
+    r.work = 0.0;
+    cudaEventCreate(&r.a);
+    cudaEventCreate(&r.b);
+    cudaEventRecord(r.a, st);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.push_back(r);
+    return static_cast<int>(g_prof.size()) - 1;
+}
+
+void prof_end(int token, cudaStream_t st, double work) {
+    if (token < 0) return;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    cudaEventRecord(g_prof[token].b, st);
+    g_prof[token].work = work;
+}
 
 int set_error(int code, const std::string& msg, int64_t index) {
     t_err.code = code;
@@ -254,6 +283,34 @@ int ezq_synchronize(void) {
 const char* ezq_version(void) { return "ezquant-b200 0.1.0 (sm_100a)"; }
 
 int64_t ezq_kernel_launches(void) { return g_launches.load(); }
+
+int ezq_profile_enable(int on) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto& r : g_prof) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    g_prof.clear();
+    g_prof_on.store(on);
+    return clear_error();
+}
+
+int ezq_profile_read(const char* family, double* ms, int64_t* launches, double* work) {
+    *ms = 0.0;
+    *launches = 0;
+    *work = 0.0;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto& r : g_prof) {
+        if (r.family != family) continue;
+        EZQ_CK(cudaEventSynchronize(r.b));
+        float t = 0.f;
+        EZQ_CK(cudaEventElapsedTime(&t, r.a, r.b));
+        *ms += t;
+        *launches += 1;
+        *work += r.work;
+    }
+    return clear_error();
+}
 
 void ezq_free(void* p) { std::free(p); }
 

@@ -172,6 +172,9 @@ def lib() -> C.CDLL:
         L.ezq_gemv_prepare.argtypes = [C.POINTER(CQWeight), P, C.POINTER(P)]
         L.ezq_gemv.argtypes = [P, P, I32, I32, P, P]
         L.ezq_gemv_plan_free.argtypes = [P]
+        L.ezq_profile_enable.argtypes = [I32]
+        L.ezq_profile_read.argtypes = [C.c_char_p, C.POINTER(D), C.POINTER(I64), C.POINTER(D)]
+        L.ezq_measure_fp64_peak.argtypes = [C.POINTER(D)]
         _lib = L
     return _lib
 
@@ -222,6 +225,22 @@ def set_device(d: int):
 
 def kernel_launches() -> int:
     return int(lib().ezq_kernel_launches())
+
+
+def profile_enable(on: bool = True):
+    check(lib().ezq_profile_enable(int(on)))
+
+
+def profile_read(family: str) -> dict:
+    ms, n, w = C.c_double(), C.c_int64(), C.c_double()
+    check(lib().ezq_profile_read(family.encode(), C.byref(ms), C.byref(n), C.byref(w)))
+    return {"ms": ms.value, "launches": n.value, "work": w.value}
+
+
+def measure_fp64_peak() -> float:
+    t = C.c_double()
+    check(lib().ezq_measure_fp64_peak(C.byref(t)))
+    return t.value
 
 
 def config_validate(cfg: Config):
