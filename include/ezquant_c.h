@@ -14,7 +14,8 @@
  *
  * Threading: all entry points are reentrant. Each calling host thread gets
  * its own CUDA stream per device (or uses the `stream` argument when it is
- * non-null) and its own last-error slot.
+ * non-null; pass cudaStreamLegacy, i.e. (void*)1, for the legacy default
+ * stream) and its own last-error slot.
  */
 #ifndef EZQUANT_C_H
 #define EZQUANT_C_H

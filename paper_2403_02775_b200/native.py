@@ -207,10 +207,18 @@ def _mem(a) -> int:
     return MEM_HOST if isinstance(a, np.ndarray) else (MEM_DEVICE if a.is_cuda else MEM_HOST)
 
 
-def _stream(stream) -> Optional[int]:
-    if stream is None:
-        return None
-    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+def _stream(stream, *tensors) -> Optional[int]:
+    """Explicit stream, else torch's current stream when any argument is a
+    torch CUDA tensor (so library work is ordered after the producer of the
+    inputs and before their consumers), else the library's own stream."""
+    if stream is not None:
+        return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    for t in tensors:
+        if t is not None and not isinstance(t, np.ndarray) and getattr(t, "is_cuda", False):
+            import torch
+            h = torch.cuda.current_stream(t.device).cuda_stream
+            return h if h else 1  # torch's legacy default stream -> cudaStreamLegacy
+    return None
 
 
 def device_count() -> int:
@@ -253,7 +261,7 @@ def tensor_stats(W, stream=None) -> dict:
     """stats.hpp:14 -> {mean, stddev, max_abs, count}."""
     rows, cols = W.shape
     st = CStats()
-    check(lib().ezq_tensor_stats(_ptr(W), rows, cols, _mem(W), _stream(stream), C.byref(st)))
+    check(lib().ezq_tensor_stats(_ptr(W), rows, cols, _mem(W), _stream(stream, W), C.byref(st)))
     return {"mean": st.mean, "stddev": st.stddev, "max_abs": st.max_abs, "count": st.count}
 
 
@@ -264,7 +272,7 @@ def detect_outliers(W, cfg: Config, stream=None):
     e = C.POINTER(COutlier)()
     n = C.c_int64(0)
     mean, std = C.c_double(0), C.c_double(0)
-    check(lib().ezq_detect_outliers(_ptr(W), rows, cols, C.byref(c), _mem(W), _stream(stream),
+    check(lib().ezq_detect_outliers(_ptr(W), rows, cols, C.byref(c), _mem(W), _stream(stream, W),
                                     C.byref(e), C.byref(n), C.byref(mean), C.byref(std)))
     out = np.zeros(n.value, dtype=OUTLIER_DTYPE)
     if n.value:
@@ -291,7 +299,7 @@ def quantize_tensor(W, cfg: Config, mode: str = "easyquant", stream=None) -> Qua
     c = cfg.to_c()
     q = C.POINTER(CQWeight)()
     check(lib().ezq_quantize_tensor(_ptr(W), rows, cols, C.byref(c), MODES[mode], _mem(W),
-                                    MEM_HOST, _stream(stream), C.byref(q)))
+                                    MEM_HOST, _stream(stream, W), C.byref(q)))
     try:
         return _from_c(q.contents)
     finally:
@@ -320,7 +328,7 @@ class DeviceBatch:
 
     def dequantize_into(self, i, out, stream=None):
         """ezq_dequantize_tensor of entry i into `out` (torch CUDA tensor or numpy)."""
-        check(lib().ezq_dequantize_tensor(self.ptrs[i], _ptr(out), _mem(out), _stream(stream)))
+        check(lib().ezq_dequantize_tensor(self.ptrs[i], _ptr(out), _mem(out), _stream(stream, out)))
         return out
 
     def close(self):
@@ -347,7 +355,7 @@ def quantize_batch(Ws: Sequence, cfg: Config, mode: str = "easyquant", out_mem: 
     failed = C.c_int(-1)
     c = cfg.to_c()
     check(lib().ezq_quantize_batch(ptrs, rows, cols, n, C.byref(c), MODES[mode], _mem(Ws[0]),
-                                   out_mem, _stream(stream), outs, C.byref(failed)))
+                                   out_mem, _stream(stream, Ws[0]), outs, C.byref(failed)))
     if out_mem == MEM_DEVICE:
         return DeviceBatch(list(outs))
     res = []
@@ -355,6 +363,39 @@ def quantize_batch(Ws: Sequence, cfg: Config, mode: str = "easyquant", out_mem: 
         res.append(_from_c(p.contents))
         lib().ezq_qweight_free(p)
     return res
+
+
+class GemvPlan:
+    """ezq_gemv_prepare / ezq_gemv over a device-resident artifact (a
+    DeviceBatch entry). x: torch CUDA tensor [batch, rows] (f32/bf16/f16)."""
+
+    DTYPES = {"torch.float32": 0, "torch.bfloat16": 1, "torch.float16": 2}
+
+    def __init__(self, batch: "DeviceBatch", i: int, stream=None):
+        self._keep = batch
+        self.rows, self.cols = batch[i].rows, batch[i].cols
+        self.p = C.c_void_p()
+        check(lib().ezq_gemv_prepare(batch.ptrs[i], _stream(stream), C.byref(self.p)))
+        self.stream = stream
+
+    def __call__(self, x, y=None, stream=None):
+        import torch
+        if y is None:
+            y = torch.empty((x.shape[0], self.cols), dtype=torch.float32, device=x.device)
+        check(lib().ezq_gemv(self.p, x.data_ptr(), self.DTYPES[str(x.dtype)], x.shape[0],
+                             y.data_ptr(), _stream(stream or self.stream, x)))
+        return y
+
+    def close(self):
+        if self.p:
+            lib().ezq_gemv_plan_free(self.p)
+            self.p = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def dequantize(q: QuantizedWeight, out=None, stream=None) -> np.ndarray:
@@ -369,7 +410,7 @@ def dequantize(q: QuantizedWeight, out=None, stream=None) -> np.ndarray:
     if out is None:
         out = np.zeros((max(q.rows, 0), max(q.cols, 0)), dtype=np.float32)
     try:
-        check(lib().ezq_dequantize_tensor(w, _ptr(out), _mem(out), _stream(stream)))
+        check(lib().ezq_dequantize_tensor(w, _ptr(out), _mem(out), _stream(stream, out)))
     finally:
         lib().ezq_qweight_free(w)
     return out

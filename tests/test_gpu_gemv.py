@@ -1,0 +1,52 @@
+"""GPU: K6 fused dequant + outlier GEMV / skinny GEMM vs dequantize_tensor +
+an fp64 GEMV (the oracle's ezqo_gemv_f64). Parity is unpinned by the
+reference (it has no GEMV); the bar is 1e-3 relative with fp32 accumulation
+(BASELINE.json north_star)."""
+import numpy as np
+import pytest
+
+from paper_2403_02775_b200.native import Config
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("rows,cols,sigma,bits", [
+    (4096, 4096, 3.0, 4), (512, 1024, 2.5758, 4), (1024, 264, 2.8070, 4),
+    (300, 77, 3.0, 4),      # generic path (odd cols)
+    (256, 128, 3.0, 3),     # k=3 byte-per-level codes
+])
+@pytest.mark.parametrize("batch", [1, 2, 5, 8, 16])
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16", "float16"])
+def test_gemv_matches_dequant_f64(gpu, O, rows, cols, sigma, bits, batch, dtype):
+    import torch
+    W = O.gaussian(rows, cols, rows + cols, 0.02)
+    O.plant_outliers(W, max(1, W.size // 200), 0.2, 1.0, 77)
+    Wd = torch.from_numpy(W).cuda()
+    b = gpu.quantize_batch([Wd], Config(bits=bits, sigma_n=sigma, steps=20), out_mem=gpu.MEM_DEVICE)
+    q = b.to_host(0)
+    What = gpu.dequantize(q)
+    plan = gpu.GemvPlan(b, 0)
+    g = torch.Generator(device="cuda").manual_seed(batch)
+    x = torch.randn(batch, rows, generator=g, device="cuda").to(getattr(torch, dtype))
+    y = plan(x).cpu().numpy().astype(np.float64)
+    yref = O.gemv_f64(What, x.float().cpu().numpy())
+    err = np.abs(y - yref).max()
+    assert err <= 1e-3 * np.abs(yref).max(), (err, np.abs(yref).max())
+    assert np.all(np.abs(y - yref) <= 1e-3 * np.abs(yref) + 1e-4 * np.abs(yref).max())
+    plan.close()
+    b.close()
+
+
+def test_gemv_outlier_term_exact_path(gpu, O):
+    """Outliers only (all-zero normals): y must equal sum x_i v exactly up to fp32."""
+    import torch
+    W = np.zeros((64, 64), np.float32)
+    W[3, 5], W[40, 5], W[7, 63] = 50.0, -20.0, 33.0
+    b = gpu.quantize_batch([torch.from_numpy(W).cuda()], Config(sigma_n=1.0), out_mem=gpu.MEM_DEVICE)
+    assert b.to_host(0).outliers.size == 3
+    plan = gpu.GemvPlan(b, 0)
+    x = torch.arange(64, dtype=torch.float32, device="cuda")[None, :]
+    y = plan(x).cpu().numpy()[0]
+    ref = O.gemv_f64(gpu.dequantize(b.to_host(0)), x.cpu().numpy())[0]
+    assert np.allclose(y, ref, rtol=1e-6, atol=1e-4)
+    assert y[5] == pytest.approx(3 * 50.0 - 40 * 20.0, rel=1e-6)
