@@ -176,6 +176,74 @@ def run_reference(args):
     return 0
 
 
+def gemv_bench(N, torch, copies=8, batches=(1, 4, 8, 16), reps=20):
+    """configs[4]: fused dequant+outlier GEMV on LLaMA-7B-shaped 4-bit weights
+    with 0 / 0.5 / 1 % outliers, batch 1-16, vs outlier-free int4 (same kernel,
+    no outliers) and dense fp16 (cuBLAS via torch.matmul). `copies` weight
+    matrices per shape are rotated so the working set exceeds L2; one round is
+    captured in a CUDA graph and replayed (device time via CUDA events)."""
+    from paper_2403_02775_b200.native import Config
+    hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    sig = {0.0: 1.0e4, 0.005: 2.8070, 0.01: 2.5758}
+    gen = torch.Generator(device="cuda").manual_seed(99)
+    rows_out = []
+
+    def timed(fn):
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            fn()
+            fn()
+        torch.cuda.current_stream().wait_stream(s)
+        with torch.cuda.graph(g):
+            fn()
+        for _ in range(3):
+            g.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps / copies * 1e3  # us per GEMV
+
+    for (r, c) in [(4096, 4096), (4096, 11008), (11008, 4096)]:
+        dense = [(torch.randn(r, c, generator=gen, device="cuda") * 0.02).half() for _ in range(copies)]
+        for ratio in (0.0, 0.005, 0.01):
+            mats = [d.float() for d in dense]
+            b = N.quantize_batch(mats, Config(sigma_n=sig[ratio]), "outliers-only", out_mem=N.MEM_DEVICE)
+            del mats
+            plans = [N.GemvPlan(b, i) for i in range(copies)]
+            n_out = sum(b[i].n_outliers for i in range(copies)) / copies
+            for B in batches:
+                x = torch.randn(B, r, generator=gen, device="cuda").to(torch.bfloat16)
+                y = torch.empty(B, c, device="cuda", dtype=torch.float32)
+                us = timed(lambda: [p(x, y) for p in plans])
+                nbytes = (r * c) / 2 + 4 * c + 8 * n_out + 8 * (c + 1) + 2 * B * r + 4 * B * c
+                rec = {"shape": f"{r}x{c}", "batch": B, "outlier_pct": 100 * ratio, "us": us,
+                       "gbps": nbytes / (us * 1e-6) / 1e9, "frac": nbytes / (us * 1e-6) / 1e9 / hbm}
+                if ratio == 0.0:
+                    xh = x.half()
+                    yd = torch.empty(B, c, device="cuda", dtype=torch.float16)
+                    rec["dense_fp16_us"] = timed(lambda: [torch.matmul(xh, d, out=yd) for d in dense])
+                rows_out.append(rec)
+            for p in plans:
+                p.close()
+            b.close()
+        del dense
+    base = {(e["shape"], e["batch"]): e["us"] for e in rows_out if e["outlier_pct"] == 0.0}
+    for e in rows_out:
+        e["overhead_vs_int4_pct"] = 100.0 * (e["us"] / base[(e["shape"], e["batch"])] - 1.0)
+    b1 = [e for e in rows_out if e["batch"] == 1 and e["outlier_pct"] == 1.0]
+    return {"metric": "dequant-GEMV HBM GB/s", "unit": "GB/s",
+            "value_b1_1pct": sum(e["gbps"] for e in b1) / len(b1),
+            "peak_gbs": hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
+            "method": f"{copies} weight copies per shape rotated (> L2), CUDA-graph replay, CUDA events",
+            "rows": rows_out}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -185,6 +253,7 @@ def main():
     ap.add_argument("--workload", default="opt-1.3b", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-gemv", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -306,6 +375,8 @@ def main():
         },
         "kernel_share": {f: prof[f]["ms"] / args.steps / (step_s * 1e3) for f in prof},
     })
+    if not args.no_gemv:
+        line["gemv"] = gemv_bench(N, torch)
     if world == 1 and not args.no_cpu_baseline:
         per_layer = 6 if args.workload != "llama-7b" else 7
         sample = shapes[:2 * per_layer] if args.workload == "opt-1.3b" else shapes[:per_layer]
