@@ -89,9 +89,9 @@ void free_qweight_arrays(ezq_qweight* q) {
         if (q->scales) cudaFreeAsync(q->scales, st);
         if (q->outliers) cudaFreeAsync(q->outliers, st);
     } else {
-        std::free(q->packed);
-        std::free(q->scales);
-        std::free(q->outliers);
+        host_free(q->packed);
+        host_free(q->scales);
+        host_free(q->outliers);
     }
     q->packed = nullptr;
     q->scales = nullptr;
@@ -388,10 +388,10 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
         q->owned = 1;
         q->packed_bytes = ezq_packed_size(hd[i].n, cfg->bits);
         if (out_mem == EZQ_MEM_HOST) {
-            q->packed = static_cast<uint8_t*>(std::malloc(std::max<int64_t>(q->packed_bytes, 1)));
-            q->scales = static_cast<float*>(std::malloc(sizeof(float) * cols[i]));
+            q->packed = static_cast<uint8_t*>(host_alloc(std::max<int64_t>(q->packed_bytes, 1)));
+            q->scales = static_cast<float*>(host_alloc(sizeof(float) * cols[i]));
             q->outliers = hs[i].n_out > 0 ? static_cast<ezq_outlier*>(
-                                                std::malloc(sizeof(ezq_outlier) * hs[i].n_out))
+                                                host_alloc(sizeof(ezq_outlier) * hs[i].n_out))
                                           : nullptr;
             cudaMemcpyAsync(q->packed, dout[i].packed, q->packed_bytes, cudaMemcpyDeviceToHost, st);
             cudaMemcpyAsync(q->scales, dout[i].scales, sizeof(float) * cols[i],
@@ -445,6 +445,108 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     return clear_error();
 }
 
+// Host-resident inputs: tensors are processed in chunks of ~kChunkBytes
+// whose H2D copies run on a second stream while the previous chunk computes
+// (double-buffered device staging), so PCIe time hides behind K3.
+int quantize_batch_host(const float* const* Ws, const int64_t* rows, const int64_t* cols, int n,
+                        const ezq_config* cfg, int mode, int out_mem, void* user_stream,
+                        ezq_qweight** outs, int* failed) {
+    constexpr int64_t kChunkBytes = 512ll << 20;
+    std::vector<std::pair<int, int>> chunks;  // [first, last)
+    int64_t max_bytes = 0;
+    for (int i = 0; i < n;) {
+        int j = i;
+        int64_t bytes = 0;
+        while (j < n && (j == i || bytes + 4 * rows[j] * cols[j] <= kChunkBytes)) {
+            bytes += 4 * std::max<int64_t>(rows[j], 0) * std::max<int64_t>(cols[j], 0);
+            ++j;
+        }
+        chunks.emplace_back(i, j);
+        max_bytes = std::max(max_bytes, bytes);
+        i = j;
+    }
+    if (chunks.size() < 2)
+        return quantize_batch(Ws, rows, cols, n, cfg, mode, EZQ_MEM_HOST, out_mem, user_stream, outs,
+                              failed);
+    for (int i = 0; i < n; ++i) {
+        outs[i] = nullptr;
+        if (rows[i] <= 0 || cols[i] <= 0)  // same precedence as the one-shot path
+            return quantize_batch(Ws, rows, cols, n, cfg, mode, EZQ_MEM_HOST, out_mem, user_stream,
+                                  outs, failed);
+    }
+    int dev;
+    if (int s = bind_device(&dev)) return s;
+    cudaStream_t st = pick_stream(user_stream, dev);
+    cudaStream_t cs = copy_stream(dev);
+    float* buf[2] = {nullptr, nullptr};
+    EZQ_CK(cudaMallocAsync(reinterpret_cast<void**>(&buf[0]), max_bytes, st));
+    EZQ_CK(cudaMallocAsync(reinterpret_cast<void**>(&buf[1]), max_bytes, st));
+    cudaEvent_t in_ready[2], done[2];
+    for (int k = 0; k < 2; ++k) {
+        cudaEventCreateWithFlags(&in_ready[k], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
+    }
+    EZQ_CK(cudaEventRecord(done[0], st));  // buffers free "now"
+    EZQ_CK(cudaEventRecord(done[1], st));
+    auto issue_copy = [&](size_t c) -> int {
+        const int b = static_cast<int>(c % 2);
+        EZQ_CK(cudaStreamWaitEvent(cs, done[b], 0));
+        int64_t off = 0;
+        for (int i = chunks[c].first; i < chunks[c].second; ++i) {
+            const int64_t nb = 4 * rows[i] * cols[i];
+            EZQ_CK(cudaMemcpyAsync(reinterpret_cast<char*>(buf[b]) + off, Ws[i], nb,
+                                   cudaMemcpyHostToDevice, cs));
+            off += nb;
+        }
+        EZQ_CK(cudaEventRecord(in_ready[b], cs));
+        return EZQ_OK;
+    };
+    int status = issue_copy(0);
+    if (!status && chunks.size() > 1) status = issue_copy(1);
+    for (size_t c = 0; c < chunks.size() && !status; ++c) {
+        const int b = static_cast<int>(c % 2);
+        const int i0 = chunks[c].first, i1 = chunks[c].second;
+        std::vector<const float*> dW;
+        int64_t off = 0;
+        for (int i = i0; i < i1; ++i) {
+            dW.push_back(reinterpret_cast<const float*>(reinterpret_cast<char*>(buf[b]) + off));
+            off += 4 * rows[i] * cols[i];
+        }
+        if (cudaStreamWaitEvent(st, in_ready[b], 0) != cudaSuccess) {
+            status = cuda_error(cudaGetLastError(), "chunk wait");
+            break;
+        }
+        int sub_failed = -1;
+        status = quantize_batch(dW.data(), rows + i0, cols + i0, i1 - i0, cfg, mode, EZQ_MEM_DEVICE,
+                                out_mem, st, outs + i0, &sub_failed);
+        if (status) {
+            if (failed) *failed = sub_failed >= 0 ? i0 + sub_failed : -1;
+            // translate device-relative bad indices is unnecessary: flat index is per tensor
+            break;
+        }
+        cudaEventRecord(done[b], st);
+        if (c + 2 < chunks.size()) status = issue_copy(c + 2);
+    }
+    cudaStreamSynchronize(cs);
+    cudaFreeAsync(buf[0], st);
+    cudaFreeAsync(buf[1], st);
+    for (int k = 0; k < 2; ++k) {
+        cudaEventDestroy(in_ready[k]);
+        cudaEventDestroy(done[k]);
+    }
+    if (status) {
+        char msg[1024];
+        int64_t idx;
+        const int code = ezq_last_error(msg, sizeof msg, &idx);
+        for (int i = 0; i < n; ++i) {
+            ezq_qweight_free(outs[i]);
+            outs[i] = nullptr;
+        }
+        return set_error(code ? code : status, msg, idx);
+    }
+    return clear_error();
+}
+
 }  // namespace ezq
 
 using namespace ezq;
@@ -454,6 +556,12 @@ extern "C" {
 int ezq_quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* cols, int n,
                        const ezq_config* cfg, int mode, int in_mem, int out_mem, void* stream,
                        ezq_qweight** outs, int* failed_index) {
+    if (in_mem == EZQ_MEM_HOST && n > 1) {
+        std::string msg;
+        if (validate_config(cfg, &msg) == EZQ_OK)  // invalid configs take the one-shot path
+            return quantize_batch_host(Ws, rows, cols, n, cfg, mode, out_mem, stream, outs,
+                                       failed_index);
+    }
     return quantize_batch(Ws, rows, cols, n, cfg, mode, in_mem, out_mem, stream, outs,
                           failed_index);
 }
@@ -476,9 +584,9 @@ int ezq_qweight_to_host(const ezq_qweight* q, ezq_qweight** out) {
     *h = *q;
     h->mem = EZQ_MEM_HOST;
     h->owned = 1;
-    h->packed = static_cast<uint8_t*>(std::malloc(std::max<int64_t>(q->packed_bytes, 1)));
-    h->scales = static_cast<float*>(std::malloc(sizeof(float) * std::max<int64_t>(q->cols, 1)));
-    h->outliers = q->n_outliers ? static_cast<ezq_outlier*>(std::malloc(sizeof(ezq_outlier) * q->n_outliers))
+    h->packed = static_cast<uint8_t*>(host_alloc(std::max<int64_t>(q->packed_bytes, 1)));
+    h->scales = static_cast<float*>(host_alloc(sizeof(float) * std::max<int64_t>(q->cols, 1)));
+    h->outliers = q->n_outliers ? static_cast<ezq_outlier*>(host_alloc(sizeof(ezq_outlier) * q->n_outliers))
                                 : nullptr;
     const cudaMemcpyKind k = q->mem == EZQ_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost;
     cudaError_t e = cudaMemcpy(h->packed, q->packed, q->packed_bytes, k);

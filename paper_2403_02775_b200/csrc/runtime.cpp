@@ -33,6 +33,7 @@ struct ErrState {
 thread_local ErrState t_err;
 thread_local int t_device = -1;
 thread_local std::unordered_map<int, cudaStream_t> t_streams;
+thread_local std::unordered_map<int, cudaStream_t> t_copy_streams;
 
 std::mutex g_mu;
 std::unordered_map<int, DeviceInfo> g_info;
@@ -116,6 +117,15 @@ cudaStream_t thread_stream(int dev) {
     return s;
 }
 
+cudaStream_t copy_stream(int dev) {
+    auto it = t_copy_streams.find(dev);
+    if (it != t_copy_streams.end()) return it->second;
+    cudaStream_t s = nullptr;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    t_copy_streams[dev] = s;
+    return s;
+}
+
 const DeviceInfo& device_info(int dev) {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_info.find(dev);
@@ -128,6 +138,52 @@ const DeviceInfo& device_info(int dev) {
 }
 
 std::string fmt_double(double v) { return std::to_string(v); }
+
+namespace {
+std::mutex g_pin_mu;
+std::unordered_map<void*, size_t> g_pin_live;                  // ptr -> size
+std::unordered_map<size_t, std::vector<void*>> g_pin_free;     // size -> blocks
+size_t g_pin_cached = 0;
+constexpr size_t kPinCacheLimit = 16ull << 30;
+}  // namespace
+
+void* host_alloc(size_t bytes) {
+    bytes = bytes ? bytes : 1;
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        auto it = g_pin_free.find(bytes);
+        if (it != g_pin_free.end() && !it->second.empty()) {
+            void* p = it->second.back();
+            it->second.pop_back();
+            g_pin_cached -= bytes;
+            g_pin_live[p] = bytes;
+            return p;
+        }
+    }
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_live[p] = bytes;
+    return p;
+}
+
+void host_free(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    auto it = g_pin_live.find(p);
+    if (it == g_pin_live.end()) return;
+    const size_t bytes = it->second;
+    g_pin_live.erase(it);
+    if (g_pin_cached + bytes <= kPinCacheLimit) {
+        g_pin_free[bytes].push_back(p);
+        g_pin_cached += bytes;
+    } else {
+        cudaFreeHost(p);
+    }
+}
 
 int validate_config(const ezq_config* c, std::string* msg) {
     if (c->bits < 2 || c->bits > 8) {

@@ -27,6 +27,7 @@ int cuda_error(cudaError_t e, const char* where);
 // Binds the calling thread's device; EZQ_ERR_NO_DEVICE when none exists.
 int bind_device(int* dev);
 cudaStream_t thread_stream(int dev);
+cudaStream_t copy_stream(int dev);  // per-thread second stream for H2D staging
 inline cudaStream_t pick_stream(void* user, int dev) {
     return user ? static_cast<cudaStream_t>(user) : thread_stream(dev);
 }
@@ -75,5 +76,12 @@ private:
 };
 
 std::string fmt_double(double v);  // std::to_string(double) formatting
+
+// Pinned host memory for library-owned host outputs: blocks are recycled by
+// exact size (repeat calls on the same shapes reuse them), so D2H copies run
+// at full PCIe rate and asynchronously. host_free() accepts only pointers
+// from host_alloc().
+void* host_alloc(size_t bytes);
+void host_free(void* p);
 
 }  // namespace ezq

@@ -119,6 +119,22 @@ class QuantizedWeight:
     sigma_n: float = 0.0
     rtn_error: Optional[float] = None
     final_error: Optional[float] = None
+    _owner: object = field(default=None, repr=False, compare=False)
+
+
+class _COwner:
+    """Keeps a library-owned host ezq_qweight alive while numpy views of its
+    arrays exist (zero-copy results); frees it with ezq_qweight_free."""
+
+    def __init__(self, ptr):
+        self.ptr = ptr
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                lib().ezq_qweight_free(self.ptr)
+        except Exception:
+            pass
 
 
 _lib = None
@@ -281,16 +297,22 @@ def detect_outliers(W, cfg: Config, stream=None):
     return out, mean.value, std.value
 
 
-def _from_c(q: CQWeight) -> QuantizedWeight:
+def _from_c(q: CQWeight, owner=None) -> QuantizedWeight:
+    """Host artifact -> QuantizedWeight. With `owner` (a _COwner of the C
+    struct) the arrays are zero-copy views kept alive by the owner; without it
+    they are copied."""
     assert q.mem == MEM_HOST
-    packed = np.ctypeslib.as_array(q.packed, shape=(q.packed_bytes,)).copy() if q.packed_bytes else np.zeros(0, np.uint8)
-    scales = np.ctypeslib.as_array(q.scales, shape=(q.cols,)).copy()
-    outl = np.zeros(q.n_outliers, dtype=OUTLIER_DTYPE)
+    cp = (lambda a: a) if owner is not None else (lambda a: a.copy())
+    packed = cp(np.ctypeslib.as_array(q.packed, shape=(q.packed_bytes,))) if q.packed_bytes else np.zeros(0, np.uint8)
+    scales = cp(np.ctypeslib.as_array(q.scales, shape=(q.cols,)))
     if q.n_outliers:
-        C.memmove(outl.ctypes.data, q.outliers, q.n_outliers * 12)
+        raw = np.ctypeslib.as_array(C.cast(q.outliers, C.POINTER(C.c_uint8)), shape=(q.n_outliers * 12,))
+        outl = cp(raw.view(OUTLIER_DTYPE))
+    else:
+        outl = np.zeros(0, dtype=OUTLIER_DTYPE)
     return QuantizedWeight(q.rows, q.cols, q.bits, packed, scales, outl, q.mean, q.stddev,
                            q.sigma_n, q.rtn_error if q.has_errors else None,
-                           q.final_error if q.has_errors else None)
+                           q.final_error if q.has_errors else None, owner)
 
 
 def quantize_tensor(W, cfg: Config, mode: str = "easyquant", stream=None) -> QuantizedWeight:
@@ -358,11 +380,7 @@ def quantize_batch(Ws: Sequence, cfg: Config, mode: str = "easyquant", out_mem: 
                                    out_mem, _stream(stream, Ws[0]), outs, C.byref(failed)))
     if out_mem == MEM_DEVICE:
         return DeviceBatch(list(outs))
-    res = []
-    for p in outs:
-        res.append(_from_c(p.contents))
-        lib().ezq_qweight_free(p)
-    return res
+    return [_from_c(p.contents, _COwner(p)) for p in outs]
 
 
 class GemvPlan:
