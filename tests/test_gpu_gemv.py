@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
     (300, 77, 3.0, 4),      # generic path (odd cols)
     (256, 128, 3.0, 3),     # k=3 byte-per-level codes
 ])
-@pytest.mark.parametrize("batch", [1, 2, 5, 8, 16])
+@pytest.mark.parametrize("batch", [1, 2, 5, 8, 16, 21])
 @pytest.mark.parametrize("dtype", ["float32", "bfloat16", "float16"])
 def test_gemv_matches_dequant_f64(gpu, O, rows, cols, sigma, bits, batch, dtype):
     import torch
@@ -50,3 +50,25 @@ def test_gemv_outlier_term_exact_path(gpu, O):
     ref = O.gemv_f64(gpu.dequantize(b.to_host(0)), x.cpu().numpy())[0]
     assert np.allclose(y, ref, rtol=1e-6, atol=1e-4)
     assert y[5] == pytest.approx(3 * 50.0 - 40 * 20.0, rel=1e-6)
+
+
+@pytest.mark.parametrize("rows,cols", [(1000, 200), (8192, 48), (64, 4096), (130, 17)])
+@pytest.mark.parametrize("batch", [1, 9, 40])
+def test_gemv_split_and_ragged(gpu, O, rows, cols, batch):
+    """Split-K tiles (few columns, many rows), ragged K (rows % 64 != 0),
+    partial 16-column tiles and multi-group batches; repeated calls reuse the
+    workspace/tickets and must give bit-identical results (fixed-order
+    reduction)."""
+    import torch
+    W = O.gaussian(rows, cols, rows ^ cols, 0.02)
+    O.plant_outliers(W, max(1, W.size // 100), 0.2, 1.0, 6)
+    b = gpu.quantize_batch([torch.from_numpy(W).cuda()], Config(steps=10), out_mem=gpu.MEM_DEVICE)
+    plan = gpu.GemvPlan(b, 0)
+    x = torch.randn(batch, rows, generator=torch.Generator(device="cuda").manual_seed(3), device="cuda")
+    y = plan(x).cpu().numpy()
+    yref = O.gemv_f64(gpu.dequantize(b.to_host(0)), x.cpu().numpy())
+    assert np.abs(y.astype(np.float64) - yref).max() <= 1e-3 * np.abs(yref).max()
+    for _ in range(3):
+        assert np.array_equal(plan(x).cpu().numpy().view(np.uint32), y.view(np.uint32))
+    plan.close()
+    b.close()
