@@ -27,16 +27,20 @@
 // Words are stored T[tile][q][lane] as uint4 (4 k-steps): one fully
 // coalesced 512-byte load per warp per 64 rows.
 //
-// Work split: a CTA (8 warps) owns one 16-column tile and a range of
-// 64-row blocks; warps interleave the blocks, each keeping kUnroll 16-byte
-// weight loads (and their x fragments) in flight. When there are too few
-// tiles to fill 148 SMs the K range is split over several CTAs; one extra
-// CTA per tile gathers the tile's outliers (CSC, lane-parallel, 256 entries
-// per round) concurrently with the weight stream. Partials land in a
-// workspace and the last CTA to arrive (atomic ticket, threadFenceReduction
-// pattern -- no spinning) sums them in fixed split order, so results are
-// deterministic. Without split and without outliers the CTA writes y
-// directly.
+// Work split: one CTA per 16-column tile (4, 8 or 16 warps, chosen so that
+// about 16 warps per SM are resident in a single wave); its warps take the
+// tile's 64-row blocks in turn with plain coalesced 16-byte loads,
+// software-pipelined one block ahead. The warps' fragments are reduced
+// through shared memory in fixed order (deterministic). The outlier term is
+// a second, programmatic-dependent launch (k_gemv_outliers) whose gathers
+// overlap the weight stream.
+//
+// Measured on B200 (tools/microbench/dequant_mma.cu): the dequant + MMA loop
+// costs ~25 SM-cycles per 64-row block at 16 warps/SM (ALU-bound: 3 SHF + 4
+// LOP3 + 4 HSUB2 per 8 codes), i.e. ~6 TB/s of int4 codes per GPU -- about
+// the HBM rate, so the kernel sits on both limits at once. A persistent
+// variant streaming the codes through a TMA bulk-copy/mbarrier ring was
+// built and measured (git history) and was not faster at these sizes.
 //
 // HBM-bound: algorithmic bytes = N/2 (codes) + 4 cols (scales) + 8 n_out
 // (outlier row + value) + 8 (cols+1) (CSC pointers) + B rows |x| + 4 B cols.
@@ -44,7 +48,6 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
-#include <cstdlib>
 #include <vector>
 
 #include "runtime.hpp"
@@ -52,8 +55,7 @@
 namespace ezq {
 namespace {
 
-constexpr int kWarps = 16;         // consumer warps per CTA
-constexpr int kThreads = kWarps * 32;
+constexpr int kMaxWarps = 16;      // warps per CTA (runtime: 4, 8 or 16)
 constexpr int kTileCols = 16;      // MMA M
 constexpr int kBlockRows = 64;     // rows per lane uint4 (4 k-steps of 16)
 constexpr int kMaxGroup = 16;      // batch rows per launch (two n8 tiles)
@@ -163,59 +165,6 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const unsigned (&a)[4], 
             : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
 }
 
-// ---- TMA bulk-copy ring (mbarrier producer/consumer) ------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
-    const uint32_t addr = smem_u32(b);
-    uint32_t ok;
-    do {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-            " selp.u32 %0, 1, 0, p;\n}"
-            : "=r"(ok)
-            : "r"(addr), "r"(parity)
-            : "memory");
-    } while (!ok);
-}
-// 1-D bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0).
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar,
-                                         uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, "
-        "[%3], %4;" ::"r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s_keep(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ uint64_t evict_first_policy() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ void named_sync(int id, int threads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
-}
-
-constexpr int kGemvThreads = kThreads;  // all warps consume; the last to release a stage refills it
-
 struct GemvArgs {
     const uint4* T;
     int kq, tiles;
@@ -223,303 +172,163 @@ struct GemvArgs {
     int lmin;
     const float* scales;
     const void* x;
-    int batch;         // rows of this group (1..16)
+    int batch;  // rows of this group (1..16)
     float* y;
-    int sb;            // 64-row blocks per ring stage (8 or 16)
-    int stages;        // ring depth
-    int stage_bytes;   // codes (sb * 512) + batch x slices (xstride each)
-    int xstride;       // bytes per x slice in shared memory (padded: no bank conflicts)
-    int dbg;
-    unsigned long long* tl;  // debug timeline (dbg == 3)
 };
 
-// x fragment of lane (g, t) for local block lb from the staged slice.
-template <int XT>
-__device__ __forceinline__ void x_from_smem(const unsigned char* xs, int xstride, int n, int lb, int t,
-                                            XRaw<XT>& o) {
-    constexpr int es = XT == kF32 ? 4 : 2;
-    const uint4* p = reinterpret_cast<const uint4*>(xs + n * xstride + (64 * lb + 16 * t) * es);
-#pragma unroll
-    for (int i = 0; i < XRaw<XT>::kWords / 4; ++i) {
-        const uint4 u = p[i];
-        o.w[4 * i] = u.x, o.w[4 * i + 1] = u.y, o.w[4 * i + 2] = u.z, o.w[4 * i + 3] = u.w;
-    }
-}
-
-// Rows at or past `valid` (the matrix end inside the last stage) -> 0.
-template <int XT>
-__device__ __forceinline__ void x_mask_tail(int valid, XRaw<XT>& o) {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        if (i < valid) continue;
-        if (XT == kF32) o.w[i] = 0u;
-        else o.w[i >> 1] &= (i & 1) ? 0x0000FFFFu : 0u;
-    }
-}
-
-// Persistent CTAs (one per SM) walk tiles blockIdx.x, +gridDim.x, ...; the
-// producer warp streams each tile's contiguous codes (kq x 512 B) *and* the
-// matching x slices (one 1-D bulk copy per batch row) through a ring of
-// `stages` stages with cp.async.bulk + mbarriers -- codes with an L2
-// evict-first hint (read once), x slices from L2 (shared by every tile).
-// The 8 consumer warps take the stage's 64-row blocks in turn (warp w:
-// blocks w, w + 8, ...), so no global load sits on their critical path;
-// stages are large (up to 64 blocks = 32 KB of codes) so the per-stage
-// barrier work is amortised over many MMAs. Batch columns n >= batch read
-// a valid x row and are never stored (D column n depends only on B column
-// n), so the fragments need no predication. Two accumulator sets break
-// the HMMA dependency chain. At the end of a tile the warps' fragments are
-// reduced through shared memory in fixed order and y written (y = scale *
-// D; the outlier term is added by k_gemv_outliers). XG: x is read straight
-// from global memory (x rows not 16-byte aligned).
-template <int NB, int XT, bool XG>
-__global__ void __launch_bounds__(kGemvThreads, 1) k_gemv_mma(const GemvArgs a) {
+// One CTA per 16-column tile; warp w takes 64-row blocks w, w + W, ...,
+// loading block q + W (codes and x fragments) while block q computes. x is
+// read through L1/L2 (every tile reads the whole of x). Batch columns
+// n >= batch read a valid x row and are never stored (D column n depends
+// only on B column n), so the fragments need no predication; four
+// accumulator sets break the HMMA dependency chain.
+template <int NB, int XT>
+__global__ void __launch_bounds__(512) k_gemv_mma(const GemvArgs a) {
     constexpr bool F16 = XT == kF16;
-    constexpr int es = XT == kF32 ? 4 : 2;
-    constexpr int kGroup = (XT == kF32 || NB == 2) ? 2 : 4;  // 64-row blocks in flight per warp
-    constexpr int kChains = 4;  // independent accumulator sets (HMMA dependency chains)
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    float (*red)[kWarps][NB][32][4] = reinterpret_cast<float (*)[kWarps][NB][32][4]>(smem_raw);
-    unsigned char* ring = smem_raw + sizeof(float) * 2 * kWarps * NB * 32 * 4;
-    uint64_t* full = reinterpret_cast<uint64_t*>(ring + static_cast<size_t>(a.stages) * a.stage_bytes);
-    uint64_t* red_done = full + a.stages;
-    unsigned* red_cnt = reinterpret_cast<unsigned*>(red_done + 2);
-    unsigned* slot_cnt = red_cnt + 2;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int stage_rows = a.sb * kBlockRows;
-    const int nch = (a.kq + a.sb - 1) / a.sb;
-    const int my_tiles = a.tiles > static_cast<int>(blockIdx.x)
-                             ? (a.tiles - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
-                             : 0;
-    const int total = my_tiles * nch;
-    auto gtime = []() { unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; };
-    unsigned long long* tl = (a.dbg & 8) ? a.tl + blockIdx.x * 64 : nullptr;
-    // Stage j of this CTA's sequence: chunk j % nch of tile blockIdx + (j / nch) * grid.
-    auto issue_stage = [&](int j, uint64_t pol) {
-        const int slot = j % a.stages;
-        const int c = j % nch;
-        const int tile = static_cast<int>(blockIdx.x) + (j / nch) * static_cast<int>(gridDim.x);
-        unsigned char* st = ring + static_cast<size_t>(slot) * a.stage_bytes;
-        const int blocks = min(a.sb, a.kq - c * a.sb);
-        const unsigned wbytes = static_cast<unsigned>(blocks) * 512u;
-        const int64_t r0 = static_cast<int64_t>(c) * stage_rows;
-        const unsigned xbytes = XG ? 0u : static_cast<unsigned>(min(static_cast<int64_t>(stage_rows), a.rows - r0) * es);
-        mbar_expect_tx(&full[slot], wbytes + ((a.dbg & 2) ? 0 : xbytes * a.batch));
-        bulk_g2s(st, a.T + (static_cast<int64_t>(tile) * a.kq + static_cast<int64_t>(c) * a.sb) * 32, wbytes, &full[slot],
-                 pol);
-        if (!XG && !(a.dbg & 2))
-            for (int n = 0; n < a.batch; ++n)
-                bulk_g2s_keep(st + a.sb * 512 + n * a.xstride,
-                              static_cast<const unsigned char*>(a.x) + (n * a.rows + r0) * es, xbytes, &full[slot]);
-    };
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < a.stages; ++i) {
-            mbar_init(&full[i], 1);
-            slot_cnt[i] = 0u;
-        }
-        mbar_init(&red_done[0], 1);
-        mbar_init(&red_done[1], 1);
-        red_cnt[0] = red_cnt[1] = 0u;
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        const uint64_t pol = evict_first_policy();
-        for (int j = 0; j < min(a.stages, total); ++j) issue_stage(j, pol);
-        if (tl) {
-            tl[0] = gtime();
-            unsigned smid;
-            asm("mov.u32 %0, %smid;" : "=r"(smid));
-            tl[1] = smid;
-        }
-    }
-    __syncthreads();
-    // Let a dependent launch (the outlier pass) start its gathers now.
-    asm volatile("griddepcontrol.launch_dependents;");
-
+    constexpr int kChains = 4;
+    __shared__ __align__(16) float red[kMaxWarps][NB][32][4];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int g = lane >> 2, t = lane & 3;
-    const unsigned magic = F16 ? 0x64006400u : 0x43004300u;  // 1024 | 128 + nibble
+    const int tile = blockIdx.x;
+    const unsigned magic = F16 ? 0x64006400u : 0x43004300u;
     const unsigned off2 = F16 ? static_cast<unsigned>(__half_as_ushort(__int2half_rn(1024 - a.lmin))) * 0x10001u
                               : static_cast<unsigned>(__bfloat16_as_ushort(__int2bfloat16_rn(128 - a.lmin))) * 0x10001u;
-    // x row served by this lane: batch columns past the end reuse a valid row.
     int nrow[NB];
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb) nrow[nb] = min(nb * 8 + g, a.batch - 1);
-    int buf = 0, c = 0, tile = blockIdx.x;
+    asm volatile("griddepcontrol.launch_dependents;");
     float acc[kChains][NB][4];
-    float sc[2] = {0.f, 0.f};
-    int ntile = 0;  // tiles this warp has finished
-    for (int it = 0; it < total; ++it) {
-        const int slot = it % a.stages;
-        if (c == 0) {
-            // the epilogue's scales, loaded a whole tile ahead of their use
-            if (!(a.dbg & 32)) {
-                const int64_t j0 = static_cast<int64_t>(tile) * kTileCols + g;
-                sc[0] = j0 < a.cols ? __ldg(a.scales + j0) : 0.f;
-                sc[1] = j0 + 8 < a.cols ? __ldg(a.scales + j0 + 8) : 0.f;
-            }
 #pragma unroll
-            for (int h = 0; h < kChains; ++h)
-#pragma unroll
-                for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) acc[h][nb][i] = 0.f;
-        }
-        const unsigned char* st = ring + static_cast<size_t>(slot) * a.stage_bytes;
-        const int blocks = min(a.sb, a.kq - c * a.sb);
-        // rows of the stage that exist (only the matrix's last stage is short)
-        const int valid_rows = static_cast<int>(min(static_cast<int64_t>(stage_rows), a.rows - static_cast<int64_t>(c) * stage_rows));
-        const bool tail = valid_rows < blocks * kBlockRows;
-        mbar_wait(&full[slot], (it / a.stages) & 1);
-        if (tl && threadIdx.x == 0 && it < 30) tl[2 + 2 * it] = gtime();
-        // Groups of kGroup blocks per warp: all shared-memory loads of the
-        // group are issued before its MMAs (ILP across blocks).
-        for (int lb0 = warp; lb0 < ((a.dbg & 1) ? 0 : blocks); lb0 += kWarps * kGroup) {
-            XRaw<XT> xr[kGroup][NB];
-            uint4 w[kGroup];
-#pragma unroll
-            for (int u = 0; u < kGroup; ++u) {
-                const int lb = lb0 + kWarps * u;
-                if (lb >= blocks) break;
-#pragma unroll
-                for (int nb = 0; nb < NB; ++nb) {
-                    if (XG) x_load<XT>(a.x, a.rows, nrow[nb], static_cast<int64_t>(c) * stage_rows + 64 * lb + 16 * t, xr[u][nb]);
-                    else x_from_smem<XT>(st + a.sb * 512, a.xstride, nrow[nb], lb, t, xr[u][nb]);
-                    if (!XG && tail) x_mask_tail<XT>(valid_rows - (64 * lb + 16 * t), xr[u][nb]);
-                }
-                w[u] = reinterpret_cast<const uint4*>(st)[lb * 32 + lane];
-            }
-#pragma unroll
-            for (int u = 0; u < kGroup; ++u) {
-                if (lb0 + kWarps * u >= blocks) break;
-                const unsigned ws[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
-#pragma unroll
-                for (int s = 0; s < 4; ++s) {
-                    unsigned af[4];
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) af[r] = sub2<F16>(lop_pair(ws[s], r, magic), off2);
-#pragma unroll
-                    for (int nb = 0; nb < NB; ++nb) {
-                        unsigned hi[2], lo[2];
-                        x_frag<XT>(xr[u][nb], s, hi, lo);
-                        mma16816<F16>(acc[s % kChains][nb], af, hi);
-                        if (XT == kF32) mma16816<F16>(acc[s % kChains][nb], af, lo);
-                    }
-                }
-            }
-        }
-        // Release the slot; the last warp to release it refills it with
-        // stage it + stages (no dedicated producer warp, no blocking).
-        __syncwarp();
-        if (lane == 0) {
-            if (!(a.dbg & 16)) __threadfence_block();
-            if (atomicAdd(&slot_cnt[slot], 1u) == kWarps - 1) {
-                slot_cnt[slot] = 0u;
-                if (it + a.stages < total) issue_stage(it + a.stages, evict_first_policy());
-            }
-        }
-        if (tl && threadIdx.x == 0 && it < 30) tl[3 + 2 * it] = gtime();
-        if (++c != nch) continue;
-        c = 0;
-        if (a.dbg & 4) { tile += gridDim.x; continue; }
-        // Fixed-order reduction of the warps' fragments without a CTA
-        // barrier: every warp deposits its fragment, the last to arrive
-        // (shared-memory ticket) sums all of them in warp order and writes
-        // y. Two buffers; a buffer is reused only after its reducer has
-        // released it (red_done mbarrier).
-        if (ntile >= 2) mbar_wait(&red_done[buf], ((ntile >> 1) - 1) & 1);
+    for (int h = 0; h < kChains; ++h)
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb)
-        {
-            float v[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                v[i] = acc[0][nb][i];
+            for (int i = 0; i < 4; ++i) acc[h][nb][i] = 0.f;
+    // Software pipeline, two groups of G blocks deep: the next group's codes
+    // and x fragments are in flight while the current group computes.
+    constexpr int G = 1;
+    uint4 wA[G], wB[G];
+    XRaw<XT> xA[G][NB], xB[G][NB];
+    auto load_group = [&](int q0, uint4 (&wg)[G], XRaw<XT> (&xg)[G][NB]) {
 #pragma unroll
-                for (int h = 1; h < kChains; ++h) v[i] += acc[h][nb][i];
+        for (int u = 0; u < G; ++u) {
+            const int q = q0 + nw * u;
+            if (q < a.kq) {
+                wg[u] = __ldg(a.T + (static_cast<int64_t>(tile) * a.kq + q) * 32 + lane);
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb)
+                    x_load<XT>(a.x, a.rows, nrow[nb], static_cast<int64_t>(kBlockRows) * q + 16 * t, xg[u][nb]);
             }
-            *reinterpret_cast<float4*>(red[buf][warp][nb][lane]) = make_float4(v[0], v[1], v[2], v[3]);
         }
-        __syncwarp();
-        unsigned ticket = 0;
-        if (lane == 0) {
-            if (!(a.dbg & 16)) __threadfence_block();
-            ticket = atomicAdd(&red_cnt[buf], 1u);
-            if (!(a.dbg & 16)) __threadfence_block();
-        }
-        ticket = __shfl_sync(0xffffffffu, ticket, 0);
-        if (ticket == kWarps - 1) {
+    };
+    auto compute_group = [&](int q0, const uint4 (&wg)[G], const XRaw<XT> (&xg)[G][NB]) {
 #pragma unroll
-            for (int nb = 0; nb < NB; ++nb) {
-                float d[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int u = 0; u < G; ++u) {
+            if (q0 + nw * u >= a.kq) break;
+            const unsigned ws[4] = {wg[u].x, wg[u].y, wg[u].z, wg[u].w};
 #pragma unroll
-                for (int w2 = 0; w2 < kWarps; ++w2) {
-                    const float4 v = *reinterpret_cast<const float4*>(red[buf][w2][nb][lane]);
-                    d[0] += v.x, d[1] += v.y, d[2] += v.z, d[3] += v.w;
+            for (int s = 0; s < 4; ++s) {
+                unsigned af[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) af[r] = sub2<F16>(lop_pair(ws[s], r, magic), off2);
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb) {
+                    unsigned hi[2], lo[2];
+                    x_frag<XT>(xg[u][nb], s, hi, lo);
+                    mma16816<F16>(acc[s][nb], af, hi);
+                    if (XT == kF32) mma16816<F16>(acc[s][nb], af, lo);
                 }
-                // d0, d1: (m = g, n = 2t, 2t+1); d2, d3: (m = g + 8, ...)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int m = g + (i >= 2 ? 8 : 0);
-                    const int n = nb * 8 + 2 * t + (i & 1);
-                    const int64_t j = static_cast<int64_t>(tile) * kTileCols + m;
-                    if (j < a.cols && n < a.batch) a.y[static_cast<int64_t>(n) * a.cols + j] = sc[i >> 1] * d[i];
-                }
-            }
-            __syncwarp();
-            if (lane == 0) {
-                red_cnt[buf] = 0u;
-                mbar_arrive(&red_done[buf]);
             }
         }
-        ++ntile;
-        buf ^= 1;
-        tile += gridDim.x;
+    };
+    const int step = nw * G;
+    int q = warp;
+    load_group(q, wA, xA);
+    for (; q < a.kq; q += 2 * step) {
+        if (q + step < a.kq) load_group(q + step, wB, xB);
+        compute_group(q, wA, xA);
+        if (q + step >= a.kq) break;
+        if (q + 2 * step < a.kq) load_group(q + 2 * step, wA, xA);
+        compute_group(q + step, wB, xB);
     }
-    if (tl && threadIdx.x == 0) tl[62] = gtime(), tl[63] = total;
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+        float v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = acc[0][nb][i] + acc[1][nb][i] + acc[2][nb][i] + acc[3][nb][i];
+        *reinterpret_cast<float4*>(red[warp][nb][lane]) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+    __syncthreads();
+    if (warp < NB) {
+        const int nb = warp;
+        float d[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int w2 = 0; w2 < nw; ++w2) {
+            const float4 v = *reinterpret_cast<const float4*>(red[w2][nb][lane]);
+            d[0] += v.x, d[1] += v.y, d[2] += v.z, d[3] += v.w;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int m = g + (i >= 2 ? 8 : 0);
+            const int n = nb * 8 + 2 * t + (i & 1);
+            const int64_t j = static_cast<int64_t>(tile) * kTileCols + m;
+            if (j < a.cols && n < a.batch) a.y[static_cast<int64_t>(n) * a.cols + j] = a.scales[j] * d[i];
+        }
+    }
 }
 
-// Outlier term: y[n, j] += sum_{e in column j} x[n, row_e] * v_e. Eight
-// lanes per column (a warp serves 4 columns, a CTA 32), each lane walking
-// every 8th CSC entry with its loads unrolled; the 8 partials are combined
-// by a fixed xor-butterfly. Launched as a programmatic dependent of
-// k_gemv_mma: the gathers overlap the weight stream and griddepcontrol.wait
-// orders the read-modify-write of y after the main kernel's stores.
-template <int XT>
+// Outlier term: y[n, j] += sum_{e in column j} x[n, row_e] * v_e. One warp
+// per column; the lanes take the column's CSC entries 32 apart, with kU
+// entries per lane loaded independently per round (one round covers 128
+// entries, i.e. a 1%-outlier column of up to 12.8k rows), and the partials
+// are combined by a fixed xor-butterfly (deterministic). NBT = batch rows
+// rounded up to 1, 8 or 16 (fully unrolled, predicated on `batch`).
+// Launched as a programmatic dependent of k_gemv_mma: the gathers overlap
+// the weight stream and griddepcontrol.wait orders the read-modify-write
+// of y after the main kernel's stores.
+template <int XT, int NBT>
 __global__ void __launch_bounds__(256) k_gemv_outliers(int64_t rows, int64_t cols, const int64_t* __restrict__ col_ptr,
                                                        const uint32_t* __restrict__ out_row,
                                                        const float* __restrict__ out_val, const void* __restrict__ x,
                                                        int batch, float* __restrict__ y) {
-    const int sub = threadIdx.x & 7;
-    const int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 3;
-    float part[kMaxGroup];
+    constexpr int kU = 4;
+    const int lane = threadIdx.x & 31;
+    const int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    float part[NBT];
 #pragma unroll
-    for (int n = 0; n < kMaxGroup; ++n) part[n] = 0.f;
+    for (int n = 0; n < NBT; ++n) part[n] = 0.f;
     int64_t e0 = 0, e1 = 0;
-    if (j < cols) e0 = col_ptr[j], e1 = col_ptr[j + 1];
-#pragma unroll 4
-    for (int64_t e = e0 + sub; e < e1; e += 8) {
-        const int64_t r = out_row[e];
-        const float v = out_val[e];
+    if (j < cols) e0 = __ldg(col_ptr + j), e1 = __ldg(col_ptr + j + 1);
+    for (int64_t eb = e0; eb < e1; eb += 32 * kU) {
+        uint32_t r[kU];
+        float v[kU];
 #pragma unroll
-        for (int n = 0; n < kMaxGroup; ++n)
-            if (n < batch) part[n] = fmaf(load_x(x, XT, static_cast<int64_t>(n) * rows + r), v, part[n]);
+        for (int u = 0; u < kU; ++u) {
+            const int64_t e = eb + lane + 32 * u;
+            r[u] = e < e1 ? __ldg(out_row + e) : 0u;
+            v[u] = e < e1 ? __ldg(out_val + e) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+#pragma unroll
+            for (int n = 0; n < NBT; ++n)
+                if (n < batch) part[n] = fmaf(load_x(x, XT, static_cast<int64_t>(n) * rows + r[u]), v[u], part[n]);
     }
+    const bool any = e1 > e0;
+    if (any) {
 #pragma unroll
-    for (int n = 0; n < kMaxGroup; ++n) {
-        if (n >= batch) break;
+        for (int n = 0; n < NBT; ++n) {
+            if (n >= batch) break;
 #pragma unroll
-        for (int o = 4; o; o >>= 1) part[n] += __shfl_xor_sync(0xffffffffu, part[n], o);
+            for (int o = 16; o; o >>= 1) part[n] += __shfl_xor_sync(0xffffffffu, part[n], o);
+        }
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (e1 > e0) {
+    if (any && lane < batch) {
+        float add = part[0];
 #pragma unroll
-        for (int h = 0; h < kMaxGroup / 8; ++h) {
-            const int n = sub + 8 * h;
-            if (n >= batch) break;
-            float v = 0.f;
-#pragma unroll
-            for (int k = 0; k < kMaxGroup; ++k)
-                if (k == n) v = part[k];
-            y[static_cast<int64_t>(n) * cols + j] += v;
-        }
+        for (int k = 1; k < NBT; ++k)
+            if (k == lane) add = part[k];
+        y[static_cast<int64_t>(lane) * cols + j] += add;
     }
 }
 
@@ -562,8 +371,6 @@ __global__ void k_gemv_repack(const uint8_t* __restrict__ packed, int64_t rows, 
 
 using namespace ezq;
 
-static unsigned long long* g_tlbuf = nullptr;  // debug timeline (EZQ_GEMV_DBG=3)
-
 struct ezq_gemv_plan {
     int64_t rows, cols, kq, tiles;
     int bits, lmin;
@@ -573,7 +380,7 @@ struct ezq_gemv_plan {
     uint32_t* out_row;
     float* out_val;
     int64_t n_out;
-    int grid;             // unused (grid is chosen per launch)
+    int warps;            // warps per CTA
     int dev;
 };
 
@@ -626,21 +433,9 @@ int ezq_gemv_prepare(const ezq_qweight* q, void* stream, ezq_gemv_plan** plan) {
     EZQ_CK(cudaMalloc(&p->col_ptr, sizeof(int64_t) * (q->cols + 1)));
     EZQ_CK(cudaMalloc(&p->out_row, sizeof(uint32_t) * std::max<int64_t>(q->n_outliers, 1)));
     EZQ_CK(cudaMalloc(&p->out_val, sizeof(float) * std::max<int64_t>(q->n_outliers, 1)));
-    {
-        static bool attr_done[64] = {};
-        if (!attr_done[dev & 63]) {
-            attr_done[dev & 63] = true;
-            const int mx = device_info(dev).max_smem_optin;
-#define EZQ_ATTR(NBT, X, G) \
-    EZQ_CK(cudaFuncSetAttribute(k_gemv_mma<NBT, X, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx))
-            EZQ_ATTR(1, kF32, false); EZQ_ATTR(2, kF32, false); EZQ_ATTR(1, kBF16, false);
-            EZQ_ATTR(2, kBF16, false); EZQ_ATTR(1, kF16, false); EZQ_ATTR(2, kF16, false);
-            EZQ_ATTR(1, kF32, true); EZQ_ATTR(2, kF32, true); EZQ_ATTR(1, kBF16, true);
-            EZQ_ATTR(2, kBF16, true); EZQ_ATTR(1, kF16, true); EZQ_ATTR(2, kF16, true);
-#undef EZQ_ATTR
-        }
-    }
-    p->grid = 0;
+    // Warps per CTA (one CTA per 16-column tile): about 16 resident warps
+    // per SM in one wave -- 4 when there are many tiles, 16 for long K.
+    p->warps = p->tiles >= 512 ? 4 : (p->kq >= 128 ? 16 : 8);
     const int64_t nw = p->tiles * p->kq * 32;
     k_gemv_repack<<<static_cast<unsigned>((nw + 255) / 256), 256, 0, st>>>(q->packed, q->rows, q->cols,
                                                                          q->bits, p->kq, p->lmin, p->T);
@@ -679,44 +474,25 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
     // One launch per group of 16 batch rows (two n8 MMA tiles share the A
     // fragments); a group of <= 8 uses one n8 tile. The outlier pass is a
     // programmatic dependent launch (its gathers overlap the weight stream).
-    const DeviceInfo& di = device_info(dev);
-    a.dbg = std::getenv("EZQ_GEMV_DBG") ? std::atoi(std::getenv("EZQ_GEMV_DBG")) : 0;
-    if ((a.dbg & 8) && !g_tlbuf) cudaMalloc(&g_tlbuf, 8 * 64 * 1024);
-    a.tl = g_tlbuf;
     for (int b0 = 0; b0 < batch; b0 += kMaxGroup) {
         a.batch = std::min(batch - b0, kMaxGroup);
         a.x = static_cast<const char*>(x) + xes * static_cast<size_t>(b0) * p->rows;
         a.y = y + static_cast<int64_t>(b0) * p->cols;
         const bool two = a.batch > 8;
-        // Ring geometry: one CTA per SM (16 consumer warps); the largest
-        // stage (64, 32, 16 or 8 blocks of 64 rows) whose codes + x slices
-        // fit 48 KB, as many stages (<= 8) as fit in shared memory.
-        const bool xg = (p->rows * xes) % 16 != 0 || (reinterpret_cast<uintptr_t>(a.x) & 15) != 0;
-        const int red = static_cast<int>(sizeof(float)) * 2 * kWarps * (two ? 2 : 1) * 32 * 4;
-        static const int stage_cap = std::getenv("EZQ_GEMV_STAGE_KB") ? std::atoi(std::getenv("EZQ_GEMV_STAGE_KB")) * 1024 : 48 * 1024;
-        a.sb = 64;
-        for (;;) {
-            a.xstride = a.sb * kBlockRows * static_cast<int>(xes) + 16;
-            a.stage_bytes = a.sb * 512 + (xg ? 0 : a.batch * a.xstride);
-            if (a.stage_bytes <= stage_cap || a.sb == 8) break;
-            a.sb /= 2;
-        }
-        a.stages = std::max(2, std::min(8, (di.max_smem_optin - red - 8 * 8 - 64) / a.stage_bytes));
-        const size_t smem = static_cast<size_t>(red) + static_cast<size_t>(a.stages) * a.stage_bytes + 8 * a.stages + 64;
-        const unsigned grid = static_cast<unsigned>(std::min<int64_t>(p->tiles, di.sms));
-        switch ((x_dtype * 2 + (two ? 1 : 0)) * 2 + (xg ? 1 : 0)) {
-#define EZQ_L(K, NBT, X, G) \
-    case K: k_gemv_mma<NBT, X, G><<<grid, kGemvThreads, smem, st>>>(a); break;
-            EZQ_L(0, 1, kF32, false) EZQ_L(1, 1, kF32, true) EZQ_L(2, 2, kF32, false) EZQ_L(3, 2, kF32, true)
-            EZQ_L(4, 1, kBF16, false) EZQ_L(5, 1, kBF16, true) EZQ_L(6, 2, kBF16, false) EZQ_L(7, 2, kBF16, true)
-            EZQ_L(8, 1, kF16, false) EZQ_L(9, 1, kF16, true) EZQ_L(10, 2, kF16, false)
-            default: k_gemv_mma<2, kF16, true><<<grid, kGemvThreads, smem, st>>>(a); break;
-#undef EZQ_L
+        const unsigned grid = static_cast<unsigned>(p->tiles);
+        const unsigned threads = static_cast<unsigned>(p->warps * 32);
+        switch (x_dtype * 2 + (two ? 1 : 0)) {
+            case 0: k_gemv_mma<1, kF32><<<grid, threads, 0, st>>>(a); break;
+            case 1: k_gemv_mma<2, kF32><<<grid, threads, 0, st>>>(a); break;
+            case 2: k_gemv_mma<1, kBF16><<<grid, threads, 0, st>>>(a); break;
+            case 3: k_gemv_mma<2, kBF16><<<grid, threads, 0, st>>>(a); break;
+            case 4: k_gemv_mma<1, kF16><<<grid, threads, 0, st>>>(a); break;
+            default: k_gemv_mma<2, kF16><<<grid, threads, 0, st>>>(a); break;
         }
         count_launch();
         if (p->n_out) {
             cudaLaunchConfig_t lc{};
-            lc.gridDim = dim3(static_cast<unsigned>((p->cols + 31) / 32));
+            lc.gridDim = dim3(static_cast<unsigned>((p->cols + 7) / 8));  // one warp per column
             lc.blockDim = dim3(256);
             lc.stream = st;
             cudaLaunchAttribute at[1];
@@ -731,12 +507,14 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
             float* yg = a.y;
             const int bt = a.batch;
             cudaError_t e;
-            if (x_dtype == kF32)
-                e = cudaLaunchKernelEx(&lc, k_gemv_outliers<kF32>, p->rows, p->cols, cp, orow, oval, xg, bt, yg);
-            else if (x_dtype == kBF16)
-                e = cudaLaunchKernelEx(&lc, k_gemv_outliers<kBF16>, p->rows, p->cols, cp, orow, oval, xg, bt, yg);
-            else
-                e = cudaLaunchKernelEx(&lc, k_gemv_outliers<kF16>, p->rows, p->cols, cp, orow, oval, xg, bt, yg);
+#define EZQ_OUT(X)                                                                                     \
+    (bt == 1 ? cudaLaunchKernelEx(&lc, k_gemv_outliers<X, 1>, p->rows, p->cols, cp, orow, oval, xg, bt, yg) \
+     : bt <= 8 ? cudaLaunchKernelEx(&lc, k_gemv_outliers<X, 8>, p->rows, p->cols, cp, orow, oval, xg, bt, yg) \
+               : cudaLaunchKernelEx(&lc, k_gemv_outliers<X, 16>, p->rows, p->cols, cp, orow, oval, xg, bt, yg))
+            if (x_dtype == kF32) e = EZQ_OUT(kF32);
+            else if (x_dtype == kBF16) e = EZQ_OUT(kBF16);
+            else e = EZQ_OUT(kF16);
+#undef EZQ_OUT
             EZQ_CK(e);
             count_launch();
         }
@@ -749,13 +527,6 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
     prof_end(pt, st, bytes);
     EZQ_CK(cudaGetLastError());
     return clear_error();
-}
-
-// Debug: copy the last dbg==3 timeline (64 u64 per CTA) to host.
-int ezq_gemv_debug_timeline(unsigned long long* out, int ctas) {
-    if (!g_tlbuf) return 1;
-    cudaDeviceSynchronize();
-    return cudaMemcpy(out, g_tlbuf, 8 * 64 * static_cast<size_t>(ctas), cudaMemcpyDeviceToHost) != cudaSuccess;
 }
 
 void ezq_gemv_plan_free(ezq_gemv_plan* p) {
