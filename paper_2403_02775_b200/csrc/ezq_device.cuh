@@ -132,6 +132,56 @@ __device__ __forceinline__ bool is_outlier(float v, double mean, double thr) {
     return fabs(__dsub_rn(static_cast<double>(v), mean)) >= thr;
 }
 
+// The predicate is monotone in v: RN(double(v) - mean) is non-decreasing in
+// v, so the outlier set is {v <= olo} U {v >= ohi} for two float bounds,
+// found by stepping float neighbours around mean -/+ thr (a few steps).
+// Computed once per tensor; the per-element test is then two FSETPs.
+// Non-finite mean/thr (a non-finite tensor, reported as an error by the
+// host) yields the empty set; the stepping loops are bounded regardless.
+__device__ __forceinline__ float outlier_hi_bound(double mean, double thr) {
+    const float kInf = __int_as_float(0x7f800000);
+    if (!isfinite(mean) || !isfinite(thr)) return kInf;
+    auto pred = [&](float v) { return __dsub_rn(static_cast<double>(v), mean) >= thr; };
+    float c = __double2float_rn(__dadd_rn(mean, thr));
+    if (isinf(c)) c = c > 0.f ? 3.40282347e38f : -3.40282347e38f;
+    if (pred(c)) {
+        for (int i = 0; i < 64; ++i) {
+            const float p = nextafterf(c, -kInf);
+            if (!pred(p)) break;
+            c = p;
+        }
+        return c;
+    }
+    for (int i = 0; i < 64; ++i) {
+        if (c == 3.40282347e38f) return kInf;  // no finite float qualifies
+        c = nextafterf(c, kInf);
+        if (pred(c)) return c;
+    }
+    return c;  // unreachable for finite mean/thr
+}
+__device__ __forceinline__ float outlier_lo_bound(double mean, double thr) {
+    const float kInf = __int_as_float(0x7f800000);
+    if (!isfinite(mean) || !isfinite(thr)) return -kInf;
+    auto pred = [&](float v) { return __dsub_rn(static_cast<double>(v), mean) <= -thr; };
+    float c = __double2float_rn(__dsub_rn(mean, thr));
+    if (isinf(c)) c = c > 0.f ? 3.40282347e38f : -3.40282347e38f;
+    if (pred(c)) {
+        for (int i = 0; i < 64; ++i) {
+            const float nx = nextafterf(c, kInf);
+            if (!pred(nx)) break;
+            c = nx;
+        }
+        return c;
+    }
+    for (int i = 0; i < 64; ++i) {
+        if (c == -3.40282347e38f) return -kInf;
+        c = nextafterf(c, -kInf);
+        if (pred(c)) return c;
+    }
+    return c;  // unreachable for finite mean/thr
+}
+__device__ __forceinline__ bool is_outlier_f(float v, float olo, float ohi) { return v <= olo || v >= ohi; }
+
 // ---- exact sequential accumulation of one element (optimize.cpp:36-49) -----
 // err += d*d and grad += d*q with separate roundings (the reference is built
 // without FMA contraction); d = s*q - x is exact since s*q is.

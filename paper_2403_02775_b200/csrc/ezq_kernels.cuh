@@ -45,6 +45,9 @@ struct TStats {
     double final_error;
     int32_t scale_zero;            // a column scale rounded to 0.0f (error)
     int32_t pad;
+    // Exact float form of the outlier predicate (outliers.cpp:23):
+    // |double(v) - mean| >= thr  <=>  v <= olo || v >= ohi  (finite v).
+    float olo, ohi;
 };
 
 // One tensor of a batch (device pointers).
@@ -81,6 +84,7 @@ struct Scratch {
     double* err_rtn;  // reference-order error at s_rtn
     double* err_fin;  // reference-order error at s_fin
     double* inv;      // 1 / double(final float scale), for K4
+    float* invf;      // float(inv), K4's certified fp32 level
 };
 
 struct CfgDev {

@@ -41,8 +41,7 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const TDesc* __restrict__
     const int64_t e0 = ((g - d.pblk_base) * kPackThreads + threadIdx.x) * kPackPerThread;
     if (e0 >= d.n) return;
     const TStats* st = d.st;
-    const double mean = st->mean, thr = st->thr;
-    const int mask = st->mask;
+    const float olo = st->olo, ohi = st->ohi;
     const int64_t C = d.cols;
     int64_t col = e0 % C;
     const double dmin = cfg.lmin, dmax = cfg.lmax;
@@ -66,16 +65,33 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const TDesc* __restrict__
         for (int k = 0; k < kPackPerThread; ++k) x[k] = (k < cnt) ? d.W[e0 + k] : 0.f;
     }
 
+    // Per-column float 1/scale for the certified fp32 level (K3b wrote it);
+    // the 16 columns are contiguous unless the run wraps a row.
+    float invf[kPackPerThread];
+    const float* ivp = sc.invf + d.col_base;
+    if (col + kPackPerThread <= C && ((d.col_base + col) & 3) == 0) {
+#pragma unroll
+        for (int k = 0; k < kPackPerThread / 4; ++k) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(ivp + col) + k);
+            invf[4 * k] = v.x, invf[4 * k + 1] = v.y, invf[4 * k + 2] = v.z, invf[4 * k + 3] = v.w;
+        }
+    } else {
+        int64_t cc = col;
+#pragma unroll
+        for (int k = 0; k < kPackPerThread; ++k) {
+            invf[k] = __ldg(ivp + cc);
+            if (++cc == C) cc = 0;
+        }
+    }
     uint8_t off[kPackPerThread];
 #pragma unroll
     for (int k = 0; k < kPackPerThread; ++k) {
         int lvl = 0;
-        if (k < cnt && !(mask && is_outlier(x[k], mean, thr))) {
-            const double inv = sc.inv[d.col_base + col];
-            const FastLevel fl{__double2float_rn(inv), fmin, fmax};
+        if (k < cnt && !is_outlier_f(x[k], olo, ohi)) {
+            const FastLevel fl{invf[k], fmin, fmax};
             float rm = 0.f;
             float q = level_fast(x[k], fl, rm);
-            if (rm >= guard) q = static_cast<float>(level_exact(x[k], inv, dmin, dmax));
+            if (rm >= guard) q = static_cast<float>(level_exact(x[k], sc.inv[d.col_base + col], dmin, dmax));
             lvl = static_cast<int>(q);
         }
         off[k] = (k < cnt) ? static_cast<uint8_t>(lvl - cfg.lmin) : 0;

@@ -132,8 +132,7 @@ __global__ void __launch_bounds__(512, 1) k_qrange(const TDesc* __restrict__ td,
         const K3Group g = groups[gi];
         const TDesc& d = td[g.tensor];
         const TStats* st = d.st;
-        const double mean = st->mean, thr = st->thr;
-        const int mask = st->mask;
+        const float olo = st->olo, ohi = st->ohi;
         const int64_t R = d.rows, C = d.cols;
 
         __syncthreads();  // previous strip fully consumed
@@ -148,7 +147,7 @@ __global__ void __launch_bounds__(512, 1) k_qrange(const TDesc* __restrict__ td,
                 for (int k = 0; k < 4; ++k) {
                     if (r0 + k < R) {
                         const float x = src[k * C];
-                        v[k] = (mask && is_outlier(x, mean, thr)) ? 0.f : x;
+                        v[k] = is_outlier_f(x, olo, ohi) ? 0.f : x;
                     }
                 }
             }
@@ -296,61 +295,18 @@ __global__ void __launch_bounds__(512, 1) k_qrange(const TDesc* __restrict__ td,
 }
 
 // ---- K3b: reference-order errors (rtn_error / final_error per column) ----
-// One CTA = 32 adjacent columns of one tensor, lane = column; warp 0 sums
-// at the initial scale, warp 1 at the chosen scale. The CTA streams 64-row x 32-column tiles (row segments of 128 contiguous bytes)
-// through an 8-stage cp.async ring; each lane then walks its column in
-// ascending row order with the reference's separate roundings (eval_dense,
-// optimize.cpp:36-49), skipping isolated outliers exactly like
-// normal_mask_apply. Two chains per lane: initial scale and chosen scale.
-// The per-column finalisation (stored float scale, per-column invariant,
-// 1/scale for K4) follows in the same thread.
-constexpr int kBTile = 64;
-constexpr int kBStages = 8;
-constexpr size_t kBSmem = sizeof(float) * kBStages * kBTile * 32;
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
-    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
-                 "r"(src_bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_bytes) {
-    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem),
-                 "r"(src_bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
-
-// Tile `t` (rows [64t, 64t+64)) of columns [c0, c0+32) into buf[64][32];
-// the CTA's 64 threads split the 512 16-byte pieces (8 each).
-__device__ __forceinline__ void k3b_issue(float* buf, const float* W, int64_t R, int64_t C,
-                                          int64_t c0, int t, int tid, bool vec) {
-    const int ncol = static_cast<int>(min(static_cast<int64_t>(32), C - c0));
-    if (vec) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int idx = i * 64 + tid;
-            const int r = idx >> 3, part = idx & 7;
-            const int64_t row = static_cast<int64_t>(t) * kBTile + r;
-            int bytes = (ncol - part * 4) * 4;
-            bytes = bytes < 0 ? 0 : (bytes > 16 ? 16 : bytes);
-            if (row >= R) bytes = 0;
-            if (bytes > 0) cp_async16(buf + r * 32 + part * 4, W + row * C + c0 + part * 4, bytes);
-        }
-    } else {
-        const int lane = tid & 31, half = tid >> 5;
-#pragma unroll 4
-        for (int r = half; r < kBTile; r += 2) {
-            const int64_t row = static_cast<int64_t>(t) * kBTile + r;
-            if (row < R && lane < ncol) cp_async4(buf + r * 32 + lane, W + row * C + c0 + lane, 4);
-        }
-    }
-}
+// One warp = 32 adjacent columns of one tensor, lane = column. Each lane
+// walks its column in ascending row order with the reference's separate
+// roundings (eval_dense, optimize.cpp:36-49), skipping isolated outliers
+// exactly like normal_mask_apply, and carries both sums -- at the initial
+// scale and at the chosen one -- so the row load, the outlier test and the
+// x -> double conversion are shared. Rows are read straight from global
+// memory (a warp's 32 loads of a row are one 128-byte segment), kRowsK3b
+// rows in flight per lane; no shared memory, so occupancy is set by
+// registers. The per-column finalisation (stored float scale, per-column
+// invariant, 1/scale for K4) follows in the same lane.
+constexpr int kRowsK3b = 8;
+constexpr int kWarpsK3b = 4;
 
 // Squared residual of one normal element at scale s in reference semantics
 // (eval_dense, optimize.cpp:37-47): the level equals level_of's; d = s*q - x
@@ -368,78 +324,56 @@ __device__ __forceinline__ double seq_sq(float x, double xd, double s, float inv
     return __dmul_rn(d, d);
 }
 
-__global__ void __launch_bounds__(64) k_seq_errors(const TDesc* __restrict__ td,
-                                                   const int2* __restrict__ tiles, int ntiles,
-                                                   Scratch sc, CfgDev cfg) {
-    extern __shared__ __align__(16) float bsm[];
-    const int tid = threadIdx.x, lane = tid & 31, which = tid >> 5;  // 0: rtn, 1: final
-    const int2 tile = tiles[blockIdx.x];
+__global__ void __launch_bounds__(kWarpsK3b * 32) k_seq_errors(const TDesc* __restrict__ td,
+                                                              const int2* __restrict__ tiles, int ntiles,
+                                                              Scratch sc, CfgDev cfg) {
+    const int lane = threadIdx.x & 31;
+    const int ti = blockIdx.x * kWarpsK3b + (threadIdx.x >> 5);
+    if (ti >= ntiles) return;
+    const int2 tile = tiles[ti];
     const TDesc& d = td[tile.x];
     const int64_t c0 = tile.y, R = d.rows, C = d.cols;
     const int64_t c = c0 + lane;
-    const bool live = c < C;
-    const int64_t gc = d.col_base + (live ? c : c0);
-    const bool vec = ((reinterpret_cast<uintptr_t>(d.W) & 15) == 0) && (C % 4 == 0);
+    if (c >= C) return;
+    const int64_t gc = d.col_base + c;
     const TStats* st = d.st;
-    const double mean = st->mean, thr = st->thr;
-    const int mask = st->mask;
+    const float olo = st->olo, ohi = st->ohi;
     const double s_r = sc.s_rtn[gc], s_f = sc.s_fin[gc];
-    const bool skip = which == 1 && s_f == s_r;  // chosen == initial: reuse rtn
-    const double s = which ? s_f : s_r;
-    const double inv = __ddiv_rn(1.0, s);
-    const float invf = __double2float_rn(inv);
+    const bool both = s_f != s_r;  // chosen == initial: one sum serves both
+    const double inv_r = __ddiv_rn(1.0, s_r), inv_f = __ddiv_rn(1.0, s_f);
+    const float invf_r = __double2float_rn(inv_r), invf_f = __double2float_rn(inv_f);
     const float fmin = static_cast<float>(cfg.lmin), fmax = static_cast<float>(cfg.lmax);
     const double dmin = cfg.lmin, dmax = cfg.lmax;
     const float guard = cfg.guard;
-    const int ntl = static_cast<int>((R + kBTile - 1) / kBTile);
-    double err = 0.0;
+    const float* col = d.W + c;
+    double er = 0.0, ef = 0.0;
+    int64_t r = 0;
+    for (; r + kRowsK3b <= R; r += kRowsK3b) {
+        float x[kRowsK3b];
 #pragma unroll
-    for (int p = 0; p < kBStages - 1; ++p) {
-        if (p < ntl) k3b_issue(bsm + p * kBTile * 32, d.W, R, C, c0, p, tid, vec);
-        cp_async_commit();
-    }
-    for (int t = 0; t < ntl; ++t) {
-        const int nt = t + kBStages - 1;
-        if (nt < ntl) k3b_issue(bsm + (nt % kBStages) * kBTile * 32, d.W, R, C, c0, nt, tid, vec);
-        cp_async_commit();
-        cp_async_wait<kBStages - 1>();
-        __syncthreads();
-        const float* buf = bsm + (t % kBStages) * kBTile * 32;
-        const int nr =
-            static_cast<int>(min(static_cast<int64_t>(kBTile), R - static_cast<int64_t>(t) * kBTile));
-        if (live && !skip) {
-            int r = 0;
-            for (; r + 16 <= nr; r += 16) {
-                double term[16];
+        for (int j = 0; j < kRowsK3b; ++j) x[j] = __ldg(col + (r + j) * C);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const float x = buf[(r + j) * 32 + lane];
-                    const double xd = static_cast<double>(x);
-                    const double sq = seq_sq(x, xd, s, invf, inv, fmin, fmax, dmin, dmax, guard);
-                    // normal_mask_apply: an isolated outlier adds exactly +0
-                    term[j] = (mask && fabs(__dsub_rn(xd, mean)) >= thr) ? 0.0 : sq;
-                }
-#pragma unroll
-                for (int j = 0; j < 16; ++j) err = __dadd_rn(err, term[j]);
-            }
-            for (; r < nr; ++r) {
-                const float x = buf[r * 32 + lane];
-                const double xd = static_cast<double>(x);
-                const double sq = seq_sq(x, xd, s, invf, inv, fmin, fmax, dmin, dmax, guard);
-                err = __dadd_rn(err, (mask && fabs(__dsub_rn(xd, mean)) >= thr) ? 0.0 : sq);
+        for (int j = 0; j < kRowsK3b; ++j) {
+            // normal_mask_apply: an isolated outlier adds exactly +0
+            const bool out = is_outlier_f(x[j], olo, ohi);
+            const double xd = static_cast<double>(x[j]);
+            const double tr = seq_sq(x[j], xd, s_r, invf_r, inv_r, fmin, fmax, dmin, dmax, guard);
+            er = __dadd_rn(er, out ? 0.0 : tr);
+            if (both) {
+                const double tf = seq_sq(x[j], xd, s_f, invf_f, inv_f, fmin, fmax, dmin, dmax, guard);
+                ef = __dadd_rn(ef, out ? 0.0 : tf);
             }
         }
-        __syncthreads();
     }
-    cp_async_wait<0>();
-    __shared__ double fin_err[32];
-    if (which == 1) fin_err[lane] = err;
-    __syncthreads();
-    if (which == 1 || !live) return;
-    const double er = err;
-    double ef = fin_err[lane];
+    for (; r < R; ++r) {
+        const float x = __ldg(col + r * C);
+        const bool out = is_outlier_f(x, olo, ohi);
+        const double xd = static_cast<double>(x);
+        er = __dadd_rn(er, out ? 0.0 : seq_sq(x, xd, s_r, invf_r, inv_r, fmin, fmax, dmin, dmax, guard));
+        if (both) ef = __dadd_rn(ef, out ? 0.0 : seq_sq(x, xd, s_f, invf_f, inv_f, fmin, fmax, dmin, dmax, guard));
+    }
     double s_store = s_f;
-    if (s_f == s_r) {
+    if (!both) {
         ef = er;
     } else if (ef > er) {
         // tree/sequential near-tie: keep the initial scale so the per-column
@@ -450,7 +384,9 @@ __global__ void __launch_bounds__(64) k_seq_errors(const TDesc* __restrict__ td,
     const float scale = __double2float_rn(s_store);
     if (!(scale > 0.f)) d.st->scale_zero = 1;  // check_scale (rtn.cpp:19-22)
     d.scales[c] = scale;
-    sc.inv[gc] = scale > 0.f ? __ddiv_rn(1.0, static_cast<double>(scale)) : 1.0;
+    const double inv = scale > 0.f ? __ddiv_rn(1.0, static_cast<double>(scale)) : 1.0;
+    sc.inv[gc] = inv;
+    sc.invf[gc] = __double2float_rn(inv);
     sc.err_rtn[gc] = er;
     sc.err_fin[gc] = ef;
 }
@@ -581,12 +517,7 @@ void launch_k3(const K3Launch& kl, const TDesc* td, const K3Group* groups, int n
 void launch_seq_errors(const TDesc* td, const int2* tiles, int ntiles, Scratch sc, CfgDev cfg,
                        cudaStream_t st) {
     if (ntiles == 0) return;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_seq_errors, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBSmem);
-        attr = true;
-    }
-    k_seq_errors<<<ntiles, 64, kBSmem, st>>>(td, tiles, ntiles, sc, cfg);
+    k_seq_errors<<<(ntiles + kWarpsK3b - 1) / kWarpsK3b, kWarpsK3b * 32, 0, st>>>(td, tiles, ntiles, sc, cfg);
     count_launch();
 }
 

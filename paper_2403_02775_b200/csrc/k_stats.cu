@@ -253,6 +253,8 @@ __global__ void __launch_bounds__(256) k_stats_merge(const TDesc* __restrict__ t
         if (threadIdx.x == 0) {
             st->mask = 0;
             st->thr = __longlong_as_double(0x7ff0000000000000ll);
+            st->olo = -__int_as_float(0x7f800000);
+            st->ohi = __int_as_float(0x7f800000);
             st->n_out = 0;
         }
         return;
@@ -300,6 +302,8 @@ __global__ void __launch_bounds__(256) k_stats_merge(const TDesc* __restrict__ t
         st->mask = (mask_mode && st->stddev != 0.0) ? 1 : 0;
         st->thr = st->mask ? __dmul_rn(static_cast<double>(sigma_n), st->stddev)
                            : __longlong_as_double(0x7ff0000000000000ll);
+        st->olo = st->mask ? outlier_lo_bound(st->mean, st->thr) : -__int_as_float(0x7f800000);
+        st->ohi = st->mask ? outlier_hi_bound(st->mean, st->thr) : __int_as_float(0x7f800000);
         st->n_out = 0;
     } else {
         st->sum = sum;
@@ -412,13 +416,13 @@ __device__ __forceinline__ float4 load4(const float* W, int64_t n, int64_t f, bo
     return v;
 }
 
-__device__ __forceinline__ unsigned pred4(const float4& v, int64_t f, int64_t n, double mean,
-                                          double thr) {
+__device__ __forceinline__ unsigned pred4(const float4& v, int64_t f, int64_t n, float olo,
+                                          float ohi) {
     unsigned m = 0;
-    if (f < n && is_outlier(v.x, mean, thr)) m |= 1u;
-    if (f + 1 < n && is_outlier(v.y, mean, thr)) m |= 2u;
-    if (f + 2 < n && is_outlier(v.z, mean, thr)) m |= 4u;
-    if (f + 3 < n && is_outlier(v.w, mean, thr)) m |= 8u;
+    if (f < n && is_outlier_f(v.x, olo, ohi)) m |= 1u;
+    if (f + 1 < n && is_outlier_f(v.y, olo, ohi)) m |= 2u;
+    if (f + 2 < n && is_outlier_f(v.z, olo, ohi)) m |= 4u;
+    if (f + 3 < n && is_outlier_f(v.w, olo, ohi)) m |= 8u;
     return m;
 }
 
@@ -432,14 +436,14 @@ __global__ void __launch_bounds__(kDT) k_detect_count(const TDesc* __restrict__ 
     const TStats* st = d.st;
     int cnt = 0;
     if (st->mask) {
-        const double mean = st->mean, thr = st->thr;
+        const float olo = st->olo, ohi = st->ohi;
         const int64_t b0 = (g - d.dblk_base) * (int64_t)kDetectBlock;
         const bool al = (reinterpret_cast<uintptr_t>(d.W) & 15) == 0;
 #pragma unroll 4
         for (int r = 0; r < kDRounds; ++r) {
             const int64_t f = b0 + 4 * ((int64_t)r * kDT + threadIdx.x);
             if (f >= d.n) break;
-            cnt += __popc(pred4(load4(d.W, d.n, f, al), f, d.n, mean, thr));
+            cnt += __popc(pred4(load4(d.W, d.n, f, al), f, d.n, olo, ohi));
         }
     }
     typedef cub::BlockReduce<int, kDT> BR;
@@ -478,7 +482,7 @@ __global__ void __launch_bounds__(kDT) k_detect_write(const TDesc* __restrict__ 
     const TDesc& d = td[t];
     const TStats* st = d.st;
     if (!st->mask || sc.blk_count[g] == 0) return;
-    const double mean = st->mean, thr = st->thr;
+    const float olo = st->olo, ohi = st->ohi;
     const int64_t b0 = (g - d.dblk_base) * (int64_t)kDetectBlock;
     const bool al = (reinterpret_cast<uintptr_t>(d.W) & 15) == 0;
     long long out = sc.blk_offset[g];
@@ -491,7 +495,7 @@ __global__ void __launch_bounds__(kDT) k_detect_write(const TDesc* __restrict__ 
         unsigned m = 0;
         if (f < d.n) {
             v = load4(d.W, d.n, f, al);
-            m = pred4(v, f, d.n, mean, thr);
+            m = pred4(v, f, d.n, olo, ohi);
         }
         if (!__syncthreads_or(m != 0)) continue;
         int ex, agg;

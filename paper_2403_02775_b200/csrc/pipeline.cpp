@@ -203,6 +203,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     for (int k = 0; k < 2; ++k) ar.reserve_n<float>(tot_chunks);
     for (int k = 0; k < 2; ++k) ar.reserve_n<long long>(tot_dblk);
     for (int k = 0; k < 5; ++k) ar.reserve_n<double>(tot_cols);
+    ar.reserve_n<float>(tot_cols);
     ar.reserve_n<int2>(tiles.size());
     ar.reserve(sizeof(double) * bc.size());
     ar.reserve(sizeof(K3Group) * tot_groups);
@@ -227,6 +228,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     sc.err_rtn = ar.take<double>(tot_cols);
     sc.err_fin = ar.take<double>(tot_cols);
     sc.inv = ar.take<double>(tot_cols);
+    sc.invf = ar.take<float>(tot_cols);
     double* d_bc = ar.take<double>(bc.size());
     K3Group* d_groups = ar.take<K3Group>(tot_groups);
     float* d_in = ar.take<float>(tot_in);
