@@ -215,6 +215,17 @@ int ezq_unpack_levels(const uint8_t* bytes, int64_t n_bytes, int64_t count, int 
                       int16_t* out);
 int ezq_dequantize_channel(const int16_t* levels, int64_t n, double scale, float* out);
 
+/* ---- .ezqt container (io.hpp:48-66; io.cpp:221-354) ------------------------ */
+/* encode_quantized: host artifact -> the reference's exact bytes (malloc'd;
+ * free with ezq_free). Validation order and messages follow io.cpp:222-263;
+ * failures are EZQ_ERR_INVALID_ARGUMENT. */
+int ezq_encode_quantized(const ezq_qweight* q, uint8_t** out, int64_t* len);
+/* decode_quantized: bytes -> library-owned host artifact. Failures are
+ * EZQ_ERR_IO_FORMAT / EZQ_ERR_IO_VERSION with the byte offset the reference
+ * reports in ezq_last_error's index (EZQ_ERR_INVALID_ARGUMENT for a k != 4
+ * payload byte outside the level span, as unpack_levels). */
+int ezq_decode_quantized(const uint8_t* bytes, int64_t len, ezq_qweight** out);
+
 /* ---- fused dequant + outlier GEMV / skinny GEMM (new) ----- */
 /* y[b, j] = sum_i x[b, i] * What[i, j] with What the dequantized `q`
  * (rows = in features, cols = out features). x: [batch, rows] (dtype 0 = f32,

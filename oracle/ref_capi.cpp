@@ -18,6 +18,7 @@
 
 #include "ezquant/error.hpp"
 #include "ezquant/io.hpp"
+#include "ezquant/model.hpp"
 #include "ezquant/optimize.hpp"
 #include "ezquant/outliers.hpp"
 #include "ezquant/pipeline.hpp"
@@ -376,6 +377,23 @@ int ref_reconstruction_error(const float* a, const float* b, int64_t rows, int64
     const OutlierSet s = to_set(r, c, nullptr, n_skip);
     const OutlierSet* sp = r ? &s : nullptr;
     *out = serial ? serial::reconstruction_error(A, B, sp) : reconstruction_error(A, B, sp);
+    return 0;
+    GUARD_END
+}
+
+// ---- model.hpp (whole-model driver, for byte-identical output checks) ----
+int ref_quantize_model(const char* manifest, const char* out_dir, const CCfg* c, int mode,
+                       int workers, int* failures) {
+    GUARD_BEGIN
+    const ModelManifest m = load_manifest(manifest);
+    *failures = quantize_model(m, to_cfg(c), static_cast<QuantMode>(mode), workers, out_dir).failures;
+    return 0;
+    GUARD_END
+}
+
+int ref_dequantize_model(const char* in_dir, const char* out_dir, int workers, int* failures) {
+    GUARD_BEGIN
+    *failures = dequantize_model(in_dir, workers, out_dir).failures;
     return 0;
     GUARD_END
 }

@@ -69,6 +69,9 @@ def lib():
         L.ref_encode.restype = I64
         L.ref_decode.argtypes = [P, I64, C.POINTER(C.c_int), C.POINTER(C.c_uint64)]
         L.ref_decode.restype = P
+        L.ref_quantize_model.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(RefConfig), C.c_int,
+                                         C.c_int, C.POINTER(C.c_int)]
+        L.ref_dequantize_model.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_int)]
         L.ref_channel_eval.argtypes = [P, I64, P, I64, D, C.POINTER(RefConfig), C.POINTER(D),
                                        C.POINTER(D)]
         L.ref_adam_step.argtypes = [C.POINTER(D), C.POINTER(D), C.POINTER(I64), D, D,
@@ -321,3 +324,18 @@ def reconstruction_error(a, b, skip=None, serial=False):
     _check(lib().ref_reconstruction_error(_p(a), _p(b), a.shape[0], a.shape[1], _p(r), _p(c), n,
                                           int(serial), C.byref(out)))
     return out.value
+
+
+def quantize_model(manifest: str, out_dir: str, cfg, mode="easyquant", workers=4) -> int:
+    """model.hpp quantize_model of the compiled reference; returns failures."""
+    c = cfg_c(cfg)
+    f = C.c_int(0)
+    _check(lib().ref_quantize_model(manifest.encode(), out_dir.encode(), C.byref(c), MODES[mode],
+                                    workers, C.byref(f)))
+    return f.value
+
+
+def dequantize_model(in_dir: str, out_dir: str, workers=4) -> int:
+    f = C.c_int(0)
+    _check(lib().ref_dequantize_model(in_dir.encode(), out_dir.encode(), workers, C.byref(f)))
+    return f.value

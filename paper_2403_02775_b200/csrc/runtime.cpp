@@ -7,7 +7,9 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <cstdlib>
 #include <unordered_map>
+#include <unordered_set>
 
 namespace ezq {
 
@@ -142,6 +144,7 @@ std::string fmt_double(double v) { return std::to_string(v); }
 namespace {
 std::mutex g_pin_mu;
 std::unordered_map<void*, size_t> g_pin_live;                  // ptr -> size
+std::unordered_set<void*> g_malloc_live;                         // pageable fallback (no device)
 std::unordered_map<size_t, std::vector<void*>> g_pin_free;     // size -> blocks
 size_t g_pin_cached = 0;
 constexpr size_t kPinCacheLimit = 16ull << 30;
@@ -162,8 +165,14 @@ void* host_alloc(size_t bytes) {
     }
     void* p = nullptr;
     if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) {
+        // No device (host-only codec use) or pinned memory exhausted:
+        // pageable memory serves host artifacts just as well.
         cudaGetLastError();
-        return nullptr;
+        p = std::malloc(bytes);
+        if (!p) return nullptr;
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        g_malloc_live.insert(p);
+        return p;
     }
     std::lock_guard<std::mutex> lk(g_pin_mu);
     g_pin_live[p] = bytes;
@@ -173,6 +182,10 @@ void* host_alloc(size_t bytes) {
 void host_free(void* p) {
     if (!p) return;
     std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (g_malloc_live.erase(p)) {
+        std::free(p);
+        return;
+    }
     auto it = g_pin_live.find(p);
     if (it == g_pin_live.end()) return;
     const size_t bytes = it->second;

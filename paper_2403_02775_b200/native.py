@@ -191,6 +191,9 @@ def lib() -> C.CDLL:
         L.ezq_profile_enable.argtypes = [I32]
         L.ezq_profile_read.argtypes = [C.c_char_p, C.POINTER(D), C.POINTER(I64), C.POINTER(D)]
         L.ezq_measure_fp64_peak.argtypes = [C.POINTER(D)]
+        L.ezq_encode_quantized.argtypes = [C.POINTER(CQWeight), C.POINTER(C.POINTER(C.c_uint8)),
+                                           C.POINTER(I64)]
+        L.ezq_decode_quantized.argtypes = [P, I64, C.POINTER(C.POINTER(CQWeight))]
         _lib = L
     return _lib
 
@@ -432,6 +435,35 @@ def dequantize(q: QuantizedWeight, out=None, stream=None) -> np.ndarray:
     finally:
         lib().ezq_qweight_free(w)
     return out
+
+
+def encode_quantized(q: QuantizedWeight) -> bytes:
+    """io.hpp:62 encode_quantized: the .ezqt bytes of a host artifact (host
+    code, no device needed)."""
+    outl = np.ascontiguousarray(q.outliers, dtype=OUTLIER_DTYPE)
+    packed = np.ascontiguousarray(q.packed, dtype=np.uint8)
+    scales = np.ascontiguousarray(q.scales, dtype=np.float32)
+    w = C.POINTER(CQWeight)()
+    check(lib().ezq_qweight_wrap(q.rows, q.cols, q.bits, _ptr(packed), packed.size, _ptr(scales),
+                                 scales.size, _ptr(outl), outl.size, q.mean, q.stddev, q.sigma_n,
+                                 MEM_HOST, C.byref(w)))
+    buf = C.POINTER(C.c_uint8)()
+    n = C.c_int64(0)
+    try:
+        check(lib().ezq_encode_quantized(w, C.byref(buf), C.byref(n)))
+        return C.string_at(buf, n.value)
+    finally:
+        lib().ezq_qweight_free(w)
+        if buf:
+            lib().ezq_free(buf)
+
+
+def decode_quantized(data: bytes) -> QuantizedWeight:
+    """io.hpp:63 decode_quantized; IoError carries the byte offset in .index."""
+    arr = np.frombuffer(data, dtype=np.uint8) if len(data) else np.zeros(1, np.uint8)
+    q = C.POINTER(CQWeight)()
+    check(lib().ezq_decode_quantized(_ptr(arr), len(data), C.byref(q)))
+    return _from_c(q.contents, _COwner(q))
 
 
 def reconstruction_error(a, b, skip: Optional[np.ndarray] = None) -> float:
