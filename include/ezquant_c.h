@@ -215,6 +215,13 @@ int ezq_unpack_levels(const uint8_t* bytes, int64_t n_bytes, int64_t count, int 
                       int16_t* out);
 int ezq_dequantize_channel(const int16_t* levels, int64_t n, double scale, float* out);
 
+/* ---- device buffers (for C/C++ callers without the CUDA runtime) ---------- */
+/* Copies n floats from host memory into a new device buffer on the calling
+ * thread's device; free with ezq_device_free. */
+int ezq_device_upload(const float* host, int64_t n, float** dev);
+void ezq_device_free(void* dev);
+int ezq_device_mem_info(size_t* free_bytes, size_t* total_bytes);
+
 /* ---- .ezqt container (io.hpp:48-66; io.cpp:221-354) ------------------------ */
 /* encode_quantized: host artifact -> the reference's exact bytes (malloc'd;
  * free with ezq_free). Validation order and messages follow io.cpp:222-263;

@@ -19,6 +19,7 @@
 #include "ezquant/error.hpp"
 #include "ezquant/io.hpp"
 #include "ezquant/model.hpp"
+#include "ezquant/report.hpp"
 #include "ezquant/optimize.hpp"
 #include "ezquant/outliers.hpp"
 #include "ezquant/pipeline.hpp"
@@ -394,6 +395,19 @@ int ref_quantize_model(const char* manifest, const char* out_dir, const CCfg* c,
 int ref_dequantize_model(const char* in_dir, const char* out_dir, int workers, int* failures) {
     GUARD_BEGIN
     *failures = dequantize_model(in_dir, workers, out_dir).failures;
+    return 0;
+    GUARD_END
+}
+
+// report.hpp sigma_sweep: JSON rows (sweep_to_json) into `out` (cap bytes).
+int ref_sigma_sweep(const char* manifest, const CCfg* c, const float* sigmas, int n, int workers,
+                    char* out, int64_t cap) {
+    GUARD_BEGIN
+    const std::vector<SweepRow> rows =
+        sigma_sweep(load_manifest(manifest), to_cfg(c), std::vector<float>(sigmas, sigmas + n), workers);
+    const std::string js = sweep_to_json(rows);
+    if (static_cast<int64_t>(js.size()) + 1 > cap) return fail(1, "output buffer too small");
+    std::memcpy(out, js.c_str(), js.size() + 1);
     return 0;
     GUARD_END
 }

@@ -72,6 +72,8 @@ def lib():
         L.ref_quantize_model.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(RefConfig), C.c_int,
                                          C.c_int, C.POINTER(C.c_int)]
         L.ref_dequantize_model.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_int)]
+        L.ref_sigma_sweep.argtypes = [C.c_char_p, C.POINTER(RefConfig), P, C.c_int, C.c_int,
+                                      C.c_char_p, I64]
         L.ref_channel_eval.argtypes = [P, I64, P, I64, D, C.POINTER(RefConfig), C.POINTER(D),
                                        C.POINTER(D)]
         L.ref_adam_step.argtypes = [C.POINTER(D), C.POINTER(D), C.POINTER(I64), D, D,
@@ -339,3 +341,13 @@ def dequantize_model(in_dir: str, out_dir: str, workers=4) -> int:
     f = C.c_int(0)
     _check(lib().ref_dequantize_model(in_dir.encode(), out_dir.encode(), workers, C.byref(f)))
     return f.value
+
+
+def sigma_sweep(manifest: str, cfg, sigmas, workers=4) -> str:
+    """report.hpp sigma_sweep of the compiled reference, as sweep_to_json text."""
+    c = cfg_c(cfg)
+    sg = np.ascontiguousarray(sigmas, np.float32)
+    buf = C.create_string_buffer(1 << 20)
+    _check(lib().ref_sigma_sweep(manifest.encode(), C.byref(c), _p(sg), sg.size, workers, buf,
+                                 1 << 20))
+    return buf.value.decode()

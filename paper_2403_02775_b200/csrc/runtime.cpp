@@ -383,6 +383,38 @@ int ezq_profile_read(const char* family, double* ms, int64_t* launches, double* 
 
 void ezq_free(void* p) { std::free(p); }
 
+int ezq_device_upload(const float* host, int64_t n, float** dev) {
+    *dev = nullptr;
+    int d;
+    if (int s = bind_device(&d)) return s;
+    float* p = nullptr;
+    const size_t bytes = sizeof(float) * static_cast<size_t>(std::max<int64_t>(n, 1));
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(EZQ_ERR_OOM, "device allocation of " + std::to_string(bytes) + " bytes failed");
+    }
+    if (n > 0) {
+        const cudaError_t e = cudaMemcpy(p, host, sizeof(float) * n, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(p);
+            return cuda_error(e, "ezq_device_upload");
+        }
+    }
+    *dev = p;
+    return clear_error();
+}
+
+void ezq_device_free(void* dev) {
+    if (dev) cudaFree(dev);
+}
+
+int ezq_device_mem_info(size_t* free_bytes, size_t* total_bytes) {
+    int d;
+    if (int s = bind_device(&d)) return s;
+    EZQ_CK(cudaMemGetInfo(free_bytes, total_bytes));
+    return clear_error();
+}
+
 // ---- host scalar utilities (bookkeeping; identical arithmetic) -----------
 double ezq_initial_scale(const float* x, int64_t n, const ezq_config* cfg) {
     double max_abs = 0.0;  // rtn.cpp:81-86

@@ -1,0 +1,188 @@
+// sigma_sweep for the B200 engine (reference report.cpp:241-313; SURVEY.md
+// §8f next #2). The reference re-reads and re-quantizes every tensor on the
+// CPU for every sigma_n. Here the model's 2-D tensors are read once (host
+// worker threads), uploaded to HBM once when they fit, and each sigma_n is
+// one ezq_quantize_batch over all of them with device-resident outputs:
+// only the per-tensor scalars (outlier count, rtn_error, final_error) are
+// read back. Sums run in manifest order exactly like the reference, so the
+// rows are bit-identical to it.
+#include <atomic>
+#include <cstdio>
+#include <ostream>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <json.hpp>
+
+#include "../../include/ezquant/sweep.hpp"
+#include "../../include/ezquant_c.h"
+
+namespace ezquant {
+
+namespace {
+
+[[noreturn]] void raise_status(int code) {
+    char msg[1024];
+    int64_t idx = -1;
+    ezq_last_error(msg, sizeof msg, &idx);
+    if (code == EZQ_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+}
+
+ezq_config to_c(const QuantConfig& c) {
+    ezq_config o;
+    ezq_config_default(&o);
+    o.bits = c.bits;
+    o.sigma_n = c.sigma_n;
+    o.lr = c.lr;
+    o.beta1 = c.adam_beta1;
+    o.beta2 = c.adam_beta2;
+    o.eps = c.adam_eps;
+    o.steps = c.steps;
+    o.select = c.select == SelectPolicy::FixedStep ? EZQ_SELECT_FIXED : EZQ_SELECT_BEST;
+    o.select_step = c.select_step;
+    o.seed = c.seed;
+    return o;
+}
+
+// Device copies of the sweep's matrices, freed on scope exit.
+struct DeviceSet {
+    std::vector<float*> ptr;
+    ~DeviceSet() {
+        for (float* p : ptr) ezq_device_free(p);
+    }
+};
+
+}  // namespace
+
+std::vector<SweepRow> sigma_sweep(const ModelManifest& manifest, const QuantConfig& base,
+                                  const std::vector<float>& sigmas, int workers) {
+    if (workers < 1) throw std::invalid_argument("workers must be >= 1");
+    const int64_t n = static_cast<int64_t>(manifest.tensors.size());
+    std::vector<int64_t> mat;  // manifest indices of the 2-D tensors
+    for (int64_t i = 0; i < n; ++i)
+        if (manifest.tensors[i].rows != 1 && manifest.tensors[i].cols != 1) mat.push_back(i);
+    const int64_t m = static_cast<int64_t>(mat.size());
+
+    // Read once on the host workers; the first failure (manifest order) wins.
+    std::vector<DenseMatrix> W(static_cast<size_t>(m));
+    std::vector<std::string> err(static_cast<size_t>(m));
+    {
+        std::atomic<int64_t> next{0};
+        auto body = [&] {
+            for (int64_t k; (k = next.fetch_add(1)) < m;) {
+                const auto& t = manifest.tensors[mat[k]];
+                try {
+                    W[k] = read_tensor_f32(manifest.base_dir / t.file, t.rows, t.cols);
+                    W[k].validate();
+                } catch (const std::exception& e) {
+                    err[k] = e.what();
+                    if (err[k].empty()) err[k] = "tensor read failed";
+                }
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int k = 1; k < std::min<int64_t>(workers, m); ++k) pool.emplace_back(body);
+        body();
+        for (auto& th : pool) th.join();
+    }
+    for (int64_t k = 0; k < m; ++k)
+        if (!err[k].empty()) throw std::runtime_error(err[k]);
+
+    // Upload once when the set fits comfortably in HBM; else each sigma
+    // streams it from host memory (ezq_quantize_batch pipelines the copies).
+    size_t total = 0;
+    for (const auto& w : W) total += w.data.size() * sizeof(float);
+    size_t free_b = 0, total_b = 0;
+    DeviceSet dev;
+    std::vector<const float*> src(static_cast<size_t>(m));
+    int in_mem = EZQ_MEM_HOST;
+    if (m > 0 && ezq_device_mem_info(&free_b, &total_b) == EZQ_OK && total + (size_t(8) << 30) < free_b) {
+        in_mem = EZQ_MEM_DEVICE;
+        for (int64_t k = 0; k < m; ++k) {
+            float* p = nullptr;
+            if (ezq_device_upload(W[k].data.data(), static_cast<int64_t>(W[k].data.size()), &p) != EZQ_OK) {
+                in_mem = EZQ_MEM_HOST;  // fall back to streaming from host memory
+                break;
+            }
+            dev.ptr.push_back(p);
+        }
+    }
+    std::vector<int64_t> rows(static_cast<size_t>(m)), cols(static_cast<size_t>(m));
+    for (int64_t k = 0; k < m; ++k) {
+        rows[k] = W[k].rows;
+        cols[k] = W[k].cols;
+        src[k] = in_mem == EZQ_MEM_DEVICE ? dev.ptr[k] : W[k].data.data();
+    }
+
+    std::vector<SweepRow> out;
+    std::vector<ezq_qweight*> q(static_cast<size_t>(m), nullptr);
+    for (float sn : sigmas) {
+        QuantConfig cfg = base;
+        cfg.sigma_n = sn;
+        cfg.validate();
+        const ezq_config c = to_c(cfg);
+        std::vector<int64_t> outl(static_cast<size_t>(n), 0);
+        std::vector<double> rtn(static_cast<size_t>(n), 0.0), fin(static_cast<size_t>(n), 0.0);
+        std::vector<int64_t> params(static_cast<size_t>(n), 0);
+        if (m > 0) {
+            int failed = -1;
+            const int s = ezq_quantize_batch(src.data(), rows.data(), cols.data(), static_cast<int>(m), &c,
+                                             EZQ_MODE_EASYQUANT, in_mem, EZQ_MEM_DEVICE, nullptr, q.data(),
+                                             &failed);
+            if (s != EZQ_OK) raise_status(s);
+            for (int64_t k = 0; k < m; ++k) {
+                const int64_t i = mat[k];
+                outl[i] = q[k]->n_outliers;
+                rtn[i] = q[k]->has_errors ? q[k]->rtn_error : 0.0;
+                fin[i] = q[k]->has_errors ? q[k]->final_error : 0.0;
+                params[i] = rows[k] * cols[k];
+                ezq_qweight_free(q[k]);
+                q[k] = nullptr;
+            }
+        }
+        SweepRow row;
+        row.sigma_n = sn;
+        int64_t total_params = 0;
+        for (int64_t i = 0; i < n; ++i) {  // manifest order, like the reference
+            row.outliers += outl[i];
+            row.rtn_error += rtn[i];
+            row.final_error += fin[i];
+            total_params += params[i];
+        }
+        row.outlier_fraction =
+            total_params > 0 ? static_cast<double>(row.outliers) / static_cast<double>(total_params) : 0.0;
+        out.push_back(row);
+    }
+    return out;
+}
+
+void print_sweep_table(const std::vector<SweepRow>& rows, std::ostream& os) {
+    char line[256];
+    std::snprintf(line, sizeof line, "%8s %12s %10s %14s %14s\n", "sigma_n", "outliers", "frac%", "rtn_error",
+                  "final_error");
+    os << line;
+    for (const auto& r : rows) {
+        std::snprintf(line, sizeof line, "%8.3g %12lld %10.4f %14.6g %14.6g\n", static_cast<double>(r.sigma_n),
+                      static_cast<long long>(r.outliers), 100.0 * r.outlier_fraction, r.rtn_error, r.final_error);
+        os << line;
+    }
+}
+
+std::string sweep_to_json(const std::vector<SweepRow>& rows) {
+    nlohmann::ordered_json j = nlohmann::ordered_json::array();
+    for (const auto& r : rows) {
+        nlohmann::ordered_json e;
+        e["sigma_n"] = r.sigma_n;
+        e["outliers"] = r.outliers;
+        e["outlier_fraction"] = r.outlier_fraction;
+        e["rtn_error"] = r.rtn_error;
+        e["final_error"] = r.final_error;
+        j.push_back(std::move(e));
+    }
+    return j.dump(2) + "\n";
+}
+
+}  // namespace ezquant

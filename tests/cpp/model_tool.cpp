@@ -4,11 +4,14 @@
 // byte-for-byte with the compiled reference.
 //   model_tool quantize <manifest.json> <out_dir> <bits> <sigma_n> <mode> <steps> <workers>
 //   model_tool dequantize <in_dir> <out_dir> <workers>
+//   model_tool sweep <manifest.json> <bits> <steps> <workers> <sigma>...   (prints sweep_to_json)
 #include <cstdio>
 #include <cstdlib>
 #include <string>
 
 #include "ezquant/model.hpp"
+#include "ezquant/sweep.hpp"
+#include <vector>
 
 int main(int argc, char** argv) {
     using namespace ezquant;
@@ -25,6 +28,16 @@ int main(int argc, char** argv) {
             for (const auto& t : r.tensors)
                 if (!t.ok) std::printf("failed %s: %s\n", t.name.c_str(), t.error.c_str());
             std::printf("failures %d\n", r.failures);
+            return 0;
+        }
+        if (cmd == "sweep" && argc >= 7) {
+            QuantConfig cfg;
+            cfg.bits = std::atoi(argv[3]);
+            cfg.steps = std::atoi(argv[4]);
+            std::vector<float> sigmas;
+            for (int k = 6; k < argc; ++k) sigmas.push_back(static_cast<float>(std::atof(argv[k])));
+            std::fputs(sweep_to_json(sigma_sweep(load_manifest(argv[2]), cfg, sigmas, std::atoi(argv[5]))).c_str(),
+                       stdout);
             return 0;
         }
         if (cmd == "dequantize" && argc == 5) {

@@ -104,6 +104,32 @@ def test_quantize_model_byte_identical_to_reference(gpu, O, tmp_path, mode, bits
         assert a[name] == b[name], name
 
 
+@pytest.mark.gpu
+def test_sigma_sweep_matches_reference(gpu, O, tmp_path):
+    """report.hpp sigma_sweep: per-sigma outlier counts/fractions and the
+    manifest-order error sums are bit-identical to the reference's (compared
+    as sweep_to_json text)."""
+    from oracle import refimpl as R
+    if not R.available():
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    from paper_2403_02775_b200.native import Config
+    d = str(tmp_path / "in")
+    man = _model(d, O)
+    # the sweep requires every 2-D tensor to load: keep the good ones
+    with open(man) as f:
+        m = json.load(f)
+    m["tensors"] = [t for t in m["tensors"] if t["name"] not in ("missing", "short", "nonfinite")]
+    with open(man, "w") as f:
+        json.dump(m, f)
+    sigmas = [1.5, 2.0, 2.5758, 3.0, 4.0]
+    ref = R.sigma_sweep(man, Config(bits=4, steps=30), sigmas, workers=4)
+    exe = _tool(tmp_path)
+    r = subprocess.run([exe, "sweep", man, "4", "30", "3"] + [repr(s) for s in sigmas],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout == ref
+
+
 def test_model_tool_compiles(N, tmp_path):
     """CPU: a reference-style whole-model caller builds against the drop-in."""
     _tool(tmp_path)
