@@ -79,16 +79,15 @@ __device__ __forceinline__ float level_fast(float x, const FastLevel& fl, float&
 
 // ---- level -> double without F2F ------------------------------------------
 // F2F.F64.F32 issues at ~16/clk/SM on B200 (measured), an eighth of the FP32
-// rate. For t = RN32(w + MAGIC) = MAGIC + q (|q| < 2^22) the bit pattern is
-// 0x4B400000 + q, so one IMAD.WIDE.U32 forms the double
-// 0x4338000080000000 + q = 1.5*2^52 + 2^31 + q and one DADD removes the bias:
-// exact for every level.
+// rate. For t = RN32(w + MAGIC) = MAGIC + q (|q| < 2^19) the bit pattern is
+// 0x4B400000 + q. Re-basing it into the HIGH word of a double whose low word
+// is 0 gives 0x41380000 + q : 0 = 1.5*2^20 + q (the high word's LSB weighs 1
+// at exponent 2^20), and one DADD removes the bias: exact for every level.
+// One IADD + one DADD per element; the zero low words are loop-invariant
+// registers (a 64-bit IMAD.WIDE form costs an extra IMAD.X for the carry).
 __device__ __forceinline__ double level_bits_to_double(float t) {
-    unsigned long long w;
-    asm("mad.wide.u32 %0, %1, 1, %2;"
-        : "=l"(w)
-        : "r"(__float_as_uint(t)), "l"(0x4338000034C00000ull));
-    return __dsub_rn(__longlong_as_double(static_cast<long long>(w)), 6755401588539392.0);
+    const int hi = static_cast<int>(__float_as_uint(t)) - 0x0A080000;  // 0x4B400000 -> 0x41380000
+    return __dsub_rn(__hiloint2double(hi, 0), 1572864.0);
 }
 
 // ---- float -> double on the ALU (XU-free) ----------------------------------
