@@ -166,6 +166,8 @@ void launch_quantize_channel(const float* x, int64_t n, double scale, CfgDev cfg
 
 // Instrumentation: kernels launched by this process.
 void count_launch(int n = 1);
+// Host (page-locked) -> device copy by SM loads (k_ingest), DMA fallback.
+int ingest_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st);
 // Optional per-family device timing (ezq_profile_enable): returns a token to
 // pass to prof_end, or -1 when profiling is off.
 int prof_begin(const char* family, cudaStream_t st);

@@ -1,5 +1,6 @@
 // Diagnostics: FP64 DFMA peak of the device (the roofline denominator of the
 // q_range kernel -- MEASURED_PEAKS.json carries no FP64 figure).
+#include "ezq_kernels.cuh"
 #include "runtime.hpp"
 
 namespace ezq {
@@ -17,7 +18,52 @@ __global__ void k_dfma_peak(double* out, int iters, double a, double b) {
     for (int k = 0; k < 16; ++k) s += r[k];
     if (s == 1234.5) out[0] = s;
 }
+
+// Zero-copy ingest: SMs read page-locked host memory directly over the bus
+// (UVA) and write device memory. Used for the chunked host-input pipeline so
+// the large H2D stream does not occupy the DMA engines that the per-call
+// descriptor uploads need (a DMA FIFO would serialize them behind it). A
+// handful of CTAs keeps enough 16-byte reads in flight for PCIe/C2C rates
+// while co-residing with the compute kernels.
+__global__ void __launch_bounds__(256) k_ingest(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                int64_t n16) {
+    constexpr int U = 4;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n16; i += stride * U) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i + u * stride < n16) v[u] = src[i + u * stride];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i + u * stride < n16) dst[i + u * stride] = v[u];
+    }
+}
 }  // namespace
+
+// Copies `bytes` from page-locked host memory to device memory with k_ingest
+// when the source is device-accessible and 16-byte aligned (else a DMA copy).
+int ingest_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    cudaPointerAttributes pa{};
+    const bool mapped = cudaPointerGetAttributes(&pa, src) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+                        pa.devicePointer != nullptr;
+    if (!mapped) cudaGetLastError();
+    const void* dsrc = mapped ? pa.devicePointer : nullptr;
+    const bool vec = mapped && ((reinterpret_cast<uintptr_t>(dsrc) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+    const size_t n16 = vec ? bytes / 16 : 0;
+    if (n16) {
+        k_ingest<<<64, 256, 0, st>>>(static_cast<const uint4*>(dsrc), static_cast<uint4*>(dst),
+                                     static_cast<int64_t>(n16));
+        count_launch();
+    }
+    const size_t rest = bytes - 16 * n16;
+    if (rest)
+        EZQ_CK(cudaMemcpyAsync(static_cast<char*>(dst) + 16 * n16, static_cast<const char*>(src) + 16 * n16, rest,
+                               cudaMemcpyHostToDevice, st));
+    EZQ_CK(cudaGetLastError());
+    return EZQ_OK;
+}
+
 }  // namespace ezq
 
 using namespace ezq;

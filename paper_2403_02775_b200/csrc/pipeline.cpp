@@ -9,6 +9,8 @@
 // K3b, column finalize, column-ordered totals, K4. One more sync publishes
 // the errors / invariant.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -71,10 +73,37 @@ TStats fresh_stats() {
 
 // Uploads `h` into arena memory `d` (async; host vector must outlive the copy
 // -> callers keep it alive until the next sync).
+// Small host->device uploads go through a per-thread pinned staging buffer:
+// a pageable cudaMemcpyAsync is host-synchronous and waits for the DMA
+// engine, i.e. behind any large H2D copy in flight (the chunked host-input
+// pipeline), which would serialize ingest and compute. The buffer is reused
+// by the next call only after this call's stream synchronization.
+struct Stager {
+    char* base = nullptr;
+    size_t cap = 0, off = 0;
+    void reset(size_t need) {
+        off = 0;
+        if (need <= cap) return;
+        if (base) host_free(base);
+        cap = std::max(need, cap * 2);
+        base = static_cast<char*>(host_alloc(cap));
+        if (!base) cap = 0;
+    }
+};
+thread_local Stager t_stage;
+
 template <class T>
 int upload(T* d, const std::vector<T>& h, cudaStream_t st) {
     if (h.empty()) return EZQ_OK;
-    EZQ_CK(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+    const size_t bytes = h.size() * sizeof(T);
+    const size_t at = (t_stage.off + 15) & ~size_t(15);
+    if (t_stage.base && at + bytes <= t_stage.cap) {
+        std::memcpy(t_stage.base + at, h.data(), bytes);
+        t_stage.off = at + bytes;
+        EZQ_CK(cudaMemcpyAsync(d, t_stage.base + at, bytes, cudaMemcpyHostToDevice, st));
+    } else {
+        EZQ_CK(cudaMemcpyAsync(d, h.data(), bytes, cudaMemcpyHostToDevice, st));
+    }
     return EZQ_OK;
 }
 
@@ -101,9 +130,13 @@ void free_qweight_arrays(ezq_qweight* q) {
 }  // namespace
 
 // ---------------------------------------------------------------------------
+// `d2h` (host outputs only): when non-null the artifact copies to host run
+// on that stream and the call returns without waiting for them (the caller
+// synchronizes it) -- the chunked host pipeline overlaps them with the next
+// chunk's compute.
 int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* cols, int n,
                    const ezq_config* cfg, int mode, int in_mem, int out_mem, void* user_stream,
-                   ezq_qweight** outs, int* failed) {
+                   ezq_qweight** outs, int* failed, cudaStream_t d2h = nullptr) {
     if (failed) *failed = -1;
     if (n <= 0) return clear_error();
     for (int i = 0; i < n; ++i) outs[i] = nullptr;
@@ -251,6 +284,12 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     }
     bool all_aligned = true;
     for (int i = 0; i < n; ++i) all_aligned &= (reinterpret_cast<uintptr_t>(hd[i].W) & 15) == 0;
+    {
+        size_t need = 64 * 16 + sizeof(TStats) * n + 2 * sizeof(TDesc) * n + 3 * sizeof(int64_t) * (n + 1) +
+                      sizeof(double) * bc.size() + sizeof(int2) * tiles.size();
+        for (auto& p : plans) need += sizeof(K3Group) * p.groups.size();
+        t_stage.reset(need);
+    }
     std::vector<TStats> hs(n, fresh_stats());
     if (int s = upload(d_stats, hs, st)) return s;
     if (int s = upload(d_desc, hd, st)) return s;
@@ -261,8 +300,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     if (int s = upload(d_tiles, tiles, st)) return s;
     for (auto& p : plans) {
         if (p.groups.empty()) continue;
-        EZQ_CK(cudaMemcpyAsync(d_groups + p.goff, p.groups.data(), sizeof(K3Group) * p.groups.size(),
-                               cudaMemcpyHostToDevice, st));
+        if (int s = upload(d_groups + p.goff, p.groups, st)) return s;
     }
 
     // ---- phase 1 ----
@@ -380,6 +418,15 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
 
     // ---- results ----
     std::vector<std::unique_ptr<ezq_qweight>> res(n);
+    cudaStream_t ost = st;  // stream of the output copies
+    if (d2h && out_mem == EZQ_MEM_HOST) {
+        cudaEvent_t ev;
+        cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        cudaEventRecord(ev, st);
+        cudaStreamWaitEvent(d2h, ev, 0);
+        cudaEventDestroy(ev);
+        ost = d2h;
+    }
     for (int i = 0; i < n; ++i) {
         res[i].reset(static_cast<ezq_qweight*>(std::calloc(1, sizeof(ezq_qweight))));
         ezq_qweight* q = res[i].get();
@@ -395,21 +442,33 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
             q->outliers = hs[i].n_out > 0 ? static_cast<ezq_outlier*>(
                                                 host_alloc(sizeof(ezq_outlier) * hs[i].n_out))
                                           : nullptr;
-            cudaMemcpyAsync(q->packed, dout[i].packed, q->packed_bytes, cudaMemcpyDeviceToHost, st);
+            cudaMemcpyAsync(q->packed, dout[i].packed, q->packed_bytes, cudaMemcpyDeviceToHost, ost);
             cudaMemcpyAsync(q->scales, dout[i].scales, sizeof(float) * cols[i],
-                            cudaMemcpyDeviceToHost, st);
+                            cudaMemcpyDeviceToHost, ost);
             if (hs[i].n_out > 0)
                 cudaMemcpyAsync(q->outliers, dout[i].outl, sizeof(ezq_outlier) * hs[i].n_out,
-                                cudaMemcpyDeviceToHost, st);
+                                cudaMemcpyDeviceToHost, ost);
         } else {
             q->packed = dout[i].packed;
             q->scales = dout[i].scales;
             q->outliers = dout[i].outl;
         }
     }
+    if (out_mem == EZQ_MEM_HOST && ost != st) {
+        for (auto& o : dout) {  // freed after the deferred copies
+            if (o.packed) cudaFreeAsync(o.packed, ost);
+            if (o.scales) cudaFreeAsync(o.scales, ost);
+            if (o.outl) cudaFreeAsync(o.outl, ost);
+            o = Out{};
+        }
+    }
     cudaError_t se = cudaStreamSynchronize(st);
     if (out_mem == EZQ_MEM_HOST) free_dout();
+    auto drain = [&]() {  // deferred copies must land before their buffers go
+        if (ost != st) cudaStreamSynchronize(ost);
+    };
     if (se != cudaSuccess) {
+        drain();
         for (auto& q : res) free_qweight_arrays(q.get()), std::free(q.release());
         return cuda_error(se, "phase-2 sync");
     }
@@ -434,6 +493,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
             msg = "optimized error exceeds round-to-nearest error";
         }
         if (code) {
+            drain();
             for (auto& q : res) {
                 free_qweight_arrays(q.get());
                 std::free(q.release());
@@ -453,13 +513,18 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
 int quantize_batch_host(const float* const* Ws, const int64_t* rows, const int64_t* cols, int n,
                         const ezq_config* cfg, int mode, int out_mem, void* user_stream,
                         ezq_qweight** outs, int* failed) {
-    constexpr int64_t kChunkBytes = 512ll << 20;
+    static const int64_t kChunkBytes = std::getenv("EZQ_CHUNK_MB") ? (std::atoll(std::getenv("EZQ_CHUNK_MB")) << 20) : (1024ll << 20);
     std::vector<std::pair<int, int>> chunks;  // [first, last)
     int64_t max_bytes = 0;
+    // The first chunk is small so compute starts after a short ingest; the
+    // later ones are large (fewer partial K3 waves, fewer host syncs).
+    static const int64_t kFirstBytes = std::getenv("EZQ_FIRST_MB") ? (std::atoll(std::getenv("EZQ_FIRST_MB")) << 20)
+                                                                    : (512ll << 20);
     for (int i = 0; i < n;) {
         int j = i;
         int64_t bytes = 0;
-        while (j < n && (j == i || bytes + 4 * rows[j] * cols[j] <= kChunkBytes)) {
+        const int64_t cap = chunks.empty() ? std::min(kFirstBytes, kChunkBytes) : kChunkBytes;
+        while (j < n && (j == i || bytes + 4 * rows[j] * cols[j] <= cap)) {
             bytes += 4 * std::max<int64_t>(rows[j], 0) * std::max<int64_t>(cols[j], 0);
             ++j;
         }
@@ -496,8 +561,7 @@ int quantize_batch_host(const float* const* Ws, const int64_t* rows, const int64
         int64_t off = 0;
         for (int i = chunks[c].first; i < chunks[c].second; ++i) {
             const int64_t nb = 4 * rows[i] * cols[i];
-            EZQ_CK(cudaMemcpyAsync(reinterpret_cast<char*>(buf[b]) + off, Ws[i], nb,
-                                   cudaMemcpyHostToDevice, cs));
+            if (int e = ingest_h2d(reinterpret_cast<char*>(buf[b]) + off, Ws[i], nb, cs)) return e;
             off += nb;
         }
         EZQ_CK(cudaEventRecord(in_ready[b], cs));
@@ -520,7 +584,7 @@ int quantize_batch_host(const float* const* Ws, const int64_t* rows, const int64
         }
         int sub_failed = -1;
         status = quantize_batch(dW.data(), rows + i0, cols + i0, i1 - i0, cfg, mode, EZQ_MEM_DEVICE,
-                                out_mem, st, outs + i0, &sub_failed);
+                                out_mem, st, outs + i0, &sub_failed, d2h_stream(dev));
         if (status) {
             if (failed) *failed = sub_failed >= 0 ? i0 + sub_failed : -1;
             // translate device-relative bad indices is unnecessary: flat index is per tensor
@@ -530,6 +594,7 @@ int quantize_batch_host(const float* const* Ws, const int64_t* rows, const int64
         if (c + 2 < chunks.size()) status = issue_copy(c + 2);
     }
     cudaStreamSynchronize(cs);
+    cudaStreamSynchronize(d2h_stream(dev));  // deferred artifact copies
     cudaFreeAsync(buf[0], st);
     cudaFreeAsync(buf[1], st);
     for (int k = 0; k < 2; ++k) {

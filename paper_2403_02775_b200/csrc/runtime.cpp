@@ -36,6 +36,7 @@ thread_local ErrState t_err;
 thread_local int t_device = -1;
 thread_local std::unordered_map<int, cudaStream_t> t_streams;
 thread_local std::unordered_map<int, cudaStream_t> t_copy_streams;
+thread_local std::unordered_map<int, cudaStream_t> t_d2h_streams;
 
 std::mutex g_mu;
 std::unordered_map<int, DeviceInfo> g_info;
@@ -119,11 +120,24 @@ cudaStream_t thread_stream(int dev) {
     return s;
 }
 
+cudaStream_t d2h_stream(int dev) {
+    auto it = t_d2h_streams.find(dev);
+    if (it != t_d2h_streams.end()) return it->second;
+    cudaStream_t s = nullptr;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    t_d2h_streams[dev] = s;
+    return s;
+}
+
 cudaStream_t copy_stream(int dev) {
     auto it = t_copy_streams.find(dev);
     if (it != t_copy_streams.end()) return it->second;
-    cudaStream_t s = nullptr;
-    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    // Highest priority: the ingest kernel's CTAs are dispatched ahead of the
+    // compute kernels' queued CTAs whenever an SM frees resources.
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStream_t s;
+    cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi);
     t_copy_streams[dev] = s;
     return s;
 }

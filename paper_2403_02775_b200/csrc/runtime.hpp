@@ -28,6 +28,7 @@ int cuda_error(cudaError_t e, const char* where);
 int bind_device(int* dev);
 cudaStream_t thread_stream(int dev);
 cudaStream_t copy_stream(int dev);  // per-thread second stream for H2D staging
+cudaStream_t d2h_stream(int dev);   // per-thread stream for deferred artifact copies
 inline cudaStream_t pick_stream(void* user, int dev) {
     return user ? static_cast<cudaStream_t>(user) : thread_stream(dev);
 }
