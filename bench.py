@@ -349,10 +349,11 @@ def main():
     k3 = prof["qrange"]
     k3_ms = k3["ms"] / max(k3["launches"], 1)
     achieved = (k3["work"] / max(k3["launches"], 1)) / (k3_ms * 1e-3) / 1e12 if k3_ms > 0 else None
-    traffic = None
+    traffic, k3_ncu = None, None
     tf = os.path.join(ROOT, "profiles", "k3_traffic.json")
     if os.path.exists(tf):
-        traffic = json.load(open(tf)).get(args.workload)
+        k3_ncu = json.load(open(tf)).get(args.workload)
+        traffic = k3_ncu["bytes_per_launch"] if k3_ncu else None
     line = base_line(args, cfg, shapes, params, world)
     line.update({
         "value": value,
@@ -372,6 +373,7 @@ def main():
             "launch_ms": k3_ms, "launches_per_step": k3["launches"] / args.steps,
             "flop_per_launch": k3["work"] / max(k3["launches"], 1),
             "peak_source": "measured (ezq_measure_fp64_peak DFMA microkernel, this run)",
+            "ncu": k3_ncu,
         },
         "kernel_share": {f: prof[f]["ms"] / args.steps / (step_s * 1e3) for f in prof},
     })
