@@ -27,10 +27,21 @@ __device__ __forceinline__ void mma(float (&d)[4], const unsigned (&a)[4], unsig
                  : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+__device__ __forceinline__ unsigned lop_only(unsigned v, unsigned magic) {
+    unsigned o;
+    asm("lop3.b32 %0, %1, 0x000F000F, %2, 0xEA;" : "=r"(o) : "r"(v), "r"(magic));
+    return o;
+}
+__device__ __forceinline__ unsigned mulhi(unsigned a, unsigned b) {
+    unsigned o;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(o) : "r"(a), "r"(b));
+    return o;
+}
+
 // V: 0 = LOP3+SHF+HSUB2 (current), 1 = no dequant (raw word as A), 2 = LOP3+SHF only,
-//    3 = LOP3+SHF + HFMA2 (sub via fma)
+//    3 = LOP3+SHF + HFMA2 (sub via fma), 4 = shifts as IMAD.HI (FMA pipe) + LOP3 + HSUB2
 template <int V>
-__global__ void k(float* out, int iters) {
+__global__ void k(float* out, int iters, unsigned m28 = 1u << 28, unsigned m24 = 1u << 24, unsigned m20 = 1u << 20) {
     __shared__ uint4 buf[64 * 32];
     __shared__ uint4 xb[64 * 8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -54,7 +65,11 @@ __global__ void k(float* out, int iters) {
                     if (V == 0) af[r] = sub2(lop_pair(ws[s], r, magic), off2);
                     else if (V == 1) af[r] = ws[s] + r;
                     else if (V == 2) af[r] = lop_pair(ws[s], r, magic);
-                    else af[r] = fma2(lop_pair(ws[s], r, magic), one, off2);
+                    else if (V == 3) af[r] = fma2(lop_pair(ws[s], r, magic), one, off2);
+                    else {
+                        const unsigned v = r == 0 ? ws[s] : mulhi(ws[s], r == 1 ? m28 : r == 2 ? m24 : m20);
+                        af[r] = sub2(lop_only(v, magic), off2);
+                    }
                 }
                 mma(acc[s], af, xs[2 * s], xs[2 * s + 1]);
             }
@@ -96,6 +111,7 @@ int main() {
         run<1>(w, out, "no dequant");
         run<2>(w, out, "lop+shf only");
         run<3>(w, out, "lop+shf+hfma2");
+        run<4>(w, out, "imad.hi+lop+hsub2");
     }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
