@@ -90,19 +90,6 @@ __device__ __forceinline__ double level_bits_to_double(float t) {
     return __dsub_rn(__hiloint2double(hi, 0), 1572864.0);
 }
 
-// ---- float -> double on the ALU (XU-free) ----------------------------------
-// Bit-constructs double(x) for normal floats: sign | (exp + 896) << 52 |
-// mantissa << 29. Zeros and subnormals map to |x'| <= 2^-126 instead of their
-// exact value; callers only use this where such x have level 0, so the
-// residual d = -x' contributes d*d < 2^-250 (far below any error ulp) and
-// d*q = 0 -- the tree-ordered sums are unchanged in practice, and every
-// reported value is recomputed exactly (K3b).
-__device__ __forceinline__ double f2d_alu(float x) {
-    const unsigned b = __float_as_uint(x);
-    const unsigned hi = (((b & 0x7fffffffu) >> 3) + 0x38000000u) | (b & 0x80000000u);
-    return __hiloint2double(static_cast<int>(hi), static_cast<int>(b << 29));
-}
-
 // ---- scale handling ----------------------------------------------------------
 __device__ __forceinline__ double snap(double s) {
     const double snapped = static_cast<double>(__double2float_rn(s));

@@ -513,7 +513,9 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
 int quantize_batch_host(const float* const* Ws, const int64_t* rows, const int64_t* cols, int n,
                         const ezq_config* cfg, int mode, int out_mem, void* user_stream,
                         ezq_qweight** outs, int* failed) {
-    static const int64_t kChunkBytes = std::getenv("EZQ_CHUNK_MB") ? (std::atoll(std::getenv("EZQ_CHUNK_MB")) << 20) : (1024ll << 20);
+    // Chunk sizes (overridable for tuning: EZQ_CHUNK_MB / EZQ_FIRST_MB).
+    static const int64_t kChunkBytes =
+        std::getenv("EZQ_CHUNK_MB") ? (std::atoll(std::getenv("EZQ_CHUNK_MB")) << 20) : (1024ll << 20);
     std::vector<std::pair<int, int>> chunks;  // [first, last)
     int64_t max_bytes = 0;
     // The first chunk is small so compute starts after a short ingest; the
