@@ -195,12 +195,30 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
         std::vector<K3Group> groups;
         size_t goff = 0;
         int grid = 0;
+        int sorted_cpb = 0;  // > 0: K3s (sorted columns), columns per CTA
     };
+    static const bool k3_sorted = std::getenv("EZQ_K3_SORTED") != nullptr;  // opt-in while K3s is slower
     std::vector<Plan> plans;
     size_t tot_groups = 0, gstrip_floats = 0;
     if (cfg_status == EZQ_OK) {
         for (auto& kv : by_rows) {
             Plan p;
+            if (k3_sorted && kv.first <= kK3sMaxRows && k3s_supported(cfg->bits)) {
+                // K3s: one warp per column; columns per CTA so that ~3 CTAs fit per SM.
+                const size_t per_col = k3s_smem(kv.first, 1);
+                const int cpb = static_cast<int>(std::max<size_t>(1, std::min<size_t>(8, (size_t(74) << 10) / per_col)));
+                p.sorted_cpb = cpb;
+                p.kl.rows = kv.first;
+                for (int i : kv.second)
+                    for (int64_t c0 = 0; c0 < cols[i]; c0 += cpb)
+                        p.groups.push_back({i, static_cast<int32_t>(c0),
+                                            static_cast<int32_t>(std::min<int64_t>(cpb, cols[i] - c0)), 0});
+                p.goff = tot_groups;
+                tot_groups += p.groups.size();
+                p.grid = static_cast<int>(p.groups.size());
+                plans.push_back(std::move(p));
+                continue;
+            }
             p.kl = plan_k3(kv.first, 0, di.sms, di.max_smem_optin);
             const int best_cb = choose_k3_width(p.kl, kv.second, cols, di);
             set_k3_width(p.kl, best_cb);
@@ -394,8 +412,12 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
             if (rows[i] == p.kl.rows) normals += static_cast<double>(hd[i].n - hs[i].n_out);
         const double steps1 = (mode == EZQ_MODE_EASYQUANT) ? cfg->steps + 1.0 : 0.0;
         const int p3 = prof_begin("qrange", st);
-        launch_k3(p.kl, d_desc, d_groups + p.goff, static_cast<int>(p.groups.size()), sc, cd,
-                  d_gstrip, p.grid, st);
+        if (p.sorted_cpb)
+            launch_k3_sorted(p.kl.rows, p.sorted_cpb, d_desc, d_groups + p.goff, static_cast<int>(p.groups.size()),
+                             sc, cd, p.grid, st);
+        else
+            launch_k3(p.kl, d_desc, d_groups + p.goff, static_cast<int>(p.groups.size()), sc, cd,
+                      d_gstrip, p.grid, st);
         prof_end(p3, st, 7.0 * normals * steps1);
     }
     int p4 = prof_begin("seqerr", st);
