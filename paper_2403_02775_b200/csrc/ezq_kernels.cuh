@@ -139,13 +139,17 @@ size_t k3_small_smem(const K3Launch& kl, int teams);
 void set_k3_width(K3Launch& kl, int teams);
 void launch_k3(const K3Launch& kl, const TDesc* td, const K3Group* groups, int ngroups,
                Scratch sc, CfgDev cfg, float* gstrip, int grid, cudaStream_t st);
-// K3s (k_qsort.cu): sorted-column q_range loop for rows <= kK3sMaxRows.
-constexpr int64_t kK3sMaxRows = 16384;
+// K3s (k_qsort.cu): sorted-column q_range loop for rows <= kK3sMaxRows:
+// a sort kernel writes per-column tables into `work`, a loop kernel reads
+// them; groups are processed in waves that fit work_bytes.
+constexpr int64_t kK3sMaxRows = 8192;
 int k3s_npad(int64_t rows);
+int k3s_dstride(int64_t rows);
 bool k3s_supported(int bits);
-size_t k3s_smem(int64_t rows, int cpb);
+int k3s_cpb(int64_t rows);               // columns per sort CTA (group width)
+size_t k3s_slot_bytes(int64_t rows);     // table + info bytes per column
 void launch_k3_sorted(int64_t rows, int cpb, const TDesc* td, const K3Group* groups, int ngroups, Scratch sc,
-                      CfgDev cfg, int grid, cudaStream_t st);
+                      CfgDev cfg, void* work, size_t work_bytes, cudaStream_t st);
 void launch_seq_errors(const TDesc* td, const int2* tiles, int ntiles, Scratch sc, CfgDev cfg,
                        cudaStream_t st);
 void launch_tensor_totals(const TDesc* td, int ntens, Scratch sc, cudaStream_t st);

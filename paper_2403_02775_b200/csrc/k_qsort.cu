@@ -3,39 +3,49 @@
 //
 // The reference evaluates err(s) = sum (s*q_i - x_i)^2 and grad(s) =
 // 2 sum (s*q_i - x_i) q_i over all normals at every one of the steps+1
-// scales, q_i = clamp(llround(x_i * (1/s))). The level is a monotone step
-// function of x, so over the column's normals sorted ascending every level
-// v owns one contiguous range, and
+// scales, q_i = clamp(llround(x_i * RN(1/s))). Regrouped,
 //
-//   err = sum_v [ n_v (s v)^2 - 2 s v S1_v + S2_v ],
-//   grad/2 = sum_v [ n_v s v^2 - v S1_v ],
+//   err(s) = A s^2 - 2 Q s + C,   grad(s) = 2 (A s - Q),
+//   A = sum q^2,  Q = sum q x,  C = sum x^2 (constant per column).
 //
-// with n_v, S1_v = sum x, S2_v = sum x^2 over the range. Per Adam step the
-// kernel therefore only (a) moves the 2^k - 1 range boundaries and (b) moves
-// the boundary prefix sums by the elements that crossed:
-//  - boundaries: level(x) >= v  <=>  RN(x * RN(1/s)) >= v - 1/2 (> for
-//    v <= 0: half away from zero), so each boundary is "x >= X_v" for one
-//    float X_v, found with the reference's exact fp64 product at a couple of
-//    candidate floats; the search over the sorted column is then float
-//    compares, galloping from the previous step's position;
-//  - prefix sums: exact 128-bit fixed point (LSB 2^(E-109) for x, 2^(2E-109)
-//    for x^2, |x| < 2^E), so crossings are integer adds and every sum is
-//    exact and order-independent; per level the sums go to double-double,
-//    the level's err/grad terms are formed there (they cancel by ~10 bits),
-//    rounded once, and summed over levels in fixed butterfly order. err and
-//    grad are thus the exact values to ~1e-16 -- the agreement regime of the
-//    reference's own sequential sums and of the streaming K3.
+// The level is a monotone step function of x, so on the column's normals
+// sorted ascending, "level(x) >= j" holds on a suffix [ib_j, n) for each of
+// the 2^k - 1 level thresholds j = lmin+1 .. lmax, and
 //
-// Work per column: one bitonic sort in shared memory plus O(levels) per step
-// instead of O(rows). Two columns per warp for k <= 4 (16 levels per group
-// of 16 lanes), one for k = 5; k > 5 uses the streaming K3.
+//   A = sum_{j>=1} (2j-1) (n - ib_j)  +  sum_{j<=0} (1-2j) ib_j,
+//   Q = sum_{j>=1} S(ib_j)  -  sum_{j<=0} P(ib_j),
+//
+// with S(k) = sum_{i>=k} x_i, P(k) = sum_{i<k} x_i. So after one sort per
+// column a step costs O(levels), not O(rows):
+//  - threshold j: level(x) >= j  <=>  RN(x * inv) >= j - 1/2 (> for j <= 0:
+//    half away from zero), i.e. "x >= X_j" for one float X_j, found with the
+//    reference's own fp64 product at a couple of candidate floats; ib_j is a
+//    galloping search from the previous step's position;
+//  - S(ib_j) and P(ib_j) are single loads from a per-column table written
+//    once after the sort (suffix sums over x >= 0, prefix sums over x < 0).
+//    Every sum used spans same-sign elements of magnitude >= s/2, so it is
+//    EXACT in fp64 (<= 13 + 24 + log2(max/(s/2)) significant bits, < 53
+//    unless s falls below max * 2^-16), and so are A, Q and their
+//    cross-lane sums, in any order;
+//  - err and grad are formed from A, Q, C in double-double and rounded once.
+// err/grad are therefore the exact values (to ~2^-100) -- at least as close
+// to the true sums as the reference's own sequential fp64 sums (the
+// agreement regime of DESIGN.md §4).
+//
+// Layout: a CTA stages cpb columns, sorts each with a block radix sort in
+// registers and replaces it by its (rows + 2)-double table; the x values are
+// recovered exactly as differences of neighbouring entries. Then two columns
+// per warp (groups of 16 lanes, k <= 4) or one (k = 5) run the loop, lane j
+// owning threshold lmin + 1 + j.
+#include <algorithm>
+#include <cstdlib>
+
+#include <cub/block/block_radix_sort.cuh>
+
 #include "ezq_kernels.cuh"
 
 namespace ezq {
 namespace {
-
-typedef __int128 i128;
-typedef unsigned __int128 u128;
 
 struct DD {
     double hi, lo;
@@ -57,85 +67,6 @@ __device__ __forceinline__ DD dd_prod(double a, double b) {
     const double p = __dmul_rn(a, b);
     return {p, fma(a, b, -p)};
 }
-__device__ __forceinline__ DD dd_mul_d(DD a, double b) {
-    DD p = dd_prod(a.hi, b);
-    p.lo = fma(a.lo, b, p.lo);
-    return two_sum(p.hi, p.lo);
-}
-
-// x * 2^bias as a 128-bit integer, truncated toward zero (exact whenever the
-// float's LSB is at or above 2^-bias: everything but negligible tails).
-__device__ __forceinline__ i128 fix_f(float x, int bias) {
-    const unsigned u = __float_as_uint(x);
-    int ex = static_cast<int>((u >> 23) & 255u);
-    unsigned m = u & 0x7fffffu;
-    if (ex == 0) {
-        if (m == 0) return 0;
-        ex = 1;
-    } else {
-        m |= 0x800000u;
-    }
-    const int sh = ex - 150 + bias;  // |x| = m * 2^(ex - 150)
-    i128 v = static_cast<i128>(m);
-    if (sh >= 0)
-        v <<= sh;
-    else
-        v = sh <= -24 ? static_cast<i128>(0) : (v >> -sh);
-    return (u >> 31) ? -v : v;
-}
-// y >= 0 (here x^2, exact in fp64) * 2^bias, truncated.
-__device__ __forceinline__ i128 fix_d(double y, int bias) {
-    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(y));
-    int ex = static_cast<int>((u >> 52) & 2047u);
-    unsigned long long m = u & 0xfffffffffffffull;
-    if (ex == 0) {
-        if (m == 0) return 0;
-        ex = 1;
-    } else {
-        m |= 0x10000000000000ull;
-    }
-    const int sh = ex - 1075 + bias;
-    i128 v = static_cast<i128>(m);
-    if (sh >= 0)
-        v <<= sh;
-    else
-        v = sh <= -53 ? static_cast<i128>(0) : (v >> -sh);
-    return v;
-}
-// 128-bit integer * 2^-bias -> double-double (top 53 bits exact, the rest
-// rounded once: relative error ~2^-106).
-__device__ __forceinline__ DD unfix(i128 v, int bias) {
-    if (v == 0) return {0.0, 0.0};
-    const bool neg = v < 0;
-    const u128 a = neg ? static_cast<u128>(-v) : static_cast<u128>(v);
-    const unsigned long long hi = static_cast<unsigned long long>(a >> 64);
-    const unsigned long long lo = static_cast<unsigned long long>(a);
-    const int lz = hi ? __clzll(static_cast<long long>(hi)) : 64 + __clzll(static_cast<long long>(lo));
-    const int top = 128 - lz;
-    const int drop = top > 53 ? top - 53 : 0;
-    const unsigned long long head = static_cast<unsigned long long>(a >> drop);  // <= 53 bits
-    const u128 rest = a - (static_cast<u128>(head) << drop);                      // < 2^drop
-    const int drop2 = drop > 64 ? drop - 64 : 0;
-    const unsigned long long tail = static_cast<unsigned long long>(rest >> drop2);
-    double d1 = ldexp(static_cast<double>(head), drop - bias);
-    double d2 = ldexp(static_cast<double>(tail), drop2 - bias);
-    if (neg) d1 = -d1, d2 = -d2;
-    return two_sum(d1, d2);
-}
-
-__device__ __forceinline__ i128 join128(long long hi, unsigned long long lo) {
-    return (static_cast<i128>(hi) << 64) | static_cast<i128>(lo);
-}
-__device__ __forceinline__ i128 shfl_up_i128(i128 v, int d, int width) {
-    const unsigned long long lo = __shfl_up_sync(0xffffffffu, static_cast<unsigned long long>(v), d, width);
-    const long long hi = __shfl_up_sync(0xffffffffu, static_cast<long long>(v >> 64), d, width);
-    return join128(hi, lo);
-}
-__device__ __forceinline__ i128 shfl_xor_i128(i128 v, int o, int width) {
-    const unsigned long long lo = __shfl_xor_sync(0xffffffffu, static_cast<unsigned long long>(v), o, width);
-    const long long hi = __shfl_xor_sync(0xffffffffu, static_cast<long long>(v >> 64), o, width);
-    return join128(hi, lo);
-}
 
 // Smallest float x with level(x) >= v at scale s: RN(x*inv) >= t (> t for
 // v <= 0), t = v - 1/2. Candidates start at RN32(t*s) (t*s is exact in
@@ -144,11 +75,20 @@ __device__ __forceinline__ float level_threshold(int v, double s, double inv) {
     const double t = static_cast<double>(v) - 0.5;
     const bool strict = v <= 0;
     const float kInf = __int_as_float(0x7f800000);
-    float c = __double2float_rn(__dmul_rn(t, s));
     auto pred = [&](float x) {
         const double u = __dmul_rn(static_cast<double>(x), inv);
         return strict ? (u > t) : (u >= t);
     };
+    float c = __double2float_rn(__dmul_rn(t, s));
+    if (c != 0.f && fabsf(c) < 3.0e38f) {
+        // float neighbours by bit steps (c != 0, finite): down / up
+        const int b = __float_as_int(c), dn = c > 0.f ? -1 : 1;
+        const float pv = __int_as_float(b + dn), nx = __int_as_float(b - dn);
+        const bool pp = pred(pv), pc = pred(c), pn = pred(nx);
+        if (!pp && pc) return c;
+        if (!pc && pn) return nx;
+        c = pp ? pv : nx;  // rare: walk on below
+    }
     if (pred(c)) {
         for (int i = 0; i < 16; ++i) {
             const float p = nextafterf(c, -kInf);
@@ -164,15 +104,33 @@ __device__ __forceinline__ float level_threshold(int v, double s, double inv) {
     return c;
 }
 
-// First index in [0, n] with a[k] >= X (a ascending; n acts as +inf),
-// galloping from `guess`.
-__device__ __forceinline__ int search_from(const float* a, int n, int guess, float X) {
+// Column table: D[k] = P(k) for k <= kz (kz = count of x < 0), D[k + 1] =
+// S(k) for kz <= k <= n. x_k = D[k+1] - D[k] (k < kz), D[k+1] - D[k+2]
+// (kz <= k < n): exact wherever a threshold can fall.
+struct ColInfo {
+    int n, kz;
+    float lo, hi;     // smallest / largest normal
+    double chi, clo;  // C = sum x^2, double-double
+};
+
+// Per-slot table: D (dstride doubles, above), then the sorted normals as
+// floats, +inf-padded to n + 8 (xs: the search runs on these).
+struct ColTab {
+    const double* D;
+    const float* xs;
+    int n;
+};
+
+// First index in [0, n] with xs[k] >= X (xs[k] = +inf for k >= n), galloping
+// from `guess`.
+__device__ __forceinline__ int search_from(const ColTab& c, int guess, float X) {
+    const int n = c.n;
     guess = min(max(guess, 0), n);
     int lo, hi;
-    if (guess == n || a[guess] >= X) {
+    if (guess == n || __ldg(c.xs + guess) >= X) {
         hi = guess;
         int step = 1, p = guess - 1;
-        while (p >= 0 && a[p] >= X) {
+        while (p >= 0 && __ldg(c.xs + p) >= X) {
             hi = p;
             step <<= 1;
             p = hi - step;
@@ -181,7 +139,7 @@ __device__ __forceinline__ int search_from(const float* a, int n, int guess, flo
     } else {
         lo = guess + 1;
         int step = 1, p = guess + 1;
-        while (p < n && a[p] < X) {
+        while (p < n && __ldg(c.xs + p) < X) {
             lo = p + 1;
             step <<= 1;
             p = lo + step - 1;
@@ -190,7 +148,7 @@ __device__ __forceinline__ int search_from(const float* a, int n, int guess, flo
     }
     while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (a[mid] >= X)
+        if (__ldg(c.xs + mid) >= X)
             hi = mid;
         else
             lo = mid + 1;
@@ -198,263 +156,384 @@ __device__ __forceinline__ int search_from(const float* a, int n, int guess, flo
     return lo;
 }
 
-// Bitonic sort of a power-of-two shared-memory array by the G lanes of a
-// group; `live` groups sort, the others only meet the warp barriers.
-template <int G>
-__device__ void group_bitonic_sort(float* a, int n, int gl, bool live) {
-    for (int k = 2; k <= n; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (live) {
-                for (int p = gl; p < (n >> 1); p += G) {
-                    const int i = ((p / j) * 2 * j) + (p % j);
-                    const int ij = i + j;
-                    const float x = a[i], y = a[ij];
-                    if ((x > y) == ((i & k) == 0)) {
-                        a[i] = y;
-                        a[ij] = x;
-                    }
-                }
-            }
-            __syncwarp();
+// Same, for a boundary that moved little since `guess`: an aligned window of
+// eight floats (two 16-byte loads, one round trip) usually holds the answer;
+// two window moves, then the galloping search.
+__device__ __forceinline__ int search_near(const ColTab& c, int guess, float X) {
+    int k0 = max(guess - 4, 0) & ~3;
+#pragma unroll 1
+    for (int r = 0; r < 3; ++r) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(c.xs + k0));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(c.xs + k0 + 4));
+        const int cnt = (a.x < X) + (a.y < X) + (a.z < X) + (a.w < X) + (b.x < X) + (b.y < X) + (b.z < X) +
+                        (b.w < X);
+        if (cnt == 0 && k0 > 0) {
+            k0 = max(k0 - 8, 0);
+        } else if (cnt == 8) {
+            k0 += 8;
+        } else {
+            return k0 + cnt;
         }
     }
+    return search_from(c, k0, X);
 }
 
-// Exact fixed-point sums of x and x^2 over a[lo, hi), by the G lanes of a
-// group (every lane of the warp must call it: the shuffles are warp-wide).
-template <int G>
-__device__ __forceinline__ void group_range_fix(const float* a, int lo, int hi, int gl, int b1, int b2, i128& s1,
-                                                i128& s2) {
-    i128 p1 = 0, p2 = 0;
-    for (int k = lo + gl; k < hi; k += G) {
-        const float x = a[k];
-        const double xd = static_cast<double>(x);
-        p1 += fix_f(x, b1);
-        p2 += fix_d(__dmul_rn(xd, xd), b2);
-    }
+constexpr int kSortRadixBits = 6;
+
+// Padded shared-memory index of table entry k (one spare double per 16: the
+// blocked writes below hit distinct bank pairs).
+__host__ __device__ __forceinline__ int dpad(int k) { return k + (k >> 4); }
+
+// CTA-wide exclusive scans of one double per thread: prefix (ascending tid)
+// and suffix (descending tid). Every partial sum is over a contiguous run of
+// threads, in a fixed order. Contains a CTA barrier.
+template <int NW>
+__device__ __forceinline__ void block_scans(double vp, double vs, double& ep, double& es, double* wp,
+                                            double* ws) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double ip = vp, is = vs;
 #pragma unroll
-    for (int o = G / 2; o; o >>= 1) {
-        p1 += shfl_xor_i128(p1, o, G);
-        p2 += shfl_xor_i128(p2, o, G);
+    for (int o = 1; o < 32; o <<= 1) {
+        const double up = __shfl_up_sync(0xffffffffu, ip, o);
+        const double dn = __shfl_down_sync(0xffffffffu, is, o);
+        if (lane >= o) ip = __dadd_rn(up, ip);
+        if (lane + o < 32) is = __dadd_rn(is, dn);
     }
-    s1 = p1;
-    s2 = p2;
+    if (lane == 31) wp[warp] = ip;
+    if (lane == 0) ws[warp] = is;
+    double xp = __shfl_up_sync(0xffffffffu, ip, 1);
+    double xs = __shfl_down_sync(0xffffffffu, is, 1);
+    if (lane == 0) xp = 0.0;
+    if (lane == 31) xs = 0.0;
+    __syncthreads();
+    double bp = 0.0, bs = 0.0;
+    for (int w = 0; w < warp; ++w) bp = __dadd_rn(bp, wp[w]);
+    for (int w = NW - 1; w > warp; --w) bs = __dadd_rn(ws[w], bs);
+    ep = __dadd_rn(bp, xp);
+    es = __dadd_rn(xs, bs);
 }
 
-// CPW columns per warp (groups of G = 32 / CPW lanes). Lane gl of a group
-// owns boundary gl (between levels lmin+gl and lmin+gl+1) and level gl.
-template <int CPW>
-__global__ void __launch_bounds__(256) k_qrange_sorted(const TDesc* __restrict__ td,
-                                                       const K3Group* __restrict__ groups, int ngroups,
-                                                       Scratch sc, CfgDev cfg, int npad, int cpb) {
-    constexpr int G = 32 / CPW;
-    extern __shared__ __align__(16) float strip[];  // [cpb][npad]
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-    const int gl = lane % G, grp = lane / G;
-    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
-    const int nb = cfg.lmax - cfg.lmin;  // boundaries (<= G - 1)
-    const bool optimize = cfg.mode == EZQ_MODE_EASYQUANT;
+// ---- K3s-a: sort each column and write its table ---------------------------
+// One CTA per group of cpb adjacent columns (slot = group * cpb + column):
+// the columns are staged (outliers and padding as +inf, sorted last), each is
+// sorted in registers with a block radix sort, and its table D (rows + 2
+// doubles) and ColInfo go to global memory for the loop kernel.
+template <int THREADS, int IPT>
+__global__ void __launch_bounds__(THREADS) k_qsort_tables(const TDesc* __restrict__ td,
+                                                          const K3Group* __restrict__ groups, int cpb,
+                                                          int dstride, int xstride, int tstride,
+                                                          double* __restrict__ tables,
+                                                          ColInfo* __restrict__ infos) {
+    constexpr int NPAD = THREADS * IPT;
+    constexpr int NW = THREADS / 32;
+    typedef cub::BlockRadixSort<float, THREADS, IPT, cub::NullType, kSortRadixBits> Sorter;
+    __shared__ double wp[NW], ws[NW], wc[NW][2];
+    __shared__ int wn[NW][2];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* stage = reinterpret_cast<float*>(smem_raw);  // [cpb][NPAD]
+    unsigned char* uni = smem_raw + sizeof(float) * static_cast<size_t>(cpb) * NPAD;
+    typename Sorter::TempStorage& sort_tmp = *reinterpret_cast<typename Sorter::TempStorage*>(uni);
+    double* Ds = reinterpret_cast<double*>(uni);  // aliases sort_tmp: used after each sort
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const float kInf = __int_as_float(0x7f800000);
 
-    for (int gi = blockIdx.x; gi < ngroups; gi += gridDim.x) {
-        const K3Group g = groups[gi];
-        const TDesc& d = td[g.tensor];
-        const float olo = d.st->olo, ohi = d.st->ohi;
-        const int64_t R = d.rows, C = d.cols;
-        __syncthreads();  // previous group's columns fully consumed
-        for (int idx = tid; idx < cpb * npad; idx += blockDim.x) {
-            const int cc = idx % cpb, r = idx / cpb;
-            float v = kInf;
-            if (cc < g.ncols && r < R) {
-                const float x = d.W[static_cast<int64_t>(r) * C + g.col0 + cc];
-                v = is_outlier_f(x, olo, ohi) ? kInf : x;
+    const K3Group g = groups[blockIdx.x];
+    const TDesc& d = td[g.tensor];
+    const float olo = d.st->olo, ohi = d.st->ohi;
+    const int64_t R = d.rows, C = d.cols;
+    for (int idx = tid; idx < cpb * NPAD; idx += THREADS) {
+        const int cc = idx % cpb, r = idx / cpb;
+        float v = kInf;
+        if (cc < g.ncols && r < R) {
+            const float x = d.W[static_cast<int64_t>(r) * C + g.col0 + cc];
+            v = is_outlier_f(x, olo, ohi) ? kInf : x;
+        }
+        stage[cc * NPAD + r] = v;
+    }
+    __syncthreads();
+    for (int c = 0; c < g.ncols; ++c) {
+        const int64_t slot = static_cast<int64_t>(blockIdx.x) * cpb + c;
+        float keys[IPT];
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) keys[i] = stage[c * NPAD + i * THREADS + tid];
+        Sorter(sort_tmp).Sort(keys);  // blocked: thread t holds ranks [t*IPT, t*IPT + IPT)
+        int cneg = 0, cfin = 0;
+        double tneg = 0.0, tpos = 0.0;
+        DD sq = {0.0, 0.0};
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            const float x = keys[i];
+            const double xd = static_cast<double>(x);
+            if (x < kInf) {
+                ++cfin;
+                sq = dd_add(sq, dd_prod(xd, xd));
+                if (x < 0.f) {
+                    ++cneg;
+                    tneg = __dadd_rn(tneg, xd);
+                }
             }
-            strip[cc * npad + r] = v;
+        }
+#pragma unroll
+        for (int i = IPT - 1; i >= 0; --i)
+            if (keys[i] >= 0.f && keys[i] < kInf) tpos = __dadd_rn(tpos, static_cast<double>(keys[i]));
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            cneg += __shfl_xor_sync(0xffffffffu, cneg, o);
+            cfin += __shfl_xor_sync(0xffffffffu, cfin, o);
+            const DD u = {__shfl_xor_sync(0xffffffffu, sq.hi, o), __shfl_xor_sync(0xffffffffu, sq.lo, o)};
+            sq = dd_add(sq, u);
+        }
+        if (lane == 0) {
+            wn[warp][0] = cneg;
+            wn[warp][1] = cfin;
+            wc[warp][0] = sq.hi;
+            wc[warp][1] = sq.lo;
+        }
+        double ep, es;
+        block_scans<NW>(tneg, tpos, ep, es, wp, ws);  // its barrier also retires sort_tmp
+        int kz = 0, n = 0;
+        for (int w = 0; w < NW; ++w) kz += wn[w][0], n += wn[w][1];
+        double P = ep;
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            const int k = tid * IPT + i;
+            if (keys[i] < 0.f) {
+                Ds[dpad(k)] = P;
+                P = __dadd_rn(P, static_cast<double>(keys[i]));
+                if (k + 1 == kz) Ds[dpad(kz)] = P;
+            }
+        }
+        double S = es;
+#pragma unroll
+        for (int i = IPT - 1; i >= 0; --i) {
+            const int k = tid * IPT + i;
+            if (keys[i] >= 0.f && keys[i] < kInf) {
+                S = __dadd_rn(S, static_cast<double>(keys[i]));
+                Ds[dpad(k + 1)] = S;
+            }
+        }
+        if (tid == 0) {
+            Ds[dpad(n + 1)] = 0.0;
+            if (kz == 0) Ds[0] = 0.0;
+            DD cs = {wc[0][0], wc[0][1]};
+            for (int w = 1; w < NW; ++w) cs = dd_add(cs, DD{wc[w][0], wc[w][1]});
+            infos[slot].n = n;
+            infos[slot].kz = kz;
+            infos[slot].chi = cs.hi;
+            infos[slot].clo = cs.lo;
+        }
+        if (n > 0) {
+#pragma unroll
+            for (int i = 0; i < IPT; ++i) {
+                const int k = tid * IPT + i;
+                if (k == 0) infos[slot].lo = keys[i];
+                if (k == n - 1) infos[slot].hi = keys[i];
+            }
         }
         __syncthreads();
-
-        for (int base = warp * CPW; base < cpb; base += nwarps * CPW) {  // warp-uniform
-            const int cc = base + grp;
-            const bool live = cc < g.ncols;
-            float* a = strip + min(cc, cpb - 1) * npad;
-            group_bitonic_sort<G>(a, npad, gl, live);
-            int n = 0;
-            if (live) {
-                int lo = 0, hi = npad;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (a[mid] < kInf)
-                        lo = mid + 1;
-                    else
-                        hi = mid;
-                }
-                n = lo;
-            }
-            const double mx =
-                n ? fmax(fabs(static_cast<double>(a[0])), fabs(static_cast<double>(a[n - 1]))) : 0.0;
-            const double s0_raw = initial_scale_from_max(mx, cfg.lmax);
-            double s_rtn = static_cast<double>(__double2float_rn(s0_raw));
-            double s_fin = s_rtn;
-            if (optimize) {  // uniform across the warp
-                // fixed-point biases from the column's magnitude: |x| < 2^E
-                const int E = mx > 0.0 ? ilogb(mx) + 1 : 0;
-                const int b1 = 109 - E, b2 = 109 - 2 * E;
-                double s = snap(s0_raw);
-                const double s0 = s;
-                double m = 0.0, vv = 0.0;
-                double e0 = 0.0, best_err = 0.0, best_s = s, fixed_s = s, fixed_err = 0.0;
-                double inv = __ddiv_rn(1.0, s);
-                const bool own_b = live && gl < nb;
-                int ib = n;
-                if (own_b) ib = search_from(a, n, n >> 1, level_threshold(cfg.lmin + gl + 1, s, inv));
-                // level sums, then prefix sums at the boundaries (all exact)
-                i128 P1 = 0, P2 = 0;
-                for (int j = 0; j <= nb; ++j) {
-                    const int lo = j == 0 ? 0 : __shfl_sync(0xffffffffu, ib, j - 1, G);
-                    const int hi = j == nb ? n : __shfl_sync(0xffffffffu, ib, j, G);
-                    i128 s1, s2;
-                    group_range_fix<G>(a, lo, hi, gl, b1, b2, s1, s2);
-                    if (gl == j) P1 = s1, P2 = s2;
-                }
+        double* out = tables + slot * tstride;
+        for (int k = tid; k < n + 2; k += THREADS) out[k] = Ds[dpad(k)];
+        float* xo = reinterpret_cast<float*>(out + dstride);
 #pragma unroll
-                for (int o = 1; o < G; o <<= 1) {
-                    const i128 u1 = shfl_up_i128(P1, o, G), u2 = shfl_up_i128(P2, o, G);
-                    if (gl >= o) P1 += u1, P2 += u2;
-                }
-                for (int t = 0;; ++t) {
-                    // ---- err and grad at s from the level ranges ----
-                    double ev = 0.0, gv = 0.0;
-                    {
-                        const int up_lo = __shfl_up_sync(0xffffffffu, ib, 1, G);
-                        const i128 lo1 = shfl_up_i128(P1, 1, G), lo2 = shfl_up_i128(P2, 1, G);
-                        const int lo_i = gl == 0 ? 0 : up_lo;
-                        const int hi_i = gl == nb ? n : ib;
-                        if (gl <= nb && hi_i > lo_i) {
-                            const i128 S1 = gl == 0 ? P1 : P1 - lo1;
-                            const i128 S2 = gl == 0 ? P2 : P2 - lo2;
-                            const double v = static_cast<double>(cfg.lmin + gl);
-                            const double cnt = static_cast<double>(hi_i - lo_i);
-                            const double sv = __dmul_rn(s, v);  // exact: float * small int
-                            const DD s1 = unfix(S1, b1), s2 = unfix(S2, b2);
-                            DD e = dd_mul_d(dd_prod(sv, sv), cnt);  // n (s v)^2
-                            e = dd_add(e, dd_mul_d(s1, -2.0 * sv));  // - 2 s v S1
-                            e = dd_add(e, s2);                       // + S2
-                            DD q = dd_mul_d(dd_prod(sv, v), cnt);   // n s v^2
-                            q = dd_add(q, dd_mul_d(s1, -v));         // - v S1
-                            ev = __dadd_rn(e.hi, e.lo);
-                            gv = __dadd_rn(q.hi, q.lo);
-                        }
-                    }
-#pragma unroll
-                    for (int o = G / 2; o; o >>= 1) {
-                        ev = __dadd_rn(ev, __shfl_xor_sync(0xffffffffu, ev, o, G));
-                        gv = __dadd_rn(gv, __shfl_xor_sync(0xffffffffu, gv, o, G));
-                    }
-                    const double err = ev;
-                    const double grad = 2.0 * gv;
-                    if (t == 0) {
-                        e0 = err;
-                        best_err = err;
-                        fixed_err = err;
-                    } else {
-                        if (err < best_err) {  // strict: earliest minimum wins (optimize.cpp:158)
-                            best_err = err;
-                            best_s = s;
-                        }
-                        if (t == cfg.fixed_at) {
-                            fixed_s = s;
-                            fixed_err = err;
-                        }
-                    }
-                    if (t == cfg.steps) break;
-                    s = snap(adam_update(m, vv, s, grad, cfg.bc1[t + 1], cfg.bc2[t + 1], cfg.adam));
-                    inv = __ddiv_rn(1.0, s);
-                    // ---- move the boundaries and their exact prefix sums ----
-                    int nib = ib;
-                    if (own_b) nib = search_from(a, n, ib, level_threshold(cfg.lmin + gl + 1, s, inv));
-                    const int lo = min(nib, ib), hi = max(nib, ib);
-                    const bool grow = nib > ib;
-                    const bool big = (hi - lo) > 8;
-                    if (!big) {
-                        for (int k = lo; k < hi; ++k) {
-                            const float x = a[k];
-                            const double xd = static_cast<double>(x);
-                            const i128 f1 = fix_f(x, b1), f2 = fix_d(__dmul_rn(xd, xd), b2);
-                            if (grow)
-                                P1 += f1, P2 += f2;
-                            else
-                                P1 -= f1, P2 -= f2;
-                        }
-                    }
-                    // large moves: the group sums each range cooperatively; all
-                    // groups iterate the warp-wide maximum count (uniform shuffles)
-                    const unsigned bigw = __ballot_sync(0xffffffffu, big);
-                    unsigned mine = bigw & gmask;
-                    int rounds = __popc(mine);
-#pragma unroll
-                    for (int o = G; o < 32; o <<= 1) rounds = max(rounds, __shfl_xor_sync(0xffffffffu, rounds, o));
-                    for (int it = 0; it < rounds; ++it) {
-                        const bool act = mine != 0;
-                        const int src = act ? ((__ffs(mine) - 1) % G) : 0;
-                        if (act) mine &= mine - 1;
-                        const int blo = __shfl_sync(0xffffffffu, lo, src, G);
-                        const int bhi = __shfl_sync(0xffffffffu, hi, src, G);
-                        const bool bgrow = __shfl_sync(0xffffffffu, grow, src, G) != 0;
-                        i128 s1, s2;
-                        group_range_fix<G>(a, act ? blo : 0, act ? bhi : 0, gl, b1, b2, s1, s2);
-                        if (act && gl == src) {
-                            if (bgrow)
-                                P1 += s1, P2 += s2;
-                            else
-                                P1 -= s1, P2 -= s2;
-                        }
-                    }
-                    ib = nib;
-                }
-                if (cfg.select == EZQ_SELECT_FIXED)
-                    s_fin = (fixed_err <= e0) ? fixed_s : s0;  // optimize.cpp:169-178
-                else
-                    s_fin = best_s;
-                s_rtn = s0;
-            }
-            if (live && gl == 0) {
-                const int64_t gcol = d.col_base + g.col0 + cc;
-                sc.s_rtn[gcol] = s_rtn;
-                sc.s_fin[gcol] = s_fin;
-            }
-        }
+        for (int i = 0; i < IPT; i += 4)  // sorted keys, +inf past n (blocked: 16-byte stores)
+            *reinterpret_cast<float4*>(xo + tid * IPT + i) = make_float4(keys[i], keys[i + 1], keys[i + 2], keys[i + 3]);
+        for (int k = NPAD + tid; k < xstride; k += THREADS) xo[k] = kInf;
+        __syncthreads();  // Ds / sort_tmp / wp / ws / wn / wc reuse
     }
+}
+
+// ---- K3s-b: the Adam loop on the tables -------------------------------------
+// CPW columns per warp (groups of G = 32 / CPW lanes); lane gl owns level
+// threshold lmin + 1 + gl. The tables are read through L1 (a step touches a
+// few lines per threshold), so occupancy is bounded by registers only.
+template <int CPW>
+__global__ void __launch_bounds__(256) k_qrange_tables(const TDesc* __restrict__ td,
+                                                       const K3Group* __restrict__ groups, int nslots, int cpb,
+                                                       int dstride, int tstride, const double* __restrict__ tables,
+                                                       const ColInfo* __restrict__ infos, Scratch sc,
+                                                       CfgDev cfg) {
+    constexpr int G = 32 / CPW;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane % G, grp = lane / G;
+    const int nb = cfg.lmax - cfg.lmin;  // thresholds (<= G - 1)
+    const int64_t wslot = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * CPW;
+    if (wslot >= nslots) return;  // warp-uniform
+    const int slot = static_cast<int>(wslot) + grp;
+    const K3Group g = groups[min(slot, nslots - 1) / cpb];
+    const int cc = slot % cpb;
+    const bool live = slot < nslots && cc < g.ncols;
+    ColInfo ci = {0, 0, 0.f, 0.f, 0.0, 0.0};
+    if (live) ci = infos[slot];
+    ColTab ct;
+    ct.D = tables + static_cast<int64_t>(live ? slot : 0) * tstride;
+    ct.xs = reinterpret_cast<const float*>(ct.D + dstride);
+    ct.n = ci.n;
+    const int n = ci.n;
+    const double mx = n ? fmax(fabs(static_cast<double>(ci.lo)), fabs(static_cast<double>(ci.hi))) : 0.0;
+    const double s0_raw = initial_scale_from_max(mx, cfg.lmax);
+    double s_rtn = static_cast<double>(__double2float_rn(s0_raw));
+    double s_fin = s_rtn;
+    if (cfg.mode == EZQ_MODE_EASYQUANT) {  // uniform across the warp
+        const DD Cd = {ci.chi, ci.clo};
+        double s = snap(s0_raw);
+        const double s0 = s;
+        double m = 0.0, vv = 0.0;
+        double e0 = 0.0, best_err = 0.0, best_s = s, fixed_s = s, fixed_err = 0.0;
+        const bool own = live && gl < nb;
+        const int j = cfg.lmin + 1 + gl;  // this lane's level threshold
+        const bool pos = j >= 1;
+        const int wA = pos ? 2 * j - 1 : 1 - 2 * j;
+        int ib = n >> 1;
+        for (int t = 0;; ++t) {
+            int a = 0;
+            double q = 0.0;
+            if (own) {
+                const double inv = __ddiv_rn(1.0, s);
+                const float X = level_threshold(j, s, inv);
+                ib = t == 0 ? search_from(ct, ib, X) : search_near(ct, ib, X);
+                a = wA * (pos ? n - ib : ib);
+                q = pos ? __ldg(ct.D + ib + 1) : -__ldg(ct.D + ib);
+            }
+#pragma unroll
+            for (int o = G / 2; o; o >>= 1) {  // exact in any order
+                a += __shfl_xor_sync(0xffffffffu, a, o, G);
+                q = __dadd_rn(q, __shfl_xor_sync(0xffffffffu, q, o, G));
+            }
+            const double Ad = static_cast<double>(a);
+            // A s^2 - 2 Q s + C: both products exact as pairs; the three
+            // leading parts summed exactly, the tails added after
+            const DD p1 = dd_prod(Ad, __dmul_rn(s, s));           // s^2 exact
+            const DD p2 = dd_prod(__dmul_rn(-2.0, q), s);
+            const DD h12 = two_sum(p1.hi, p2.hi);
+            const DD h = two_sum(h12.hi, Cd.hi);
+            const double tail = __dadd_rn(__dadd_rn(__dadd_rn(h.lo, h12.lo), __dadd_rn(p1.lo, p2.lo)), Cd.lo);
+            const double err = __dadd_rn(h.hi, tail);
+            const double grad = 2.0 * __dsub_rn(__dmul_rn(Ad, s), q);  // A s exact
+            if (t == 0) {
+                e0 = err;
+                best_err = err;
+                fixed_err = err;
+            } else {
+                if (err < best_err) {  // strict: earliest minimum wins (optimize.cpp:158)
+                    best_err = err;
+                    best_s = s;
+                }
+                if (t == cfg.fixed_at) {
+                    fixed_s = s;
+                    fixed_err = err;
+                }
+            }
+            if (t == cfg.steps) break;
+            s = snap(adam_update(m, vv, s, grad, cfg.bc1[t + 1], cfg.bc2[t + 1], cfg.adam));
+        }
+        if (cfg.select == EZQ_SELECT_FIXED)
+            s_fin = (fixed_err <= e0) ? fixed_s : s0;  // optimize.cpp:169-178
+        else
+            s_fin = best_s;
+        s_rtn = s0;
+    }
+    if (live && gl == 0) {
+        const TDesc& d = td[g.tensor];
+        const int64_t gcol = d.col_base + g.col0 + cc;
+        sc.s_rtn[gcol] = s_rtn;
+        sc.s_fin[gcol] = s_fin;
+    }
+}
+
+struct SortShape {
+    int threads, ipt;
+};
+SortShape sort_shape(int npad) {
+    switch (npad) {
+        case 1024: return {128, 8};
+        case 2048: return {128, 16};
+        case 4096: return {256, 16};
+        default: return {512, 16};
+    }
+}
+
+template <int THREADS, int IPT>
+size_t sort_union_bytes() {
+    typedef cub::BlockRadixSort<float, THREADS, IPT, cub::NullType, kSortRadixBits> Sorter;
+    const size_t d = sizeof(double) * static_cast<size_t>(dpad(THREADS * IPT + 2) + 1);
+    return std::max(sizeof(typename Sorter::TempStorage), d);
+}
+
+size_t sort_smem(int npad, int cpb) {
+    size_t u = 0;
+    switch (npad) {
+        case 1024: u = sort_union_bytes<128, 8>(); break;
+        case 2048: u = sort_union_bytes<128, 16>(); break;
+        case 4096: u = sort_union_bytes<256, 16>(); break;
+        default: u = sort_union_bytes<512, 16>(); break;
+    }
+    return sizeof(float) * static_cast<size_t>(npad) * cpb + ((u + 15) & ~size_t(15));
+}
+
+template <int THREADS, int IPT>
+void launch_sort_t(int ngroups, int cpb, int dstride, int xstride, int tstride, const TDesc* td,
+                   const K3Group* groups, double* tables, ColInfo* infos, cudaStream_t st) {
+    auto k = k_qsort_tables<THREADS, IPT>;
+    const size_t smem = sort_smem(THREADS * IPT, cpb);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k<<<ngroups, THREADS, smem, st>>>(td, groups, cpb, dstride, xstride, tstride, tables, infos);
 }
 
 }  // namespace
 
 int k3s_npad(int64_t rows) {
-    int n = 32;
+    int n = 1024;
     while (n < rows) n <<= 1;
     return n;
 }
 
-size_t k3s_smem(int64_t rows, int cpb) { return sizeof(float) * static_cast<size_t>(k3s_npad(rows)) * cpb; }
+int k3s_dstride(int64_t rows) { return static_cast<int>((rows + 2 + 1) & ~int64_t(1)); }
+static int k3s_xstride(int64_t rows) { return static_cast<int>(std::max<int64_t>(k3s_npad(rows), rows + 8) + 3) & ~3; }
+static int k3s_tstride(int64_t rows) { return k3s_dstride(rows) + k3s_xstride(rows) / 2; }
 
 bool k3s_supported(int bits) { return bits >= 2 && bits <= 5; }
 
-void launch_k3_sorted(int64_t rows, int cpb, const TDesc* td, const K3Group* groups, int ngroups, Scratch sc,
-                      CfgDev cfg, int grid, cudaStream_t st) {
-    if (ngroups == 0) return;
+int k3s_cpb(int64_t rows) {
+    // staged columns per sort CTA: ~32 KB of floats (coalesced row reads)
     const int npad = k3s_npad(rows);
-    const size_t smem = k3s_smem(rows, cpb);
+    return std::max(1, std::min(8, (32 << 10) / (4 * npad)));
+}
+
+size_t k3s_slot_bytes(int64_t rows) { return sizeof(double) * k3s_tstride(rows) + sizeof(ColInfo); }
+
+void launch_k3_sorted(int64_t rows, int cpb, const TDesc* td, const K3Group* groups, int ngroups, Scratch sc,
+                      CfgDev cfg, void* work, size_t work_bytes, cudaStream_t st) {
+    if (ngroups == 0) return;
+    const int npad = k3s_npad(rows), dstride = k3s_dstride(rows);
+    const int xstride = k3s_xstride(rows), tstride = k3s_tstride(rows);
+    // Waves of groups whose tables fit the work buffer, in stream order.
+    // (Overlapping a wave's sort with the previous loop on side streams was
+    // measured slower on B200: 83.5 vs 77.0 ms for the OPT-1.3B set.)
+    const size_t per_group = k3s_slot_bytes(rows) * cpb;
+    const int wave = static_cast<int>(std::max<size_t>(1, std::min<size_t>(ngroups, work_bytes / per_group)));
+    double* tables = static_cast<double*>(work);
+    ColInfo* infos = reinterpret_cast<ColInfo*>(tables + static_cast<size_t>(wave) * cpb * tstride);
+    const SortShape sh = sort_shape(npad);
     const int cpw = (cfg.lmax - cfg.lmin) <= 15 ? 2 : 1;
-    const int threads = 32 * ((cpb + cpw - 1) / cpw);
-    if (cpw == 2) {
-        auto k = k_qrange_sorted<2>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        k<<<grid, threads, smem, st>>>(td, groups, ngroups, sc, cfg, npad, cpb);
-    } else {
-        auto k = k_qrange_sorted<1>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        k<<<grid, threads, smem, st>>>(td, groups, ngroups, sc, cfg, npad, cpb);
+    for (int g0 = 0; g0 < ngroups; g0 += wave) {
+        const int ng = std::min(wave, ngroups - g0);
+        switch (sh.threads * 100 + sh.ipt) {
+            case 12808: launch_sort_t<128, 8>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
+            case 12816: launch_sort_t<128, 16>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
+            case 25616: launch_sort_t<256, 16>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
+            default: launch_sort_t<512, 16>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
+        }
+        const int nslots = ng * cpb;
+        const int warps = (nslots + cpw - 1) / cpw;
+        const int grid = (warps + 7) / 8;
+        if (cpw == 2)
+            k_qrange_tables<2><<<grid, 256, 0, st>>>(td, groups + g0, nslots, cpb, dstride, tstride, tables, infos, sc,
+                                                          cfg);
+        else
+            k_qrange_tables<1><<<grid, 256, 0, st>>>(td, groups + g0, nslots, cpb, dstride, tstride, tables, infos, sc,
+                                                          cfg);
+        count_launch(2);
     }
-    count_launch();
 }
 
 }  // namespace ezq

@@ -197,17 +197,21 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
         int grid = 0;
         int sorted_cpb = 0;  // > 0: K3s (sorted columns), columns per CTA
     };
-    static const bool k3_sorted = std::getenv("EZQ_K3_SORTED") != nullptr;  // opt-in while K3s is slower
+    static const bool k3_sorted = std::getenv("EZQ_K3_STREAMING") == nullptr;  // A/B: streaming K3 only
     std::vector<Plan> plans;
-    size_t tot_groups = 0, gstrip_floats = 0;
+    size_t tot_groups = 0, gstrip_floats = 0, k3s_work = 0;
+    static const size_t k3s_work_cap = [] {
+        const char* e = std::getenv("EZQ_K3S_WORK_MB");
+        return (e ? static_cast<size_t>(std::atoll(e)) : size_t(2048)) << 20;
+    }();
     if (cfg_status == EZQ_OK) {
         for (auto& kv : by_rows) {
             Plan p;
-            if (k3_sorted && kv.first <= kK3sMaxRows && k3s_supported(cfg->bits)) {
-                // K3s: one warp per column; columns per CTA so that ~3 CTAs fit per SM.
-                const size_t per_col = k3s_smem(kv.first, 1);
-                const int cpb = static_cast<int>(std::max<size_t>(1, std::min<size_t>(8, (size_t(74) << 10) / per_col)));
+            if (k3_sorted && eq && kv.first <= kK3sMaxRows && k3s_supported(cfg->bits)) {
+                // K3s: a CTA sorts its columns, then two columns per warp.
+                const int cpb = k3s_cpb(kv.first);
                 p.sorted_cpb = cpb;
+                const size_t per_group = k3s_slot_bytes(kv.first) * cpb;
                 p.kl.rows = kv.first;
                 for (int i : kv.second)
                     for (int64_t c0 = 0; c0 < cols[i]; c0 += cpb)
@@ -216,6 +220,9 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
                 p.goff = tot_groups;
                 tot_groups += p.groups.size();
                 p.grid = static_cast<int>(p.groups.size());
+                k3s_work = std::max(k3s_work, per_group * std::max<size_t>(1, std::min<size_t>(
+                                                              p.groups.size(), k3s_work_cap / per_group)) +
+                                                  512);
                 plans.push_back(std::move(p));
                 continue;
             }
@@ -260,6 +267,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     ar.reserve(sizeof(K3Group) * tot_groups);
     ar.reserve(sizeof(float) * tot_in);
     ar.reserve(sizeof(float) * gstrip_floats);
+    ar.reserve(k3s_work);
     if (int s = ar.allocate(st)) return s;
     TStats* d_stats = ar.take<TStats>(n);
     TDesc* d_desc = ar.take<TDesc>(n);
@@ -284,6 +292,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     K3Group* d_groups = ar.take<K3Group>(tot_groups);
     float* d_in = ar.take<float>(tot_in);
     float* d_gstrip = ar.take<float>(gstrip_floats);
+    void* d_k3s_work = ar.take<unsigned char>(k3s_work);
     int2* d_tiles = ar.take<int2>(tiles.size());
     if (!ar.ok()) return set_error(EZQ_ERR_CUDA, "internal: arena overflow (quantize_batch)");
 
@@ -414,7 +423,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
         const int p3 = prof_begin("qrange", st);
         if (p.sorted_cpb)
             launch_k3_sorted(p.kl.rows, p.sorted_cpb, d_desc, d_groups + p.goff, static_cast<int>(p.groups.size()),
-                             sc, cd, p.grid, st);
+                             sc, cd, d_k3s_work, k3s_work, st);
         else
             launch_k3(p.kl, d_desc, d_groups + p.goff, static_cast<int>(p.groups.size()), sc, cd,
                       d_gstrip, p.grid, st);
