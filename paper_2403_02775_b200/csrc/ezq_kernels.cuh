@@ -144,7 +144,6 @@ void launch_k3(const K3Launch& kl, const TDesc* td, const K3Group* groups, int n
 // them; groups are processed in waves that fit work_bytes.
 constexpr int64_t kK3sMaxRows = 8192;
 int k3s_npad(int64_t rows);
-int k3s_dstride(int64_t rows);
 bool k3s_supported(int bits);
 int k3s_cpb(int64_t rows);               // columns per sort CTA (group width)
 size_t k3s_slot_bytes(int64_t rows);     // table + info bytes per column

@@ -156,10 +156,12 @@ __device__ __forceinline__ int search_from(const ColTab& c, int guess, float X) 
     return lo;
 }
 
-// Same, for a boundary that moved little since `guess`: an aligned window of
-// eight floats (two 16-byte loads, one round trip) usually holds the answer;
-// two window moves, then the galloping search.
-__device__ __forceinline__ int search_near(const ColTab& c, int guess, float X) {
+// Same, starting from a predicted index: an aligned window of eight floats
+// (two 16-byte loads, one round trip) usually holds the answer; two window
+// moves, then the galloping search. `span` returns x[k0+7] - x[k0] of the
+// final window (the local spacing for the next prediction; +inf/0 when the
+// window reached the padding or a run of equal values).
+__device__ __forceinline__ int search_near(const ColTab& c, int guess, float X, float& span) {
     int k0 = max(guess - 4, 0) & ~3;
 #pragma unroll 1
     for (int r = 0; r < 3; ++r) {
@@ -167,6 +169,7 @@ __device__ __forceinline__ int search_near(const ColTab& c, int guess, float X) 
         const float4 b = __ldg(reinterpret_cast<const float4*>(c.xs + k0 + 4));
         const int cnt = (a.x < X) + (a.y < X) + (a.z < X) + (a.w < X) + (b.x < X) + (b.y < X) + (b.z < X) +
                         (b.w < X);
+        span = b.w - a.x;
         if (cnt == 0 && k0 > 0) {
             k0 = max(k0 - 8, 0);
         } else if (cnt == 8) {
@@ -175,6 +178,7 @@ __device__ __forceinline__ int search_near(const ColTab& c, int guess, float X) 
             return k0 + cnt;
         }
     }
+    span = 0.f;
     return search_from(c, k0, X);
 }
 
@@ -241,14 +245,20 @@ __global__ void __launch_bounds__(THREADS) k_qsort_tables(const TDesc* __restric
     const TDesc& d = td[g.tensor];
     const float olo = d.st->olo, ohi = d.st->ohi;
     const int64_t R = d.rows, C = d.cols;
-    for (int idx = tid; idx < cpb * NPAD; idx += THREADS) {
-        const int cc = idx % cpb, r = idx / cpb;
-        float v = kInf;
-        if (cc < g.ncols && r < R) {
-            const float x = d.W[static_cast<int64_t>(r) * C + g.col0 + cc];
-            v = is_outlier_f(x, olo, ohi) ? kInf : x;
+    for (int base = 0; base < cpb * NPAD; base += 8 * THREADS) {  // 8 loads in flight
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int idx = base + u * THREADS + tid;
+            const int cc = idx % cpb, r = idx / cpb;
+            v[u] = (cc < g.ncols && r < R) ? __ldg(d.W + static_cast<int64_t>(r) * C + g.col0 + cc) : kInf;
         }
-        stage[cc * NPAD + r] = v;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int idx = base + u * THREADS + tid;
+            const int cc = idx % cpb, r = idx / cpb;
+            stage[cc * NPAD + r] = is_outlier_f(v[u], olo, ohi) ? kInf : v[u];
+        }
     }
     __syncthreads();
     for (int c = 0; c < g.ncols; ++c) {
@@ -257,25 +267,39 @@ __global__ void __launch_bounds__(THREADS) k_qsort_tables(const TDesc* __restric
 #pragma unroll
         for (int i = 0; i < IPT; ++i) keys[i] = stage[c * NPAD + i * THREADS + tid];
         Sorter(sort_tmp).Sort(keys);  // blocked: thread t holds ranks [t*IPT, t*IPT + IPT)
+        // counts, sums of x per sign, and C = sum x^2: x^2 is exact in fp64
+        // and, walking the negatives up and the non-negatives down, each
+        // term is no larger than the running sum, so Fast2Sum keeps C exact
+        // to double-double
         int cneg = 0, cfin = 0;
         double tneg = 0.0, tpos = 0.0;
         DD sq = {0.0, 0.0};
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
-            const float x = keys[i];
-            const double xd = static_cast<double>(x);
-            if (x < kInf) {
-                ++cfin;
-                sq = dd_add(sq, dd_prod(xd, xd));
-                if (x < 0.f) {
-                    ++cneg;
-                    tneg = __dadd_rn(tneg, xd);
-                }
+            const double xd = static_cast<double>(keys[i]);
+            if (keys[i] < 0.f) {
+                ++cneg;
+                tneg = __dadd_rn(tneg, xd);
+                const double y = __dmul_rn(xd, xd), t = __dadd_rn(sq.hi, y);
+                sq.lo = __dadd_rn(sq.lo, __dsub_rn(y, __dsub_rn(t, sq.hi)));
+                sq.hi = t;
             }
         }
+        DD sp = {0.0, 0.0};
 #pragma unroll
-        for (int i = IPT - 1; i >= 0; --i)
-            if (keys[i] >= 0.f && keys[i] < kInf) tpos = __dadd_rn(tpos, static_cast<double>(keys[i]));
+        for (int i = IPT - 1; i >= 0; --i) {
+            const double xd = static_cast<double>(keys[i]);
+            if (keys[i] >= 0.f && keys[i] < kInf) {
+                tpos = __dadd_rn(tpos, xd);
+                const double y = __dmul_rn(xd, xd), t = __dadd_rn(sp.hi, y);
+                sp.lo = __dadd_rn(sp.lo, __dsub_rn(y, __dsub_rn(t, sp.hi)));
+                sp.hi = t;
+            }
+        }
+        sq = dd_add(two_sum(sq.hi, sq.lo), two_sum(sp.hi, sp.lo));
+        cfin = cneg;
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) cfin += keys[i] >= 0.f && keys[i] < kInf;
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
             cneg += __shfl_xor_sync(0xffffffffu, cneg, o);
@@ -343,19 +367,22 @@ __global__ void __launch_bounds__(THREADS) k_qsort_tables(const TDesc* __restric
 }
 
 // ---- K3s-b: the Adam loop on the tables -------------------------------------
-// CPW columns per warp (groups of G = 32 / CPW lanes); lane gl owns level
-// threshold lmin + 1 + gl. The tables are read through L1 (a step touches a
-// few lines per threshold), so occupancy is bounded by registers only.
-template <int CPW>
+// G lanes per column (32 / G columns per warp), each lane owning TPL level
+// thresholds: index u * G + gl -> level lmin + 1 + index. The per-step scalar
+// work (err/grad, Adam) is shared by the column's lanes, so packing more
+// columns per warp divides it; the TPL searches of a lane are independent
+// (ILP). The tables are read through L1 (a step touches a few lines per
+// threshold), so occupancy is bounded by registers only.
+template <int G, int TPL>
 __global__ void __launch_bounds__(256) k_qrange_tables(const TDesc* __restrict__ td,
                                                        const K3Group* __restrict__ groups, int nslots, int cpb,
                                                        int dstride, int tstride, const double* __restrict__ tables,
                                                        const ColInfo* __restrict__ infos, Scratch sc,
                                                        CfgDev cfg) {
-    constexpr int G = 32 / CPW;
+    constexpr int CPW = 32 / G;
     const int lane = threadIdx.x & 31;
     const int gl = lane % G, grp = lane / G;
-    const int nb = cfg.lmax - cfg.lmin;  // thresholds (<= G - 1)
+    const int nb = cfg.lmax - cfg.lmin;  // thresholds (<= G * TPL)
     const int64_t wslot = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * CPW;
     if (wslot >= nslots) return;  // warp-uniform
     const int slot = static_cast<int>(wslot) + grp;
@@ -379,20 +406,44 @@ __global__ void __launch_bounds__(256) k_qrange_tables(const TDesc* __restrict__
         const double s0 = s;
         double m = 0.0, vv = 0.0;
         double e0 = 0.0, best_err = 0.0, best_s = s, fixed_s = s, fixed_err = 0.0;
-        const bool own = live && gl < nb;
-        const int j = cfg.lmin + 1 + gl;  // this lane's level threshold
-        const bool pos = j >= 1;
-        const int wA = pos ? 2 * j - 1 : 1 - 2 * j;
-        int ib = n >> 1;
+        bool own[TPL];
+        int jl[TPL], wA[TPL], ib[TPL];
+        float Xp[TPL], span[TPL];  // previous threshold; x[k0+7] - x[k0] near it
+#pragma unroll
+        for (int u = 0; u < TPL; ++u) {
+            const int idx = u * G + gl;
+            own[u] = live && idx < nb;
+            jl[u] = cfg.lmin + 1 + idx;
+            wA[u] = jl[u] >= 1 ? 2 * jl[u] - 1 : 1 - 2 * jl[u];
+            ib[u] = n >> 1;
+            Xp[u] = 0.f;
+            span[u] = 0.f;
+        }
         for (int t = 0;; ++t) {
             int a = 0;
             double q = 0.0;
-            if (own) {
-                const double inv = __ddiv_rn(1.0, s);
+            const double inv = __ddiv_rn(1.0, s);
+#pragma unroll
+            for (int u = 0; u < TPL; ++u) {
+                if (!own[u]) continue;
+                const int j = jl[u];
                 const float X = level_threshold(j, s, inv);
-                ib = t == 0 ? search_from(ct, ib, X) : search_near(ct, ib, X);
-                a = wA * (pos ? n - ib : ib);
-                q = pos ? __ldg(ct.D + ib + 1) : -__ldg(ct.D + ib);
+                if (t == 0) {
+                    ib[u] = search_from(ct, ib[u], X);
+                    span[u] = 0.f;
+                    if (ib[u] + 4 <= n && ib[u] >= 4) span[u] = __ldg(ct.xs + ib[u] + 3) - __ldg(ct.xs + ib[u] - 4);
+                } else {
+                    // predict the shift from the threshold's move and the
+                    // spacing seen around the old position
+                    const float sp = span[u];
+                    const float dk = (sp > 0.f && sp < 3.0e38f) ? (X - Xp[u]) * (7.f / sp) : 0.f;
+                    const int guess = ib[u] + static_cast<int>(rintf(fminf(fmaxf(dk, -256.f), 256.f)));
+                    ib[u] = search_near(ct, min(max(guess, 0), n), X, span[u]);
+                }
+                Xp[u] = X;
+                const bool pos = j >= 1;
+                a += wA[u] * (pos ? n - ib[u] : ib[u]);
+                q = __dadd_rn(q, pos ? __ldg(ct.D + ib[u] + 1) : -__ldg(ct.D + ib[u]));
             }
 #pragma unroll
             for (int o = G / 2; o; o >>= 1) {  // exact in any order
@@ -402,7 +453,7 @@ __global__ void __launch_bounds__(256) k_qrange_tables(const TDesc* __restrict__
             const double Ad = static_cast<double>(a);
             // A s^2 - 2 Q s + C: both products exact as pairs; the three
             // leading parts summed exactly, the tails added after
-            const DD p1 = dd_prod(Ad, __dmul_rn(s, s));           // s^2 exact
+            const DD p1 = dd_prod(Ad, __dmul_rn(s, s));  // s^2 exact
             const DD p2 = dd_prod(__dmul_rn(-2.0, q), s);
             const DD h12 = two_sum(p1.hi, p2.hi);
             const DD h = two_sum(h12.hi, Cd.hi);
@@ -438,6 +489,16 @@ __global__ void __launch_bounds__(256) k_qrange_tables(const TDesc* __restrict__
         sc.s_rtn[gcol] = s_rtn;
         sc.s_fin[gcol] = s_fin;
     }
+}
+
+template <int G, int TPL>
+void launch_loop_t(int nslots, int cpb, int dstride, int tstride, const TDesc* td, const K3Group* groups,
+                   const double* tables, const ColInfo* infos, const Scratch& sc, const CfgDev& cfg,
+                   cudaStream_t st) {
+    constexpr int CPW = 32 / G;
+    const int warps = (nslots + CPW - 1) / CPW;
+    const int grid = (warps + 7) / 8;
+    k_qrange_tables<G, TPL><<<grid, 256, 0, st>>>(td, groups, nslots, cpb, dstride, tstride, tables, infos, sc, cfg);
 }
 
 struct SortShape {
@@ -487,7 +548,7 @@ int k3s_npad(int64_t rows) {
     return n;
 }
 
-int k3s_dstride(int64_t rows) { return static_cast<int>((rows + 2 + 1) & ~int64_t(1)); }
+static int k3s_dstride(int64_t rows) { return static_cast<int>((rows + 2 + 1) & ~int64_t(1)); }
 static int k3s_xstride(int64_t rows) { return static_cast<int>(std::max<int64_t>(k3s_npad(rows), rows + 8) + 3) & ~3; }
 static int k3s_tstride(int64_t rows) { return k3s_dstride(rows) + k3s_xstride(rows) / 2; }
 
@@ -514,7 +575,6 @@ void launch_k3_sorted(int64_t rows, int cpb, const TDesc* td, const K3Group* gro
     double* tables = static_cast<double*>(work);
     ColInfo* infos = reinterpret_cast<ColInfo*>(tables + static_cast<size_t>(wave) * cpb * tstride);
     const SortShape sh = sort_shape(npad);
-    const int cpw = (cfg.lmax - cfg.lmin) <= 15 ? 2 : 1;
     for (int g0 = 0; g0 < ngroups; g0 += wave) {
         const int ng = std::min(wave, ngroups - g0);
         switch (sh.threads * 100 + sh.ipt) {
@@ -524,14 +584,10 @@ void launch_k3_sorted(int64_t rows, int cpb, const TDesc* td, const K3Group* gro
             default: launch_sort_t<512, 16>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
         }
         const int nslots = ng * cpb;
-        const int warps = (nslots + cpw - 1) / cpw;
-        const int grid = (warps + 7) / 8;
-        if (cpw == 2)
-            k_qrange_tables<2><<<grid, 256, 0, st>>>(td, groups + g0, nslots, cpb, dstride, tstride, tables, infos, sc,
-                                                          cfg);
+        if (cfg.lmax - cfg.lmin <= 15)
+            launch_loop_t<16, 1>(nslots, cpb, dstride, tstride, td, groups + g0, tables, infos, sc, cfg, st);
         else
-            k_qrange_tables<1><<<grid, 256, 0, st>>>(td, groups + g0, nslots, cpb, dstride, tstride, tables, infos, sc,
-                                                          cfg);
+            launch_loop_t<32, 1>(nslots, cpb, dstride, tstride, td, groups + g0, tables, infos, sc, cfg, st);
         count_launch(2);
     }
 }
