@@ -498,7 +498,11 @@ void launch_loop_t(int nslots, int cpb, int dstride, int tstride, const TDesc* t
     constexpr int CPW = 32 / G;
     const int warps = (nslots + CPW - 1) / CPW;
     const int grid = (warps + 7) / 8;
-    k_qrange_tables<G, TPL><<<grid, 256, 0, st>>>(td, groups, nslots, cpb, dstride, tstride, tables, infos, sc, cfg);
+    static const int occ_smem = std::getenv("EZQ_K3S_LOOP_SMEM") ? std::atoi(std::getenv("EZQ_K3S_LOOP_SMEM")) : 0;
+    if (occ_smem > 48 * 1024)
+        cudaFuncSetAttribute(k_qrange_tables<G, TPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, occ_smem);
+    k_qrange_tables<G, TPL><<<grid, 256, occ_smem, st>>>(td, groups, nslots, cpb, dstride, tstride, tables, infos,
+                                                          sc, cfg);
 }
 
 struct SortShape {

@@ -100,7 +100,8 @@ int upload(T* d, const std::vector<T>& h, cudaStream_t st) {
     if (t_stage.base && at + bytes <= t_stage.cap) {
         std::memcpy(t_stage.base + at, h.data(), bytes);
         t_stage.off = at + bytes;
-        EZQ_CK(cudaMemcpyAsync(d, t_stage.base + at, bytes, cudaMemcpyHostToDevice, st));
+        // SM loads, not the DMA queue: no wait behind bulk H2D copies
+        if (int e = ingest_h2d(d, t_stage.base + at, bytes, st)) return e;
     } else {
         EZQ_CK(cudaMemcpyAsync(d, h.data(), bytes, cudaMemcpyHostToDevice, st));
     }
@@ -186,6 +187,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     dblk_base[n] = tot_dblk;
     pblk_base[n] = tot_pblk;
 
+    trace("qb: descriptors done");
     // ---- K3 plans: one launch per distinct row count ----
     const bool eq = mode == EZQ_MODE_EASYQUANT;
     std::map<int64_t, std::vector<int>> by_rows;
@@ -252,6 +254,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     std::vector<double> bc;
     bias_tables(cfg, bc);
 
+    trace("qb: plans done");
     // ---- arena ----
     Arena ar;
     ar.reserve(sizeof(TStats) * n);
@@ -296,6 +299,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     int2* d_tiles = ar.take<int2>(tiles.size());
     if (!ar.ok()) return set_error(EZQ_ERR_CUDA, "internal: arena overflow (quantize_batch)");
 
+    trace("qb: arena done");
     // ---- inputs ----
     int64_t in_off = 0;
     for (int i = 0; i < n; ++i) {
@@ -330,6 +334,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
         if (int s = upload(d_groups + p.goff, p.groups, st)) return s;
     }
 
+    trace("qb: inputs done");
     // ---- phase 1 ----
     int64_t tot_elems = 0;
     for (int i = 0; i < n; ++i) tot_elems += hd[i].n;
@@ -351,7 +356,9 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     }
     EZQ_CK(cudaGetLastError());
     EZQ_CK(cudaMemcpyAsync(hs.data(), d_stats, sizeof(TStats) * n, cudaMemcpyDeviceToHost, st));
+    trace("phase1 sync begin", n);
     EZQ_CK(cudaStreamSynchronize(st));
+    trace("phase1 sync end", n);
     for (int i = 0; i < n; ++i) {
         if (hs[i].bad_index != kNoBad) {  // types.cpp:17-20
             if (failed) *failed = i;
@@ -370,6 +377,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
             }
     }
 
+    trace("qb: phase1 checked");
     // ---- outputs (device) ----
     struct Out {
         uint8_t* packed = nullptr;
@@ -404,6 +412,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
         return s;
     }
 
+    trace("qb: outputs allocated");
     // ---- phase 2 ----
     const CfgDev cd = make_cfg(cfg, mode, d_bc);
     int64_t tot_out = 0;
@@ -413,6 +422,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
         launch_detect_write(d_desc, d_dblk_base, n, tot_dblk, sc, st);
         prof_end(p2, st, 4.0 * tot_elems + 12.0 * tot_out);
     }
+    trace("qb: detect launched");
     for (auto& p : plans) {
         // Algorithmic work: 7 flop (1 DMUL + 3 DFMA) per normal element-step.
         double normals = 0.0;
@@ -428,11 +438,13 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
             launch_k3(p.kl, d_desc, d_groups + p.goff, static_cast<int>(p.groups.size()), sc, cd,
                       d_gstrip, p.grid, st);
         prof_end(p3, st, 7.0 * normals * steps1);
+        trace("qb: k3 plan launched", p.kl.rows);
     }
     int p4 = prof_begin("seqerr", st);
     launch_seq_errors(d_desc, d_tiles, static_cast<int>(tiles.size()), sc, cd, st);
     launch_tensor_totals(d_desc, n, sc, st);
     prof_end(p4, st, 4.0 * tot_elems);
+    trace("qb: seqerr launched");
     int64_t tot_packed = 0;
     for (int i = 0; i < n; ++i) tot_packed += ezq_packed_size(hd[i].n, cfg->bits);
     p4 = prof_begin("pack", st);
@@ -447,6 +459,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     }
     EZQ_CK(cudaMemcpyAsync(hs.data(), d_stats, sizeof(TStats) * n, cudaMemcpyDeviceToHost, st));
 
+    trace("qb: phase2 launched");
     // ---- results ----
     std::vector<std::unique_ptr<ezq_qweight>> res(n);
     cudaStream_t ost = st;  // stream of the output copies
@@ -493,7 +506,9 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
             o = Out{};
         }
     }
+    trace("phase2 sync begin", n);
     cudaError_t se = cudaStreamSynchronize(st);
+    trace("phase2 sync end", n);
     if (out_mem == EZQ_MEM_HOST) free_dout();
     auto drain = [&]() {  // deferred copies must land before their buffers go
         if (ost != st) cudaStreamSynchronize(ost);
@@ -553,11 +568,22 @@ int quantize_batch_host(const float* const* Ws, const int64_t* rows, const int64
     // later ones are large (fewer partial K3 waves, fewer host syncs).
     static const int64_t kFirstBytes = std::getenv("EZQ_FIRST_MB") ? (std::atoll(std::getenv("EZQ_FIRST_MB")) << 20)
                                                                     : (512ll << 20);
+    // ... and so is the last: its compute and D2H are the exposed tail.
+    static const int64_t kLastBytes = std::getenv("EZQ_LAST_MB") ? (std::atoll(std::getenv("EZQ_LAST_MB")) << 20)
+                                                                  : (256ll << 20);
+    int tail = n;
+    for (int64_t b = 0; tail > 1;) {
+        const int64_t tb = 4 * std::max<int64_t>(rows[tail - 1], 0) * std::max<int64_t>(cols[tail - 1], 0);
+        if (b + tb > kLastBytes && tail < n) break;
+        b += tb;
+        --tail;
+    }
     for (int i = 0; i < n;) {
         int j = i;
         int64_t bytes = 0;
         const int64_t cap = chunks.empty() ? std::min(kFirstBytes, kChunkBytes) : kChunkBytes;
-        while (j < n && (j == i || bytes + 4 * rows[j] * cols[j] <= cap)) {
+        const int end = i < tail ? tail : n;
+        while (j < end && (j == i || bytes + 4 * rows[j] * cols[j] <= cap)) {
             bytes += 4 * std::max<int64_t>(rows[j], 0) * std::max<int64_t>(cols[j], 0);
             ++j;
         }
@@ -579,8 +605,14 @@ int quantize_batch_host(const float* const* Ws, const int64_t* rows, const int64
     cudaStream_t st = pick_stream(user_stream, dev);
     cudaStream_t cs = copy_stream(dev);
     float* buf[2] = {nullptr, nullptr};
-    EZQ_CK(cudaMallocAsync(reinterpret_cast<void**>(&buf[0]), max_bytes, st));
-    EZQ_CK(cudaMallocAsync(reinterpret_cast<void**>(&buf[1]), max_bytes, st));
+    size_t buf_cap[2] = {0, 0};
+    for (int k = 0; k < 2; ++k) {
+        buf[k] = static_cast<float*>(block_get(max_bytes, st, &buf_cap[k]));
+        if (!buf[k]) {
+            if (k) block_put(buf[0], buf_cap[0], st);
+            return cuda_error(cudaErrorMemoryAllocation, "chunk buffers");
+        }
+    }
     cudaEvent_t in_ready[2], done[2];
     for (int k = 0; k < 2; ++k) {
         cudaEventCreateWithFlags(&in_ready[k], cudaEventDisableTiming);
@@ -594,12 +626,17 @@ int quantize_batch_host(const float* const* Ws, const int64_t* rows, const int64
         int64_t off = 0;
         for (int i = chunks[c].first; i < chunks[c].second; ++i) {
             const int64_t nb = 4 * rows[i] * cols[i];
-            if (int e = ingest_h2d(reinterpret_cast<char*>(buf[b]) + off, Ws[i], nb, cs)) return e;
+            static const bool dma = std::getenv("EZQ_H2D_SM") == nullptr;
+            if (dma)
+                EZQ_CK(cudaMemcpyAsync(reinterpret_cast<char*>(buf[b]) + off, Ws[i], nb, cudaMemcpyHostToDevice, cs));
+            else if (int e = ingest_h2d(reinterpret_cast<char*>(buf[b]) + off, Ws[i], nb, cs))
+                return e;
             off += nb;
         }
         EZQ_CK(cudaEventRecord(in_ready[b], cs));
         return EZQ_OK;
     };
+    trace("host batch start", static_cast<long long>(chunks.size()));
     int status = issue_copy(0);
     if (!status && chunks.size() > 1) status = issue_copy(1);
     for (size_t c = 0; c < chunks.size() && !status; ++c) {
@@ -626,10 +663,12 @@ int quantize_batch_host(const float* const* Ws, const int64_t* rows, const int64
         cudaEventRecord(done[b], st);
         if (c + 2 < chunks.size()) status = issue_copy(c + 2);
     }
+    trace("host batch drain");
     cudaStreamSynchronize(cs);
     cudaStreamSynchronize(d2h_stream(dev));  // deferred artifact copies
-    cudaFreeAsync(buf[0], st);
-    cudaFreeAsync(buf[1], st);
+    trace("host batch end");
+    block_put(buf[0], buf_cap[0], st);
+    block_put(buf[1], buf_cap[1], st);
     for (int k = 0; k < 2; ++k) {
         cudaEventDestroy(in_ready[k]);
         cudaEventDestroy(done[k]);

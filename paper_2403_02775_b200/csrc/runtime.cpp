@@ -6,6 +6,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <chrono>
+#include <cstdio>
 #include <mutex>
 #include <cstdlib>
 #include <unordered_map>
@@ -155,6 +157,18 @@ const DeviceInfo& device_info(int dev) {
 
 std::string fmt_double(double v) { return std::to_string(v); }
 
+bool trace_on() {
+    static const bool on = std::getenv("EZQ_TRACE") != nullptr;
+    return on;
+}
+
+void trace(const char* what, long long a) {
+    if (!trace_on()) return;
+    static const auto t0 = std::chrono::steady_clock::now();
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, "[ezq %10.3f ms] %s %lld\n", ms, what, a);
+}
+
 namespace {
 std::mutex g_pin_mu;
 std::unordered_map<void*, size_t> g_pin_live;                  // ptr -> size
@@ -178,6 +192,7 @@ void* host_alloc(size_t bytes) {
         }
     }
     void* p = nullptr;
+    trace("host_alloc miss", static_cast<long long>(bytes));
     if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) {
         // No device (host-only codec use) or pinned memory exhausted:
         // pageable memory serves host artifacts just as well.
@@ -283,21 +298,111 @@ CfgDev make_cfg(const ezq_config* c, int mode, const double* bc_dev) {
     return d;
 }
 
+// Device scratch blocks are recycled across calls: cudaMallocAsync of a
+// size the pool has not seen maps fresh memory (tens to hundreds of ms for
+// GB-sized arenas, measured on B200), which made repeated batch calls
+// erratic. A returned block carries an event recorded on its last stream;
+// the next user waits on it.
+namespace {
+struct CachedBlock {
+    void* p;
+    size_t bytes;
+    int dev;
+    cudaEvent_t ready;
+};
+std::mutex g_blk_mu;
+std::vector<CachedBlock> g_blk_free;
+size_t g_blk_cached = 0;
+constexpr size_t kBlkCacheLimit = 12ull << 30;
+}  // namespace
+
+void* block_get(size_t need, cudaStream_t st, size_t* got) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lk(g_blk_mu);
+        int best = -1;
+        for (int i = 0; i < static_cast<int>(g_blk_free.size()); ++i) {
+            const CachedBlock& b = g_blk_free[i];
+            if (b.dev != dev || b.bytes < need || b.bytes > 2 * need + (size_t(64) << 20)) continue;
+            if (best < 0 || b.bytes < g_blk_free[best].bytes) best = i;
+        }
+        if (best >= 0) {
+            CachedBlock b = g_blk_free[best];
+            g_blk_free.erase(g_blk_free.begin() + best);
+            g_blk_cached -= b.bytes;
+            cudaStreamWaitEvent(st, b.ready, 0);
+            cudaEventDestroy(b.ready);
+            *got = b.bytes;
+            return b.p;
+        }
+    }
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, need, st) != cudaSuccess) {
+        cudaGetLastError();
+        // release the cache and retry once
+        std::vector<CachedBlock> drop;
+        {
+            std::lock_guard<std::mutex> lk(g_blk_mu);
+            drop.swap(g_blk_free);
+            g_blk_cached = 0;
+        }
+        for (auto& b : drop) {
+            cudaStreamWaitEvent(st, b.ready, 0);
+            cudaEventDestroy(b.ready);
+            cudaFreeAsync(b.p, st);
+        }
+        if (cudaMallocAsync(&p, need, st) != cudaSuccess) return nullptr;
+    }
+    *got = need;
+    return p;
+}
+
+void block_put(void* p, size_t bytes, cudaStream_t st) {
+    if (!p) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (bytes > kBlkCacheLimit) {
+        cudaFreeAsync(p, st);
+        return;
+    }
+    cudaEvent_t ev;
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    cudaEventRecord(ev, st);
+    std::vector<CachedBlock> evict;
+    {
+        std::lock_guard<std::mutex> lk(g_blk_mu);
+        g_blk_free.push_back({p, bytes, dev, ev});
+        g_blk_cached += bytes;
+        while (g_blk_cached > kBlkCacheLimit && !g_blk_free.empty()) {  // oldest first
+            evict.push_back(g_blk_free.front());
+            g_blk_cached -= g_blk_free.front().bytes;
+            g_blk_free.erase(g_blk_free.begin());
+        }
+    }
+    for (auto& b : evict) {
+        cudaStreamWaitEvent(st, b.ready, 0);
+        cudaEventDestroy(b.ready);
+        cudaFreeAsync(b.p, st);
+    }
+}
+
 int Arena::allocate(cudaStream_t st) {
     owner_ = st;
     off_ = 0;
     if (need_ == 0) return EZQ_OK;
-    EZQ_CK(cudaMallocAsync(reinterpret_cast<void**>(&base_), need_, st));
+    base_ = static_cast<char*>(block_get(need_, st, &cap_));
+    if (!base_) return cuda_error(cudaErrorMemoryAllocation, "arena allocation");
     return EZQ_OK;
 }
 
 void Arena::release(cudaStream_t st) {
-    if (base_) cudaFreeAsync(base_, st);
+    block_put(base_, cap_, st);
     base_ = nullptr;
 }
 
 Arena::~Arena() {
-    if (base_) cudaFreeAsync(base_, owner_);
+    if (base_) block_put(base_, cap_, owner_);
 }
 
 }  // namespace ezq

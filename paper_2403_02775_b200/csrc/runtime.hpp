@@ -48,7 +48,12 @@ int validate_config(const ezq_config* cfg, std::string* msg);
 CfgDev make_cfg(const ezq_config* cfg, int mode, const double* bc_dev);
 void bias_tables(const ezq_config* cfg, std::vector<double>& host);  // bc1 | bc2
 
-// Bump allocator over one cudaMallocAsync block.
+// Recycled device scratch (see runtime.cpp): block_get waits on the block's
+// last use; block_put records it on `st`.
+void* block_get(size_t need, cudaStream_t st, size_t* got);
+void block_put(void* p, size_t bytes, cudaStream_t st);
+
+// Bump allocator over one recycled device block.
 class Arena {
 public:
     // Every take() realigns to 256 bytes; reserve() must be called once per
@@ -72,11 +77,15 @@ public:
 
 private:
     char* base_ = nullptr;
-    size_t need_ = 0, off_ = 0;
+    size_t need_ = 0, off_ = 0, cap_ = 0;
     cudaStream_t owner_ = nullptr;
 };
 
 std::string fmt_double(double v);  // std::to_string(double) formatting
+
+// EZQ_TRACE=1: host-side timestamps of the pipeline phases on stderr.
+bool trace_on();
+void trace(const char* what, long long a = -1);
 
 // Pinned host memory for library-owned host outputs: blocks are recycled by
 // exact size (repeat calls on the same shapes reuse them), so D2H copies run
