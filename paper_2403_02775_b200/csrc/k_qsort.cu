@@ -492,10 +492,11 @@ __global__ void __launch_bounds__(256) k_qrange_tables(const TDesc* __restrict__
 }
 
 template <int G, int TPL>
-void launch_loop_t(int nslots, int cpb, int dstride, int tstride, const TDesc* td, const K3Group* groups,
+void launch_loop_t(int64_t nslots64, int cpb, int dstride, int tstride, const TDesc* td, const K3Group* groups,
                    const double* tables, const ColInfo* infos, const Scratch& sc, const CfgDev& cfg,
                    cudaStream_t st) {
     constexpr int CPW = 32 / G;
+    const int nslots = static_cast<int>(nslots64);
     const int warps = (nslots + CPW - 1) / CPW;
     const int grid = (warps + 7) / 8;
     static const int occ_smem = std::getenv("EZQ_K3S_LOOP_SMEM") ? std::atoi(std::getenv("EZQ_K3S_LOOP_SMEM")) : 0;
@@ -581,17 +582,22 @@ void launch_k3_sorted(int64_t rows, int cpb, const TDesc* td, const K3Group* gro
     const SortShape sh = sort_shape(npad);
     for (int g0 = 0; g0 < ngroups; g0 += wave) {
         const int ng = std::min(wave, ngroups - g0);
+        const int64_t nslots = static_cast<int64_t>(ng) * cpb;
+        const int ps = prof_begin("qsort", st);
         switch (sh.threads * 100 + sh.ipt) {
             case 12808: launch_sort_t<128, 8>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
             case 12816: launch_sort_t<128, 16>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
             case 25616: launch_sort_t<256, 16>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
             default: launch_sort_t<512, 16>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
         }
-        const int nslots = ng * cpb;
+        prof_end(ps, st, static_cast<double>(nslots) * static_cast<double>(rows));
+        // work: column-steps (a step = one err/grad evaluation + Adam update)
+        const int pl = prof_begin("qrange", st);
         if (cfg.lmax - cfg.lmin <= 15)
             launch_loop_t<16, 1>(nslots, cpb, dstride, tstride, td, groups + g0, tables, infos, sc, cfg, st);
         else
             launch_loop_t<32, 1>(nslots, cpb, dstride, tstride, td, groups + g0, tables, infos, sc, cfg, st);
+        prof_end(pl, st, static_cast<double>(nslots) * (cfg.mode == EZQ_MODE_EASYQUANT ? cfg.steps + 1 : 1));
         count_launch(2);
     }
 }

@@ -430,14 +430,15 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
         for (int i = 0; i < n; ++i)
             if (rows[i] == p.kl.rows) normals += static_cast<double>(hd[i].n - hs[i].n_out);
         const double steps1 = (mode == EZQ_MODE_EASYQUANT) ? cfg->steps + 1.0 : 0.0;
-        const int p3 = prof_begin("qrange", st);
-        if (p.sorted_cpb)
+        if (p.sorted_cpb) {  // profiled inside ("qsort" / "qrange")
             launch_k3_sorted(p.kl.rows, p.sorted_cpb, d_desc, d_groups + p.goff, static_cast<int>(p.groups.size()),
                              sc, cd, d_k3s_work, k3s_work, st);
-        else
+        } else {
+            const int p3 = prof_begin("qrange_stream", st);
             launch_k3(p.kl, d_desc, d_groups + p.goff, static_cast<int>(p.groups.size()), sc, cd,
                       d_gstrip, p.grid, st);
-        prof_end(p3, st, 7.0 * normals * steps1);
+            prof_end(p3, st, 7.0 * normals * steps1);
+        }
         trace("qb: k3 plan launched", p.kl.rows);
     }
     int p4 = prof_begin("seqerr", st);

@@ -14,6 +14,6 @@ for rows, cols in sorted(set(shapes)):
         torch.cuda.synchronize(); t = time.perf_counter()
         N.quantize_batch(Ws, cfg, out_mem=N.MEM_DEVICE).close()
         torch.cuda.synchronize(); dt = time.perf_counter() - t
-        prof = N.profile_read("qrange")
+        prof = {"ms": N.profile_read("qrange")["ms"] + N.profile_read("qsort")["ms"]}
         N.profile_enable(False)
         print(f"{rows}x{cols} x4 steps={steps}: total {dt*1e3:.1f} ms, qrange {prof['ms']:.1f} ms")

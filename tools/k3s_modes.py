@@ -16,6 +16,6 @@ for _ in range(3):
     N.quantize_batch(Ws, cfg, out_mem=N.MEM_DEVICE).close()
 torch.cuda.synchronize()
 dt = (time.perf_counter() - t0) / 3
-prof = N.profile_read("qrange")
+prof = {"ms": N.profile_read("qrange")["ms"] + N.profile_read("qsort")["ms"]}
 N.profile_enable(False)
 print(f"dev->dev {dt*1e3:.1f} ms/call, qrange {prof['ms']/3:.1f} ms/call")
