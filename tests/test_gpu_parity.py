@@ -293,3 +293,46 @@ def test_property_roundtrip_large(gpu, O):
     mask[o["row"], o["col"]] = False
     inside = mask & (W <= 8 * s) & (W >= -7 * s)
     assert np.all(np.abs(d.astype(np.float64) - W)[inside] <= (s / 2 + 1e-6).repeat(W.shape[0], 0)[inside])
+
+
+# ---- sorted-column K3 (K3s) edge cases ----------------------------------------
+def _k3s_cases(O):
+    rng = np.random.default_rng(4242)
+    out = []
+    # heavy duplicates: a handful of distinct values (runs of equal keys, zero spacing)
+    W = (np.round(rng.standard_normal((2048, 40)) * 4) / 4 * 0.02).astype(np.float32)
+    out.append(("duplicates", W, Config()))
+    # one-signed columns (no negatives / no non-negatives), a zero column, mixed magnitudes
+    W = O.gaussian(1500, 24, 77, 0.02)
+    W[:, 0] = np.abs(W[:, 0])
+    W[:, 1] = -np.abs(W[:, 1]) - np.float32(1e-3)
+    W[:, 2] = 0.0
+    W[:, 3] *= np.float32(1e4)
+    W[:, 4] *= np.float32(1e-4)
+    W[:5, 5] = np.float32(7.0)          # a few large values in one column (planted outliers)
+    out.append(("signs_zero_scales", W.astype(np.float32), Config()))
+    # tiny magnitudes (subnormal neighbourhood) and huge ones
+    out.append(("tiny", (O.gaussian(700, 16, 78) * np.float32(1e-36)).astype(np.float32), Config()))
+    out.append(("huge", (O.gaussian(700, 16, 79) * np.float32(1e30)).astype(np.float32), Config()))
+    # large Adam steps: boundaries jump far (galloping fallback)
+    out.append(("big_lr", O.gaussian(2048, 32, 80, 0.02), Config(lr=3e-2)))
+    # k = 5 (one column per warp) and k = 2, 3 at a K3s row count
+    out.append(("k5", O.gaussian(2048, 33, 81, 0.02), Config(bits=5)))
+    out.append(("k3", O.gaussian(3000, 33, 82, 0.02), Config(bits=3)))
+    out.append(("k2", O.gaussian(1024, 33, 83, 0.02), Config(bits=2)))
+    # the K3s / streaming row boundary
+    out.append(("rows8192_k5", O.gaussian(8192, 9, 84, 0.02), Config(bits=5, steps=80)))
+    out.append(("rows8193", O.gaussian(8193, 9, 85, 0.02), Config(steps=80)))
+    # fixed-step selection, short trajectories
+    out.append(("fixed3", O.gaussian(2048, 16, 86, 0.02), Config(select="fixed", select_step=2, steps=3)))
+    out.append(("steps0", O.gaussian(2048, 16, 87, 0.02), Config(steps=0)))
+    return out
+
+
+@pytest.mark.parametrize("idx", range(12))
+def test_k3s_edge_cases(gpu, O, idx):
+    name, W, cfg = _k3s_cases(O)[idx]
+    q = gpu.quantize_tensor(W, cfg)
+    r = O.quantize(W, cfg, "easyquant")
+    assert r["status"] == "ok", name
+    assert_same_quant(q, r)
