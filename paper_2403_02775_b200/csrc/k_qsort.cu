@@ -114,7 +114,7 @@ struct ColInfo {
 };
 
 // Per-slot table: D (dstride doubles, above), then the sorted normals as
-// floats, +inf-padded to n + 8 (xs: the search runs on these).
+// floats, +inf-padded to n + 16 (xs: the search runs on these).
 struct ColTab {
     const double* D;
     const float* xs;
@@ -156,25 +156,26 @@ __device__ __forceinline__ int search_from(const ColTab& c, int guess, float X) 
     return lo;
 }
 
-// Same, starting from a predicted index: an aligned window of eight floats
-// (two 16-byte loads, one round trip) usually holds the answer; two window
-// moves, then the galloping search. `span` returns x[k0+7] - x[k0] of the
+// Same, starting from a predicted index: an aligned window of sixteen floats
+// (four 16-byte loads, one round trip) usually holds the answer; one window
+// move, then the galloping search. `span` returns x[k0+15] - x[k0] of the
 // final window (the local spacing for the next prediction; +inf/0 when the
 // window reached the padding or a run of equal values).
 __device__ __forceinline__ int search_near(const ColTab& c, int guess, float X, float& span) {
-    int k0 = max(guess - 4, 0) & ~3;
+    int k0 = max(guess - 6, 0) & ~3;  // guess sits at k0 + 6 .. k0 + 9
 #pragma unroll 1
-    for (int r = 0; r < 3; ++r) {
-        const float4 a = __ldg(reinterpret_cast<const float4*>(c.xs + k0));
-        const float4 b = __ldg(reinterpret_cast<const float4*>(c.xs + k0 + 4));
+    for (int r = 0; r < 2; ++r) {
+        const float4* w = reinterpret_cast<const float4*>(c.xs + k0);
+        const float4 a = __ldg(w), b = __ldg(w + 1), e = __ldg(w + 2), f = __ldg(w + 3);
         const int cnt = (a.x < X) + (a.y < X) + (a.z < X) + (a.w < X) + (b.x < X) + (b.y < X) + (b.z < X) +
-                        (b.w < X);
-        span = b.w - a.x;
+                        (b.w < X) + (e.x < X) + (e.y < X) + (e.z < X) + (e.w < X) + (f.x < X) + (f.y < X) +
+                        (f.z < X) + (f.w < X);
         if (cnt == 0 && k0 > 0) {
-            k0 = max(k0 - 8, 0);
-        } else if (cnt == 8) {
-            k0 += 8;
+            k0 = max(k0 - 16, 0);
+        } else if (cnt == 16) {
+            k0 += 16;
         } else {
+            span = f.w - a.x;  // 15 gaps: the local spacing for the next prediction
             return k0 + cnt;
         }
     }
@@ -431,12 +432,12 @@ __global__ void __launch_bounds__(256) k_qrange_tables(const TDesc* __restrict__
                 if (t == 0) {
                     ib[u] = search_from(ct, ib[u], X);
                     span[u] = 0.f;
-                    if (ib[u] + 4 <= n && ib[u] >= 4) span[u] = __ldg(ct.xs + ib[u] + 3) - __ldg(ct.xs + ib[u] - 4);
+                    if (ib[u] + 8 <= n && ib[u] >= 8) span[u] = __ldg(ct.xs + ib[u] + 7) - __ldg(ct.xs + ib[u] - 8);
                 } else {
                     // predict the shift from the threshold's move and the
                     // spacing seen around the old position
                     const float sp = span[u];
-                    const float dk = (sp > 0.f && sp < 3.0e38f) ? (X - Xp[u]) * (7.f / sp) : 0.f;
+                    const float dk = (sp > 0.f && sp < 3.0e38f) ? (X - Xp[u]) * (15.f / sp) : 0.f;
                     const int guess = ib[u] + static_cast<int>(rintf(fminf(fmaxf(dk, -256.f), 256.f)));
                     ib[u] = search_near(ct, min(max(guess, 0), n), X, span[u]);
                 }
@@ -510,10 +511,11 @@ struct SortShape {
     int threads, ipt;
 };
 SortShape sort_shape(int npad) {
+    static const int alt = std::getenv("EZQ_K3S_SORT_ALT") ? std::atoi(std::getenv("EZQ_K3S_SORT_ALT")) : 0;
     switch (npad) {
         case 1024: return {128, 8};
-        case 2048: return {128, 16};
-        case 4096: return {256, 16};
+        case 2048: return alt ? SortShape{256, 8} : SortShape{128, 16};
+        case 4096: return alt ? SortShape{512, 8} : SortShape{256, 16};
         default: return {512, 16};
     }
 }
@@ -525,22 +527,17 @@ size_t sort_union_bytes() {
     return std::max(sizeof(typename Sorter::TempStorage), d);
 }
 
-size_t sort_smem(int npad, int cpb) {
-    size_t u = 0;
-    switch (npad) {
-        case 1024: u = sort_union_bytes<128, 8>(); break;
-        case 2048: u = sort_union_bytes<128, 16>(); break;
-        case 4096: u = sort_union_bytes<256, 16>(); break;
-        default: u = sort_union_bytes<512, 16>(); break;
-    }
-    return sizeof(float) * static_cast<size_t>(npad) * cpb + ((u + 15) & ~size_t(15));
+template <int THREADS, int IPT>
+size_t sort_smem(int cpb) {
+    const size_t u = sort_union_bytes<THREADS, IPT>();
+    return sizeof(float) * static_cast<size_t>(THREADS * IPT) * cpb + ((u + 15) & ~size_t(15));
 }
 
 template <int THREADS, int IPT>
 void launch_sort_t(int ngroups, int cpb, int dstride, int xstride, int tstride, const TDesc* td,
                    const K3Group* groups, double* tables, ColInfo* infos, cudaStream_t st) {
     auto k = k_qsort_tables<THREADS, IPT>;
-    const size_t smem = sort_smem(THREADS * IPT, cpb);
+    const size_t smem = sort_smem<THREADS, IPT>(cpb);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k<<<ngroups, THREADS, smem, st>>>(td, groups, cpb, dstride, xstride, tstride, tables, infos);
 }
@@ -554,15 +551,16 @@ int k3s_npad(int64_t rows) {
 }
 
 static int k3s_dstride(int64_t rows) { return static_cast<int>((rows + 2 + 1) & ~int64_t(1)); }
-static int k3s_xstride(int64_t rows) { return static_cast<int>(std::max<int64_t>(k3s_npad(rows), rows + 8) + 3) & ~3; }
+static int k3s_xstride(int64_t rows) { return static_cast<int>(std::max<int64_t>(k3s_npad(rows), rows + 16) + 3) & ~3; }
 static int k3s_tstride(int64_t rows) { return k3s_dstride(rows) + k3s_xstride(rows) / 2; }
 
 bool k3s_supported(int bits) { return bits >= 2 && bits <= 5; }
 
 int k3s_cpb(int64_t rows) {
     // staged columns per sort CTA: ~32 KB of floats (coalesced row reads)
+    static const int kb = std::getenv("EZQ_K3S_STAGE_KB") ? std::atoi(std::getenv("EZQ_K3S_STAGE_KB")) : 32;
     const int npad = k3s_npad(rows);
-    return std::max(1, std::min(8, (32 << 10) / (4 * npad)));
+    return std::max(1, std::min(8, (kb << 10) / (4 * npad)));
 }
 
 size_t k3s_slot_bytes(int64_t rows) { return sizeof(double) * k3s_tstride(rows) + sizeof(ColInfo); }
@@ -588,6 +586,8 @@ void launch_k3_sorted(int64_t rows, int cpb, const TDesc* td, const K3Group* gro
             case 12808: launch_sort_t<128, 8>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
             case 12816: launch_sort_t<128, 16>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
             case 25616: launch_sort_t<256, 16>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
+            case 25608: launch_sort_t<256, 8>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
+            case 51208: launch_sort_t<512, 8>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
             default: launch_sort_t<512, 16>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
         }
         prof_end(ps, st, static_cast<double>(nslots) * static_cast<double>(rows));
