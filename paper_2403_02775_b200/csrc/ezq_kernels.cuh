@@ -97,6 +97,8 @@ struct CfgDev {
     AdamConsts adam;
     const double* bc1;  // [steps+1], index t
     const double* bc2;
+    const double* rbc1;  // RN(1 / bc1[t]), RN(1 / bc2[t])
+    const double* rbc2;
 };
 
 // ---- K3 work decomposition -------------------------------------------------

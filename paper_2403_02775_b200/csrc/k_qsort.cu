@@ -246,19 +246,19 @@ __global__ void __launch_bounds__(THREADS) k_qsort_tables(const TDesc* __restric
     const TDesc& d = td[g.tensor];
     const float olo = d.st->olo, ohi = d.st->ohi;
     const int64_t R = d.rows, C = d.cols;
+    const int lcpb = __ffs(cpb) - 1;  // cpb is a power of two
     for (int base = 0; base < cpb * NPAD; base += 8 * THREADS) {  // 8 loads in flight
         float v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int idx = base + u * THREADS + tid;
-            const int cc = idx % cpb, r = idx / cpb;
+            const int cc = idx & (cpb - 1), r = idx >> lcpb;
             v[u] = (cc < g.ncols && r < R) ? __ldg(d.W + static_cast<int64_t>(r) * C + g.col0 + cc) : kInf;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int idx = base + u * THREADS + tid;
-            const int cc = idx % cpb, r = idx / cpb;
-            stage[cc * NPAD + r] = is_outlier_f(v[u], olo, ohi) ? kInf : v[u];
+            stage[(idx & (cpb - 1)) * NPAD + (idx >> lcpb)] = is_outlier_f(v[u], olo, ohi) ? kInf : v[u];
         }
     }
     __syncthreads();
@@ -274,23 +274,21 @@ __global__ void __launch_bounds__(THREADS) k_qsort_tables(const TDesc* __restric
         // to double-double
         int cneg = 0, cfin = 0;
         double tneg = 0.0, tpos = 0.0;
-        DD sq = {0.0, 0.0};
+        DD sq = {0.0, 0.0}, sp = {0.0, 0.0};
 #pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-            const double xd = static_cast<double>(keys[i]);
-            if (keys[i] < 0.f) {
-                ++cneg;
+        for (int i = 0; i < IPT; ++i) {  // two independent chains: negatives up, the rest down
+            const float xn = keys[i], xp = keys[IPT - 1 - i];
+            cneg += xn < 0.f;
+            cfin += xn < kInf;
+            if (xn < 0.f) {
+                const double xd = static_cast<double>(xn);
                 tneg = __dadd_rn(tneg, xd);
                 const double y = __dmul_rn(xd, xd), t = __dadd_rn(sq.hi, y);
                 sq.lo = __dadd_rn(sq.lo, __dsub_rn(y, __dsub_rn(t, sq.hi)));
                 sq.hi = t;
             }
-        }
-        DD sp = {0.0, 0.0};
-#pragma unroll
-        for (int i = IPT - 1; i >= 0; --i) {
-            const double xd = static_cast<double>(keys[i]);
-            if (keys[i] >= 0.f && keys[i] < kInf) {
+            if (xp >= 0.f && xp < kInf) {
+                const double xd = static_cast<double>(xp);
                 tpos = __dadd_rn(tpos, xd);
                 const double y = __dmul_rn(xd, xd), t = __dadd_rn(sp.hi, y);
                 sp.lo = __dadd_rn(sp.lo, __dsub_rn(y, __dsub_rn(t, sp.hi)));
@@ -298,9 +296,6 @@ __global__ void __launch_bounds__(THREADS) k_qsort_tables(const TDesc* __restric
             }
         }
         sq = dd_add(two_sum(sq.hi, sq.lo), two_sum(sp.hi, sp.lo));
-        cfin = cneg;
-#pragma unroll
-        for (int i = 0; i < IPT; ++i) cfin += keys[i] >= 0.f && keys[i] < kInf;
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
             cneg += __shfl_xor_sync(0xffffffffu, cneg, o);
@@ -423,7 +418,7 @@ __global__ void __launch_bounds__(256) k_qrange_tables(const TDesc* __restrict__
         for (int t = 0;; ++t) {
             int a = 0;
             double q = 0.0;
-            const double inv = __ddiv_rn(1.0, s);
+            const double inv = __drcp_rn(s);  // RN(1/s), as the reference's 1.0 / s
 #pragma unroll
             for (int u = 0; u < TPL; ++u) {
                 if (!own[u]) continue;
@@ -437,7 +432,7 @@ __global__ void __launch_bounds__(256) k_qrange_tables(const TDesc* __restrict__
                     // predict the shift from the threshold's move and the
                     // spacing seen around the old position
                     const float sp = span[u];
-                    const float dk = (sp > 0.f && sp < 3.0e38f) ? (X - Xp[u]) * (15.f / sp) : 0.f;
+                    const float dk = (sp > 0.f && sp < 3.0e38f) ? __fdividef(15.f * (X - Xp[u]), sp) : 0.f;
                     const int guess = ib[u] + static_cast<int>(rintf(fminf(fmaxf(dk, -256.f), 256.f)));
                     ib[u] = search_near(ct, min(max(guess, 0), n), X, span[u]);
                 }
@@ -476,7 +471,8 @@ __global__ void __launch_bounds__(256) k_qrange_tables(const TDesc* __restrict__
                 }
             }
             if (t == cfg.steps) break;
-            s = snap(adam_update(m, vv, s, grad, cfg.bc1[t + 1], cfg.bc2[t + 1], cfg.adam));
+            s = snap(adam_update_tab(m, vv, s, grad, cfg.bc1[t + 1], cfg.bc2[t + 1], cfg.rbc1[t + 1],
+                                     cfg.rbc2[t + 1], cfg.adam));
         }
         if (cfg.select == EZQ_SELECT_FIXED)
             s_fin = (fixed_err <= e0) ? fixed_s : s0;  // optimize.cpp:169-178
@@ -500,10 +496,10 @@ void launch_loop_t(int64_t nslots64, int cpb, int dstride, int tstride, const TD
     const int nslots = static_cast<int>(nslots64);
     const int warps = (nslots + CPW - 1) / CPW;
     const int grid = (warps + 7) / 8;
-    static const int occ_smem = std::getenv("EZQ_K3S_LOOP_SMEM") ? std::atoi(std::getenv("EZQ_K3S_LOOP_SMEM")) : 0;
-    if (occ_smem > 48 * 1024)
-        cudaFuncSetAttribute(k_qrange_tables<G, TPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, occ_smem);
-    k_qrange_tables<G, TPL><<<grid, 256, occ_smem, st>>>(td, groups, nslots, cpb, dstride, tstride, tables, infos,
+    static const int carve = std::getenv("EZQ_K3S_CARVE") ? std::atoi(std::getenv("EZQ_K3S_CARVE")) : -1;
+    if (carve >= 0)  // tables are read through L1: the shared-memory carveout
+        cudaFuncSetAttribute(k_qrange_tables<G, TPL>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+    k_qrange_tables<G, TPL><<<grid, 256, 0, st>>>(td, groups, nslots, cpb, dstride, tstride, tables, infos,
                                                           sc, cfg);
 }
 

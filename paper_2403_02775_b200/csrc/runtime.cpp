@@ -265,12 +265,14 @@ int validate_config(const ezq_config* c, std::string* msg) {
 
 void bias_tables(const ezq_config* c, std::vector<double>& h) {
     const int n = (c->steps > 0 ? c->steps : 0) + 1;
-    h.assign(2 * static_cast<size_t>(n), 1.0);
+    h.assign(4 * static_cast<size_t>(n), 1.0);
     for (int t = 1; t < n; ++t) {
         // optimize.cpp:90-91 evaluates exactly these with glibc pow.
         h[t] = 1.0 - std::pow(c->beta1, static_cast<double>(t));
         h[n + t] = 1.0 - std::pow(c->beta2, static_cast<double>(t));
     }
+    // correctly rounded reciprocals (IEEE division) for div_by_table
+    for (int t = 0; t < 2 * n; ++t) h[2 * n + t] = 1.0 / h[t];
 }
 
 CfgDev make_cfg(const ezq_config* c, int mode, const double* bc_dev) {
@@ -295,6 +297,8 @@ CfgDev make_cfg(const ezq_config* c, int mode, const double* bc_dev) {
     const int n = (c->steps > 0 ? c->steps : 0) + 1;
     d.bc1 = bc_dev;
     d.bc2 = bc_dev ? bc_dev + n : nullptr;
+    d.rbc1 = bc_dev ? bc_dev + 2 * n : nullptr;
+    d.rbc2 = bc_dev ? bc_dev + 3 * n : nullptr;
     return d;
 }
 

@@ -44,7 +44,7 @@ const DeviceInfo& device_info(int dev);
 int validate_config(const ezq_config* cfg, std::string* msg);
 
 // Builds the device-side config; the bias-correction tables must be uploaded
-// by the caller into `bc` (2 * (steps + 1) doubles: bc1 then bc2).
+// by the caller into `bc` (4 * (steps + 1) doubles: bc1, bc2, 1/bc1, 1/bc2).
 CfgDev make_cfg(const ezq_config* cfg, int mode, const double* bc_dev);
 void bias_tables(const ezq_config* cfg, std::vector<double>& host);  // bc1 | bc2
 
