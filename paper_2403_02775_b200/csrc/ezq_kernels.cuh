@@ -106,7 +106,7 @@ struct K3Group {
     int32_t tensor;
     int32_t col0;
     int32_t ncols;
-    int32_t pad;
+    int32_t row0;  // K3s row piece: first row (0 for the streaming K3)
 };
 
 struct K3Launch {
@@ -141,14 +141,20 @@ size_t k3_small_smem(const K3Launch& kl, int teams);
 void set_k3_width(K3Launch& kl, int teams);
 void launch_k3(const K3Launch& kl, const TDesc* td, const K3Group* groups, int ngroups,
                Scratch sc, CfgDev cfg, float* gstrip, int grid, cudaStream_t st);
-// K3s (k_qsort.cu): sorted-column q_range loop for rows <= kK3sMaxRows:
-// a sort kernel writes per-column tables into `work`, a loop kernel reads
-// them; groups are processed in waves that fit work_bytes.
-constexpr int64_t kK3sMaxRows = 8192;
+// K3s (k_qsort.cu): sorted-column q_range loop. Columns longer than
+// kK3sPieceRows are sorted in k3s_pieces(rows) independent row pieces whose
+// counts and sums add. A sort kernel writes per-piece tables into `work`, a
+// loop kernel reads them; groups are processed in waves that fit work_bytes.
+constexpr int64_t kK3sPieceRows = 8192;
+constexpr int kK3sMaxPieces = 8;
+int k3s_pieces(int64_t rows);            // 0: not supported (use the streaming K3)
+int64_t k3s_piece_rows(int64_t rows);    // rows of a (full) piece
 int k3s_npad(int64_t rows);
 bool k3s_supported(int bits);
-int k3s_cpb(int64_t rows);               // columns per sort CTA (group width)
-size_t k3s_slot_bytes(int64_t rows);     // table + info bytes per column
+int k3s_cpb(int64_t piece_rows);         // columns per sort CTA (group width)
+size_t k3s_slot_bytes(int64_t piece_rows);  // table + info bytes per column piece
+// groups: for every column group, `pieces` consecutive entries (row0 = 0,
+// piece_rows, 2 piece_rows, ...).
 void launch_k3_sorted(int64_t rows, int cpb, const TDesc* td, const K3Group* groups, int ngroups, Scratch sc,
                       CfgDev cfg, void* work, size_t work_bytes, cudaStream_t st);
 void launch_seq_errors(const TDesc* td, const int2* tiles, int ntiles, Scratch sc, CfgDev cfg,

@@ -225,7 +225,7 @@ __device__ __forceinline__ void block_scans(double vp, double vs, double& ep, do
 // doubles) and ColInfo go to global memory for the loop kernel.
 template <int THREADS, int IPT>
 __global__ void __launch_bounds__(THREADS) k_qsort_tables(const TDesc* __restrict__ td,
-                                                          const K3Group* __restrict__ groups, int cpb,
+                                                          const K3Group* __restrict__ groups, int cpb, int prows,
                                                           int dstride, int xstride, int tstride,
                                                           double* __restrict__ tables,
                                                           ColInfo* __restrict__ infos) {
@@ -245,7 +245,9 @@ __global__ void __launch_bounds__(THREADS) k_qsort_tables(const TDesc* __restric
     const K3Group g = groups[blockIdx.x];
     const TDesc& d = td[g.tensor];
     const float olo = d.st->olo, ohi = d.st->ohi;
-    const int64_t R = d.rows, C = d.cols;
+    const int64_t C = d.cols;
+    const int64_t R = min(static_cast<int64_t>(prows), d.rows - g.row0);  // this piece's rows
+    const float* W0 = d.W + static_cast<int64_t>(g.row0) * C + g.col0;
     const int lcpb = __ffs(cpb) - 1;  // cpb is a power of two
     for (int base = 0; base < cpb * NPAD; base += 8 * THREADS) {  // 8 loads in flight
         float v[8];
@@ -253,7 +255,7 @@ __global__ void __launch_bounds__(THREADS) k_qsort_tables(const TDesc* __restric
         for (int u = 0; u < 8; ++u) {
             const int idx = base + u * THREADS + tid;
             const int cc = idx & (cpb - 1), r = idx >> lcpb;
-            v[u] = (cc < g.ncols && r < R) ? __ldg(d.W + static_cast<int64_t>(r) * C + g.col0 + cc) : kInf;
+            v[u] = (cc < g.ncols && r < R) ? __ldg(W0 + static_cast<int64_t>(r) * C + cc) : kInf;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -503,6 +505,139 @@ void launch_loop_t(int64_t nslots64, int cpb, int dstride, int tstride, const TD
                                                           sc, cfg);
 }
 
+// ---- K3s-b for row pieces / k = 5: one column per warp ------------------------
+// A column of P pieces has P tables; "level >= j" counts and sums add over
+// pieces, so every (threshold, piece) pair is searched independently: lane
+// l takes pairs l, l + 32, ... (PPL per lane) and the warp butterfly sums A
+// and Q -- exact, as every term is (same argument as above). Slots: column c
+// of column group g, piece p is slot (g * P + p) * cpb + c.
+template <int PPL>
+__global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__ td,
+                                                       const K3Group* __restrict__ groups, int ncolgroups, int P,
+                                                       int cpb, int dstride, int tstride,
+                                                       const double* __restrict__ tables,
+                                                       const ColInfo* __restrict__ infos, Scratch sc, CfgDev cfg) {
+    const int lane = threadIdx.x & 31;
+    const int cidx = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int g = cidx / cpb, cc = cidx % cpb;
+    if (g >= ncolgroups) return;  // warp-uniform
+    const K3Group G0 = groups[g * P];
+    if (cc >= G0.ncols) return;  // warp-uniform
+    const int nb = cfg.lmax - cfg.lmin;
+    // column totals over the pieces, in piece order
+    int nall = 0;
+    double mx = 0.0;
+    DD Cd = {0.0, 0.0};
+    for (int p = 0; p < P; ++p) {
+        const ColInfo ci = infos[(g * P + p) * cpb + cc];
+        nall += ci.n;
+        if (ci.n) mx = fmax(mx, fmax(fabs(static_cast<double>(ci.lo)), fabs(static_cast<double>(ci.hi))));
+        Cd = dd_add(Cd, DD{ci.chi, ci.clo});
+    }
+    const double s0_raw = initial_scale_from_max(mx, cfg.lmax);
+    double s_rtn = static_cast<double>(__double2float_rn(s0_raw));
+    double s_fin = s_rtn;
+    if (cfg.mode == EZQ_MODE_EASYQUANT) {  // uniform across the warp
+        double s = snap(s0_raw);
+        const double s0 = s;
+        double m = 0.0, vv = 0.0;
+        double e0 = 0.0, best_err = 0.0, best_s = s, fixed_s = s, fixed_err = 0.0;
+        bool own[PPL];
+        int jl[PPL], np[PPL], ib[PPL];
+        ColTab ct[PPL];
+        float Xp[PPL], sp[PPL];
+#pragma unroll
+        for (int u = 0; u < PPL; ++u) {
+            const int pair = lane + 32 * u;
+            own[u] = pair < nb * P;
+            const int thr = own[u] ? pair % nb : 0, piece = own[u] ? pair / nb : 0;
+            const int slot = (g * P + piece) * cpb + cc;
+            jl[u] = cfg.lmin + 1 + thr;
+            ct[u].D = tables + static_cast<int64_t>(slot) * tstride;
+            ct[u].xs = reinterpret_cast<const float*>(ct[u].D + dstride);
+            ct[u].n = np[u] = own[u] ? infos[slot].n : 0;
+            ib[u] = np[u] >> 1;
+            Xp[u] = 0.f;
+            sp[u] = 0.f;
+        }
+        for (int t = 0;; ++t) {
+            int a = 0;
+            double q = 0.0;
+            const double inv = __drcp_rn(s);  // RN(1/s), as the reference's 1.0 / s
+#pragma unroll
+            for (int u = 0; u < PPL; ++u) {
+                if (!own[u]) continue;
+                const int j = jl[u], n = np[u];
+                const float X = level_threshold(j, s, inv);
+                if (t == 0) {
+                    ib[u] = search_from(ct[u], ib[u], X);
+                    if (ib[u] + 8 <= n && ib[u] >= 8) sp[u] = __ldg(ct[u].xs + ib[u] + 7) - __ldg(ct[u].xs + ib[u] - 8);
+                } else {
+                    const float spu = sp[u];
+                    const float dk = (spu > 0.f && spu < 3.0e38f) ? __fdividef(15.f * (X - Xp[u]), spu) : 0.f;
+                    const int guess = ib[u] + static_cast<int>(rintf(fminf(fmaxf(dk, -256.f), 256.f)));
+                    ib[u] = search_near(ct[u], min(max(guess, 0), n), X, sp[u]);
+                }
+                Xp[u] = X;
+                const bool pos = j >= 1;
+                a += (pos ? 2 * j - 1 : 1 - 2 * j) * (pos ? n - ib[u] : ib[u]);
+                q = __dadd_rn(q, pos ? __ldg(ct[u].D + ib[u] + 1) : -__ldg(ct[u].D + ib[u]));
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {  // exact in any order
+                a += __shfl_xor_sync(0xffffffffu, a, o);
+                q = __dadd_rn(q, __shfl_xor_sync(0xffffffffu, q, o));
+            }
+            const double Ad = static_cast<double>(a);
+            const DD p1 = dd_prod(Ad, __dmul_rn(s, s));  // s^2 exact
+            const DD p2 = dd_prod(__dmul_rn(-2.0, q), s);
+            const DD h12 = two_sum(p1.hi, p2.hi);
+            const DD h = two_sum(h12.hi, Cd.hi);
+            const double tail = __dadd_rn(__dadd_rn(__dadd_rn(h.lo, h12.lo), __dadd_rn(p1.lo, p2.lo)), Cd.lo);
+            const double err = __dadd_rn(h.hi, tail);
+            const double grad = 2.0 * __dsub_rn(__dmul_rn(Ad, s), q);  // A s exact
+            if (t == 0) {
+                e0 = err;
+                best_err = err;
+                fixed_err = err;
+            } else {
+                if (err < best_err) {  // strict: earliest minimum wins (optimize.cpp:158)
+                    best_err = err;
+                    best_s = s;
+                }
+                if (t == cfg.fixed_at) {
+                    fixed_s = s;
+                    fixed_err = err;
+                }
+            }
+            if (t == cfg.steps) break;
+            s = snap(adam_update_tab(m, vv, s, grad, cfg.bc1[t + 1], cfg.bc2[t + 1], cfg.rbc1[t + 1],
+                                     cfg.rbc2[t + 1], cfg.adam));
+        }
+        if (cfg.select == EZQ_SELECT_FIXED)
+            s_fin = (fixed_err <= e0) ? fixed_s : s0;  // optimize.cpp:169-178
+        else
+            s_fin = best_s;
+        s_rtn = s0;
+    }
+    if (lane == 0) {
+        const TDesc& d = td[G0.tensor];
+        const int64_t gcol = d.col_base + G0.col0 + cc;
+        sc.s_rtn[gcol] = s_rtn;
+        sc.s_fin[gcol] = s_fin;
+    }
+}
+
+template <int PPL>
+void launch_pieces_t(int ncolgroups, int P, int cpb, int dstride, int tstride, const TDesc* td,
+                     const K3Group* groups, const double* tables, const ColInfo* infos, const Scratch& sc,
+                     const CfgDev& cfg, cudaStream_t st) {
+    const int64_t cols = static_cast<int64_t>(ncolgroups) * cpb;  // one warp each
+    const int grid = static_cast<int>((cols + 7) / 8);
+    k_qrange_pieces<PPL><<<grid, 256, 0, st>>>(td, groups, ncolgroups, P, cpb, dstride, tstride, tables, infos, sc,
+                                                cfg);
+}
+
 struct SortShape {
     int threads, ipt;
 };
@@ -512,6 +647,7 @@ SortShape sort_shape(int npad) {
         case 1024: return {128, 8};
         case 2048: return alt ? SortShape{256, 8} : SortShape{128, 16};
         case 4096: return alt ? SortShape{512, 8} : SortShape{256, 16};
+        case 6144: return {384, 16};
         default: return {512, 16};
     }
 }
@@ -530,20 +666,31 @@ size_t sort_smem(int cpb) {
 }
 
 template <int THREADS, int IPT>
-void launch_sort_t(int ngroups, int cpb, int dstride, int xstride, int tstride, const TDesc* td,
+void launch_sort_t(int ngroups, int cpb, int prows, int dstride, int xstride, int tstride, const TDesc* td,
                    const K3Group* groups, double* tables, ColInfo* infos, cudaStream_t st) {
     auto k = k_qsort_tables<THREADS, IPT>;
     const size_t smem = sort_smem<THREADS, IPT>(cpb);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k<<<ngroups, THREADS, smem, st>>>(td, groups, cpb, dstride, xstride, tstride, tables, infos);
+    k<<<ngroups, THREADS, smem, st>>>(td, groups, cpb, prows, dstride, xstride, tstride, tables, infos);
 }
 
 }  // namespace
 
 int k3s_npad(int64_t rows) {
+    if (rows > 4096 && rows <= 6144) return 6144;  // 384 threads x 16 (e.g. 12288- and 11008-row pieces)
     int n = 1024;
     while (n < rows) n <<= 1;
     return n;
+}
+
+int k3s_pieces(int64_t rows) {
+    const int64_t p = (rows + kK3sPieceRows - 1) / kK3sPieceRows;
+    return p <= kK3sMaxPieces ? static_cast<int>(std::max<int64_t>(p, 1)) : 0;
+}
+
+int64_t k3s_piece_rows(int64_t rows) {
+    const int p = std::max(k3s_pieces(rows), 1);
+    return (rows + p - 1) / p;
 }
 
 static int k3s_dstride(int64_t rows) { return static_cast<int>((rows + 2 + 1) & ~int64_t(1)); }
@@ -554,9 +701,8 @@ bool k3s_supported(int bits) { return bits >= 2 && bits <= 5; }
 
 int k3s_cpb(int64_t rows) {
     // staged columns per sort CTA: ~32 KB of floats (coalesced row reads)
-    static const int kb = std::getenv("EZQ_K3S_STAGE_KB") ? std::atoi(std::getenv("EZQ_K3S_STAGE_KB")) : 32;
     const int npad = k3s_npad(rows);
-    return std::max(1, std::min(8, (kb << 10) / (4 * npad)));
+    return std::max(1, std::min(8, (32 << 10) / (4 * npad)));
 }
 
 size_t k3s_slot_bytes(int64_t rows) { return sizeof(double) * k3s_tstride(rows) + sizeof(ColInfo); }
@@ -564,36 +710,52 @@ size_t k3s_slot_bytes(int64_t rows) { return sizeof(double) * k3s_tstride(rows) 
 void launch_k3_sorted(int64_t rows, int cpb, const TDesc* td, const K3Group* groups, int ngroups, Scratch sc,
                       CfgDev cfg, void* work, size_t work_bytes, cudaStream_t st) {
     if (ngroups == 0) return;
-    const int npad = k3s_npad(rows), dstride = k3s_dstride(rows);
-    const int xstride = k3s_xstride(rows), tstride = k3s_tstride(rows);
-    // Waves of groups whose tables fit the work buffer, in stream order.
-    // (Overlapping a wave's sort with the previous loop on side streams was
-    // measured slower on B200: 83.5 vs 77.0 ms for the OPT-1.3B set.)
-    const size_t per_group = k3s_slot_bytes(rows) * cpb;
-    const int wave = static_cast<int>(std::max<size_t>(1, std::min<size_t>(ngroups, work_bytes / per_group)));
+    const int P = k3s_pieces(rows);
+    const int64_t pr = k3s_piece_rows(rows);
+    const int npad = k3s_npad(pr), dstride = k3s_dstride(pr);
+    const int xstride = k3s_xstride(pr), tstride = k3s_tstride(pr);
+    const int nb = cfg.lmax - cfg.lmin;
+    // Waves of whole column groups (P consecutive groups each) whose tables
+    // fit the work buffer, in stream order. (Overlapping a wave's sort with
+    // the previous loop on side streams was measured slower on B200: 83.5 vs
+    // 77.0 ms for the OPT-1.3B set.)
+    const size_t per_group = k3s_slot_bytes(pr) * cpb;
+    int wave = static_cast<int>(std::max<size_t>(P, std::min<size_t>(ngroups, work_bytes / per_group)));
+    wave -= wave % P;
     double* tables = static_cast<double*>(work);
     ColInfo* infos = reinterpret_cast<ColInfo*>(tables + static_cast<size_t>(wave) * cpb * tstride);
     const SortShape sh = sort_shape(npad);
+    const int ppl = (nb * P + 31) / 32;  // (threshold, piece) pairs per lane
     for (int g0 = 0; g0 < ngroups; g0 += wave) {
         const int ng = std::min(wave, ngroups - g0);
         const int64_t nslots = static_cast<int64_t>(ng) * cpb;
         const int ps = prof_begin("qsort", st);
+        const int ipr = static_cast<int>(pr);
         switch (sh.threads * 100 + sh.ipt) {
-            case 12808: launch_sort_t<128, 8>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
-            case 12816: launch_sort_t<128, 16>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
-            case 25616: launch_sort_t<256, 16>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
-            case 25608: launch_sort_t<256, 8>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
-            case 51208: launch_sort_t<512, 8>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
-            default: launch_sort_t<512, 16>(ng, cpb, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
+            case 12808: launch_sort_t<128, 8>(ng, cpb, ipr, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
+            case 12816: launch_sort_t<128, 16>(ng, cpb, ipr, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
+            case 25616: launch_sort_t<256, 16>(ng, cpb, ipr, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
+            case 38416: launch_sort_t<384, 16>(ng, cpb, ipr, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
+            case 25608: launch_sort_t<256, 8>(ng, cpb, ipr, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
+            case 51208: launch_sort_t<512, 8>(ng, cpb, ipr, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
+            default: launch_sort_t<512, 16>(ng, cpb, ipr, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
         }
-        prof_end(ps, st, static_cast<double>(nslots) * static_cast<double>(rows));
+        prof_end(ps, st, static_cast<double>(nslots) * static_cast<double>(pr));
         // work: column-steps (a step = one err/grad evaluation + Adam update)
         const int pl = prof_begin("qrange", st);
-        if (cfg.lmax - cfg.lmin <= 15)
+        const int ncg = ng / P;
+        if (P == 1 && nb <= 15) {
             launch_loop_t<16, 1>(nslots, cpb, dstride, tstride, td, groups + g0, tables, infos, sc, cfg, st);
-        else
-            launch_loop_t<32, 1>(nslots, cpb, dstride, tstride, td, groups + g0, tables, infos, sc, cfg, st);
-        prof_end(pl, st, static_cast<double>(nslots) * (cfg.mode == EZQ_MODE_EASYQUANT ? cfg.steps + 1 : 1));
+        } else {
+            switch (ppl) {
+                case 1: launch_pieces_t<1>(ncg, P, cpb, dstride, tstride, td, groups + g0, tables, infos, sc, cfg, st); break;
+                case 2: launch_pieces_t<2>(ncg, P, cpb, dstride, tstride, td, groups + g0, tables, infos, sc, cfg, st); break;
+                case 3: launch_pieces_t<3>(ncg, P, cpb, dstride, tstride, td, groups + g0, tables, infos, sc, cfg, st); break;
+                case 4: launch_pieces_t<4>(ncg, P, cpb, dstride, tstride, td, groups + g0, tables, infos, sc, cfg, st); break;
+                default: launch_pieces_t<8>(ncg, P, cpb, dstride, tstride, td, groups + g0, tables, infos, sc, cfg, st); break;
+            }
+        }
+        prof_end(pl, st, static_cast<double>(ncg) * cpb * (cfg.mode == EZQ_MODE_EASYQUANT ? cfg.steps + 1 : 1));
         count_launch(2);
     }
 }

@@ -209,22 +209,27 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     if (cfg_status == EZQ_OK) {
         for (auto& kv : by_rows) {
             Plan p;
-            if (k3_sorted && eq && kv.first <= kK3sMaxRows && k3s_supported(cfg->bits)) {
-                // K3s: a CTA sorts its columns, then two columns per warp.
-                const int cpb = k3s_cpb(kv.first);
+            const int pieces = k3s_pieces(kv.first);
+            if (k3_sorted && eq && pieces > 0 && k3s_supported(cfg->bits)) {
+                // K3s: a CTA sorts a group of columns (one row piece), then a
+                // loop kernel runs the columns' Adam loops on the tables.
+                const int64_t pr = k3s_piece_rows(kv.first);
+                const int cpb = k3s_cpb(pr);
                 p.sorted_cpb = cpb;
-                const size_t per_group = k3s_slot_bytes(kv.first) * cpb;
+                const size_t per_group = k3s_slot_bytes(pr) * cpb;
                 p.kl.rows = kv.first;
                 for (int i : kv.second)
                     for (int64_t c0 = 0; c0 < cols[i]; c0 += cpb)
-                        p.groups.push_back({i, static_cast<int32_t>(c0),
-                                            static_cast<int32_t>(std::min<int64_t>(cpb, cols[i] - c0)), 0});
+                        for (int q = 0; q < pieces; ++q)
+                            p.groups.push_back({i, static_cast<int32_t>(c0),
+                                                static_cast<int32_t>(std::min<int64_t>(cpb, cols[i] - c0)),
+                                                static_cast<int32_t>(q * pr)});
                 p.goff = tot_groups;
                 tot_groups += p.groups.size();
                 p.grid = static_cast<int>(p.groups.size());
-                k3s_work = std::max(k3s_work, per_group * std::max<size_t>(1, std::min<size_t>(
-                                                              p.groups.size(), k3s_work_cap / per_group)) +
-                                                  512);
+                const size_t wave_groups =
+                    std::max<size_t>(pieces, std::min<size_t>(p.groups.size(), k3s_work_cap / per_group));
+                k3s_work = std::max(k3s_work, per_group * wave_groups + 512);
                 plans.push_back(std::move(p));
                 continue;
             }
