@@ -323,6 +323,11 @@ constexpr size_t kBlkCacheLimit = 12ull << 30;
 void* block_get(size_t need, cudaStream_t st, size_t* got) {
     int dev = 0;
     cudaGetDevice(&dev);
+    {  // size classes: 8 per octave (>= 1 MB granules), so similar calls share blocks
+        size_t gran = size_t(1) << 20;
+        while (gran * 16 <= need) gran <<= 1;
+        need = (need + gran - 1) / gran * gran;
+    }
     {
         std::lock_guard<std::mutex> lk(g_blk_mu);
         int best = -1;

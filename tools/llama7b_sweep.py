@@ -33,7 +33,7 @@ def main():
     for bits in (4, 3):
         for sigma in (3.2905, 2.8070, 2.5758):
             cfg = Config(bits=bits, sigma_n=sigma)
-            N.quantize_batch(Ws[:7], cfg, out_mem=N.MEM_DEVICE).close()  # warm
+            N.quantize_batch(Ws, cfg, out_mem=N.MEM_DEVICE).close()  # warm (allocations, caches)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             b = N.quantize_batch(Ws, cfg, out_mem=N.MEM_DEVICE)
