@@ -218,6 +218,83 @@ __device__ __forceinline__ void block_scans(double vp, double vs, double& ep, do
     es = __dadd_rn(xs, bs);
 }
 
+// Sort of one staged column (THREADS x IPT floats, +inf last) into blocked
+// order. Instead of a full 32-bit radix sort (6 passes) the keys are binned
+// by value -- bin(x) = min(NB - 2, trunc((x - min) * (NB - 2) / (max - min))),
+// +inf -> NB - 1, NB ~ 2 x keys -- which is monotone in x (each float op is),
+// so sorting by the 11-14-bit bin (2-3 passes, key-value) leaves every key
+// within its bin of the final position; odd-even transposition rounds over
+// the blocked array then finish the order (one or two rounds at ~0.5 keys
+// per bin), checked block-wide; columns still unsorted after 8 rounds
+// (e.g. a few huge values squeezing the rest into one bin) take the full
+// float radix sort.
+template <int THREADS, int IPT>
+struct ColumnSorter {
+    static constexpr int NPAD = THREADS * IPT;
+    static constexpr int BBITS = NPAD <= 1024 ? 11 : NPAD <= 2048 ? 12 : NPAD <= 4096 ? 13 : 14;
+    static constexpr int NB = 1 << BBITS;
+    typedef cub::BlockRadixSort<float, THREADS, IPT, cub::NullType, kSortRadixBits> Full;
+    typedef cub::BlockRadixSort<unsigned short, THREADS, IPT, float, kSortRadixBits> Binned;
+    static constexpr size_t kTemp =
+        sizeof(typename Full::TempStorage) > sizeof(typename Binned::TempStorage) ? sizeof(typename Full::TempStorage)
+                                                                                  : sizeof(typename Binned::TempStorage);
+
+    __device__ __forceinline__ static void cas(float& a, float& b) {
+        const float lo = fminf(a, b), hi = fmaxf(a, b);
+        a = lo;
+        b = hi;
+    }
+
+    // temp: kTemp bytes; edge: 2 * THREADS floats; red: 2 * (THREADS / 32) floats
+    __device__ static void sort(float (&keys)[IPT], void* temp, float* edge, float* red) {
+        constexpr int NW = THREADS / 32;
+        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+        const float kInf = __int_as_float(0x7f800000);
+        float mn = kInf, mx = -kInf;
+#pragma unroll
+        for (int i = 0; i < IPT; ++i)
+            if (keys[i] < kInf) mn = fminf(mn, keys[i]), mx = fmaxf(mx, keys[i]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane == 0) red[warp] = mn, red[NW + warp] = mx;
+        __syncthreads();
+        mn = red[0];
+        mx = red[NW];
+        for (int w = 1; w < NW; ++w) mn = fminf(mn, red[w]), mx = fmaxf(mx, red[NW + w]);
+        if (!(mn <= mx)) return;  // no finite keys: all +inf (block-uniform)
+        const float span = mx - mn;
+        const float scale = (span > 0.f && span < kInf) ? static_cast<float>(NB - 2) / span : 0.f;
+        unsigned short bk[IPT];
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            const float t = (keys[i] - mn) * scale;
+            bk[i] = keys[i] < kInf ? static_cast<unsigned short>(t < static_cast<float>(NB - 2) ? static_cast<int>(t) : NB - 2)
+                                   : static_cast<unsigned short>(NB - 1);
+        }
+        Binned(*static_cast<typename Binned::TempStorage*>(temp)).Sort(bk, keys, 0, BBITS);
+        for (int round = 0; round < 8; ++round) {
+#pragma unroll
+            for (int i = 0; i + 1 < IPT; i += 2) cas(keys[i], keys[i + 1]);
+#pragma unroll
+            for (int i = 1; i + 1 < IPT; i += 2) cas(keys[i], keys[i + 1]);
+            __syncthreads();  // edge reuse
+            edge[tid] = keys[0];
+            edge[THREADS + tid] = keys[IPT - 1];
+            __syncthreads();
+            if (tid + 1 < THREADS) keys[IPT - 1] = fminf(keys[IPT - 1], edge[tid + 1]);
+            if (tid > 0) keys[0] = fmaxf(keys[0], edge[THREADS + tid - 1]);
+            bool ok = true;
+#pragma unroll
+            for (int i = 0; i + 1 < IPT; ++i) ok &= keys[i] <= keys[i + 1];
+            if (!__syncthreads_or(!ok)) return;
+        }
+        Full(*static_cast<typename Full::TempStorage*>(temp)).Sort(keys);
+    }
+};
+
 // ---- K3s-a: sort each column and write its table ---------------------------
 // One CTA per group of cpb adjacent columns (slot = group * cpb + column):
 // the columns are staged (outliers and padding as +inf, sorted last), each is
@@ -231,13 +308,14 @@ __global__ void __launch_bounds__(THREADS) k_qsort_tables(const TDesc* __restric
                                                           ColInfo* __restrict__ infos) {
     constexpr int NPAD = THREADS * IPT;
     constexpr int NW = THREADS / 32;
-    typedef cub::BlockRadixSort<float, THREADS, IPT, cub::NullType, kSortRadixBits> Sorter;
+    typedef ColumnSorter<THREADS, IPT> Sorter;
     __shared__ double wp[NW], ws[NW], wc[NW][2];
     __shared__ int wn[NW][2];
+    __shared__ float edge[2 * THREADS], red[2 * NW];
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* stage = reinterpret_cast<float*>(smem_raw);  // [cpb][NPAD]
     unsigned char* uni = smem_raw + sizeof(float) * static_cast<size_t>(cpb) * NPAD;
-    typename Sorter::TempStorage& sort_tmp = *reinterpret_cast<typename Sorter::TempStorage*>(uni);
+    void* sort_tmp = uni;
     double* Ds = reinterpret_cast<double*>(uni);  // aliases sort_tmp: used after each sort
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const float kInf = __int_as_float(0x7f800000);
@@ -269,7 +347,7 @@ __global__ void __launch_bounds__(THREADS) k_qsort_tables(const TDesc* __restric
         float keys[IPT];
 #pragma unroll
         for (int i = 0; i < IPT; ++i) keys[i] = stage[c * NPAD + i * THREADS + tid];
-        Sorter(sort_tmp).Sort(keys);  // blocked: thread t holds ranks [t*IPT, t*IPT + IPT)
+        Sorter::sort(keys, sort_tmp, edge, red);  // blocked: thread t holds ranks [t*IPT, t*IPT + IPT)
         // counts, sums of x per sign, and C = sum x^2: x^2 is exact in fp64
         // and, walking the negatives up and the non-negatives down, each
         // term is no larger than the running sum, so Fast2Sum keeps C exact
@@ -654,9 +732,8 @@ SortShape sort_shape(int npad) {
 
 template <int THREADS, int IPT>
 size_t sort_union_bytes() {
-    typedef cub::BlockRadixSort<float, THREADS, IPT, cub::NullType, kSortRadixBits> Sorter;
     const size_t d = sizeof(double) * static_cast<size_t>(dpad(THREADS * IPT + 2) + 1);
-    return std::max(sizeof(typename Sorter::TempStorage), d);
+    return std::max(ColumnSorter<THREADS, IPT>::kTemp, d);
 }
 
 template <int THREADS, int IPT>
