@@ -576,9 +576,6 @@ void launch_loop_t(int64_t nslots64, int cpb, int dstride, int tstride, const TD
     const int nslots = static_cast<int>(nslots64);
     const int warps = (nslots + CPW - 1) / CPW;
     const int grid = (warps + 7) / 8;
-    static const int carve = std::getenv("EZQ_K3S_CARVE") ? std::atoi(std::getenv("EZQ_K3S_CARVE")) : -1;
-    if (carve >= 0)  // tables are read through L1: the shared-memory carveout
-        cudaFuncSetAttribute(k_qrange_tables<G, TPL>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
     k_qrange_tables<G, TPL><<<grid, 256, 0, st>>>(td, groups, nslots, cpb, dstride, tstride, tables, infos,
                                                           sc, cfg);
 }
@@ -720,11 +717,10 @@ struct SortShape {
     int threads, ipt;
 };
 SortShape sort_shape(int npad) {
-    static const int alt = std::getenv("EZQ_K3S_SORT_ALT") ? std::atoi(std::getenv("EZQ_K3S_SORT_ALT")) : 0;
     switch (npad) {
         case 1024: return {128, 8};
-        case 2048: return alt ? SortShape{256, 8} : SortShape{128, 16};
-        case 4096: return alt ? SortShape{512, 8} : SortShape{256, 16};
+        case 2048: return {128, 16};  // 256 x 8 measured slower (fewer keys per thread)
+        case 4096: return {256, 16};
         case 6144: return {384, 16};
         default: return {512, 16};
     }
@@ -813,8 +809,6 @@ void launch_k3_sorted(int64_t rows, int cpb, const TDesc* td, const K3Group* gro
             case 12816: launch_sort_t<128, 16>(ng, cpb, ipr, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
             case 25616: launch_sort_t<256, 16>(ng, cpb, ipr, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
             case 38416: launch_sort_t<384, 16>(ng, cpb, ipr, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
-            case 25608: launch_sort_t<256, 8>(ng, cpb, ipr, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
-            case 51208: launch_sort_t<512, 8>(ng, cpb, ipr, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
             default: launch_sort_t<512, 16>(ng, cpb, ipr, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
         }
         prof_end(ps, st, static_cast<double>(nslots) * static_cast<double>(pr));
