@@ -51,15 +51,15 @@ __device__ __forceinline__ void p1_elem(P1& a, float v, unsigned long long flat)
 // ---- cp.async-pipelined chunk passes --------------------------------------
 // One warp owns 32 consecutive global chunks (lane c <-> chunk c, so each
 // lane runs exactly the reference's sequential chain for its chunk). The warp
-// streams the chunks through SMEM in 64-element tiles with cp.async (8-stage
-// ring, seven tiles = 56 KB in flight per warp: enough to cover HBM latency
-// at the ~29 GB/s one warp's 32 DADD chains consume): each cp.async instruction moves two
+// streams the chunks through SMEM in 64-element tiles with cp.async (3-stage
+// ring: the per-warp issue rate, not HBM latency, bounds a warp, so a short
+// ring that lets ~13 warps share an SM beats a deep one): each cp.async instruction moves two
 // contiguous 256-byte chunk segments, so HBM sees fully coalesced traffic
 // while every lane reads its own tile with conflict-free LDS.128 (68-float
 // row pitch). Requires 16-byte aligned tensors (else the simple kernels run).
 constexpr int kTile = 64;
 constexpr int kPitch = kTile + 4;
-constexpr int kStages = 8;       // 7 tiles (56 KB) in flight per warp
+constexpr int kStages = 3;  // 2 tiles (16 KB) in flight per warp: ~13 warps/SM (8 stages: 3 warps/SM, 1.4 ms slower per OPT-1.3B step)
 constexpr int kWarpsPerCta = 1;
 constexpr int kTilesPerChunk = static_cast<int>(kStatsChunk / kTile);
 constexpr size_t kStatsSmem = sizeof(float) * kStages * 32 * kPitch * kWarpsPerCta;
