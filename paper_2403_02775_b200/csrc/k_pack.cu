@@ -30,41 +30,13 @@ __device__ __forceinline__ int find_tensor(const int64_t* base, int ntens, int64
     return lo;
 }
 
-__global__ void __launch_bounds__(kPackThreads) k_pack(const TDesc* __restrict__ td,
-                                                       const int64_t* __restrict__ pblk_base,
-                                                       int ntens, int64_t total, Scratch sc,
-                                                       CfgDev cfg) {
-    const int64_t g = blockIdx.x;
-    if (g >= total) return;
-    const int t = find_tensor(pblk_base, ntens, g);
-    const TDesc& d = td[t];
-    const int64_t e0 = ((g - d.pblk_base) * kPackThreads + threadIdx.x) * kPackPerThread;
-    if (e0 >= d.n) return;
-    const TStats* st = d.st;
-    const float olo = st->olo, ohi = st->ohi;
-    const int64_t C = d.cols;
-    int64_t col = e0 % C;
+// Per-element path of k_pack (row wraps, ragged tails, unaligned columns).
+__device__ __forceinline__ void pack_levels_slow(const float (&x)[kPackPerThread], uint8_t (&off)[kPackPerThread], int64_t col, int64_t cnt, int64_t C,
+                                              const TDesc& d, const Scratch& sc, const CfgDev& cfg, float olo,
+                                              float ohi) {
     const double dmin = cfg.lmin, dmax = cfg.lmax;
     const float fmin = static_cast<float>(cfg.lmin), fmax = static_cast<float>(cfg.lmax);
     const float guard = cfg.guard;
-    const int64_t cnt = min(static_cast<int64_t>(kPackPerThread), d.n - e0);
-
-    float x[kPackPerThread];
-    if (cnt == kPackPerThread && (reinterpret_cast<uintptr_t>(d.W + e0) & 15) == 0) {
-        const float4* p4 = reinterpret_cast<const float4*>(d.W + e0);
-#pragma unroll
-        for (int k = 0; k < kPackPerThread / 4; ++k) {
-            const float4 v = __ldg(p4 + k);
-            x[4 * k] = v.x;
-            x[4 * k + 1] = v.y;
-            x[4 * k + 2] = v.z;
-            x[4 * k + 3] = v.w;
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < kPackPerThread; ++k) x[k] = (k < cnt) ? d.W[e0 + k] : 0.f;
-    }
-
     // Per-column float 1/scale for the certified fp32 level (K3b wrote it);
     // the 16 columns are contiguous unless the run wraps a row.
     float invf[kPackPerThread];
@@ -83,7 +55,6 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const TDesc* __restrict__
             if (++cc == C) cc = 0;
         }
     }
-    uint8_t off[kPackPerThread];
 #pragma unroll
     for (int k = 0; k < kPackPerThread; ++k) {
         int lvl = 0;
@@ -98,6 +69,78 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const TDesc* __restrict__
         if (++col == C) col = 0;
     }
 
+}
+
+__global__ void __launch_bounds__(kPackThreads) k_pack(const TDesc* __restrict__ td,
+                                                       const int64_t* __restrict__ pblk_base,
+                                                       int ntens, int64_t total, Scratch sc,
+                                                       CfgDev cfg) {
+    const int64_t g = blockIdx.x;
+    if (g >= total) return;
+    const int t = find_tensor(pblk_base, ntens, g);
+    const TDesc& d = td[t];
+    const int64_t e0 = ((g - d.pblk_base) * kPackThreads + threadIdx.x) * kPackPerThread;
+    if (e0 >= d.n) return;
+    const TStats* st = d.st;
+    const float olo = st->olo, ohi = st->ohi;
+    const int64_t C = d.cols;
+    const int64_t col = e0 % C;
+    const int64_t cnt = min(static_cast<int64_t>(kPackPerThread), d.n - e0);
+
+    float x[kPackPerThread];
+    if (cnt == kPackPerThread && (reinterpret_cast<uintptr_t>(d.W + e0) & 15) == 0) {
+        const float4* p4 = reinterpret_cast<const float4*>(d.W + e0);
+#pragma unroll
+        for (int k = 0; k < kPackPerThread / 4; ++k) {
+            const float4 v = __ldg(p4 + k);
+            x[4 * k] = v.x;
+            x[4 * k + 1] = v.y;
+            x[4 * k + 2] = v.z;
+            x[4 * k + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kPackPerThread; ++k) x[k] = (k < cnt) ? d.W[e0 + k] : 0.f;
+    }
+
+    uint8_t off[kPackPerThread];
+    const float fmin = static_cast<float>(cfg.lmin), fmax = static_cast<float>(cfg.lmax);
+    if (cnt == kPackPerThread && col + kPackPerThread <= C && ((d.col_base + col) & 3) == 0) {
+        // Common case: 16 contiguous columns of one row. Certified fp32 levels
+        // for the group (one guard test), the level's offset byte straight
+        // from the magic-added bits (0x4B400000 + q), outlier slots -> level 0.
+        const float4* iv4 = reinterpret_cast<const float4*>(sc.invf + d.col_base + col);
+        float rmax = 0.f;
+        unsigned tb[kPackPerThread];
+#pragma unroll
+        for (int k4 = 0; k4 < kPackPerThread / 4; ++k4) {
+            const float4 v = __ldg(iv4 + k4);
+            const float iv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int k = 4 * k4 + j;
+                float u = __fmul_rn(x[k], iv[j]);
+                u = fminf(fmaxf(u, fmin), fmax);
+                const float t = __fadd_rn(u, kMagic);
+                rmax = fmaxf(rmax, fabsf(__fsub_rn(u, __fsub_rn(t, kMagic))));
+                tb[k] = __float_as_uint(t);
+            }
+        }
+        if (rmax >= cfg.guard) {  // an element near a rounding boundary: reference fp64 levels
+            const double dmin = cfg.lmin, dmax = cfg.lmax;
+#pragma unroll
+            for (int k = 0; k < kPackPerThread; ++k) {
+                const double q = level_exact(x[k], sc.inv[d.col_base + col + k], dmin, dmax);
+                tb[k] = __float_as_uint(__fadd_rn(static_cast<float>(q), kMagic));
+            }
+        }
+        const unsigned base = __float_as_uint(kMagic) + static_cast<unsigned>(cfg.lmin);
+#pragma unroll
+        for (int k = 0; k < kPackPerThread; ++k)
+            off[k] = is_outlier_f(x[k], olo, ohi) ? static_cast<uint8_t>(-cfg.lmin) : static_cast<uint8_t>(tb[k] - base);
+    } else {
+        pack_levels_slow(x, off, col, cnt, C, d, sc, cfg, olo, ohi);
+    }
     if (cfg.bits == 4) {
         uint8_t b[kPackPerThread / 2];
 #pragma unroll
