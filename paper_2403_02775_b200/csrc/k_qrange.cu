@@ -352,16 +352,39 @@ __global__ void __launch_bounds__(kWarpsK3b * 32) k_seq_errors(const TDesc* __re
         float x[kRowsK3b];
 #pragma unroll
         for (int j = 0; j < kRowsK3b; ++j) x[j] = __ldg(col + (r + j) * C);
+        // certified fp32 levels for the group at both scales, one guard test
+        // per scale (exact fp64 levels for the group when it trips)
+        float tr[kRowsK3b], tf[kRowsK3b];
+        float rr = 0.f, rf = 0.f;
+#pragma unroll
+        for (int j = 0; j < kRowsK3b; ++j) {
+            float u = fminf(fmaxf(__fmul_rn(x[j], invf_r), fmin), fmax);
+            tr[j] = __fadd_rn(u, kMagic);
+            rr = fmaxf(rr, fabsf(__fsub_rn(u, __fsub_rn(tr[j], kMagic))));
+            u = fminf(fmaxf(__fmul_rn(x[j], invf_f), fmin), fmax);
+            tf[j] = __fadd_rn(u, kMagic);
+            rf = fmaxf(rf, fabsf(__fsub_rn(u, __fsub_rn(tf[j], kMagic))));
+        }
+        if (rr >= guard) {
+#pragma unroll
+            for (int j = 0; j < kRowsK3b; ++j)
+                tr[j] = __fadd_rn(static_cast<float>(level_exact(static_cast<double>(x[j]), inv_r, dmin, dmax)), kMagic);
+        }
+        if (both && rf >= guard) {
+#pragma unroll
+            for (int j = 0; j < kRowsK3b; ++j)
+                tf[j] = __fadd_rn(static_cast<float>(level_exact(static_cast<double>(x[j]), inv_f, dmin, dmax)), kMagic);
+        }
 #pragma unroll
         for (int j = 0; j < kRowsK3b; ++j) {
             // normal_mask_apply: an isolated outlier adds exactly +0
             const bool out = is_outlier_f(x[j], olo, ohi);
             const double xd = static_cast<double>(x[j]);
-            const double tr = seq_sq(x[j], xd, s_r, invf_r, inv_r, fmin, fmax, dmin, dmax, guard);
-            er = __dadd_rn(er, out ? 0.0 : tr);
+            const double dr = fma(s_r, level_bits_to_double(tr[j]), -xd);  // exact: s*q is
+            er = __dadd_rn(er, out ? 0.0 : __dmul_rn(dr, dr));
             if (both) {
-                const double tf = seq_sq(x[j], xd, s_f, invf_f, inv_f, fmin, fmax, dmin, dmax, guard);
-                ef = __dadd_rn(ef, out ? 0.0 : tf);
+                const double df = fma(s_f, level_bits_to_double(tf[j]), -xd);
+                ef = __dadd_rn(ef, out ? 0.0 : __dmul_rn(df, df));
             }
         }
     }
