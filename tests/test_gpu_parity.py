@@ -326,10 +326,16 @@ def _k3s_cases(O):
     # fixed-step selection, short trajectories
     out.append(("fixed3", O.gaussian(2048, 16, 86, 0.02), Config(select="fixed", select_step=2, steps=3)))
     out.append(("steps0", O.gaussian(2048, 16, 87, 0.02), Config(steps=0)))
+    # row pieces: 3 pieces (16385 rows), k = 5 over 2 pieces (2 pairs per lane), 6 pieces
+    out.append(("pieces3", O.gaussian(16385, 5, 88, 0.02), Config(steps=60)))
+    out.append(("pieces2_k5", O.gaussian(12288, 5, 89, 0.02), Config(bits=5, steps=60)))
+    W = O.gaussian(49152, 3, 90, 0.02)
+    O.plant_outliers(W, 40, 0.2, 1.0, 91)
+    out.append(("pieces6", W, Config(steps=40)))
     return out
 
 
-@pytest.mark.parametrize("idx", range(12))
+@pytest.mark.parametrize("idx", range(15))
 def test_k3s_edge_cases(gpu, O, idx):
     name, W, cfg = _k3s_cases(O)[idx]
     q = gpu.quantize_tensor(W, cfg)
