@@ -221,23 +221,24 @@ __device__ __forceinline__ void block_scans(double vp, double vs, double& ep, do
 // Sort of one staged column (THREADS x IPT floats, +inf last) into blocked
 // order. Instead of a full 32-bit radix sort (6 passes) the keys are binned
 // by value -- bin(x) = min(NB - 2, trunc((x - min) * (NB - 2) / (max - min))),
-// +inf -> NB - 1, NB ~ 2 x keys -- which is monotone in x (each float op is),
-// so sorting by the 11-14-bit bin (2-3 passes, key-value) leaves every key
-// within its bin of the final position; odd-even transposition rounds over
-// the blocked array then finish the order (one or two rounds at ~0.5 keys
-// per bin), checked block-wide; columns still unsorted after 8 rounds
-// (e.g. a few huge values squeezing the rest into one bin) take the full
-// float radix sort.
+// +inf -> NB - 1, NB = one bin per key slot -- which is monotone in x (each
+// float op is), so a counting sort by bin (shared-memory histogram, warp
+// scans, atomic scatter) leaves every key within its bin of the final
+// position; odd-even transposition rounds over the blocked array then finish
+// the order (one or two rounds at ~1 key per bin), checked block-wide;
+// columns still unsorted after 8 rounds (e.g. a few huge values squeezing the
+// rest into one bin) take the full float radix sort. Equal keys may land in
+// any order, which changes nothing downstream.
 template <int THREADS, int IPT>
 struct ColumnSorter {
     static constexpr int NPAD = THREADS * IPT;
-    static constexpr int BBITS = NPAD <= 1024 ? 11 : NPAD <= 2048 ? 12 : NPAD <= 4096 ? 13 : 14;
-    static constexpr int NB = 1 << BBITS;
+    static constexpr int NW = THREADS / 32;
+    static constexpr int NB = NPAD;  // bins
     typedef cub::BlockRadixSort<float, THREADS, IPT, cub::NullType, kSortRadixBits> Full;
-    typedef cub::BlockRadixSort<unsigned short, THREADS, IPT, float, kSortRadixBits> Binned;
+    static constexpr size_t kCount = sizeof(int) * NB + sizeof(float) * (NPAD + NPAD / 16);
     static constexpr size_t kTemp =
-        sizeof(typename Full::TempStorage) > sizeof(typename Binned::TempStorage) ? sizeof(typename Full::TempStorage)
-                                                                                  : sizeof(typename Binned::TempStorage);
+        sizeof(typename Full::TempStorage) > kCount ? sizeof(typename Full::TempStorage) : kCount;
+    static_assert((NB / NW) % 32 == 0, "bins per warp");
 
     __device__ __forceinline__ static void cas(float& a, float& b) {
         const float lo = fminf(a, b), hi = fmaxf(a, b);
@@ -267,14 +268,54 @@ struct ColumnSorter {
         if (!(mn <= mx)) return;  // no finite keys: all +inf (block-uniform)
         const float span = mx - mn;
         const float scale = (span > 0.f && span < kInf) ? static_cast<float>(NB - 2) / span : 0.f;
-        unsigned short bk[IPT];
+        int* cnt = static_cast<int*>(temp);                  // [NB]
+        float* outv = reinterpret_cast<float*>(cnt + NB);    // [NPAD + NPAD/16], one pad per 16
+        int* wsum = reinterpret_cast<int*>(red);             // red is free again after the barrier below
+        int bk[IPT];
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
             const float t = (keys[i] - mn) * scale;
-            bk[i] = keys[i] < kInf ? static_cast<unsigned short>(t < static_cast<float>(NB - 2) ? static_cast<int>(t) : NB - 2)
-                                   : static_cast<unsigned short>(NB - 1);
+            bk[i] = keys[i] < kInf ? (t < static_cast<float>(NB - 2) ? static_cast<int>(t) : NB - 2) : NB - 1;
         }
-        Binned(*static_cast<typename Binned::TempStorage*>(temp)).Sort(bk, keys, 0, BBITS);
+        for (int k = tid; k < NB; k += THREADS) cnt[k] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) atomicAdd(cnt + bk[i], 1);
+        __syncthreads();
+        // exclusive scan of the counts: warp w owns bins [w * NB / NW, ...)
+        constexpr int PER = NB / NW;
+        int* cw = cnt + warp * PER;
+        int tot = 0;
+        for (int k = 0; k < PER; k += 32) tot += cw[k + lane];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if (lane == 0) wsum[warp] = tot;
+        __syncthreads();
+        int run = 0;
+        for (int w = 0; w < warp; ++w) run += wsum[w];
+        for (int k = 0; k < PER; k += 32) {
+            const int v = cw[k + lane];
+            int inc = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += u;
+            }
+            cw[k + lane] = run + inc - v;
+            run += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            const int pos = atomicAdd(cnt + bk[i], 1);
+            outv[pos + (pos >> 4)] = keys[i];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            const int k = tid * IPT + i;
+            keys[i] = outv[k + (k >> 4)];
+        }
         for (int round = 0; round < 8; ++round) {
 #pragma unroll
             for (int i = 0; i + 1 < IPT; i += 2) cas(keys[i], keys[i + 1]);
