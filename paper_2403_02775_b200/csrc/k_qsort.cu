@@ -185,9 +185,10 @@ __device__ __forceinline__ int search_near(const ColTab& c, int guess, float X, 
 
 constexpr int kSortRadixBits = 6;
 
-// Padded shared-memory index of table entry k (one spare double per 16: the
-// blocked writes below hit distinct bank pairs).
-__host__ __device__ __forceinline__ int dpad(int k) { return k + (k >> 4); }
+// Padded shared-memory index of table entry k (two spare doubles per 32: the
+// blocked writes below hit at most 2-way bank conflicts, and pairs (k, k+1)
+// with k even stay 16-byte aligned for the vector copy out).
+__host__ __device__ __forceinline__ int dpad(int k) { return k + 2 * (k >> 5); }  // even for even k
 
 // CTA-wide exclusive scans of one double per thread: prefix (ascending tid)
 // and suffix (descending tid). Every partial sum is over a contiguous run of
@@ -235,10 +236,9 @@ struct ColumnSorter {
     static constexpr int NW = THREADS / 32;
     static constexpr int NB = NPAD;  // bins
     typedef cub::BlockRadixSort<float, THREADS, IPT, cub::NullType, kSortRadixBits> Full;
-    static constexpr size_t kCount = sizeof(int) * NB + sizeof(float) * (NPAD + NPAD / 16);
+    static constexpr size_t kCount = sizeof(int) * (NB + NB / 16) + sizeof(float) * (NPAD + NPAD / 16);
     static constexpr size_t kTemp =
         sizeof(typename Full::TempStorage) > kCount ? sizeof(typename Full::TempStorage) : kCount;
-    static_assert((NB / NW) % 32 == 0, "bins per warp");
 
     __device__ __forceinline__ static void cas(float& a, float& b) {
         const float lo = fminf(a, b), hi = fmaxf(a, b);
@@ -268,41 +268,43 @@ struct ColumnSorter {
         if (!(mn <= mx)) return;  // no finite keys: all +inf (block-uniform)
         const float span = mx - mn;
         const float scale = (span > 0.f && span < kInf) ? static_cast<float>(NB - 2) / span : 0.f;
-        int* cnt = static_cast<int*>(temp);                  // [NB]
-        float* outv = reinterpret_cast<float*>(cnt + NB);    // [NPAD + NPAD/16], one pad per 16
-        int* wsum = reinterpret_cast<int*>(red);             // red is free again after the barrier below
+        // bins padded one int per 16 (bin b at b + b / 16): thread t owns bins
+        // [t IPT, t IPT + IPT) for the scan, conflict-free
+        int* cnt = static_cast<int*>(temp);                    // [NB + NB / 16]
+        float* outv = reinterpret_cast<float*>(cnt + NB + NB / 16);  // [NPAD + NPAD/16], one pad per 16
+        int* wsum = reinterpret_cast<int*>(red);               // red is free again after the barrier below
         int bk[IPT];
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
             const float t = (keys[i] - mn) * scale;
-            bk[i] = keys[i] < kInf ? (t < static_cast<float>(NB - 2) ? static_cast<int>(t) : NB - 2) : NB - 1;
+            const int b = keys[i] < kInf ? (t < static_cast<float>(NB - 2) ? static_cast<int>(t) : NB - 2) : NB - 1;
+            bk[i] = b + (b >> 4);
         }
-        for (int k = tid; k < NB; k += THREADS) cnt[k] = 0;
+        for (int k = tid; k < NB + NB / 16; k += THREADS) cnt[k] = 0;
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < IPT; ++i) atomicAdd(cnt + bk[i], 1);
         __syncthreads();
-        // exclusive scan of the counts: warp w owns bins [w * NB / NW, ...)
-        constexpr int PER = NB / NW;
-        int* cw = cnt + warp * PER;
+        // exclusive scan of the counts: per-thread runs, then the thread totals
+        int* cw = cnt + tid * IPT + ((tid * IPT) >> 4);
         int tot = 0;
-        for (int k = 0; k < PER; k += 32) tot += cw[k + lane];
 #pragma unroll
-        for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-        if (lane == 0) wsum[warp] = tot;
+        for (int j = 0; j < IPT; ++j) tot += cw[j + (j >> 4)];
+        int inc = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        if (lane == 31) wsum[warp] = inc;
         __syncthreads();
-        int run = 0;
+        int run = inc - tot;
         for (int w = 0; w < warp; ++w) run += wsum[w];
-        for (int k = 0; k < PER; k += 32) {
-            const int v = cw[k + lane];
-            int inc = v;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int u = __shfl_up_sync(0xffffffffu, inc, o);
-                if (lane >= o) inc += u;
-            }
-            cw[k + lane] = run + inc - v;
-            run += __shfl_sync(0xffffffffu, inc, 31);
+        for (int j = 0; j < IPT; ++j) {
+            const int v = cw[j + (j >> 4)];
+            cw[j + (j >> 4)] = run;
+            run += v;
         }
         __syncthreads();
 #pragma unroll
@@ -368,13 +370,17 @@ __global__ void __launch_bounds__(THREADS) k_qsort_tables(const TDesc* __restric
     const int64_t R = min(static_cast<int64_t>(prows), d.rows - g.row0);  // this piece's rows
     const float* W0 = d.W + static_cast<int64_t>(g.row0) * C + g.col0;
     const int lcpb = __ffs(cpb) - 1;  // cpb is a power of two
+    const int cc0 = tid & (cpb - 1);   // a thread's column never changes (THREADS % cpb == 0)
+    const int rstep = THREADS >> lcpb;  // rows between a thread's consecutive loads
     for (int base = 0; base < cpb * NPAD; base += 8 * THREADS) {  // 8 loads in flight
         float v[8];
+        const int r0 = (base + tid) >> lcpb;
+        const float* src = W0 + static_cast<int64_t>(r0) * C + cc0;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            const int idx = base + u * THREADS + tid;
-            const int cc = idx & (cpb - 1), r = idx >> lcpb;
-            v[u] = (cc < g.ncols && r < R) ? __ldg(W0 + static_cast<int64_t>(r) * C + cc) : kInf;
+            const int r = r0 + u * rstep;
+            v[u] = (cc0 < g.ncols && r < R) ? __ldg(src) : kInf;
+            src += static_cast<int64_t>(rstep) * C;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -473,7 +479,8 @@ __global__ void __launch_bounds__(THREADS) k_qsort_tables(const TDesc* __restric
         }
         __syncthreads();
         double* out = tables + slot * tstride;
-        for (int k = tid; k < n + 2; k += THREADS) out[k] = Ds[dpad(k)];
+        for (int k = 2 * tid; k < n + 2; k += 2 * THREADS)  // 16-byte copies (entry n + 2 is scratch)
+            *reinterpret_cast<double2*>(out + k) = *reinterpret_cast<const double2*>(Ds + dpad(k));
         float* xo = reinterpret_cast<float*>(out + dstride);
 #pragma unroll
         for (int i = 0; i < IPT; i += 4)  // sorted keys, +inf past n (blocked: 16-byte stores)
