@@ -65,6 +65,8 @@ struct TDesc {
     uint8_t* packed;
     float* scales;
     ezq_outlier* outliers;
+    int32_t pack_fused;  // K3b writes the packed codes (k != 4 or even cols); K4 skips the tensor
+    int32_t pad_;
 };
 
 // Batch-wide scratch (device pointers into one arena).
@@ -85,6 +87,7 @@ struct Scratch {
     double* err_fin;  // reference-order error at s_fin
     double* inv;      // 1 / double(final float scale), for K4
     float* invf;      // float(inv), K4's certified fp32 level
+    uint8_t* repack;  // 1: K3b packed at s_fin but stored s_rtn (re-packed by k_repack)
 };
 
 struct CfgDev {
@@ -159,6 +162,8 @@ void launch_k3_sorted(int64_t rows, int cpb, const TDesc* td, const K3Group* gro
                       CfgDev cfg, void* work, size_t work_bytes, cudaStream_t st);
 void launch_seq_errors(const TDesc* td, const int2* tiles, int ntiles, Scratch sc, CfgDev cfg,
                        cudaStream_t st);
+// Re-packs the (rare) fused-pack columns whose stored scale is s_rtn.
+void launch_repack(const TDesc* td, const int2* tiles, int ntiles, Scratch sc, CfgDev cfg, cudaStream_t st);
 void launch_tensor_totals(const TDesc* td, int ntens, Scratch sc, cudaStream_t st);
 void launch_pack(const TDesc* td, const int64_t* pblk_base, int ntens, int64_t total_blocks,
                  Scratch sc, CfgDev cfg, cudaStream_t st);

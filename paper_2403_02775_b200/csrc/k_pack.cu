@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const TDesc* __restrict__
     if (g >= total) return;
     const int t = find_tensor(pblk_base, ntens, g);
     const TDesc& d = td[t];
+    if (d.pack_fused) return;  // K3b wrote this tensor's codes
     const int64_t e0 = ((g - d.pblk_base) * kPackThreads + threadIdx.x) * kPackPerThread;
     if (e0 >= d.n) return;
     const TStats* st = d.st;

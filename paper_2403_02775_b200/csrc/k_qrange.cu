@@ -334,20 +334,35 @@ __global__ void __launch_bounds__(kWarpsK3b * 32) k_seq_errors(const TDesc* __re
     const TDesc& d = td[tile.x];
     const int64_t c0 = tile.y, R = d.rows, C = d.cols;
     const int64_t c = c0 + lane;
-    if (c >= C) return;
-    const int64_t gc = d.col_base + c;
+    const bool act = c < C;  // idle lanes stay for the nibble-pair shuffles
+    const int64_t gc = d.col_base + (act ? c : c0);
     const TStats* st = d.st;
     const float olo = st->olo, ohi = st->ohi;
     const double s_r = sc.s_rtn[gc], s_f = sc.s_fin[gc];
+    // Fused K4: the codes at s_fin (pack_levels, rtn.cpp:123-149, outlier
+    // slots at level 0) are written here; a column that ends up storing s_rtn
+    // is flagged and re-packed by k_repack.
+    const bool fused = d.pack_fused != 0;
+    const unsigned lbase = __float_as_uint(kMagic) + static_cast<unsigned>(cfg.lmin);
+    const unsigned lzero = static_cast<unsigned>(-cfg.lmin);
     const bool both = s_f != s_r;  // chosen == initial: one sum serves both
     const double inv_r = __ddiv_rn(1.0, s_r), inv_f = __ddiv_rn(1.0, s_f);
     const float invf_r = __double2float_rn(inv_r), invf_f = __double2float_rn(inv_f);
     const float fmin = static_cast<float>(cfg.lmin), fmax = static_cast<float>(cfg.lmax);
     const double dmin = cfg.lmin, dmax = cfg.lmax;
     const float guard = cfg.guard;
-    const float* col = d.W + c;
+    const float* col = d.W + (act ? c : c0);
     double er = 0.0, ef = 0.0;
     int64_t r = 0;
+    auto put = [&](int64_t row, unsigned tbits, bool out) {  // all lanes call it (shuffle)
+        const unsigned off = out ? lzero : tbits - lbase;
+        if (cfg.bits == 4) {
+            const unsigned hi = __shfl_down_sync(0xffffffffu, off, 1);
+            if (act && (c & 1) == 0) d.packed[(row * C + c) >> 1] = static_cast<uint8_t>(off | (hi << 4));
+        } else if (act) {
+            d.packed[row * C + c] = static_cast<uint8_t>(off);
+        }
+    };
     for (; r + kRowsK3b <= R; r += kRowsK3b) {
         float x[kRowsK3b];
 #pragma unroll
@@ -375,6 +390,11 @@ __global__ void __launch_bounds__(kWarpsK3b * 32) k_seq_errors(const TDesc* __re
             for (int j = 0; j < kRowsK3b; ++j)
                 tf[j] = __fadd_rn(static_cast<float>(level_exact(static_cast<double>(x[j]), inv_f, dmin, dmax)), kMagic);
         }
+        if (fused) {  // warp-uniform
+#pragma unroll
+            for (int j = 0; j < kRowsK3b; ++j)
+                put(r + j, __float_as_uint(both ? tf[j] : tr[j]), is_outlier_f(x[j], olo, ohi));
+        }
 #pragma unroll
         for (int j = 0; j < kRowsK3b; ++j) {
             // normal_mask_apply: an isolated outlier adds exactly +0
@@ -394,7 +414,12 @@ __global__ void __launch_bounds__(kWarpsK3b * 32) k_seq_errors(const TDesc* __re
         const double xd = static_cast<double>(x);
         er = __dadd_rn(er, out ? 0.0 : seq_sq(x, xd, s_r, invf_r, inv_r, fmin, fmax, dmin, dmax, guard));
         if (both) ef = __dadd_rn(ef, out ? 0.0 : seq_sq(x, xd, s_f, invf_f, inv_f, fmin, fmax, dmin, dmax, guard));
+        if (fused) {
+            const double q = level_exact(xd, inv_f, dmin, dmax);
+            put(r, __float_as_uint(__fadd_rn(static_cast<float>(q), kMagic)), out);
+        }
     }
+    if (!act) return;
     double s_store = s_f;
     if (!both) {
         ef = er;
@@ -404,6 +429,7 @@ __global__ void __launch_bounds__(kWarpsK3b * 32) k_seq_errors(const TDesc* __re
         s_store = s_r;
         ef = er;
     }
+    if (fused) sc.repack[gc] = (s_store != s_f) ? 1 : 0;
     const float scale = __double2float_rn(s_store);
     if (!(scale > 0.f)) d.st->scale_zero = 1;  // check_scale (rtn.cpp:19-22)
     d.scales[c] = scale;
@@ -412,6 +438,48 @@ __global__ void __launch_bounds__(kWarpsK3b * 32) k_seq_errors(const TDesc* __re
     sc.invf[gc] = __double2float_rn(inv);
     sc.err_rtn[gc] = er;
     sc.err_fin[gc] = ef;
+}
+
+// Fix-up of the fused pack: columns flagged by K3b (stored scale s_rtn, codes
+// written at s_fin) get their codes recomputed at the stored scale with the
+// reference's fp64 level; for k = 4 the even lane of a nibble pair rewrites
+// the shared byte (both nibbles at their columns' stored scales). Warps whose
+// 32 columns carry no flag return at once.
+__global__ void __launch_bounds__(kWarpsK3b * 32) k_repack(const TDesc* __restrict__ td,
+                                                          const int2* __restrict__ tiles, int ntiles, Scratch sc,
+                                                          CfgDev cfg) {
+    const int lane = threadIdx.x & 31;
+    const int ti = blockIdx.x * kWarpsK3b + (threadIdx.x >> 5);
+    if (ti >= ntiles) return;
+    const int2 tile = tiles[ti];
+    const TDesc& d = td[tile.x];
+    if (!d.pack_fused) return;
+    const int64_t C = d.cols, R = d.rows, c = tile.y + lane;
+    const bool act = c < C;
+    const bool flag = act && sc.repack[d.col_base + c];
+    const bool nflag = __shfl_down_sync(0xffffffffu, flag, 1) != 0;
+    if (!__any_sync(0xffffffffu, flag)) return;
+    const bool k4 = cfg.bits == 4;
+    const bool mine = k4 ? (act && (c & 1) == 0 && (flag || nflag)) : flag;
+    if (!mine) return;
+    const double dmin = cfg.lmin, dmax = cfg.lmax;
+    const float olo = d.st->olo, ohi = d.st->ohi;
+    const double inv0 = sc.inv[d.col_base + c];
+    const double inv1 = (k4 && c + 1 < C) ? sc.inv[d.col_base + c + 1] : 1.0;
+    auto off = [&](float x, double inv) -> unsigned {
+        if (is_outlier_f(x, olo, ohi)) return static_cast<unsigned>(-cfg.lmin);
+        return static_cast<unsigned>(static_cast<int>(level_exact(static_cast<double>(x), inv, dmin, dmax)) - cfg.lmin);
+    };
+    for (int64_t r = 0; r < R; ++r) {
+        const float x0 = d.W[r * C + c];
+        if (k4) {
+            const unsigned lo = off(x0, inv0);
+            const unsigned hi = c + 1 < C ? off(d.W[r * C + c + 1], inv1) : 0u;
+            d.packed[(r * C + c) >> 1] = static_cast<uint8_t>(lo | (hi << 4));
+        } else {
+            d.packed[r * C + c] = static_cast<uint8_t>(off(x0, inv0));
+        }
+    }
 }
 
 // Column-ordered tensor totals (pipeline.cpp:96-103): one CTA per tensor
@@ -541,6 +609,12 @@ void launch_seq_errors(const TDesc* td, const int2* tiles, int ntiles, Scratch s
                        cudaStream_t st) {
     if (ntiles == 0) return;
     k_seq_errors<<<(ntiles + kWarpsK3b - 1) / kWarpsK3b, kWarpsK3b * 32, 0, st>>>(td, tiles, ntiles, sc, cfg);
+    count_launch();
+}
+
+void launch_repack(const TDesc* td, const int2* tiles, int ntiles, Scratch sc, CfgDev cfg, cudaStream_t st) {
+    if (ntiles == 0) return;
+    k_repack<<<(ntiles + kWarpsK3b - 1) / kWarpsK3b, kWarpsK3b * 32, 0, st>>>(td, tiles, ntiles, sc, cfg);
     count_launch();
 }
 

@@ -181,6 +181,8 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
         tot_pblk += ceil_div(N, kPackBlock);
         d.col_base = tot_cols;
         tot_cols += cols[i];
+        // K3b packs unless k = 4 nibble pairs could straddle rows (odd cols)
+        d.pack_fused = (cfg_status == EZQ_OK && (cfg->bits != 4 || cols[i] % 2 == 0)) ? 1 : 0;
         if (in_mem == EZQ_MEM_HOST) tot_in += N;
     }
     chunk_base[n] = tot_chunks;
@@ -270,6 +272,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     for (int k = 0; k < 2; ++k) ar.reserve_n<long long>(tot_dblk);
     for (int k = 0; k < 5; ++k) ar.reserve_n<double>(tot_cols);
     ar.reserve_n<float>(tot_cols);
+    ar.reserve_n<uint8_t>(tot_cols);
     ar.reserve_n<int2>(tiles.size());
     ar.reserve(sizeof(double) * bc.size());
     ar.reserve(sizeof(K3Group) * tot_groups);
@@ -296,6 +299,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     sc.err_fin = ar.take<double>(tot_cols);
     sc.inv = ar.take<double>(tot_cols);
     sc.invf = ar.take<float>(tot_cols);
+    sc.repack = ar.take<uint8_t>(tot_cols);
     double* d_bc = ar.take<double>(bc.size());
     K3Group* d_groups = ar.take<K3Group>(tot_groups);
     float* d_in = ar.take<float>(tot_in);
@@ -448,13 +452,18 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     }
     int p4 = prof_begin("seqerr", st);
     launch_seq_errors(d_desc, d_tiles, static_cast<int>(tiles.size()), sc, cd, st);
+    static const bool force_repack = std::getenv("EZQ_FORCE_REPACK") != nullptr;  // test aid: exercise k_repack
+    if (force_repack) EZQ_CK(cudaMemsetAsync(sc.repack, 1, tot_cols, st));
+    launch_repack(d_desc, d_tiles, static_cast<int>(tiles.size()), sc, cd, st);
     launch_tensor_totals(d_desc, n, sc, st);
     prof_end(p4, st, 4.0 * tot_elems);
     trace("qb: seqerr launched");
     int64_t tot_packed = 0;
     for (int i = 0; i < n; ++i) tot_packed += ezq_packed_size(hd[i].n, cfg->bits);
     p4 = prof_begin("pack", st);
-    launch_pack(d_desc, d_pblk_base, n, tot_pblk, sc, cd, st);
+    bool any_unfused = false;
+    for (int i = 0; i < n; ++i) any_unfused |= hd[i].pack_fused == 0;
+    if (any_unfused) launch_pack(d_desc, d_pblk_base, n, tot_pblk, sc, cd, st);
     prof_end(p4, st, 4.0 * tot_elems + static_cast<double>(tot_packed));
     {
         cudaError_t e = cudaGetLastError();

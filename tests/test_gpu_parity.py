@@ -342,3 +342,33 @@ def test_k3s_edge_cases(gpu, O, idx):
     r = O.quantize(W, cfg, "easyquant")
     assert r["status"] == "ok", name
     assert_same_quant(q, r)
+
+
+def test_forced_repack_matches(gpu, O):
+    """The fused pack's fix-up (k_repack) rewrites every flagged column at its
+    stored scale; forcing the flag on every column (EZQ_FORCE_REPACK) must give
+    the same bytes as the oracle (k = 4 even/odd column counts, k = 3)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests"); sys.path.insert(0, ".")
+from oracle import pyoracle as O
+from paper_2403_02775_b200 import native as N
+from paper_2403_02775_b200.native import Config
+O.build()
+for (r, c, bits, seed) in [(513, 64, 4, 1), (300, 37, 4, 2), (257, 40, 3, 3), (1024, 24, 5, 4)]:
+    W = O.gaussian(r, c, seed, 0.02)
+    O.plant_outliers(W, 20, 0.2, 1.0, seed + 7)
+    cfg = Config(bits=bits, steps=40)
+    q = N.quantize_tensor(W, cfg)
+    ref = O.quantize(W, cfg, "easyquant")
+    assert np.array_equal(q.packed, ref["packed"]), (r, c, bits)
+    assert np.array_equal(q.scales.view(np.uint32), np.asarray(ref["scales"]).view(np.uint32))
+print("ok")
+'''
+    env = dict(os.environ, EZQ_FORCE_REPACK="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
