@@ -90,15 +90,6 @@ struct Acc {
     double ea, eb, ga, gb;
 };
 
-__device__ __forceinline__ void elem_fast(float x, const FastLevel& fl, double s, float& rmax,
-                                          double& e, double& g) {
-    const float q = level_fast(x, fl, rmax);
-    const double qd = static_cast<double>(q);
-    const double d = fma(s, qd, -static_cast<double>(x));
-    e = fma(d, d, e);
-    g = fma(d, qd, g);
-}
-
 __device__ __forceinline__ void elem_exact(float x, double inv, double dmin, double dmax,
                                            double s, double& e, double& g) {
     const double xd = static_cast<double>(x);

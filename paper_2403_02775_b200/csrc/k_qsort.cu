@@ -233,7 +233,6 @@ __device__ __forceinline__ void block_scans(double vp, double vs, double& ep, do
 template <int THREADS, int IPT>
 struct ColumnSorter {
     static constexpr int NPAD = THREADS * IPT;
-    static constexpr int NW = THREADS / 32;
     static constexpr int NB = NPAD;  // bins
     typedef cub::BlockRadixSort<float, THREADS, IPT, cub::NullType, kSortRadixBits> Full;
     static constexpr size_t kCount = sizeof(int) * (NB + NB / 16) + sizeof(float) * (NPAD + NPAD / 16);

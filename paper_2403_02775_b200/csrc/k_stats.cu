@@ -61,7 +61,6 @@ constexpr int kTile = 64;
 constexpr int kPitch = kTile + 4;
 constexpr int kStages = 3;  // 2 tiles (16 KB) in flight per warp: ~13 warps/SM (8 stages: 3 warps/SM, 1.4 ms slower per OPT-1.3B step)
 constexpr int kWarpsPerCta = 1;
-constexpr int kTilesPerChunk = static_cast<int>(kStatsChunk / kTile);
 constexpr size_t kStatsSmem = sizeof(float) * kStages * 32 * kPitch * kWarpsPerCta;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
