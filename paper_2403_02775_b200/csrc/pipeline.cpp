@@ -204,10 +204,20 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     static const bool k3_sorted = std::getenv("EZQ_K3_STREAMING") == nullptr;  // A/B: streaming K3 only
     std::vector<Plan> plans;
     size_t tot_groups = 0, gstrip_floats = 0, k3s_work = 0;
-    static const size_t k3s_work_cap = [] {
+    static const size_t k3s_work_env = [] {
         const char* e = std::getenv("EZQ_K3S_WORK_MB");
         return (e ? static_cast<size_t>(std::atoll(e)) : size_t(2048)) << 20;
     }();
+    // The tables may take at most an eighth of the free device memory (>= 128 MB;
+    // smaller buffers only mean more, shorter waves).
+    size_t k3s_work_cap = k3s_work_env;
+    {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess)
+            k3s_work_cap = std::min(k3s_work_cap, std::max<size_t>(size_t(128) << 20, fr / 8));
+        else
+            cudaGetLastError();
+    }
     if (cfg_status == EZQ_OK) {
         for (auto& kv : by_rows) {
             Plan p;
