@@ -253,7 +253,7 @@ def k3_roofline(args, prof, fp64_peak, clocks):
     rate: 4 warp-instructions/clk/SM x SMs x SM clock. achieved = the ncu
     instruction count per column-step (profiles/k3s_ncu.json, same workload)
     x the column-steps of the launches / their live duration. The streaming
-    K3 (k_qrange, rows > 8192 or bits > 5) keeps its FP64 roofline."""
+    K3 (k_qrange, bits > 5) keeps its FP64 roofline."""
     import torch
     k3 = prof["qrange"]
     ncu = None
