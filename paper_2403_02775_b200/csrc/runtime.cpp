@@ -333,7 +333,7 @@ void* block_get(size_t need, cudaStream_t st, size_t* got) {
         int best = -1;
         for (int i = 0; i < static_cast<int>(g_blk_free.size()); ++i) {
             const CachedBlock& b = g_blk_free[i];
-            if (b.dev != dev || b.bytes < need || b.bytes > 2 * need + (size_t(64) << 20)) continue;
+            if (b.dev != dev || b.bytes < need) continue;  // best fit: any cached block that is large enough
             if (best < 0 || b.bytes < g_blk_free[best].bytes) best = i;
         }
         if (best >= 0) {
