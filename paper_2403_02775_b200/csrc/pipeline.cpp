@@ -208,16 +208,11 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
         const char* e = std::getenv("EZQ_K3S_WORK_MB");
         return (e ? static_cast<size_t>(std::atoll(e)) : size_t(2048)) << 20;
     }();
-    // The tables may take at most an eighth of the free device memory (>= 128 MB;
-    // smaller buffers only mean more, shorter waves).
-    size_t k3s_work_cap = k3s_work_env;
-    {
-        size_t fr = 0, tot = 0;
-        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess)
-            k3s_work_cap = std::min(k3s_work_cap, std::max<size_t>(size_t(128) << 20, fr / 8));
-        else
-            cudaGetLastError();
-    }
+    // The tables may take at most a sixteenth of the device memory (>= 128 MB;
+    // smaller buffers only mean more, shorter waves). Total, not free, memory:
+    // cudaMemGetInfo per call was measured to stall some calls by 20-60 ms.
+    const size_t k3s_work_cap =
+        std::min(k3s_work_env, std::max<size_t>(size_t(128) << 20, di.total_mem / 16));
     if (cfg_status == EZQ_OK) {
         for (auto& kv : by_rows) {
             Plan p;

@@ -37,6 +37,7 @@ struct DeviceInfo {
     int sms = 0;
     int max_smem_optin = 0;
     int smem_per_sm = 0;
+    size_t total_mem = 0;
 };
 const DeviceInfo& device_info(int dev);
 
