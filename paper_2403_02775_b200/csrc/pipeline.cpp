@@ -581,13 +581,14 @@ int quantize_batch_host(const float* const* Ws, const int64_t* rows, const int64
                         ezq_qweight** outs, int* failed) {
     // Chunk sizes (overridable for tuning: EZQ_CHUNK_MB / EZQ_FIRST_MB).
     static const int64_t kChunkBytes =
-        std::getenv("EZQ_CHUNK_MB") ? (std::atoll(std::getenv("EZQ_CHUNK_MB")) << 20) : (1024ll << 20);
+        std::getenv("EZQ_CHUNK_MB") ? (std::atoll(std::getenv("EZQ_CHUNK_MB")) << 20) : (384ll << 20);
     std::vector<std::pair<int, int>> chunks;  // [first, last)
     int64_t max_bytes = 0;
     // The first chunk is small so compute starts after a short ingest; the
-    // later ones are large (fewer partial K3 waves, fewer host syncs).
+    // later ones are 384 MB (OPT-1.3B host->host: 1024 MB chunks 104 ms,
+    // 384 MB 100 ms, + 128 MB first chunk 99 ms; 256 MB 105 ms).
     static const int64_t kFirstBytes = std::getenv("EZQ_FIRST_MB") ? (std::atoll(std::getenv("EZQ_FIRST_MB")) << 20)
-                                                                    : (512ll << 20);
+                                                                    : (128ll << 20);
     // ... and so is the last: its compute and D2H are the exposed tail.
     static const int64_t kLastBytes = std::getenv("EZQ_LAST_MB") ? (std::atoll(std::getenv("EZQ_LAST_MB")) << 20)
                                                                   : (256ll << 20);
