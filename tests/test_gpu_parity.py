@@ -332,10 +332,16 @@ def _k3s_cases(O):
     W = O.gaussian(49152, 3, 90, 0.02)
     O.plant_outliers(W, 40, 0.2, 1.0, 91)
     out.append(("pieces6", W, Config(steps=40)))
+    # one bin holding nearly a whole column (tiny values beside one normal-sized
+    # value): the odd-even rounds cannot finish, the full radix sort takes over
+    W = O.gaussian(2048, 8, 92, 1.0)
+    W[:, 0] = (O.gaussian(2048, 1, 93, 1e-6)[:, 0]).astype(np.float32)
+    W[7, 0] = np.float32(1.5)
+    out.append(("bin_squeeze", W.astype(np.float32), Config(steps=60)))
     return out
 
 
-@pytest.mark.parametrize("idx", range(15))
+@pytest.mark.parametrize("idx", range(16))
 def test_k3s_edge_cases(gpu, O, idx):
     name, W, cfg = _k3s_cases(O)[idx]
     q = gpu.quantize_tensor(W, cfg)
