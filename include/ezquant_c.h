@@ -169,6 +169,17 @@ int ezq_quantize_tensor(const float* W, int64_t rows, int64_t cols, const ezq_co
 int ezq_quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* cols, int n,
                        const ezq_config* cfg, int mode, int in_mem, int out_mem, void* stream,
                        ezq_qweight** outs, int* failed_index);
+/* brute_force_optimal_scale (optimize.cpp:186-229) for every column of a
+ * batch, on the device: the reference's grid (grid_points scales in
+ * [s0/8, 1.25 s0] plus s0) over each column's normals (outliers isolated
+ * exactly as ezq_quantize_batch does). best_scale / best_error receive one
+ * double per column, tensors in order. The errors are the exact values of the
+ * grid objective (not the reference's sequential fp64 sums), so an argmin can
+ * differ from the reference's only between near-equal grid points. k <= 5,
+ * rows <= 65536. */
+int ezq_grid_oracle_batch(const float* const* Ws, const int64_t* rows, const int64_t* cols, int n,
+                          const ezq_config* cfg, int grid_points, int in_mem, void* stream, double* best_scale,
+                          double* best_error, int* failed_index);
 /* dequantize_tensor (pipeline.cpp:117-142): unpack, rescale
  * float(double(s_j) * l), scatter outliers. `q` arrays may be host or device
  * (q->mem); `out` is rows*cols floats in `out_mem`. */

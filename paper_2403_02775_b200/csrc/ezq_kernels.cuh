@@ -158,8 +158,10 @@ int k3s_cpb(int64_t piece_rows);         // columns per sort CTA (group width)
 size_t k3s_slot_bytes(int64_t piece_rows);  // table + info bytes per column piece
 // groups: for every column group, `pieces` consecutive entries (row0 = 0,
 // piece_rows, 2 piece_rows, ...).
+// grid_points > 0: run the brute-force grid oracle on the tables instead of
+// the Adam loop (best grid scale / error per column into s_fin / err_fin).
 void launch_k3_sorted(int64_t rows, int cpb, const TDesc* td, const K3Group* groups, int ngroups, Scratch sc,
-                      CfgDev cfg, void* work, size_t work_bytes, cudaStream_t st);
+                      CfgDev cfg, void* work, size_t work_bytes, cudaStream_t st, int grid_points = 0);
 void launch_seq_errors(const TDesc* td, const int2* tiles, int ntiles, Scratch sc, CfgDev cfg,
                        cudaStream_t st);
 // Re-packs the (rare) fused-pack columns whose stored scale is s_rtn.

@@ -760,6 +760,125 @@ void launch_pieces_t(int ncolgroups, int P, int cpb, int dstride, int tstride, c
                                                 cfg);
 }
 
+// ---- Grid oracle on the tables (brute_force_optimal_scale, optimize.cpp:186-229)
+// One column per warp, (threshold, piece) pairs over the lanes as in
+// k_qrange_pieces. The grid is the reference's: `points` scales
+// lo + (hi - lo) i / (points - 1), lo = s0 / 8, hi = 1.25 s0, plus s0 itself,
+// ascending and de-duplicated; err at each is the exact A s^2 - 2 Q s + C
+// (the scales are doubles here, so s^2 is a double-double); the strict-<
+// ascending scan keeps the smaller scale on ties. Writes the best grid scale
+// and its error to s_fin / err_fin.
+template <int PPL>
+__global__ void __launch_bounds__(256) k_grid_tables(const TDesc* __restrict__ td,
+                                                     const K3Group* __restrict__ groups, int ncolgroups, int P,
+                                                     int cpb, int dstride, int tstride,
+                                                     const double* __restrict__ tables,
+                                                     const ColInfo* __restrict__ infos, Scratch sc, CfgDev cfg,
+                                                     int points) {
+    const int lane = threadIdx.x & 31;
+    const int cidx = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int g = cidx / cpb, cc = cidx % cpb;
+    if (g >= ncolgroups) return;  // warp-uniform
+    const K3Group G0 = groups[g * P];
+    if (cc >= G0.ncols) return;  // warp-uniform
+    const int nb = cfg.lmax - cfg.lmin;
+    int nall = 0;
+    double mx = 0.0;
+    DD Cd = {0.0, 0.0};
+    for (int p = 0; p < P; ++p) {
+        const ColInfo ci = infos[(g * P + p) * cpb + cc];
+        nall += ci.n;
+        if (ci.n) mx = fmax(mx, fmax(fabs(static_cast<double>(ci.lo)), fabs(static_cast<double>(ci.hi))));
+        Cd = dd_add(Cd, DD{ci.chi, ci.clo});
+    }
+    double best_s = 1.0, best_e = 0.0;  // empty column: {1.0, 0.0} (optimize.cpp:198)
+    if (nall > 0) {
+        const double s0 = initial_scale_from_max(mx, cfg.lmax);
+        const double lo = s0 / 8.0, hi = s0 * 1.25;
+        bool own[PPL];
+        int jl[PPL], np[PPL], ib[PPL];
+        ColTab ct[PPL];
+#pragma unroll
+        for (int u = 0; u < PPL; ++u) {
+            const int pair = lane + 32 * u;
+            own[u] = pair < nb * P;
+            const int thr = own[u] ? pair % nb : 0, piece = own[u] ? pair / nb : 0;
+            const int slot = (g * P + piece) * cpb + cc;
+            jl[u] = cfg.lmin + 1 + thr;
+            ct[u].D = tables + static_cast<int64_t>(slot) * tstride;
+            ct[u].xs = reinterpret_cast<const float*>(ct[u].D + dstride);
+            ct[u].n = np[u] = own[u] ? infos[slot].n : 0;
+            ib[u] = np[u] >> 1;
+        }
+        bool s0_done = false, first = true;
+        double prev = 0.0;
+        for (int i = 0; i <= points; ++i) {  // warp-uniform
+            double s;
+            if (i < points) {
+                const double gi = lo + (hi - lo) * static_cast<double>(i) / static_cast<double>(points - 1);
+                if (!s0_done && s0 <= gi) {  // merge s0 into the ascending grid
+                    s = s0;
+                    s0_done = true;
+                    --i;
+                } else {
+                    s = gi;
+                }
+            } else {
+                if (s0_done) break;
+                s = s0;
+                s0_done = true;
+            }
+            if (!first && s == prev) continue;  // std::unique
+            prev = s;
+            int a = 0;
+            double q = 0.0;
+            const double inv = __drcp_rn(s);
+#pragma unroll
+            for (int u = 0; u < PPL; ++u) {
+                if (!own[u]) continue;
+                const int j = jl[u];
+                ib[u] = search_from(ct[u], ib[u], level_threshold(j, s, inv));
+                const bool pos = j >= 1;
+                a += (pos ? 2 * j - 1 : 1 - 2 * j) * (pos ? np[u] - ib[u] : ib[u]);
+                q = __dadd_rn(q, pos ? __ldg(ct[u].D + ib[u] + 1) : -__ldg(ct[u].D + ib[u]));
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                a += __shfl_xor_sync(0xffffffffu, a, o);
+                q = __dadd_rn(q, __shfl_xor_sync(0xffffffffu, q, o));
+            }
+            const double Ad = static_cast<double>(a);
+            const DD ss = dd_prod(s, s);
+            DD e = dd_prod(Ad, ss.hi);
+            e.lo = fma(Ad, ss.lo, e.lo);
+            e = dd_add(e, dd_prod(__dmul_rn(-2.0, q), s));
+            e = dd_add(e, Cd);
+            const double err = __dadd_rn(e.hi, e.lo);
+            if (first || err < best_e) {
+                best_e = err;
+                best_s = s;
+            }
+            first = false;
+        }
+    }
+    if (lane == 0) {
+        const TDesc& d = td[G0.tensor];
+        const int64_t gcol = d.col_base + G0.col0 + cc;
+        sc.s_fin[gcol] = best_s;
+        sc.err_fin[gcol] = best_e;
+    }
+}
+
+template <int PPL>
+void launch_grid_t(int ncolgroups, int P, int cpb, int dstride, int tstride, const TDesc* td,
+                   const K3Group* groups, const double* tables, const ColInfo* infos, const Scratch& sc,
+                   const CfgDev& cfg, int points, cudaStream_t st) {
+    const int64_t cols = static_cast<int64_t>(ncolgroups) * cpb;
+    const int grid = static_cast<int>((cols + 7) / 8);
+    k_grid_tables<PPL><<<grid, 256, 0, st>>>(td, groups, ncolgroups, P, cpb, dstride, tstride, tables, infos, sc, cfg,
+                                              points);
+}
+
 struct SortShape {
     int threads, ipt;
 };
@@ -828,7 +947,7 @@ int k3s_cpb(int64_t rows) {
 size_t k3s_slot_bytes(int64_t rows) { return sizeof(double) * k3s_tstride(rows) + sizeof(ColInfo); }
 
 void launch_k3_sorted(int64_t rows, int cpb, const TDesc* td, const K3Group* groups, int ngroups, Scratch sc,
-                      CfgDev cfg, void* work, size_t work_bytes, cudaStream_t st) {
+                      CfgDev cfg, void* work, size_t work_bytes, cudaStream_t st, int grid_points) {
     if (ngroups == 0) return;
     const int P = k3s_pieces(rows);
     const int64_t pr = k3s_piece_rows(rows);
@@ -860,8 +979,19 @@ void launch_k3_sorted(int64_t rows, int cpb, const TDesc* td, const K3Group* gro
         }
         prof_end(ps, st, static_cast<double>(nslots) * static_cast<double>(pr));
         // work: column-steps (a step = one err/grad evaluation + Adam update)
-        const int pl = prof_begin("qrange", st);
         const int ncg = ng / P;
+        if (grid_points > 0) {  // grid oracle instead of the Adam loop
+            switch (ppl) {
+                case 1: launch_grid_t<1>(ncg, P, cpb, dstride, tstride, td, groups + g0, tables, infos, sc, cfg, grid_points, st); break;
+                case 2: launch_grid_t<2>(ncg, P, cpb, dstride, tstride, td, groups + g0, tables, infos, sc, cfg, grid_points, st); break;
+                case 3: launch_grid_t<3>(ncg, P, cpb, dstride, tstride, td, groups + g0, tables, infos, sc, cfg, grid_points, st); break;
+                case 4: launch_grid_t<4>(ncg, P, cpb, dstride, tstride, td, groups + g0, tables, infos, sc, cfg, grid_points, st); break;
+                default: launch_grid_t<8>(ncg, P, cpb, dstride, tstride, td, groups + g0, tables, infos, sc, cfg, grid_points, st); break;
+            }
+            count_launch(2);
+            continue;
+        }
+        const int pl = prof_begin("qrange", st);
         if (P == 1 && nb <= 15) {
             launch_loop_t<16, 1>(nslots, cpb, dstride, tstride, td, groups + g0, tables, infos, sc, cfg, st);
         } else {

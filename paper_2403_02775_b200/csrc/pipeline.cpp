@@ -135,9 +135,18 @@ void free_qweight_arrays(ezq_qweight* q) {
 // on that stream and the call returns without waiting for them (the caller
 // synchronizes it) -- the chunked host pipeline overlaps them with the next
 // chunk's compute.
+// `grid` (ezq_grid_oracle_batch): no artifacts; the brute-force grid oracle
+// runs on the K3s tables and the per-column best grid scale / error are
+// copied to grid->scale / grid->error (batch column order).
+struct GridReq {
+    int points;
+    double* scale;
+    double* error;
+};
+
 int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* cols, int n,
                    const ezq_config* cfg, int mode, int in_mem, int out_mem, void* user_stream,
-                   ezq_qweight** outs, int* failed, cudaStream_t d2h = nullptr) {
+                   ezq_qweight** outs, int* failed, cudaStream_t d2h = nullptr, const GridReq* grid = nullptr) {
     if (failed) *failed = -1;
     if (n <= 0) return clear_error();
     for (int i = 0; i < n; ++i) outs[i] = nullptr;
@@ -217,7 +226,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
         for (auto& kv : by_rows) {
             Plan p;
             const int pieces = k3s_pieces(kv.first);
-            if (k3_sorted && eq && pieces > 0 && k3s_supported(cfg->bits)) {
+            if ((k3_sorted || grid) && eq && pieces > 0 && k3s_supported(cfg->bits)) {
                 // K3s: a CTA sorts a group of columns (one row piece), then a
                 // loop kernel runs the columns' Adam loops on the tables.
                 const int64_t pr = k3s_piece_rows(kv.first);
@@ -392,6 +401,21 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     }
 
     trace("qb: phase1 checked");
+    if (grid) {  // ---- grid oracle: tables + grid scan, no artifacts ----
+        const CfgDev cd = make_cfg(cfg, mode, d_bc);
+        for (auto& p : plans) {
+            if (!p.sorted_cpb)
+                return set_error(EZQ_ERR_INVALID_ARGUMENT, "grid oracle needs the sorted-column path (k <= 5, "
+                                                           "rows <= 65536)");
+            launch_k3_sorted(p.kl.rows, p.sorted_cpb, d_desc, d_groups + p.goff, static_cast<int>(p.groups.size()),
+                             sc, cd, d_k3s_work, k3s_work, st, grid->points);
+        }
+        EZQ_CK(cudaGetLastError());
+        EZQ_CK(cudaMemcpyAsync(grid->scale, sc.s_fin, sizeof(double) * tot_cols, cudaMemcpyDeviceToHost, st));
+        EZQ_CK(cudaMemcpyAsync(grid->error, sc.err_fin, sizeof(double) * tot_cols, cudaMemcpyDeviceToHost, st));
+        EZQ_CK(cudaStreamSynchronize(st));
+        return clear_error();
+    }
     // ---- outputs (device) ----
     struct Out {
         uint8_t* packed = nullptr;
@@ -724,6 +748,17 @@ int ezq_quantize_batch(const float* const* Ws, const int64_t* rows, const int64_
     }
     return quantize_batch(Ws, rows, cols, n, cfg, mode, in_mem, out_mem, stream, outs,
                           failed_index);
+}
+
+int ezq_grid_oracle_batch(const float* const* Ws, const int64_t* rows, const int64_t* cols, int n,
+                          const ezq_config* cfg, int grid_points, int in_mem, void* stream, double* best_scale,
+                          double* best_error, int* failed_index) {
+    if (grid_points < 2) return set_error(EZQ_ERR_INVALID_ARGUMENT, "grid_points must be >= 2");
+    if (!best_scale || !best_error) return set_error(EZQ_ERR_INVALID_ARGUMENT, "null output");
+    std::vector<ezq_qweight*> outs(static_cast<size_t>(std::max(n, 1)), nullptr);
+    const GridReq g{grid_points, best_scale, best_error};
+    return quantize_batch(Ws, rows, cols, n, cfg, EZQ_MODE_EASYQUANT, in_mem, EZQ_MEM_HOST, stream, outs.data(),
+                          failed_index, nullptr, &g);
 }
 
 int ezq_quantize_tensor(const float* W, int64_t rows, int64_t cols, const ezq_config* cfg,

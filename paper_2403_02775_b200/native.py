@@ -162,6 +162,8 @@ def lib() -> C.CDLL:
         L.ezq_quantize_batch.argtypes = [C.POINTER(P), C.POINTER(I64), C.POINTER(I64), I32,
                                          C.POINTER(CConfig), I32, I32, I32, P,
                                          C.POINTER(C.POINTER(CQWeight)), C.POINTER(C.c_int)]
+        L.ezq_grid_oracle_batch.argtypes = [C.POINTER(P), C.POINTER(I64), C.POINTER(I64), I32,
+                                            C.POINTER(CConfig), I32, I32, P, P, P, C.POINTER(C.c_int)]
         L.ezq_dequantize_tensor.argtypes = [C.POINTER(CQWeight), P, I32, P]
         L.ezq_qweight_wrap.argtypes = [I64, I64, I32, P, I64, P, I64, P, I64, D, D, C.c_float,
                                        I32, C.POINTER(C.POINTER(CQWeight))]
@@ -526,6 +528,28 @@ def brute_force_scale(x, mask, cfg: Config, grid_points: int = 2000):
     check(lib().ezq_brute_force_scale(_ptr(x), x.size, _ptr(m), nm, C.byref(c), grid_points,
                                       C.byref(s), C.byref(e)))
     return s.value, e.value
+
+
+def grid_oracle_batch(Ws: Sequence, cfg: Config, grid_points: int = 2000, stream=None):
+    """ezq_grid_oracle_batch: the reference's brute-force grid optimum
+    (optimize.cpp:186-229) for every column of every tensor, on the device.
+    Returns a list of (best_scale, best_error) float64 arrays, one per tensor."""
+    n = len(Ws)
+    ptrs = (C.c_void_p * n)(*[_ptr(w) for w in Ws])
+    rows = (C.c_int64 * n)(*[w.shape[0] for w in Ws])
+    cols = (C.c_int64 * n)(*[w.shape[1] for w in Ws])
+    tot = sum(int(w.shape[1]) for w in Ws)
+    sc, er = np.zeros(tot, np.float64), np.zeros(tot, np.float64)
+    failed = C.c_int(-1)
+    c = cfg.to_c()
+    check(lib().ezq_grid_oracle_batch(ptrs, rows, cols, n, C.byref(c), grid_points, _mem(Ws[0]),
+                                      _stream(stream, Ws[0]), _ptr(sc), _ptr(er), C.byref(failed)))
+    out, o = [], 0
+    for w in Ws:
+        k = int(w.shape[1])
+        out.append((sc[o:o + k], er[o:o + k]))
+        o += k
+    return out
 
 
 def quantize_channel(x, scale: float, cfg: Config) -> np.ndarray:

@@ -378,3 +378,21 @@ print("ok")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("rows,cols,bits,seed", [(300, 20, 4, 1), (2048, 8, 3, 2), (9000, 3, 4, 3), (1500, 6, 5, 4)])
+def test_grid_oracle_batch(gpu, O, rows, cols, bits, seed):
+    """ezq_grid_oracle_batch (device, K3s tables) vs the single-channel grid
+    oracle ezq_brute_force_scale (bit-exact with the reference's
+    brute_force_optimal_scale) on every column's normals: same best scale, the
+    error to 1e-12 (exact objective vs the reference's sequential sums)."""
+    W = O.gaussian(rows, cols, seed, 0.02)
+    O.plant_outliers(W, max(1, rows * cols // 200), 0.2, 1.0, seed + 11)
+    cfg = Config(bits=bits)
+    (scales, errs), = gpu.grid_oracle_batch([W], cfg, 500)
+    out, _, _ = gpu.detect_outliers(W, cfg)
+    for c in range(cols):
+        mask = np.sort(out["row"][out["col"] == c]).astype(np.uint32)
+        s_ref, e_ref = gpu.brute_force_scale(W[:, c].copy(), mask if mask.size else None, cfg, 500)
+        assert scales[c] == s_ref, (c, scales[c], s_ref)
+        assert abs(errs[c] - e_ref) <= 1e-12 * max(abs(e_ref), 1e-300), (c, errs[c], e_ref)
