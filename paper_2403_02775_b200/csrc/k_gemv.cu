@@ -185,7 +185,7 @@ struct GemvArgs {
 template <int NB, int XT>
 __global__ void __launch_bounds__(512) k_gemv_mma(const GemvArgs a) {
     constexpr bool F16 = XT == kF16;
-    constexpr int kChains = 4;
+    constexpr int kChains = NB == 1 ? 4 : 2;  // NB = 2: fewer live accumulators, more resident warps
     __shared__ __align__(16) float red[kMaxWarps][NB][32][4];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int g = lane >> 2, t = lane & 3;
@@ -235,8 +235,8 @@ __global__ void __launch_bounds__(512) k_gemv_mma(const GemvArgs a) {
                 for (int nb = 0; nb < NB; ++nb) {
                     unsigned hi[2], lo[2];
                     x_frag<XT>(xg[u][nb], s, hi, lo);
-                    mma16816<F16>(acc[s][nb], af, hi);
-                    if (XT == kF32) mma16816<F16>(acc[s][nb], af, lo);
+                    mma16816<F16>(acc[s % kChains][nb], af, hi);
+                    if (XT == kF32) mma16816<F16>(acc[s % kChains][nb], af, lo);
                 }
             }
         }
@@ -255,7 +255,11 @@ __global__ void __launch_bounds__(512) k_gemv_mma(const GemvArgs a) {
     for (int nb = 0; nb < NB; ++nb) {
         float v[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] = acc[0][nb][i] + acc[1][nb][i] + acc[2][nb][i] + acc[3][nb][i];
+        for (int i = 0; i < 4; ++i) {
+            v[i] = acc[0][nb][i];
+#pragma unroll
+            for (int h = 1; h < kChains; ++h) v[i] += acc[h][nb][i];
+        }
         *reinterpret_cast<float4*>(red[warp][nb][lane]) = make_float4(v[0], v[1], v[2], v[3]);
     }
     __syncthreads();
@@ -480,7 +484,9 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
         a.y = y + static_cast<int64_t>(b0) * p->cols;
         const bool two = a.batch > 8;
         const unsigned grid = static_cast<unsigned>(p->tiles);
-        const unsigned threads = static_cast<unsigned>(p->warps * 32);
+        // two n8 tiles hold twice the accumulators: at most 8 warps per CTA so
+        // that two CTAs share an SM and a 16-warp plan stays one wave
+        const unsigned threads = static_cast<unsigned>((two ? std::min(p->warps, 8) : p->warps) * 32);
         switch (x_dtype * 2 + (two ? 1 : 0)) {
             case 0: k_gemv_mma<1, kF32><<<grid, threads, 0, st>>>(a); break;
             case 1: k_gemv_mma<2, kF32><<<grid, threads, 0, st>>>(a); break;
