@@ -289,11 +289,22 @@ __global__ void __launch_bounds__(512) k_gemv_mma(const GemvArgs a) {
 // Launched as a programmatic dependent of k_gemv_mma: the gathers overlap
 // the weight stream and griddepcontrol.wait orders the read-modify-write
 // of y after the main kernel's stores.
+// x [batch][rows] (any dtype) -> xt [rows][16] f32 (exact), so the outlier
+// pass reads a row's batch values with NBT/4 16-byte loads instead of NBT
+// scalar gathers.
+__global__ void __launch_bounds__(256) k_gemv_xt(const void* __restrict__ x, int xt_type, int64_t rows, int batch,
+                                                 float* __restrict__ xt) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * 16 + (threadIdx.x >> 4);
+    const int n = threadIdx.x & 15;
+    if (r < rows) xt[r * 16 + n] = n < batch ? load_x(x, xt_type, static_cast<int64_t>(n) * rows + r) : 0.f;
+}
+
 template <int XT, int NBT>
 __global__ void __launch_bounds__(256) k_gemv_outliers(int64_t rows, int64_t cols, const int64_t* __restrict__ col_ptr,
                                                        const uint32_t* __restrict__ out_row,
                                                        const float* __restrict__ out_val, const void* __restrict__ x,
-                                                       int batch, float* __restrict__ y) {
+                                                       int batch, float* __restrict__ y,
+                                                       const float* __restrict__ xt) {
     constexpr int kU = 4;
     const int lane = threadIdx.x & 31;
     const int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -311,11 +322,24 @@ __global__ void __launch_bounds__(256) k_gemv_outliers(int64_t rows, int64_t col
             r[u] = e < e1 ? __ldg(out_row + e) : 0u;
             v[u] = e < e1 ? __ldg(out_val + e) : 0.f;
         }
+        if (NBT > 8) {  // transposed x: one 16-byte load per 4 batch rows
 #pragma unroll
-        for (int u = 0; u < kU; ++u)
+            for (int u = 0; u < kU; ++u)
 #pragma unroll
-            for (int n = 0; n < NBT; ++n)
-                if (n < batch) part[n] = fmaf(load_x(x, XT, static_cast<int64_t>(n) * rows + r[u]), v[u], part[n]);
+                for (int n4 = 0; n4 < NBT / 4; ++n4) {
+                    const float4 xv = __ldg(reinterpret_cast<const float4*>(xt + static_cast<int64_t>(r[u]) * 16) + n4);
+                    const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (4 * n4 + k < batch) part[4 * n4 + k] = fmaf(xs[k], v[u], part[4 * n4 + k]);
+                }
+        } else {
+#pragma unroll
+            for (int u = 0; u < kU; ++u)
+#pragma unroll
+                for (int n = 0; n < NBT; ++n)
+                    if (n < batch) part[n] = fmaf(load_x(x, XT, static_cast<int64_t>(n) * rows + r[u]), v[u], part[n]);
+        }
     }
     const bool any = e1 > e0;
     if (any) {
@@ -386,6 +410,7 @@ struct ezq_gemv_plan {
     int64_t n_out;
     int warps;            // warps per CTA
     int dev;
+    float* xt;            // batch > 1 with outliers: x transposed [rows][16] f32 (owned)
 };
 
 extern "C" {
@@ -435,6 +460,8 @@ int ezq_gemv_prepare(const ezq_qweight* q, void* stream, ezq_gemv_plan** plan) {
     p->dev = dev;
     EZQ_CK(cudaMalloc(&p->T, sizeof(uint4) * p->tiles * p->kq * 32));
     EZQ_CK(cudaMalloc(&p->col_ptr, sizeof(int64_t) * (q->cols + 1)));
+    p->xt = nullptr;
+    if (q->n_outliers > 0) EZQ_CK(cudaMalloc(&p->xt, sizeof(float) * 16 * static_cast<size_t>(q->rows)));
     EZQ_CK(cudaMalloc(&p->out_row, sizeof(uint32_t) * std::max<int64_t>(q->n_outliers, 1)));
     EZQ_CK(cudaMalloc(&p->out_val, sizeof(float) * std::max<int64_t>(q->n_outliers, 1)));
     // Warps per CTA (one CTA per 16-column tile): about 16 resident warps
@@ -483,6 +510,11 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
         a.x = static_cast<const char*>(x) + xes * static_cast<size_t>(b0) * p->rows;
         a.y = y + static_cast<int64_t>(b0) * p->cols;
         const bool two = a.batch > 8;
+        if (p->n_out && a.batch > 8) {  // transposed x for the outlier pass (pays off from 9 batch rows)
+            k_gemv_xt<<<static_cast<unsigned>((p->rows + 15) / 16), 256, 0, st>>>(a.x, x_dtype, p->rows, a.batch,
+                                                                                  p->xt);
+            count_launch();
+        }
         const unsigned grid = static_cast<unsigned>(p->tiles);
         // two n8 tiles hold twice the accumulators: at most 8 warps per CTA so
         // that two CTAs share an SM and a 16-warp plan stays one wave
@@ -512,11 +544,12 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
             const void* xg = a.x;
             float* yg = a.y;
             const int bt = a.batch;
+            const float* xtg = p->xt;
             cudaError_t e;
 #define EZQ_OUT(X)                                                                                     \
-    (bt == 1 ? cudaLaunchKernelEx(&lc, k_gemv_outliers<X, 1>, p->rows, p->cols, cp, orow, oval, xg, bt, yg) \
-     : bt <= 8 ? cudaLaunchKernelEx(&lc, k_gemv_outliers<X, 8>, p->rows, p->cols, cp, orow, oval, xg, bt, yg) \
-               : cudaLaunchKernelEx(&lc, k_gemv_outliers<X, 16>, p->rows, p->cols, cp, orow, oval, xg, bt, yg))
+    (bt == 1 ? cudaLaunchKernelEx(&lc, k_gemv_outliers<X, 1>, p->rows, p->cols, cp, orow, oval, xg, bt, yg, xtg) \
+     : bt <= 8 ? cudaLaunchKernelEx(&lc, k_gemv_outliers<X, 8>, p->rows, p->cols, cp, orow, oval, xg, bt, yg, xtg) \
+               : cudaLaunchKernelEx(&lc, k_gemv_outliers<X, 16>, p->rows, p->cols, cp, orow, oval, xg, bt, yg, xtg))
             if (x_dtype == kF32) e = EZQ_OUT(kF32);
             else if (x_dtype == kBF16) e = EZQ_OUT(kBF16);
             else e = EZQ_OUT(kF16);
@@ -539,6 +572,7 @@ void ezq_gemv_plan_free(ezq_gemv_plan* p) {
     if (!p) return;
     cudaFree(p->T);
     cudaFree(p->col_ptr);
+    if (p->xt) cudaFree(p->xt);
     cudaFree(p->out_row);
     cudaFree(p->out_val);
     delete p;
