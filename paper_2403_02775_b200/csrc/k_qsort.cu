@@ -67,6 +67,18 @@ __device__ __forceinline__ DD dd_prod(double a, double b) {
     const double p = __dmul_rn(a, b);
     return {p, fma(a, b, -p)};
 }
+// Normalized double-doubles (hi = RN(hi + lo)) compare lexicographically.
+__device__ __forceinline__ bool dd_lt(DD a, DD b) { return a.hi < b.hi || (a.hi == b.hi && a.lo < b.lo); }
+__device__ __forceinline__ bool dd_le(DD a, DD b) { return a.hi < b.hi || (a.hi == b.hi && a.lo <= b.lo); }
+// err(s) - C = A s^2 - 2 Q s (s a float: s^2 exact), normalized: the
+// selection only compares errors of one column, so the column constant
+// C = sum x^2 drops out and the comparison is of the exact values.
+__device__ __forceinline__ DD err_minus_c(double Ad, double q, double s) {
+    const DD p1 = dd_prod(Ad, __dmul_rn(s, s));
+    const DD p2 = dd_prod(__dmul_rn(-2.0, q), s);
+    const DD h = two_sum(p1.hi, p2.hi);
+    return two_sum(h.hi, __dadd_rn(h.lo, __dadd_rn(p1.lo, p2.lo)));
+}
 
 // Smallest float x with level(x) >= v at scale s: RN(x*inv) >= t (> t for
 // v <= 0), t = v - 1/2. Candidates start at RN32(t*s) (t*s is exact in
@@ -345,7 +357,7 @@ struct ColumnSorter {
 template <int THREADS, int IPT>
 __global__ void __launch_bounds__(THREADS) k_qsort_tables(const TDesc* __restrict__ td,
                                                           const K3Group* __restrict__ groups, int cpb, int prows,
-                                                          int dstride, int xstride, int tstride,
+                                                          int dstride, int xstride, int tstride, int need_c,
                                                           double* __restrict__ tables,
                                                           ColInfo* __restrict__ infos) {
     constexpr int NPAD = THREADS * IPT;
@@ -400,34 +412,44 @@ __global__ void __launch_bounds__(THREADS) k_qsort_tables(const TDesc* __restric
         // to double-double
         int cneg = 0, cfin = 0;
         double tneg = 0.0, tpos = 0.0;
-        DD sq = {0.0, 0.0}, sp = {0.0, 0.0};
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {  // two independent chains: negatives up, the rest down
             const float xn = keys[i], xp = keys[IPT - 1 - i];
             cneg += xn < 0.f;
             cfin += xn < kInf;
-            if (xn < 0.f) {
-                const double xd = static_cast<double>(xn);
-                tneg = __dadd_rn(tneg, xd);
-                const double y = __dmul_rn(xd, xd), t = __dadd_rn(sq.hi, y);
-                sq.lo = __dadd_rn(sq.lo, __dsub_rn(y, __dsub_rn(t, sq.hi)));
-                sq.hi = t;
+            if (xn < 0.f) tneg = __dadd_rn(tneg, static_cast<double>(xn));
+            if (xp >= 0.f && xp < kInf) tpos = __dadd_rn(tpos, static_cast<double>(xp));
+        }
+        DD sq = {0.0, 0.0};
+        if (need_c) {  // C = sum x^2 (grid oracle only: the Adam loop compares err - C)
+            DD sp = {0.0, 0.0};
+#pragma unroll
+            for (int i = 0; i < IPT; ++i) {
+                const float xn = keys[i], xp = keys[IPT - 1 - i];
+                if (xn < 0.f) {
+                    const double xd = static_cast<double>(xn);
+                    const double y = __dmul_rn(xd, xd), t = __dadd_rn(sq.hi, y);
+                    sq.lo = __dadd_rn(sq.lo, __dsub_rn(y, __dsub_rn(t, sq.hi)));
+                    sq.hi = t;
+                }
+                if (xp >= 0.f && xp < kInf) {
+                    const double xd = static_cast<double>(xp);
+                    const double y = __dmul_rn(xd, xd), t = __dadd_rn(sp.hi, y);
+                    sp.lo = __dadd_rn(sp.lo, __dsub_rn(y, __dsub_rn(t, sp.hi)));
+                    sp.hi = t;
+                }
             }
-            if (xp >= 0.f && xp < kInf) {
-                const double xd = static_cast<double>(xp);
-                tpos = __dadd_rn(tpos, xd);
-                const double y = __dmul_rn(xd, xd), t = __dadd_rn(sp.hi, y);
-                sp.lo = __dadd_rn(sp.lo, __dsub_rn(y, __dsub_rn(t, sp.hi)));
-                sp.hi = t;
+            sq = dd_add(two_sum(sq.hi, sq.lo), two_sum(sp.hi, sp.lo));
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const DD u = {__shfl_xor_sync(0xffffffffu, sq.hi, o), __shfl_xor_sync(0xffffffffu, sq.lo, o)};
+                sq = dd_add(sq, u);
             }
         }
-        sq = dd_add(two_sum(sq.hi, sq.lo), two_sum(sp.hi, sp.lo));
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
             cneg += __shfl_xor_sync(0xffffffffu, cneg, o);
             cfin += __shfl_xor_sync(0xffffffffu, cfin, o);
-            const DD u = {__shfl_xor_sync(0xffffffffu, sq.hi, o), __shfl_xor_sync(0xffffffffu, sq.lo, o)};
-            sq = dd_add(sq, u);
         }
         if (lane == 0) {
             wn[warp][0] = cneg;
@@ -524,11 +546,11 @@ __global__ void __launch_bounds__(256) k_qrange_tables(const TDesc* __restrict__
     double s_rtn = static_cast<double>(__double2float_rn(s0_raw));
     double s_fin = s_rtn;
     if (cfg.mode == EZQ_MODE_EASYQUANT) {  // uniform across the warp
-        const DD Cd = {ci.chi, ci.clo};
         double s = snap(s0_raw);
         const double s0 = s;
         double m = 0.0, vv = 0.0;
-        double e0 = 0.0, best_err = 0.0, best_s = s, fixed_s = s, fixed_err = 0.0;
+        DD e0 = {0.0, 0.0}, best_err = {0.0, 0.0}, fixed_err = {0.0, 0.0};
+        double best_s = s, fixed_s = s;
         bool own[TPL];
         int jl[TPL], wA[TPL], ib[TPL];
         float Xp[TPL], span[TPL];  // previous threshold; x[k0+7] - x[k0] near it
@@ -576,19 +598,14 @@ __global__ void __launch_bounds__(256) k_qrange_tables(const TDesc* __restrict__
             const double Ad = static_cast<double>(a);
             // A s^2 - 2 Q s + C: both products exact as pairs; the three
             // leading parts summed exactly, the tails added after
-            const DD p1 = dd_prod(Ad, __dmul_rn(s, s));  // s^2 exact
-            const DD p2 = dd_prod(__dmul_rn(-2.0, q), s);
-            const DD h12 = two_sum(p1.hi, p2.hi);
-            const DD h = two_sum(h12.hi, Cd.hi);
-            const double tail = __dadd_rn(__dadd_rn(__dadd_rn(h.lo, h12.lo), __dadd_rn(p1.lo, p2.lo)), Cd.lo);
-            const double err = __dadd_rn(h.hi, tail);
+            const DD err = err_minus_c(Ad, q, s);
             const double grad = 2.0 * __dsub_rn(__dmul_rn(Ad, s), q);  // A s exact
             if (t == 0) {
                 e0 = err;
                 best_err = err;
                 fixed_err = err;
             } else {
-                if (err < best_err) {  // strict: earliest minimum wins (optimize.cpp:158)
+                if (dd_lt(err, best_err)) {  // strict: earliest minimum wins (optimize.cpp:158)
                     best_err = err;
                     best_s = s;
                 }
@@ -602,7 +619,7 @@ __global__ void __launch_bounds__(256) k_qrange_tables(const TDesc* __restrict__
                                      cfg.rbc2[t + 1], cfg.adam));
         }
         if (cfg.select == EZQ_SELECT_FIXED)
-            s_fin = (fixed_err <= e0) ? fixed_s : s0;  // optimize.cpp:169-178
+            s_fin = dd_le(fixed_err, e0) ? fixed_s : s0;  // optimize.cpp:169-178
         else
             s_fin = best_s;
         s_rtn = s0;
@@ -649,12 +666,10 @@ __global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__
     // column totals over the pieces, in piece order
     int nall = 0;
     double mx = 0.0;
-    DD Cd = {0.0, 0.0};
     for (int p = 0; p < P; ++p) {
         const ColInfo ci = infos[(g * P + p) * cpb + cc];
         nall += ci.n;
         if (ci.n) mx = fmax(mx, fmax(fabs(static_cast<double>(ci.lo)), fabs(static_cast<double>(ci.hi))));
-        Cd = dd_add(Cd, DD{ci.chi, ci.clo});
     }
     const double s0_raw = initial_scale_from_max(mx, cfg.lmax);
     double s_rtn = static_cast<double>(__double2float_rn(s0_raw));
@@ -663,7 +678,8 @@ __global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__
         double s = snap(s0_raw);
         const double s0 = s;
         double m = 0.0, vv = 0.0;
-        double e0 = 0.0, best_err = 0.0, best_s = s, fixed_s = s, fixed_err = 0.0;
+        DD e0 = {0.0, 0.0}, best_err = {0.0, 0.0}, fixed_err = {0.0, 0.0};
+        double best_s = s, fixed_s = s;
         bool own[PPL];
         int jl[PPL], np[PPL], ib[PPL];
         ColTab ct[PPL];
@@ -711,19 +727,14 @@ __global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__
                 q = __dadd_rn(q, __shfl_xor_sync(0xffffffffu, q, o));
             }
             const double Ad = static_cast<double>(a);
-            const DD p1 = dd_prod(Ad, __dmul_rn(s, s));  // s^2 exact
-            const DD p2 = dd_prod(__dmul_rn(-2.0, q), s);
-            const DD h12 = two_sum(p1.hi, p2.hi);
-            const DD h = two_sum(h12.hi, Cd.hi);
-            const double tail = __dadd_rn(__dadd_rn(__dadd_rn(h.lo, h12.lo), __dadd_rn(p1.lo, p2.lo)), Cd.lo);
-            const double err = __dadd_rn(h.hi, tail);
+            const DD err = err_minus_c(Ad, q, s);
             const double grad = 2.0 * __dsub_rn(__dmul_rn(Ad, s), q);  // A s exact
             if (t == 0) {
                 e0 = err;
                 best_err = err;
                 fixed_err = err;
             } else {
-                if (err < best_err) {  // strict: earliest minimum wins (optimize.cpp:158)
+                if (dd_lt(err, best_err)) {  // strict: earliest minimum wins (optimize.cpp:158)
                     best_err = err;
                     best_s = s;
                 }
@@ -737,7 +748,7 @@ __global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__
                                      cfg.rbc2[t + 1], cfg.adam));
         }
         if (cfg.select == EZQ_SELECT_FIXED)
-            s_fin = (fixed_err <= e0) ? fixed_s : s0;  // optimize.cpp:169-178
+            s_fin = dd_le(fixed_err, e0) ? fixed_s : s0;  // optimize.cpp:169-178
         else
             s_fin = best_s;
         s_rtn = s0;
@@ -905,12 +916,12 @@ size_t sort_smem(int cpb) {
 }
 
 template <int THREADS, int IPT>
-void launch_sort_t(int ngroups, int cpb, int prows, int dstride, int xstride, int tstride, const TDesc* td,
+void launch_sort_t(int ngroups, int cpb, int prows, int dstride, int xstride, int tstride, int need_c, const TDesc* td,
                    const K3Group* groups, double* tables, ColInfo* infos, cudaStream_t st) {
     auto k = k_qsort_tables<THREADS, IPT>;
     const size_t smem = sort_smem<THREADS, IPT>(cpb);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k<<<ngroups, THREADS, smem, st>>>(td, groups, cpb, prows, dstride, xstride, tstride, tables, infos);
+    k<<<ngroups, THREADS, smem, st>>>(td, groups, cpb, prows, dstride, xstride, tstride, need_c, tables, infos);
 }
 
 }  // namespace
@@ -971,11 +982,11 @@ void launch_k3_sorted(int64_t rows, int cpb, const TDesc* td, const K3Group* gro
         const int ps = prof_begin("qsort", st);
         const int ipr = static_cast<int>(pr);
         switch (sh.threads * 100 + sh.ipt) {
-            case 12808: launch_sort_t<128, 8>(ng, cpb, ipr, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
-            case 12816: launch_sort_t<128, 16>(ng, cpb, ipr, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
-            case 25616: launch_sort_t<256, 16>(ng, cpb, ipr, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
-            case 38416: launch_sort_t<384, 16>(ng, cpb, ipr, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
-            default: launch_sort_t<512, 16>(ng, cpb, ipr, dstride, xstride, tstride, td, groups + g0, tables, infos, st); break;
+            case 12808: launch_sort_t<128, 8>(ng, cpb, ipr, dstride, xstride, tstride, grid_points > 0, td, groups + g0, tables, infos, st); break;
+            case 12816: launch_sort_t<128, 16>(ng, cpb, ipr, dstride, xstride, tstride, grid_points > 0, td, groups + g0, tables, infos, st); break;
+            case 25616: launch_sort_t<256, 16>(ng, cpb, ipr, dstride, xstride, tstride, grid_points > 0, td, groups + g0, tables, infos, st); break;
+            case 38416: launch_sort_t<384, 16>(ng, cpb, ipr, dstride, xstride, tstride, grid_points > 0, td, groups + g0, tables, infos, st); break;
+            default: launch_sort_t<512, 16>(ng, cpb, ipr, dstride, xstride, tstride, grid_points > 0, td, groups + g0, tables, infos, st); break;
         }
         prof_end(ps, st, static_cast<double>(nslots) * static_cast<double>(pr));
         // work: column-steps (a step = one err/grad evaluation + Adam update)
