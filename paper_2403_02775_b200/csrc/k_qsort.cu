@@ -27,10 +27,11 @@
 //    EXACT in fp64 (<= 13 + 24 + log2(max/(s/2)) significant bits, < 53
 //    unless s falls below max * 2^-16), and so are A, Q and their
 //    cross-lane sums, in any order;
-//  - err and grad are formed from A, Q, C in double-double and rounded once.
-// err/grad are therefore the exact values (to ~2^-100) -- at least as close
-// to the true sums as the reference's own sequential fp64 sums (the
-// agreement regime of DESIGN.md §4).
+//  - grad = 2 (A s - Q) is rounded once from exact terms; the selection
+//    compares err - C = A s^2 - 2 Q s as exact double-doubles (C is constant
+//    per column), so both are the exact values (to ~2^-100) -- at least as
+//    close to the true sums as the reference's own sequential fp64 sums (the
+//    agreement regime of DESIGN.md §4).
 //
 // Layout: a CTA stages cpb columns, sorts each with a block radix sort in
 // registers and replaces it by its (rows + 2)-double table; the x values are
