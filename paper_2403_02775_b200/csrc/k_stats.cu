@@ -48,44 +48,47 @@ __device__ __forceinline__ void p1_elem(P1& a, float v, unsigned long long flat)
     if (!isfinite(v) && a.bad == ~0ull) a.bad = flat;
 }
 
-// ---- cp.async-pipelined chunk passes --------------------------------------
+// ---- TMA-pipelined chunk passes -------------------------------------------
 // One warp owns 32 consecutive global chunks (lane c <-> chunk c, so each
 // lane runs exactly the reference's sequential chain for its chunk). The warp
-// streams the chunks through SMEM in 64-element tiles with cp.async (3-stage
-// ring: the per-warp issue rate, not HBM latency, bounds a warp, so a short
-// ring that lets ~13 warps share an SM beats a deep one): each cp.async instruction moves two
-// contiguous 256-byte chunk segments, so HBM sees fully coalesced traffic
-// while every lane reads its own tile with conflict-free LDS.128 (68-float
-// row pitch). Requires 16-byte aligned tensors (else the simple kernels run).
+// streams the chunks through SMEM in 64-element tiles: each lane's 256-byte
+// tile row arrives by one cp.async.bulk on the stage's mbarrier (3-stage ring:
+// 2 tiles in flight per warp, ~8 warps/SM; 16 cp.async per lane per tile, the
+// previous fill, cost 0.7 ms per OPT-1.3B step), and every lane reads its own
+// row with conflict-free LDS.128 (68-float row pitch). Partial tiles are read
+// from global memory. Requires 16-byte aligned tensors (else the simple
+// kernels run).
 constexpr int kTile = 64;
 constexpr int kPitch = kTile + 4;
-constexpr int kStages = 3;  // 2 tiles (16 KB) in flight per warp: ~13 warps/SM (8 stages: 3 warps/SM, 1.4 ms slower per OPT-1.3B step)
+constexpr int kStages = 3;  // 2 tiles in flight per warp (4 or 6 stages measured slower: fewer warps/SM)
 constexpr int kWarpsPerCta = 1;
-constexpr size_t kStatsSmem = sizeof(float) * kStages * 32 * kPitch * kWarpsPerCta;
+constexpr size_t kRingBytes = sizeof(float) * kStages * 32 * kPitch;  // per warp
+constexpr size_t kStatsSmem = (kRingBytes + sizeof(unsigned long long) * kStages) * kWarpsPerCta;
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
-    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
-                 "r"(src_bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+// Ring fill: a lane's full 256-byte tile row is one cp.async.bulk (TMA)
+// completing on the stage's mbarrier (lane 0 posts the expected bytes of the
+// whole warp first); partial tiles are read from global memory by the
+// consumer instead. All lanes call it (the byte count is a warp reduction).
+__device__ __forceinline__ void issue_tile_bulk(float* row, unsigned bar, const float* my_ptr, int my_cnt, int t) {
+    const bool full = my_ptr != nullptr && (t + 1) * kTile <= my_cnt;
+    const unsigned total = __reduce_add_sync(0xffffffffu, full ? 256u : 0u);
+    if ((threadIdx.x & 31) == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(total) : "memory");
+    __syncwarp();
+    if (full) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the row was read by this lane before
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 256, [%2];"
+                     ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(row))), "l"(my_ptr + t * kTile), "r"(bar)
+                     : "memory");
+    }
 }
 
-// Each lane copies its OWN chunk's tile (16 x 16-byte cp.async, 256 B
-// contiguous): no address shuffles; every 32-byte sector is fully used.
-__device__ __forceinline__ void issue_tile(float* row, const float* my_ptr, int my_cnt, int t) {
-    if (my_ptr == nullptr) return;
-    const int e0 = t * kTile;
-#pragma unroll
-    for (int part = 0; part < kTile / 4; ++part) {
-        const int e = e0 + part * 4;
-        int bytes = (my_cnt - e) * 4;
-        bytes = bytes < 0 ? 0 : (bytes > 16 ? 16 : bytes);
-        if (bytes > 0) cp_async16(row + part * 4, my_ptr + e, bytes);
+__device__ __forceinline__ void wait_bar(unsigned bar, unsigned phase) {
+    unsigned ok = 0;
+    for (long long spin = 0; !ok; ++spin) {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(ok) : "r"(bar), "r"(phase) : "memory");
+        if (spin > (1ll << 26)) __trap();  // never hang the device on a lost transfer
     }
 }
 
@@ -104,6 +107,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_stats_pipe(const TDesc* _
     extern __shared__ __align__(16) float sbuf[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     float* ring = sbuf + warp * kStages * 32 * kPitch;
+    unsigned long long* bars =
+        reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(sbuf) + kRingBytes * kWarpsPerCta) +
+        warp * kStages;
     const int64_t g = (static_cast<int64_t>(blockIdx.x) * kWarpsPerCta + warp) * 32 + lane;
     const float* ptr = nullptr;
     int cnt = 0;
@@ -131,16 +137,19 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_stats_pipe(const TDesc* _
     float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000), amax = 0.f;
     unsigned long long bad = ~0ull;
 
-#pragma unroll
-    for (int p = 0; p < kStages - 1; ++p) {
-        if (p < ntiles) issue_tile(myrow0 + p * 32 * kPitch, ptr, cnt, p);
-        cp_async_commit();
+    if (lane == 0) {
+        for (int k = 0; k < kStages; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bars + k))));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    __syncwarp();
+    auto bar_of = [&](int k) { return static_cast<unsigned>(__cvta_generic_to_shared(bars + k)); };
+#pragma unroll
+    for (int p = 0; p < kStages - 1; ++p) issue_tile_bulk(myrow0 + p * 32 * kPitch, bar_of(p), ptr, cnt, p);
     for (int tile = 0; tile < max_tiles; ++tile) {
         const int nt = tile + kStages - 1;
-        if (nt < ntiles) issue_tile(myrow0 + (nt % kStages) * 32 * kPitch, ptr, cnt, nt);
-        cp_async_commit();
-        cp_async_wait<kStages - 1>();
+        issue_tile_bulk(myrow0 + (nt % kStages) * 32 * kPitch, bar_of(nt % kStages), ptr, cnt, nt);
+        wait_bar(bar_of(tile % kStages), static_cast<unsigned>((tile / kStages) & 1));
         const float* r1 = myrow0 + (tile % kStages) * 32 * kPitch;
         const int e0 = tile * kTile;
         if (tile < ntiles) {
@@ -208,7 +217,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_stats_pipe(const TDesc* _
                 }
             } else {
                 for (int k = 0; k < n; ++k) {
-                    const float v = r1[k];
+                    const float v = __ldg(ptr + e0 + k);  // partial tiles are not staged
                     if (PASS2) {
                         const double dv = __dsub_rn(static_cast<double>(v), mean);
                         acc = __dadd_rn(acc, __dmul_rn(dv, dv));
@@ -223,7 +232,6 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_stats_pipe(const TDesc* _
             }
         }
     }
-    cp_async_wait<0>();
     if (ptr == nullptr) return;
     if (PASS2) {
         sc.p_dev[g] = acc;
