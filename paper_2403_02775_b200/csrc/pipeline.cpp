@@ -272,6 +272,10 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     std::vector<int2> tiles;
     for (int i = 0; i < n; ++i)
         for (int64_t c0 = 0; c0 < cols[i]; c0 += 32) tiles.push_back(make_int2(i, (int)c0));
+    // longest columns first: a K3b warp walks its tile's rows, so the tall
+    // tensors' tiles go into the first waves instead of forming the tail
+    std::stable_sort(tiles.begin(), tiles.end(),
+                     [&](const int2& a, const int2& b) { return rows[a.x] > rows[b.x]; });
     std::vector<double> bc;
     bias_tables(cfg, bc);
 
