@@ -215,7 +215,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     size_t tot_groups = 0, gstrip_floats = 0, k3s_work = 0;
     static const size_t k3s_work_env = [] {
         const char* e = std::getenv("EZQ_K3S_WORK_MB");
-        return (e ? static_cast<size_t>(std::atoll(e)) : size_t(2048)) << 20;
+        return (e ? static_cast<size_t>(std::atoll(e)) : size_t(8192)) << 20;
     }();
     // The tables may take at most a sixteenth of the device memory (>= 128 MB;
     // smaller buffers only mean more, shorter waves). Total, not free, memory:
