@@ -396,3 +396,25 @@ def test_grid_oracle_batch(gpu, O, rows, cols, bits, seed):
         s_ref, e_ref = gpu.brute_force_scale(W[:, c].copy(), mask if mask.size else None, cfg, 500)
         assert scales[c] == s_ref, (c, scales[c], s_ref)
         assert abs(errs[c] - e_ref) <= 1e-12 * max(abs(e_ref), 1e-300), (c, errs[c], e_ref)
+
+
+@pytest.mark.parametrize("seed", range(64))
+def test_randomized_parity(gpu, O, seed):
+    """Randomized configurations vs the oracle (bit-exact): shapes across the
+    K3s piece boundaries, k = 2..5, sigma_n, lr, steps, selection rule,
+    planted outliers, mixed magnitudes."""
+    rng = np.random.default_rng(1000 + seed)
+    rows = int(rng.choice([1, 7, 33, 300, 1024, 2047, 2048, 4097, 6000, 8192, 8193, 12288]))
+    cols = int(rng.integers(1, 24 if rows > 4000 else 48))
+    scale = float(10.0 ** rng.uniform(-4, 1))
+    W = O.gaussian(rows, cols, 5000 + seed, scale)
+    if rng.random() < 0.6 and rows * cols > 10:
+        O.plant_outliers(W, max(1, rows * cols // 300), 5 * scale, 40 * scale, 6000 + seed)
+    select = "fixed" if rng.random() < 0.25 else "best"
+    cfg = Config(bits=int(rng.integers(2, 6)), sigma_n=float(rng.choice([1.5, 2.5, 3.0, 4.0])),
+                 lr=float(10.0 ** rng.uniform(-4, -2)) * (scale / 0.02), steps=int(rng.choice([0, 1, 17, 60, 200])),
+                 select=select, select_step=int(rng.integers(0, 20)))
+    q = gpu.quantize_tensor(W, cfg)
+    r = O.quantize(W, cfg, "easyquant")
+    assert r["status"] == "ok"
+    assert_same_quant(q, r)
