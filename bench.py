@@ -54,15 +54,50 @@ def rank_env():
 
 
 class ClockSampler:
-    """nvidia-smi sampling of SM clocks + throttle reasons during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: in-process NVML every
+    5 ms (the device found by its PCI bus id, so CUDA_VISIBLE_DEVICES is respected), else
+    `nvidia-smi -lms 200`."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, dev):
-        self.dev, self.rows, self.proc = dev, [], None
+        self.dev, self.rows, self.proc, self.nvml, self.stop = dev, [], None, None, None
+
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        pr = torch.cuda.get_device_properties(self.dev)
+        bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        bits = [pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap]
+        return pynvml, h, bits
+
+    def _poll(self):
+        nv, h, bits = self.nvml
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append([str(sm), str(mx), ""] +
+                                 ["Active" if rs & b else "Not Active" for b in bits])
+            except Exception:
+                break
+            self.stop.wait(0.005)
 
     def __enter__(self):
+        try:
+            self.nvml = self._nvml_handle()
+            self.stop = threading.Event()
+            self.th = threading.Thread(target=self._poll, daemon=True)
+            self.th.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}",
@@ -79,6 +114,9 @@ class ClockSampler:
             self.rows.append([x.strip() for x in line.split(",")])
 
     def __exit__(self, *a):
+        if self.nvml:
+            self.stop.set()
+            self.th.join(timeout=5)
         if self.proc:
             self.proc.terminate()
             try:
@@ -91,12 +129,11 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
+        reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4)
                           if len(r) > 3 + i and r[3 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(self.rows), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 def cpu_reference_time(shapes, cfg, seed=7):
