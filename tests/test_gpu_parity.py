@@ -295,6 +295,26 @@ def test_property_roundtrip_large(gpu, O):
     assert np.all(np.abs(d.astype(np.float64) - W)[inside] <= (s / 2 + 1e-6).repeat(W.shape[0], 0)[inside])
 
 
+def test_property_bench_workload(gpu, O):
+    """The bench workload at full size (BASELINE configs[1]: the OPT-1.3B weight set, 24 x
+    (4 x 2048x2048 + 2048x8192 + 8192x2048) = 1.2e9 weights) in one device-resident batch, as
+    bench.py runs it: bit-identical on repeat, final <= rtn for every tensor, and every 7th
+    tensor (21, all three shapes and every layer position) bit-exact against the oracle."""
+    import torch
+    shapes = ([(2048, 2048)] * 4 + [(2048, 8192), (8192, 2048)]) * 24
+    g = torch.Generator(device="cuda").manual_seed(7)
+    Ws = [torch.randn(s, device="cuda", generator=g) * 0.02 for s in shapes]
+    b1 = gpu.quantize_batch(Ws, Config())
+    b2 = gpu.quantize_batch(Ws, Config())
+    for x, y in zip(b1, b2):
+        assert np.array_equal(x.packed, y.packed) and np.array_equal(x.scales, y.scales)
+        assert np.array_equal(x.outliers, y.outliers)
+        assert (x.rtn_error, x.final_error) == (y.rtn_error, y.final_error)
+        assert x.final_error <= x.rtn_error
+    for i in range(0, len(shapes), 7):
+        assert_same_quant(b1[i], O.quantize(Ws[i].cpu().numpy(), Config()))
+
+
 # ---- sorted-column K3 (K3s) edge cases ----------------------------------------
 def _k3s_cases(O):
     rng = np.random.default_rng(4242)
