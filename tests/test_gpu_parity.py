@@ -295,13 +295,19 @@ def test_property_roundtrip_large(gpu, O):
     assert np.all(np.abs(d.astype(np.float64) - W)[inside] <= (s / 2 + 1e-6).repeat(W.shape[0], 0)[inside])
 
 
-def test_property_bench_workload(gpu, O):
-    """The bench workload at full size (BASELINE configs[1]: the OPT-1.3B weight set, 24 x
-    (4 x 2048x2048 + 2048x8192 + 8192x2048) = 1.2e9 weights) in one device-resident batch, as
-    bench.py runs it: bit-identical on repeat, final <= rtn for every tensor, and every 7th
-    tensor (21, all three shapes and every layer position) bit-exact against the oracle."""
+@pytest.mark.parametrize("workload", ["opt-1.3b", "llama-7b"])
+def test_property_bench_workload(gpu, O, workload):
+    """The bench workloads at full size, each in one device-resident batch as bench.py runs
+    them -- BASELINE configs[1] (OPT-1.3B set: 24 x (4 x 2048^2 + 2048x8192 + 8192x2048) = 1.2e9
+    weights) and configs[2] (LLaMA-7B set: 32 x (4 x 4096^2 + 2 x 4096x11008 + 11008x4096) =
+    6.5e9 weights; the 11008-row tensors take the row-piece path): bit-identical on repeat,
+    final <= rtn for every tensor, and a stride sample that hits every layer position
+    (OPT: every 7th of 144; LLaMA: every 32nd of 224) bit-exact against the oracle."""
     import torch
-    shapes = ([(2048, 2048)] * 4 + [(2048, 8192), (8192, 2048)]) * 24
+    if workload == "opt-1.3b":
+        shapes, stride = ([(2048, 2048)] * 4 + [(2048, 8192), (8192, 2048)]) * 24, 7
+    else:
+        shapes, stride = ([(4096, 4096)] * 4 + [(4096, 11008)] * 2 + [(11008, 4096)]) * 32, 32
     g = torch.Generator(device="cuda").manual_seed(7)
     Ws = [torch.randn(s, device="cuda", generator=g) * 0.02 for s in shapes]
     b1 = gpu.quantize_batch(Ws, Config())
@@ -311,7 +317,8 @@ def test_property_bench_workload(gpu, O):
         assert np.array_equal(x.outliers, y.outliers)
         assert (x.rtn_error, x.final_error) == (y.rtn_error, y.final_error)
         assert x.final_error <= x.rtn_error
-    for i in range(0, len(shapes), 7):
+    del b2
+    for i in range(0, len(shapes), stride):
         assert_same_quant(b1[i], O.quantize(Ws[i].cpu().numpy(), Config()))
 
 
