@@ -295,19 +295,23 @@ def test_property_roundtrip_large(gpu, O):
     assert np.all(np.abs(d.astype(np.float64) - W)[inside] <= (s / 2 + 1e-6).repeat(W.shape[0], 0)[inside])
 
 
-@pytest.mark.parametrize("workload", ["opt-1.3b", "llama-7b"])
+@pytest.mark.parametrize("workload", ["opt-1.3b", "llama-7b", "opt-175b-layer"])
 def test_property_bench_workload(gpu, O, workload):
     """The bench workloads at full size, each in one device-resident batch as bench.py runs
     them -- BASELINE configs[1] (OPT-1.3B set: 24 x (4 x 2048^2 + 2048x8192 + 8192x2048) = 1.2e9
     weights) and configs[2] (LLaMA-7B set: 32 x (4 x 4096^2 + 2 x 4096x11008 + 11008x4096) =
     6.5e9 weights; the 11008-row tensors take the row-piece path): bit-identical on repeat,
     final <= rtn for every tensor, and a stride sample that hits every layer position
-    (OPT: every 7th of 144; LLaMA: every 32nd of 224) bit-exact against the oracle."""
+    (OPT: every 7th of 144; LLaMA: every 32nd of 224) bit-exact against the oracle. Plus one
+    OPT-175B layer (configs[3]'s unit: 4 x 12288^2 + 12288x49152 + 49152x12288 = 1.8e9 weights;
+    49152 rows = 6 row pieces), its 12288^2 and 49152x12288 tensors against the oracle."""
     import torch
     if workload == "opt-1.3b":
         shapes, stride = ([(2048, 2048)] * 4 + [(2048, 8192), (8192, 2048)]) * 24, 7
-    else:
+    elif workload == "llama-7b":
         shapes, stride = ([(4096, 4096)] * 4 + [(4096, 11008)] * 2 + [(11008, 4096)]) * 32, 32
+    else:
+        shapes, stride = [(12288, 12288)] * 4 + [(12288, 49152), (49152, 12288)], 5
     g = torch.Generator(device="cuda").manual_seed(7)
     Ws = [torch.randn(s, device="cuda", generator=g) * 0.02 for s in shapes]
     b1 = gpu.quantize_batch(Ws, Config())
@@ -319,7 +323,20 @@ def test_property_bench_workload(gpu, O, workload):
         assert x.final_error <= x.rtn_error
     del b2
     for i in range(0, len(shapes), stride):
-        assert_same_quant(b1[i], O.quantize(Ws[i].cpu().numpy(), Config()))
+        W = Ws[i].cpu().numpy()
+        r = O.quantize(W, Config())
+        if workload != "opt-175b-layer":
+            assert_same_quant(b1[i], r)
+            continue
+        # Known near-tie: at 49152 rows the reference's sequential fp64 error sums
+        # can order two Adam steps whose exact errors differ by ~1e-14 the other way; K3s
+        # selects on the exact errors. Held to the north_star gate (scales 1e-5 relative,
+        # +-1 code flips <= 1e-4 of elements) and to the one column this seed is known to hit.
+        assert_same_quant(b1[i], r, W=W, scale_rtol=1e-5, code_flip_frac=1e-4)
+        diff = np.count_nonzero(b1[i].scales.view(np.uint32) != np.asarray(r["scales"]).view(np.uint32))
+        assert diff <= 1, diff
+        assert b1[i].final_error == pytest.approx(r["final_error"], rel=1e-12)
+        assert b1[i].rtn_error == r["rtn_error"]
 
 
 # ---- sorted-column K3 (K3s) edge cases ----------------------------------------
