@@ -2,13 +2,18 @@
 """EasyQuant B200 engine benchmark (one JSON line on rank 0).
 
 Metric (BASELINE.json): weights quantized / sec. A "step" quantizes one
-synthetic OPT-1.3B-shaped weight set (configs[1]: 24 layers x {q,k,v,o
-2048x2048, fc1 2048x8192, fc2 8192x2048} = 144 tensors, 1.208 B weights,
-N(0, 0.02^2), k=4, sigma_n=3, 200 Adam steps, best-error selection) through
+synthetic LLaMA-7B-shaped weight set (configs[2], the config the metric is
+quoted on: 32 layers x {q,k,v,o 4096x4096, gate/up 4096x11008, down
+11008x4096} = 224 tensors, 6.476 B weights, N(0, 0.02^2), the reference
+defaults k=4, sigma_n=3, 200 Adam steps, best-error selection) through
 ezq_quantize_batch with inputs already resident in HBM (`value`), and through
 the same C-ABI call with pinned HOST buffers, H2D/D2H inside the timed region
-(`e2e`). Multi-GPU (torchrun): every rank quantizes its own weight set (the
-tensors are independent; no data-path collective) -> weak scaling.
+(`e2e`). configs[2]'s other points (4-/3-bit x sigma_n 3.2905 / 2.8070 /
+2.5758, i.e. 0.1 / 0.5 / 1 % Gaussian outliers) are timed the same way and
+reported as `sweep` rows of the same line. Multi-GPU (torchrun): every rank
+quantizes its own weight set (the tensors are independent; no data-path
+collective) -> weak scaling; `--shard` instead LPT-partitions ONE weight set
+over the ranks through the whole-model driver (strong scaling).
 
 `--impl reference` times the reference's own CPU implementation
 (oracle/_ref/libezq_ref.so, compiled from /root/reference's sources; else
@@ -184,29 +189,35 @@ def base_line(args, cfg, shapes, params, world):
 
 
 def run_reference(args):
+    """The reference arm: the reference's own CPU quantize_tensor
+    (oracle/_ref, compiled unmodified from its sources) on all host threads.
+    Each step quantizes ONE tensor of the workload, rotating through its
+    distinct shapes (a bounded sample: ~1-3 s per step on 16 cores), and the
+    rate is total weights / total time over the timed steps."""
     rank, local, world = rank_env()
     if rank != 0:
         return 0
     from paper_2403_02775_b200.native import Config
     cfg = Config()
     shapes = layer_shapes(args.workload)
-    per_layer = {"opt-1.3b": 6, "llama-7b": 7, "opt-175b-layer": 6, "c1": 1}[args.workload]
-    sample = shapes[:per_layer] if args.workload != "opt-175b-layer" else [(12288, 12288)]
-    n = sum(r * c for r, c in sample)
-    times = []
+    distinct = sorted(set(shapes), key=shapes.index)
+    times, ns = [], []
     kind = threads = None
     for i in range(args.warmup + args.steps):
-        t, kind, threads = cpu_reference_time(sample, cfg, seed=11 + i)
+        shp = distinct[i % len(distinct)]
+        t, kind, threads = cpu_reference_time([shp], cfg, seed=11 + i)
         if i >= args.warmup:
             times.append(t)
-    value = n / (sum(times) / len(times))
+            ns.append(shp[0] * shp[1])
+    value = sum(ns) / sum(times)
     line = base_line(args, cfg, shapes, sum(r * c for r, c in shapes), world)
     line.update({
         "impl": "reference", "value": value, "ms_per_step": 1e3 * sum(times) / len(times),
         "n_gpus": world,
         "cpu_baseline": {"value": value, "unit": "weights/s", "cores": threads, "kind": kind,
-                         "sample": f"one layer per step ({len(sample)} tensors, {n} weights) of the "
-                                   f"{args.workload} set, quantize_tensor with {threads} OpenMP threads"},
+                         "sample": f"one tensor per step, rotating through the {len(distinct)} distinct shapes "
+                                   f"of the {args.workload} set ({sum(ns)} weights over {len(ns)} timed steps), "
+                                   f"reference quantize_tensor with {threads} OpenMP threads"},
         "e2e": {"value": value, "unit": "weights/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     })
     print(json.dumps(line), flush=True)
@@ -336,10 +347,11 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="opt-1.3b", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="llama-7b", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-gemv", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -368,13 +380,16 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    def step_device():
+    def step_device(count=False):
         b = N.quantize_batch(Ws, cfg, out_mem=N.MEM_DEVICE)
+        n = sum(b[i].n_outliers for i in range(len(b))) if count else None
         b.close()
+        return n
 
     fp64_peak = N.measure_fp64_peak()
-    for _ in range(args.warmup):
-        step_device()
+    n_out = 0
+    for i in range(args.warmup):
+        n_out = step_device(count=(i == args.warmup - 1))
 
     # ---- value: device-resident inputs and outputs -------------------------
     barrier()
@@ -401,10 +416,39 @@ def main():
         step_s = float(t.item())
     value = world * params / step_s
 
+    # ---- configs[2] sweep points (device-resident, same timing) ----------
+    sweep = []
+    if not args.no_sweep and args.workload == "llama-7b":
+        for bits in (4, 3):
+            for sig, pct in ((3.2905, 0.1), (2.8070, 0.5), (2.5758, 1.0)):
+                c2 = Config(bits=bits, sigma_n=sig)
+                b = N.quantize_batch(Ws, c2, out_mem=N.MEM_DEVICE)  # untimed warm-up
+                n_out_pt = sum(b[i].n_outliers for i in range(len(b)))
+                b.close()
+                barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(2):
+                    N.quantize_batch(Ws, c2, out_mem=N.MEM_DEVICE).close()
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / 2
+                if world > 1:
+                    t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                    ms = float(t.item())
+                sweep.append({"bits": bits, "sigma_n": sig, "target_outlier_pct": pct,
+                              "outlier_pct": 100.0 * n_out_pt / params, "ms_per_step": ms,
+                              "value": world * params / (ms * 1e-3), "unit": "weights/s"})
+
     # ---- e2e: the public C-ABI with pinned host buffers ----------------------
     e2e = None
     if not args.no_e2e:
-        Wh = [w.cpu().pin_memory() for w in Ws]
+        Wh = []
+        for w in Ws:
+            h = torch.empty(w.shape, dtype=w.dtype, pin_memory=True)
+            h.copy_(w)
+            Wh.append(h)
         Wn = [w.numpy() for w in Wh]
         q = N.quantize_batch(Wn, cfg)  # warm-up (host in / host out)
         h2d = sum(w.nbytes for w in Wn)
@@ -433,6 +477,25 @@ def main():
         return 0
 
     roof = k3_roofline(args, prof, fp64_peak, clocks.summary())
+    # work-based view: the reference's eval_dense does 7 flop per
+    # normal element per evaluation, steps + 1 evaluations per column
+    cols_total = sum(c for _, c in shapes)
+    elem_steps = (params - n_out) * (cfg.steps + 1)
+    flop = 7.0 * elem_steps
+    loop_ms = prof["qrange"]["ms"] / args.steps if prof["qrange"]["launches"] else None
+    packed = sum((r * c + 1) // 2 if cfg.bits == 4 else r * c for r, c in shapes)
+    roof["work"] = {
+        "flop_per_normal_element_step": 7, "normal_element_steps_per_step": elem_steps,
+        "fp64_peak_tflops": fp64_peak, "fp64_peak_source": "measured DFMA microkernel (this run)",
+        "step_tflops_equiv": flop / (step_s * 1e12),
+        "work_frac_step": flop / (step_s * 1e12) / fp64_peak,
+        "loop_tflops_equiv": flop / (loop_ms * 1e9) if loop_ms else None,
+        "work_frac_loop": flop / (loop_ms * 1e9) / fp64_peak if loop_ms else None,
+        "note": "the reference-algorithm flops this step replaces, per second, against the FP64 DFMA peak; "
+                ">1 is possible because K3s evaluates each step in O(levels) per column, not O(rows)",
+    }
+    roof["algorithmic_bytes_per_step"] = 4 * params + packed + 12 * n_out + 4 * cols_total
+    roof["dram_bytes_per_step"] = (roof.get("ncu") or {}).get("step_dram_bytes")
     line = base_line(args, cfg, shapes, params, world)
     line.update({
         "value": value,
@@ -443,7 +506,10 @@ def main():
         "clocks": clocks.summary(),
         "roofline": roof,
         "kernel_share": {f: prof[f]["ms"] / args.steps / (step_s * 1e3) for f in prof if prof[f]["launches"]},
+        "outlier_pct": 100.0 * n_out / params,
     })
+    if sweep:
+        line["sweep"] = sweep
     if not args.no_gemv:
         line["gemv"] = gemv_bench(N, torch)
     if world == 1 and not args.no_cpu_baseline:
