@@ -131,6 +131,11 @@ int ezq_synchronize(void);
 const char* ezq_version(void);
 /* Number of kernels launched by this process (instrumentation for bench). */
 int64_t ezq_kernel_launches(void);
+/* Cumulative count of columns whose Adam-step selection was a near-tie the
+ * exact evaluation could not certify against the reference's sequential fp64
+ * sums, re-evaluated in reference order; `fallback`: of those, columns that
+ * ran the whole reference loop (candidate slots overflowed). */
+int ezq_tie_stats(int64_t* resolved, int64_t* fallback);
 
 /* ---- instrumentation (bench / profiling) ------------------------------------ */
 /* When enabled, every kernel launch of the named families is bracketed by

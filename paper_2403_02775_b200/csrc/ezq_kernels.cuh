@@ -44,6 +44,8 @@ struct TStats {
     double rtn_error;              // tensor totals, column-ordered sums
     double final_error;
     int32_t scale_zero;            // a column scale rounded to 0.0f (error)
+    int32_t ties;                  // near-tie columns re-evaluated in reference order (k_resolve_ties)
+    int32_t tie_fallback;          // ... of which ran the whole reference loop (slots overflowed)
     int32_t pad;
     // Exact float form of the outlier predicate (outliers.cpp:23):
     // |double(v) - mean| >= thr  <=>  v <= olo || v >= ohi  (finite v).
@@ -88,7 +90,17 @@ struct Scratch {
     double* inv;      // 1 / double(final float scale), for K4
     float* invf;      // float(inv), K4's certified fp32 level
     uint8_t* repack;  // 1: K3b packed at s_fin but stored s_rtn (re-packed by k_repack)
+    // Selection near-ties (K3s loop -> k_resolve_ties): per
+    // column the count of candidate scales whose exact errors lie within the
+    // reference's sequential-sum rounding of the best (0 = certified), with
+    // kTieFixed for a fixed-step comparison; kTieMax slots of candidate scale
+    // and approximate full error, in step order.
+    int32_t* tie_n;
+    double* tie_s;
+    double* tie_e;
 };
+constexpr int kTieMax = 8;
+constexpr int kTieFixed = 1 << 20;
 
 struct CfgDev {
     int bits, lmin, lmax, mode;  // mode: EZQ_MODE_*
@@ -96,7 +108,7 @@ struct CfgDev {
     float sigma_n, guard;
     float guard_sat;  // K3 saturating-FFMA level guard (level_guard_sat)
     float sat_b;      // RN32(-lmin / span)
-    int pad2;
+    int tie_cap;      // candidate slots used per column (<= kTieMax; 0 = no near-tie resolution)
     AdamConsts adam;
     const double* bc1;  // [steps+1], index t
     const double* bc2;
@@ -164,6 +176,9 @@ void launch_k3_sorted(int64_t rows, int cpb, const TDesc* td, const K3Group* gro
                       CfgDev cfg, void* work, size_t work_bytes, cudaStream_t st, int grid_points = 0);
 void launch_seq_errors(const TDesc* td, const int2* tiles, int ntiles, Scratch sc, CfgDev cfg,
                        cudaStream_t st);
+// Re-evaluates the K3s loop's uncertified near-tie columns in reference order
+// (sc.tie_*), fixing s_fin before K3b. Streaming-K3 columns carry tie_n = 0.
+void launch_resolve_ties(const TDesc* td, const int2* tiles, int ntiles, Scratch sc, CfgDev cfg, cudaStream_t st);
 // Re-packs the (rare) fused-pack columns whose stored scale is s_rtn.
 void launch_repack(const TDesc* td, const int2* tiles, int ntiles, Scratch sc, CfgDev cfg, cudaStream_t st);
 void launch_tensor_totals(const TDesc* td, int ntens, Scratch sc, cudaStream_t st);
@@ -191,6 +206,8 @@ void launch_quantize_channel(const float* x, int64_t n, double scale, CfgDev cfg
 
 // Instrumentation: kernels launched by this process.
 void count_launch(int n = 1);
+// Instrumentation: near-tie columns resolved (ezq_tie_stats).
+void note_ties(int64_t resolved, int64_t fallback);
 // Host (page-locked) -> device copy by SM loads (k_ingest), DMA fallback.
 int ingest_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st);
 // Optional per-family device timing (ezq_profile_enable): returns a token to

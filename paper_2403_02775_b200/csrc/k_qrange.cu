@@ -431,6 +431,106 @@ __global__ void __launch_bounds__(kWarpsK3b * 32) k_seq_errors(const TDesc* __re
     sc.err_fin[gc] = ef;
 }
 
+// ---- near-tie resolution ------------------------------------
+// Reference-order error of one column at scale s (eval_dense's err,
+// optimize.cpp:36-49, isolated outliers skipped as normal_mask_apply does),
+// strided reads. Used for the candidate scales the K3s loop could not certify.
+__device__ double column_seq_err(const float* col, int64_t R, int64_t C, double s, float olo, float ohi,
+                                 const CfgDev& cfg) {
+    const double inv = __ddiv_rn(1.0, s);
+    const double dmin = cfg.lmin, dmax = cfg.lmax;
+    double e = 0.0;
+    for (int64_t r = 0; r < R; ++r) {
+        const float x = __ldg(col + r * C);
+        if (is_outlier_f(x, olo, ohi)) continue;
+        const double xd = static_cast<double>(x);
+        const double d = fma(s, level_exact(xd, inv, dmin, dmax), -xd);  // exact: s*q is
+        e = __dadd_rn(e, __dmul_rn(d, d));
+    }
+    return e;
+}
+
+// The reference's whole q_range loop for one column in its own order
+// (optimize_channel_range, optimize.cpp:118-184): the fallback for a column
+// whose candidates overflowed the slots. The gradient sum is exact in any
+// order, so this reproduces the reference bit for bit.
+__device__ double column_ref_optimize(const float* col, int64_t R, int64_t C, double s0, float olo, float ohi,
+                                      const CfgDev& cfg) {
+    const double dmin = cfg.lmin, dmax = cfg.lmax;
+    double s = s0, m = 0.0, v = 0.0, best_e = 0.0, best_s = s0, e0 = 0.0, fixed_s = s0, fixed_e = 0.0;
+    for (int t = 0;; ++t) {
+        const double inv = __ddiv_rn(1.0, s);
+        double e = 0.0, g = 0.0;
+        for (int64_t r = 0; r < R; ++r) {
+            const float x = __ldg(col + r * C);
+            if (is_outlier_f(x, olo, ohi)) continue;
+            seq_accumulate(static_cast<double>(x), level_exact(static_cast<double>(x), inv, dmin, dmax), s, e, g);
+        }
+        if (t == 0) {
+            e0 = best_e = fixed_e = e;
+        } else {
+            if (e < best_e) best_e = e, best_s = s;
+            if (t == cfg.fixed_at) fixed_s = s, fixed_e = e;
+        }
+        if (t == cfg.steps) break;
+        s = snap(adam_update_tab(m, v, s, 2.0 * g, cfg.bc1[t + 1], cfg.bc2[t + 1], cfg.rbc1[t + 1], cfg.rbc2[t + 1],
+                                 cfg.adam));
+    }
+    if (cfg.select == EZQ_SELECT_FIXED) return fixed_e <= e0 ? fixed_s : s0;
+    return best_s;
+}
+
+// One warp = one K3b tile (32 adjacent columns); a lane resolves its column
+// when the K3s loop left candidates: filter them against the final best
+// (bound as in k_qsort.cu tie_gamma, with rows >= normals), drop repeated
+// scales, evaluate each in reference order and apply the reference's rule
+// (strict-< earliest minimum; fixed step: fixed_err <= e0). Warps without a
+// flagged column return at once.
+__global__ void __launch_bounds__(kWarpsK3b * 32) k_resolve_ties(const TDesc* __restrict__ td,
+                                                                const int2* __restrict__ tiles, int ntiles,
+                                                                Scratch sc, CfgDev cfg) {
+    const int lane = threadIdx.x & 31;
+    const int ti = blockIdx.x * kWarpsK3b + (threadIdx.x >> 5);
+    if (ti >= ntiles) return;
+    const int2 tile = tiles[ti];
+    const TDesc& d = td[tile.x];
+    const int64_t c = tile.y + lane, R = d.rows, C = d.cols;
+    const int tn = c < C ? sc.tie_n[d.col_base + c] : 0;
+    if (tn == 0) return;
+    const int64_t gc = d.col_base + c;
+    const int cnt = tn & (kTieFixed - 1);
+    const bool fixed = (tn & kTieFixed) != 0;
+    const float* col = d.W + c;
+    const float olo = d.st->olo, ohi = d.st->ohi;
+    atomicAdd(&d.st->ties, 1);
+    if (cnt > cfg.tie_cap) {  // slots overflowed: the reference loop itself
+        atomicAdd(&d.st->tie_fallback, 1);
+        sc.s_fin[gc] = column_ref_optimize(col, R, C, sc.s_rtn[gc], olo, ohi, cfg);
+        return;
+    }
+    const double* ts = sc.tie_s + gc * kTieMax;
+    const double* te = sc.tie_e + gc * kTieMax;
+    double e1 = te[0];
+    for (int i = 1; i < cnt; ++i) e1 = fmin(e1, te[i]);
+    const double gam = (static_cast<double>(R) + 8.0) * 1.1102230246251565e-16 * 1.02;
+    double best_s = 0.0, best_e = 0.0;
+    int k = 0;
+    for (int i = 0; i < cnt; ++i) {
+        const double s = ts[i];
+        if (!fixed && te[i] - e1 > gam * (te[i] + e1)) continue;
+        bool dup = false;
+        for (int j = 0; j < i; ++j) dup |= ts[j] == s;
+        if (dup) continue;
+        const double e = column_seq_err(col, R, C, s, olo, ohi, cfg);
+        if (k == 0 || (fixed ? e <= best_e : e < best_e)) {  // fixed: [s0, s_fixed]
+            best_e = e;
+            best_s = s;
+        }
+        ++k;
+    }
+    if (k > 1) sc.s_fin[gc] = best_s;
+}
+
 // Fix-up of the fused pack: columns flagged by K3b (stored scale s_rtn, codes
 // written at s_fin) get their codes recomputed at the stored scale with the
 // reference's fp64 level; for k = 4 the even lane of a nibble pair rewrites
@@ -600,6 +700,12 @@ void launch_seq_errors(const TDesc* td, const int2* tiles, int ntiles, Scratch s
                        cudaStream_t st) {
     if (ntiles == 0) return;
     k_seq_errors<<<(ntiles + kWarpsK3b - 1) / kWarpsK3b, kWarpsK3b * 32, 0, st>>>(td, tiles, ntiles, sc, cfg);
+    count_launch();
+}
+
+void launch_resolve_ties(const TDesc* td, const int2* tiles, int ntiles, Scratch sc, CfgDev cfg, cudaStream_t st) {
+    if (ntiles == 0 || cfg.mode != EZQ_MODE_EASYQUANT) return;
+    k_resolve_ties<<<(ntiles + kWarpsK3b - 1) / kWarpsK3b, kWarpsK3b * 32, 0, st>>>(td, tiles, ntiles, sc, cfg);
     count_launch();
 }
 

@@ -81,6 +81,61 @@ __device__ __forceinline__ DD err_minus_c(double Ad, double q, double s) {
     return two_sum(h.hi, __dadd_rn(h.lo, __dadd_rn(p1.lo, p2.lo)));
 }
 
+// ---- selection near-ties -------------------------------------
+// The reference's eval_dense sums the squared residuals sequentially in fp64,
+// so its error of a step is within gamma_n * err of the exact one (n
+// rounded products and additions of non-negative terms, gamma_n = n u /
+// (1 - n u)); its gradient sum is exact (every partial sum of the d*q terms
+// is a multiple of one quantum and fits 53 bits), so only the best-error
+// selection can differ. A step whose exact error lies within
+// gamma * (err_a + err_b) of the running best is a candidate: the column's
+// candidates (distinct scales, step order) go to sc.tie_* and
+// k_resolve_ties re-evaluates them in reference order. gamma here is
+// (n + 8) u with 1% slack, in float (the comparison uses double approximations
+// of the exact errors, ~1e-16 relative, far inside the slack).
+__device__ __forceinline__ float tie_gamma(int n) {
+    return (static_cast<float>(n) + 8.0f) * 1.1102230246251565e-16f * 1.01f;
+}
+// Candidate bookkeeping of one column (state identical on every lane; `writer`
+// stores). best/err are err - C; cfull = C (estimate) converts to full errors.
+struct TieTrack {
+    int nc;
+    __device__ __forceinline__ void push(bool writer, const Scratch& sc, int64_t gcol, int cap, double s,
+                                         double efull) {
+        if (writer && nc < cap) {
+            sc.tie_s[gcol * kTieMax + nc] = s;
+            sc.tie_e[gcol * kTieMax + nc] = efull;
+        }
+        ++nc;
+    }
+    // Called for t >= 1 before the best is updated; lt = err < best.
+    __device__ __forceinline__ void step(bool writer, const Scratch& sc, int64_t gcol, int cap, bool lt,
+                                         DD err, DD best, double s, double best_s, float gam, double cfull) {
+        if (!lt && s == best_s) return;  // same scale, same error in both orders
+        const double gap = fabs(__dadd_rn(__dsub_rn(err.hi, best.hi), __dsub_rn(err.lo, best.lo)));
+        const double ef = __dadd_rn(err.hi, cfull), bf = __dadd_rn(best.hi, cfull);
+        if (gap <= static_cast<double>(gam) * __dadd_rn(ef, bf)) {
+            if (nc == 0) push(writer, sc, gcol, cap, best_s, bf);
+            push(writer, sc, gcol, cap, s, ef);
+        } else if (lt) {
+            nc = 0;  // every earlier candidate is now beyond the bound
+        }
+    }
+    // fixed-step selection (optimize.cpp:169-178): fixed_err <= e0
+    __device__ __forceinline__ void fixed(bool writer, const Scratch& sc, int64_t gcol, int cap, DD fe, DD e0,
+                                          double fs, double s0, float gam, double cfull) {
+        nc = 0;
+        if (fs == s0) return;
+        const double gap = fabs(__dadd_rn(__dsub_rn(fe.hi, e0.hi), __dsub_rn(fe.lo, e0.lo)));
+        const double ef = __dadd_rn(fe.hi, cfull), bf = __dadd_rn(e0.hi, cfull);
+        if (gap <= static_cast<double>(gam) * __dadd_rn(ef, bf)) {
+            push(writer, sc, gcol, cap, s0, bf);
+            push(writer, sc, gcol, cap, fs, ef);
+            nc |= kTieFixed;
+        }
+    }
+};
+
 // Smallest float x with level(x) >= v at scale s: RN(x*inv) >= t (> t for
 // v <= 0), t = v - 1/2. Candidates start at RN32(t*s) (t*s is exact in
 // fp64) and step by float neighbours (one or two steps in practice).
@@ -422,7 +477,15 @@ __global__ void __launch_bounds__(THREADS) k_qsort_tables(const TDesc* __restric
             if (xp >= 0.f && xp < kInf) tpos = __dadd_rn(tpos, static_cast<double>(xp));
         }
         DD sq = {0.0, 0.0};
-        if (need_c) {  // C = sum x^2 (grid oracle only: the Adam loop compares err - C)
+        if (!need_c) {
+            // the Adam loop compares err - C and needs C only for the
+            // near-tie bound (an estimate: the bound carries the slack)
+#pragma unroll
+            for (int i = 0; i < IPT; ++i)
+                if (keys[i] < kInf) sq.hi = fma(static_cast<double>(keys[i]), static_cast<double>(keys[i]), sq.hi);
+#pragma unroll
+            for (int o = 16; o; o >>= 1) sq.hi = __dadd_rn(sq.hi, __shfl_xor_sync(0xffffffffu, sq.hi, o));
+        } else {  // C = sum x^2 exactly as a double-double (grid oracle)
             DD sp = {0.0, 0.0};
 #pragma unroll
             for (int i = 0; i < IPT; ++i) {
@@ -520,7 +583,7 @@ __global__ void __launch_bounds__(THREADS) k_qsort_tables(const TDesc* __restric
 // (ILP). The tables are read through L1 (a step touches a few lines per
 // threshold), so occupancy is bounded by registers only.
 template <int G, int TPL>
-__global__ void __launch_bounds__(256) k_qrange_tables(const TDesc* __restrict__ td,
+__global__ void __launch_bounds__(256, 4) k_qrange_tables(const TDesc* __restrict__ td,
                                                        const K3Group* __restrict__ groups, int nslots, int cpb,
                                                        int dstride, int tstride, const double* __restrict__ tables,
                                                        const ColInfo* __restrict__ infos, Scratch sc,
@@ -546,12 +609,16 @@ __global__ void __launch_bounds__(256) k_qrange_tables(const TDesc* __restrict__
     const double s0_raw = initial_scale_from_max(mx, cfg.lmax);
     double s_rtn = static_cast<double>(__double2float_rn(s0_raw));
     double s_fin = s_rtn;
+    const int64_t gcol = live ? td[g.tensor].col_base + g.col0 + cc : 0;
+    TieTrack tie{0};
     if (cfg.mode == EZQ_MODE_EASYQUANT) {  // uniform across the warp
         double s = snap(s0_raw);
         const double s0 = s;
         double m = 0.0, vv = 0.0;
         DD e0 = {0.0, 0.0}, best_err = {0.0, 0.0}, fixed_err = {0.0, 0.0};
         double best_s = s, fixed_s = s;
+        const float gam = tie_gamma(n);
+        const bool track = cfg.tie_cap > 0 && cfg.select != EZQ_SELECT_FIXED;
         bool own[TPL];
         int jl[TPL], wA[TPL], ib[TPL];
         float Xp[TPL], span[TPL];  // previous threshold; x[k0+7] - x[k0] near it
@@ -606,7 +673,9 @@ __global__ void __launch_bounds__(256) k_qrange_tables(const TDesc* __restrict__
                 best_err = err;
                 fixed_err = err;
             } else {
-                if (dd_lt(err, best_err)) {  // strict: earliest minimum wins (optimize.cpp:158)
+                const bool lt = dd_lt(err, best_err);  // strict: earliest minimum wins (optimize.cpp:158)
+                if (track) tie.step(live && gl == 0, sc, gcol, cfg.tie_cap, lt, err, best_err, s, best_s, gam, ci.chi);
+                if (lt) {
                     best_err = err;
                     best_s = s;
                 }
@@ -619,17 +688,18 @@ __global__ void __launch_bounds__(256) k_qrange_tables(const TDesc* __restrict__
             s = snap(adam_update_tab(m, vv, s, grad, cfg.bc1[t + 1], cfg.bc2[t + 1], cfg.rbc1[t + 1],
                                      cfg.rbc2[t + 1], cfg.adam));
         }
-        if (cfg.select == EZQ_SELECT_FIXED)
+        if (cfg.select == EZQ_SELECT_FIXED) {
             s_fin = dd_le(fixed_err, e0) ? fixed_s : s0;  // optimize.cpp:169-178
-        else
+            if (cfg.tie_cap > 0) tie.fixed(live && gl == 0, sc, gcol, cfg.tie_cap, fixed_err, e0, fixed_s, s0, gam, ci.chi);
+        } else {
             s_fin = best_s;
+        }
         s_rtn = s0;
     }
     if (live && gl == 0) {
-        const TDesc& d = td[g.tensor];
-        const int64_t gcol = d.col_base + g.col0 + cc;
         sc.s_rtn[gcol] = s_rtn;
         sc.s_fin[gcol] = s_fin;
+        sc.tie_n[gcol] = tie.nc;
     }
 }
 
@@ -666,21 +736,26 @@ __global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__
     const int nb = cfg.lmax - cfg.lmin;
     // column totals over the pieces, in piece order
     int nall = 0;
-    double mx = 0.0;
+    double mx = 0.0, call = 0.0;
     for (int p = 0; p < P; ++p) {
         const ColInfo ci = infos[(g * P + p) * cpb + cc];
         nall += ci.n;
+        call += ci.chi;
         if (ci.n) mx = fmax(mx, fmax(fabs(static_cast<double>(ci.lo)), fabs(static_cast<double>(ci.hi))));
     }
     const double s0_raw = initial_scale_from_max(mx, cfg.lmax);
     double s_rtn = static_cast<double>(__double2float_rn(s0_raw));
     double s_fin = s_rtn;
+    const int64_t gcol = td[G0.tensor].col_base + G0.col0 + cc;
+    TieTrack tie{0};
     if (cfg.mode == EZQ_MODE_EASYQUANT) {  // uniform across the warp
         double s = snap(s0_raw);
         const double s0 = s;
         double m = 0.0, vv = 0.0;
         DD e0 = {0.0, 0.0}, best_err = {0.0, 0.0}, fixed_err = {0.0, 0.0};
         double best_s = s, fixed_s = s;
+        const float gam = tie_gamma(nall);
+        const bool track = cfg.tie_cap > 0 && cfg.select != EZQ_SELECT_FIXED;
         bool own[PPL];
         int jl[PPL], np[PPL], ib[PPL];
         ColTab ct[PPL];
@@ -735,7 +810,9 @@ __global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__
                 best_err = err;
                 fixed_err = err;
             } else {
-                if (dd_lt(err, best_err)) {  // strict: earliest minimum wins (optimize.cpp:158)
+                const bool lt = dd_lt(err, best_err);  // strict: earliest minimum wins (optimize.cpp:158)
+                if (track) tie.step(lane == 0, sc, gcol, cfg.tie_cap, lt, err, best_err, s, best_s, gam, call);
+                if (lt) {
                     best_err = err;
                     best_s = s;
                 }
@@ -748,17 +825,18 @@ __global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__
             s = snap(adam_update_tab(m, vv, s, grad, cfg.bc1[t + 1], cfg.bc2[t + 1], cfg.rbc1[t + 1],
                                      cfg.rbc2[t + 1], cfg.adam));
         }
-        if (cfg.select == EZQ_SELECT_FIXED)
+        if (cfg.select == EZQ_SELECT_FIXED) {
             s_fin = dd_le(fixed_err, e0) ? fixed_s : s0;  // optimize.cpp:169-178
-        else
+            if (cfg.tie_cap > 0) tie.fixed(lane == 0, sc, gcol, cfg.tie_cap, fixed_err, e0, fixed_s, s0, gam, call);
+        } else {
             s_fin = best_s;
+        }
         s_rtn = s0;
     }
     if (lane == 0) {
-        const TDesc& d = td[G0.tensor];
-        const int64_t gcol = d.col_base + G0.col0 + cc;
         sc.s_rtn[gcol] = s_rtn;
         sc.s_fin[gcol] = s_fin;
+        sc.tie_n[gcol] = tie.nc;
     }
 }
 

@@ -291,6 +291,8 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     for (int k = 0; k < 5; ++k) ar.reserve_n<double>(tot_cols);
     ar.reserve_n<float>(tot_cols);
     ar.reserve_n<uint8_t>(tot_cols);
+    ar.reserve_n<int32_t>(tot_cols);
+    for (int k = 0; k < 2; ++k) ar.reserve_n<double>(tot_cols * kTieMax);
     ar.reserve_n<int2>(tiles.size());
     ar.reserve(sizeof(double) * bc.size());
     ar.reserve(sizeof(K3Group) * tot_groups);
@@ -318,6 +320,9 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     sc.inv = ar.take<double>(tot_cols);
     sc.invf = ar.take<float>(tot_cols);
     sc.repack = ar.take<uint8_t>(tot_cols);
+    sc.tie_n = ar.take<int32_t>(tot_cols);
+    sc.tie_s = ar.take<double>(tot_cols * kTieMax);
+    sc.tie_e = ar.take<double>(tot_cols * kTieMax);
     double* d_bc = ar.take<double>(bc.size());
     K3Group* d_groups = ar.take<K3Group>(tot_groups);
     float* d_in = ar.take<float>(tot_in);
@@ -457,6 +462,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     trace("qb: outputs allocated");
     // ---- phase 2 ----
     const CfgDev cd = make_cfg(cfg, mode, d_bc);
+    EZQ_CK(cudaMemsetAsync(sc.tie_n, 0, sizeof(int32_t) * tot_cols, st));  // streaming-K3 columns: certified
     int64_t tot_out = 0;
     for (int i = 0; i < n; ++i) tot_out += hs[i].n_out;
     if (mode != EZQ_MODE_RTN) {
@@ -484,6 +490,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
         trace("qb: k3 plan launched", p.kl.rows);
     }
     int p4 = prof_begin("seqerr", st);
+    launch_resolve_ties(d_desc, d_tiles, static_cast<int>(tiles.size()), sc, cd, st);
     launch_seq_errors(d_desc, d_tiles, static_cast<int>(tiles.size()), sc, cd, st);
     static const bool force_repack = std::getenv("EZQ_FORCE_REPACK") != nullptr;  // test aid: exercise k_repack
     if (force_repack) EZQ_CK(cudaMemsetAsync(sc.repack, 1, tot_cols, st));
@@ -566,6 +573,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
         for (auto& q : res) free_qweight_arrays(q.get()), std::free(q.release());
         return cuda_error(se, "phase-2 sync");
     }
+    for (int i = 0; i < n; ++i) note_ties(hs[i].ties, hs[i].tie_fallback);
     for (int i = 0; i < n; ++i) {
         ezq_qweight* q = res[i].get();
         q->n_outliers = hs[i].n_out;

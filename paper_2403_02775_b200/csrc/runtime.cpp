@@ -17,6 +17,11 @@ namespace ezq {
 
 static std::atomic<int64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+static std::atomic<int64_t> g_ties{0}, g_tie_fallback{0};
+void note_ties(int64_t resolved, int64_t fallback) {
+    g_ties += resolved;
+    g_tie_fallback += fallback;
+}
 
 namespace {
 
@@ -291,6 +296,14 @@ CfgDev make_cfg(const ezq_config* c, int mode, const double* bc_dev) {
     d.guard = level_guard(d.lmax);
     d.guard_sat = level_guard_sat(d.lmin, d.lmax);
     d.sat_b = static_cast<float>(static_cast<double>(-d.lmin) / static_cast<double>(d.lmax - d.lmin));
+    // EZQ_TIE_CAP (test aid, 0..kTieMax): fewer candidate slots send more
+    // near-tie columns down the full reference-order fallback
+    static const int tie_cap = [] {
+        const char* e = std::getenv("EZQ_TIE_CAP");
+        const int v = e ? std::atoi(e) : kTieMax;
+        return v < 0 ? 0 : (v > kTieMax ? kTieMax : v);
+    }();
+    d.tie_cap = tie_cap;
     d.adam.b1 = c->beta1;
     d.adam.b2 = c->beta2;
     d.adam.c1 = 1.0 - c->beta1;
@@ -483,6 +496,12 @@ int ezq_synchronize(void) {
 const char* ezq_version(void) { return "ezquant-b200 0.1.0 (sm_100a)"; }
 
 int64_t ezq_kernel_launches(void) { return g_launches.load(); }
+
+int ezq_tie_stats(int64_t* resolved, int64_t* fallback) {
+    if (resolved) *resolved = g_ties.load();
+    if (fallback) *fallback = g_tie_fallback.load();
+    return EZQ_OK;
+}
 
 int ezq_profile_enable(int on) {
     std::lock_guard<std::mutex> lk(g_prof_mu);

@@ -153,6 +153,7 @@ def lib() -> C.CDLL:
         L.ezq_set_device.argtypes = [I32]
         L.ezq_version.restype = C.c_char_p
         L.ezq_kernel_launches.restype = I64
+        L.ezq_tie_stats.argtypes = [C.POINTER(I64), C.POINTER(I64)]
         L.ezq_tensor_stats.argtypes = [P, I64, I64, I32, P, C.POINTER(CStats)]
         L.ezq_detect_outliers.argtypes = [P, I64, I64, C.POINTER(CConfig), I32, P,
                                           C.POINTER(C.POINTER(COutlier)), C.POINTER(I64),
@@ -254,6 +255,13 @@ def set_device(d: int):
 
 def kernel_launches() -> int:
     return int(lib().ezq_kernel_launches())
+
+
+def tie_stats() -> tuple:
+    """Cumulative (resolved, fallback) near-tie columns (ezq_tie_stats)."""
+    a, b = C.c_int64(0), C.c_int64(0)
+    check(lib().ezq_tie_stats(C.byref(a), C.byref(b)))
+    return int(a.value), int(b.value)
 
 
 def profile_enable(on: bool = True):

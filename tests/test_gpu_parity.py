@@ -295,48 +295,76 @@ def test_property_roundtrip_large(gpu, O):
     assert np.all(np.abs(d.astype(np.float64) - W)[inside] <= (s / 2 + 1e-6).repeat(W.shape[0], 0)[inside])
 
 
-@pytest.mark.parametrize("workload", ["opt-1.3b", "llama-7b", "opt-175b-layer"])
-def test_property_bench_workload(gpu, O, workload):
+_WEIGHTS = {}
+
+
+def _bench_weights(workload):
+    """The bench's weight sets on the device (generated once per workload)."""
+    import torch
+    if workload not in _WEIGHTS:
+        _WEIGHTS.clear()
+        torch.cuda.empty_cache()
+        if workload == "opt-1.3b":
+            shapes = ([(2048, 2048)] * 4 + [(2048, 8192), (8192, 2048)]) * 24
+        elif workload == "llama-7b":
+            shapes = ([(4096, 4096)] * 4 + [(4096, 11008)] * 2 + [(11008, 4096)]) * 32
+        else:
+            shapes = [(12288, 12288)] * 4 + [(12288, 49152), (49152, 12288)]
+        g = torch.Generator(device="cuda").manual_seed(7)
+        _WEIGHTS[workload] = [torch.randn(s, device="cuda", generator=g) * 0.02 for s in shapes]
+    return _WEIGHTS[workload]
+
+
+# BASELINE configs[1] (default point), configs[2] (LLaMA-7B set: the reference defaults plus
+# the 4-/3-bit x 0.1/0.5/1% outlier sweep, report.cpp:241-284) and configs[3]'s unit (one
+# OPT-175B layer, at the default sigma_n and at ~1% outliers).
+BENCH_POINTS = [("opt-1.3b", 4, 3.0)] + [("llama-7b", 4, 3.0)] + \
+    [("llama-7b", b, s) for b in (4, 3) for s in (3.2905, 2.8070, 2.5758)] + \
+    [("opt-175b-layer", 4, 3.0), ("opt-175b-layer", 4, 2.5758)]
+
+
+@pytest.mark.parametrize("workload,bits,sigma_n", BENCH_POINTS)
+def test_property_bench_workload(gpu, O, workload, bits, sigma_n):
     """The bench workloads at full size, each in one device-resident batch as bench.py runs
     them -- BASELINE configs[1] (OPT-1.3B set: 24 x (4 x 2048^2 + 2048x8192 + 8192x2048) = 1.2e9
-    weights) and configs[2] (LLaMA-7B set: 32 x (4 x 4096^2 + 2 x 4096x11008 + 11008x4096) =
-    6.5e9 weights; the 11008-row tensors take the row-piece path): bit-identical on repeat,
-    final <= rtn for every tensor, and a stride sample that hits every layer position
-    (OPT: every 7th of 144; LLaMA: every 32nd of 224) bit-exact against the oracle. Plus one
-    OPT-175B layer (configs[3]'s unit: 4 x 12288^2 + 12288x49152 + 49152x12288 = 1.8e9 weights;
-    49152 rows = 6 row pieces), its 12288^2 and 49152x12288 tensors against the oracle."""
-    import torch
-    if workload == "opt-1.3b":
-        shapes, stride = ([(2048, 2048)] * 4 + [(2048, 8192), (8192, 2048)]) * 24, 7
-    elif workload == "llama-7b":
-        shapes, stride = ([(4096, 4096)] * 4 + [(4096, 11008)] * 2 + [(11008, 4096)]) * 32, 32
-    else:
-        shapes, stride = [(12288, 12288)] * 4 + [(12288, 49152), (49152, 12288)], 5
-    g = torch.Generator(device="cuda").manual_seed(7)
-    Ws = [torch.randn(s, device="cuda", generator=g) * 0.02 for s in shapes]
-    b1 = gpu.quantize_batch(Ws, Config())
-    b2 = gpu.quantize_batch(Ws, Config())
-    for x, y in zip(b1, b2):
-        assert np.array_equal(x.packed, y.packed) and np.array_equal(x.scales, y.scales)
-        assert np.array_equal(x.outliers, y.outliers)
-        assert (x.rtn_error, x.final_error) == (y.rtn_error, y.final_error)
+    weights), configs[2] (LLaMA-7B set: 32 x (4 x 4096^2 + 2 x 4096x11008 + 11008x4096) =
+    6.5e9 weights; the 11008-row tensors take the row-piece path) at every sweep point, and
+    one OPT-175B layer (configs[3]'s unit: 4 x 12288^2 + 12288x49152 + 49152x12288 = 1.8e9
+    weights; 49152 rows = 6 row pieces). Checks: bit-identical on repeat, final <= rtn for
+    every tensor, a stride sample hitting every layer position (OPT-1.3B: every 7th of 144;
+    LLaMA: every 32nd of 224; the OPT-175B layer: the 12288^2 and 49152-row tensors)
+    bit-exact against the oracle (C restatement), and one tensor per shape bit-exact against
+    the compiled reference itself (oracle/_ref, when present)."""
+    Ws = _bench_weights(workload)
+    cfg = Config(bits=bits, sigma_n=sigma_n)
+    b1 = gpu.quantize_batch(Ws, cfg)
+    if (bits, sigma_n) in ((4, 3.0), (3, 2.5758)):
+        b2 = gpu.quantize_batch(Ws, cfg)
+        for x, y in zip(b1, b2):
+            assert np.array_equal(x.packed, y.packed) and np.array_equal(x.scales, y.scales)
+            assert np.array_equal(x.outliers, y.outliers)
+            assert (x.rtn_error, x.final_error) == (y.rtn_error, y.final_error)
+        del b2
+    for x in b1:
         assert x.final_error <= x.rtn_error
-    del b2
-    for i in range(0, len(shapes), stride):
-        W = Ws[i].cpu().numpy()
-        r = O.quantize(W, Config())
-        if workload != "opt-175b-layer":
-            assert_same_quant(b1[i], r)
-            continue
-        # Known near-tie (DESIGN §4): at 49152 rows the reference's sequential fp64 error sums
-        # can order two Adam steps whose exact errors differ by ~1e-14 the other way; K3s
-        # selects on the exact errors. Held to the north_star gate (scales 1e-5 relative,
-        # +-1 code flips <= 1e-4 of elements) and to the one column this seed is known to hit.
-        assert_same_quant(b1[i], r, W=W, scale_rtol=1e-5, code_flip_frac=1e-4)
-        diff = np.count_nonzero(b1[i].scales.view(np.uint32) != np.asarray(r["scales"]).view(np.uint32))
-        assert diff <= 1, diff
-        assert b1[i].final_error == pytest.approx(r["final_error"], rel=1e-12)
-        assert b1[i].rtn_error == r["rtn_error"]
+    stride = {"opt-1.3b": 7, "llama-7b": 32, "opt-175b-layer": 5}[workload]
+    for i in range(0, len(Ws), stride):
+        r = O.quantize(Ws[i].cpu().numpy(), cfg)
+        assert_same_quant(b1[i], r)
+    from oracle import refimpl
+    if refimpl.available():
+        first = {}
+        for i, w in enumerate(Ws):
+            first.setdefault(tuple(w.shape), i)
+        if workload == "opt-175b-layer":
+            first = {(12288, 12288): 0}  # the 49152-row tensor is the C restatement's (above)
+        for i in first.values():
+            r = refimpl.quantize(Ws[i].cpu().numpy(), cfg)
+            q = b1[i]
+            assert np.array_equal(q.outliers, r.outliers)
+            assert np.array_equal(q.scales.view(np.uint32), r.scales.view(np.uint32))
+            assert np.array_equal(q.packed, r.packed)
+            assert (q.mean, q.stddev, q.rtn_error, q.final_error) == (r.mean, r.stddev, r.rtn_error, r.final_error)
 
 
 # ---- sorted-column K3 (K3s) edge cases ----------------------------------------
@@ -464,15 +492,61 @@ def test_randomized_parity(gpu, O, seed):
     assert_same_quant(q, r)
 
 
-@pytest.mark.xfail(strict=True, reason="known selection near-tie (DESIGN §4): K3s selects on exact "
-                   "errors, the reference on sequential fp64 sums; the fix is planned")
 def test_near_tie_column_k3s(gpu, O):
+    """The OPT-175B near-tie column: two Adam steps whose exact errors differ by
+    1.7e-14; the reference's sequential fp64 sums order them the other way. The K3s loop
+    flags the column and k_resolve_ties re-evaluates the candidates in reference order."""
     g = load_golden("near_tie_col.npz")
     W = np.ascontiguousarray(g["x"][:, None])
     cfg = Config(sigma_n=100.0)  # the fixture holds the normals only: no outliers
+    t0 = gpu.tie_stats()[0]
     q = gpu.quantize_tensor(W, cfg)
+    assert gpu.tie_stats()[0] > t0, "the near-tie was not flagged"
     r = O.quantize(W, cfg)
     assert np.array_equal(q.scales.view(np.uint32), np.asarray(r["scales"]).view(np.uint32))
+    assert q.final_error == r["final_error"]
+
+
+@pytest.mark.parametrize("cap", ["0", "1", "2"])
+def test_near_tie_resolution_paths(gpu, cap):
+    """3-bit columns at ~1% outliers are near-tie-rich (Adam settles within a few float ulps
+    of a local optimum; tools/cert_sim.c: 8-20% of columns flagged). EZQ_TIE_CAP=1 sends
+    every column with >= 2 candidates to the whole reference-order loop (the overflow
+    fallback), 2 exercises the candidate re-evaluation with overflow, 0 turns resolution
+    off -- the first two must be bit-exact against the oracle on every column."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests"); sys.path.insert(0, ".")
+from oracle import pyoracle as O
+from paper_2403_02775_b200 import native as N
+from paper_2403_02775_b200.native import Config
+O.build()
+bad = 0
+for (r, c, bits, sig, seed, sel) in [(4096, 96, 3, 2.5758, 1, "best"), (11008, 24, 3, 3.2905, 2, "best"),
+                                     (2048, 64, 3, 2.5758, 3, "fixed")]:
+    W = O.gaussian(r, c, seed, 0.02)
+    cfg = Config(bits=bits, sigma_n=sig, select=sel, select_step=150)
+    q = N.quantize_tensor(W, cfg)
+    ref = O.quantize(W, cfg, "easyquant")
+    bad += int(np.count_nonzero(q.scales.view(np.uint32) != np.asarray(ref["scales"]).view(np.uint32)))
+    bad += int(not np.array_equal(q.packed, ref["packed"]))
+print("ties", *N.tie_stats(), "bad", bad)
+'''
+    env = dict(os.environ, EZQ_TIE_CAP=cap)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    _, resolved, fallback, _, bad = out.stdout.split()[-5:]
+    if cap == "0":
+        assert int(resolved) == 0
+        return
+    assert int(resolved) > 0, out.stdout
+    if cap == "1":
+        assert int(fallback) > 0, out.stdout
+    assert int(bad) == 0, out.stdout
 
 
 def test_near_tie_column_channel_api(gpu):
