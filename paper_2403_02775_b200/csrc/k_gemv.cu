@@ -165,119 +165,240 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const unsigned (&a)[4], 
             : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
 }
 
+// ---- K6 main kernel: persistent, TMA-fed ------------------------------------
+// The codes of a tile are contiguous (T[tile][q][lane]), so the whole
+// artifact is one array of 512-byte blocks in (tile, q) order. Each CTA owns
+// a contiguous range of ~nblk/grid blocks and streams it through a ring of
+// kRing stages x kStageBlocks blocks with cp.async.bulk (one elected producer
+// lane, mbarrier full/empty pairs): ~100 KB of codes in flight per SM, which
+// is what an HBM-latency-bound stream needs (Little's law: ~5 MB in flight
+// GPU-wide at 6.5 TB/s), without holding them in registers. kCW consumer
+// warps take the range's blocks round-robin (LDS.128 from the ring, x
+// fragments from L1/L2 one block ahead), dequantize to exact levels and run
+// the MMAs. At every tile boundary the warps' fragments meet in shared memory
+// (fixed order); a tile cut by a range boundary is split across CTAs: each
+// writes its partial to a workspace and the last to arrive (ticket) sums the
+// partials in CTA order -- deterministic, bit-identical across calls.
+constexpr int kCW = 4;            // consumer warps per CTA
+constexpr int kStageBlocks = 16;  // 64-row blocks per ring stage (8 KB)
+constexpr int kRing = 4;          // ring stages per CTA (32 KB)
+constexpr int kStreamThreads = (kCW + 1) * 32;
+constexpr int kStreamCtasPerSm = 3;
+
 struct GemvArgs {
     const uint4* T;
-    int kq, tiles;
+    int64_t kq;    // 64-row blocks per tile
+    int64_t nblk;  // tiles * kq
+    int grid;      // CTAs (ranges)
     int64_t rows, cols;
     int lmin;
     const float* scales;
     const void* x;
     int batch;  // rows of this group (1..16)
     float* y;
+    float* ws;     // split-tile partials [tiles][maxsplit][16 batch][16 cols]
+    int* tickets;  // [tiles], self-resetting
+    int maxsplit;
 };
 
-// One CTA per 16-column tile; warp w takes 64-row blocks w, w + W, ...,
-// loading block q + W (codes and x fragments) while block q computes. x is
-// read through L1/L2 (every tile reads the whole of x). Batch columns
-// n >= batch read a valid x row and are never stored (D column n depends
-// only on B column n), so the fragments need no predication; four
-// accumulator sets break the HMMA dependency chain.
+__host__ __device__ __forceinline__ int64_t range_begin(int64_t c, int64_t nblk, int64_t grid) {
+    return c * nblk / grid;
+}
+// CTA whose range holds block b.
+__device__ __forceinline__ int64_t range_of(int64_t b, int64_t nblk, int64_t grid) {
+    int64_t c = (b * grid) / nblk;
+    while (c > 0 && range_begin(c, nblk, grid) > b) --c;
+    while (c + 1 < grid && range_begin(c + 1, nblk, grid) <= b) ++c;
+    return c;
+}
+
+__device__ __forceinline__ void bar_wait(unsigned bar, unsigned phase) {
+    unsigned ok = 0;
+    for (long long spin = 0; !ok; ++spin) {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(ok) : "r"(bar), "r"(phase) : "memory");
+        if (spin > (1ll << 28)) __trap();  // never hang the device on a lost transfer
+    }
+}
+
+__device__ __forceinline__ void named_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 template <int NB, int XT>
-__global__ void __launch_bounds__(512) k_gemv_mma(const GemvArgs a) {
+__global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) k_gemv_stream(const GemvArgs a) {
     constexpr bool F16 = XT == kF16;
-    constexpr int kChains = NB == 1 ? 4 : 2;  // NB = 2: fewer live accumulators, more resident warps
-    __shared__ __align__(16) float red[kMaxWarps][NB][32][4];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    constexpr int kChains = NB == 1 ? 4 : 2;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint4* ring = reinterpret_cast<uint4*>(smem);  // [kRing][kStageBlocks][32]
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + kRing * kStageBlocks * 512);
+    float* red = reinterpret_cast<float*>(bars + 2 * kRing);  // [2][kCW][NB][32][4]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t cta = blockIdx.x;
+    const int64_t b0 = range_begin(cta, a.nblk, a.grid), b1 = range_begin(cta + 1, a.nblk, a.grid);
+    const int64_t nb = b1 - b0;
+    const int nst = static_cast<int>((nb + kStageBlocks - 1) / kStageBlocks);
+    const unsigned full0 = static_cast<unsigned>(__cvta_generic_to_shared(bars));
+    const unsigned empty0 = full0 + 8 * kRing;
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < kRing; ++k) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full0 + 8 * k));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * k), "r"(kCW));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;");
+
+    if (warp == kCW) {  // ---- producer: one elected lane streams the range
+        if (lane == 0) {
+            const uint4* src = a.T + b0 * 32;
+            for (int k = 0; k < nst; ++k) {
+                const int slot = k % kRing;
+                if (k >= kRing) bar_wait(empty0 + 8 * slot, ((k / kRing) - 1) & 1);
+                const unsigned bytes =
+                    static_cast<unsigned>(min(static_cast<int64_t>(kStageBlocks), nb - k * kStageBlocks)) * 512u;
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full0 + 8 * slot),
+                             "r"(bytes)
+                             : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        static_cast<unsigned>(__cvta_generic_to_shared(ring + slot * kStageBlocks * 32))),
+                    "l"(src + static_cast<int64_t>(k) * kStageBlocks * 32), "r"(bytes), "r"(full0 + 8 * slot)
+                    : "memory");
+            }
+        }
+        return;
+    }
+
+    // ---- consumers
     const int g = lane >> 2, t = lane & 3;
-    const int tile = blockIdx.x;
     const unsigned magic = F16 ? 0x64006400u : 0x43004300u;
     const unsigned off2 = F16 ? static_cast<unsigned>(__half_as_ushort(__int2half_rn(1024 - a.lmin))) * 0x10001u
                               : static_cast<unsigned>(__bfloat16_as_ushort(__int2bfloat16_rn(128 - a.lmin))) * 0x10001u;
     int nrow[NB];
 #pragma unroll
-    for (int nb = 0; nb < NB; ++nb) nrow[nb] = min(nb * 8 + g, a.batch - 1);
-    asm volatile("griddepcontrol.launch_dependents;");
-    float acc[kChains][NB][4];
+    for (int n8 = 0; n8 < NB; ++n8) nrow[n8] = min(n8 * 8 + g, a.batch - 1);
+    const int64_t tile_first = b0 / a.kq, tile_last = nb > 0 ? (b1 - 1) / a.kq : tile_first - 1;
+    int tcount = 0;
+    for (int64_t tile = tile_first; tile <= tile_last; ++tile, ++tcount) {
+        const int64_t ta = max(b0, tile * a.kq), tb = min(b1, (tile + 1) * a.kq);  // this CTA's blocks of the tile
+        float acc[kChains][NB][4];
 #pragma unroll
-    for (int h = 0; h < kChains; ++h)
+        for (int h = 0; h < kChains; ++h)
 #pragma unroll
-        for (int nb = 0; nb < NB; ++nb)
+            for (int n8 = 0; n8 < NB; ++n8)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) acc[h][nb][i] = 0.f;
-    // Software pipeline, two groups of G blocks deep: the next group's codes
-    // and x fragments are in flight while the current group computes.
-    constexpr int G = 1;
-    uint4 wA[G], wB[G];
-    XRaw<XT> xA[G][NB], xB[G][NB];
-    auto load_group = [&](int q0, uint4 (&wg)[G], XRaw<XT> (&xg)[G][NB]) {
+                for (int i = 0; i < 4; ++i) acc[h][n8][i] = 0.f;
+        // my blocks: i in [ta, tb) with (i - b0) % kCW == warp
+        int64_t i = ta + ((warp - (ta - b0)) % kCW + kCW) % kCW;
+        XRaw<XT> xc[NB];
+        if (i < tb) {
 #pragma unroll
-        for (int u = 0; u < G; ++u) {
-            const int q = q0 + nw * u;
-            if (q < a.kq) {
-                wg[u] = __ldg(a.T + (static_cast<int64_t>(tile) * a.kq + q) * 32 + lane);
-#pragma unroll
-                for (int nb = 0; nb < NB; ++nb)
-                    x_load<XT>(a.x, a.rows, nrow[nb], static_cast<int64_t>(kBlockRows) * q + 16 * t, xg[u][nb]);
-            }
+            for (int n8 = 0; n8 < NB; ++n8)
+                x_load<XT>(a.x, a.rows, nrow[n8], kBlockRows * (i - tile * a.kq) + 16 * t, xc[n8]);
         }
-    };
-    auto compute_group = [&](int q0, const uint4 (&wg)[G], const XRaw<XT> (&xg)[G][NB]) {
+        for (; i < tb; i += kCW) {
+            const int64_t j = i - b0;  // position in the range
+            const int k = static_cast<int>(j / kStageBlocks), slot = k % kRing;
+            bar_wait(full0 + 8 * slot, (k / kRing) & 1);
+            const uint4 w = ring[(slot * kStageBlocks + static_cast<int>(j % kStageBlocks)) * 32 + lane];
+            // release the stage after my last block in it (or my last block)
+            if (j % kStageBlocks >= kStageBlocks - kCW || i + kCW >= b1) {
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * slot) : "memory");
+            }
+            XRaw<XT> xn[NB];
+            if (i + kCW < tb) {
 #pragma unroll
-        for (int u = 0; u < G; ++u) {
-            if (q0 + nw * u >= a.kq) break;
-            const unsigned ws[4] = {wg[u].x, wg[u].y, wg[u].z, wg[u].w};
+                for (int n8 = 0; n8 < NB; ++n8)
+                    x_load<XT>(a.x, a.rows, nrow[n8], kBlockRows * (i + kCW - tile * a.kq) + 16 * t, xn[n8]);
+            }
+            const unsigned ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
             for (int s = 0; s < 4; ++s) {
                 unsigned af[4];
 #pragma unroll
                 for (int r = 0; r < 4; ++r) af[r] = sub2<F16>(lop_pair(ws[s], r, magic), off2);
 #pragma unroll
-                for (int nb = 0; nb < NB; ++nb) {
+                for (int n8 = 0; n8 < NB; ++n8) {
                     unsigned hi[2], lo[2];
-                    x_frag<XT>(xg[u][nb], s, hi, lo);
-                    mma16816<F16>(acc[s % kChains][nb], af, hi);
-                    if (XT == kF32) mma16816<F16>(acc[s % kChains][nb], af, lo);
+                    x_frag<XT>(xc[n8], s, hi, lo);
+                    mma16816<F16>(acc[s % kChains][n8], af, hi);
+                    if (XT == kF32) mma16816<F16>(acc[s % kChains][n8], af, lo);
                 }
             }
+#pragma unroll
+            for (int n8 = 0; n8 < NB; ++n8) xc[n8] = xn[n8];
         }
-    };
-    const int step = nw * G;
-    int q = warp;
-    load_group(q, wA, xA);
-    for (; q < a.kq; q += 2 * step) {
-        if (q + step < a.kq) load_group(q + step, wB, xB);
-        compute_group(q, wA, xA);
-        if (q + step >= a.kq) break;
-        if (q + 2 * step < a.kq) load_group(q + 2 * step, wA, xA);
-        compute_group(q + step, wB, xB);
+        // ---- flush the tile: warps meet in shared memory (fixed order)
+        float* rb = red + (tcount & 1) * (kCW * NB * 32 * 4);
+#pragma unroll
+        for (int n8 = 0; n8 < NB; ++n8) {
+            float v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                v[q] = acc[0][n8][q];
+#pragma unroll
+                for (int h = 1; h < kChains; ++h) v[q] += acc[h][n8][q];
+            }
+            *reinterpret_cast<float4*>(rb + ((warp * NB + n8) * 32 + lane) * 4) = make_float4(v[0], v[1], v[2], v[3]);
+        }
+        named_sync(1, kCW * 32);
+        if (warp != static_cast<int>(tile % kCW)) continue;
+        float d[NB][4];
+#pragma unroll
+        for (int n8 = 0; n8 < NB; ++n8) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) d[n8][q] = 0.f;
+            for (int w2 = 0; w2 < kCW; ++w2) {
+                const float4 v = *reinterpret_cast<const float4*>(rb + ((w2 * NB + n8) * 32 + lane) * 4);
+                d[n8][0] += v.x, d[n8][1] += v.y, d[n8][2] += v.z, d[n8][3] += v.w;
+            }
+        }
+        const bool whole = ta == tile * a.kq && tb == (tile + 1) * a.kq;
+        if (!whole) {
+            // split tile: partial to the workspace, the last CTA to arrive sums
+            const int64_t c_first = range_of(tile * a.kq, a.nblk, a.grid);
+            const int64_t c_last = range_of((tile + 1) * a.kq - 1, a.nblk, a.grid);
+            const int nsplit = static_cast<int>(c_last - c_first + 1);
+            float* wsl = a.ws + (tile * a.maxsplit + (cta - c_first)) * 256;
+#pragma unroll
+            for (int n8 = 0; n8 < NB; ++n8)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) wsl[(n8 * 32 + lane) * 4 + q] = d[n8][q];
+            __threadfence();
+            __syncwarp();
+            int last = 0;
+            if (lane == 0) last = atomicAdd(a.tickets + tile, 1) == nsplit - 1;
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (!last) continue;
+            __threadfence();
+            const float* wst = a.ws + tile * a.maxsplit * 256;
+#pragma unroll
+            for (int n8 = 0; n8 < NB; ++n8)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    float sum = 0.f;
+                    for (int sp = 0; sp < nsplit; ++sp) sum += __ldcg(wst + sp * 256 + (n8 * 32 + lane) * 4 + q);
+                    d[n8][q] = sum;
+                }
+            if (lane == 0) a.tickets[tile] = 0;  // ready for the next call
+        }
+#pragma unroll
+        for (int n8 = 0; n8 < NB; ++n8)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int m = g + (q >= 2 ? 8 : 0);
+                const int n = n8 * 8 + 2 * t + (q & 1);
+                const int64_t jc = tile * kTileCols + m;
+                if (jc < a.cols && n < a.batch) a.y[static_cast<int64_t>(n) * a.cols + jc] = a.scales[jc] * d[n8][q];
+            }
     }
-#pragma unroll
-    for (int nb = 0; nb < NB; ++nb) {
-        float v[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            v[i] = acc[0][nb][i];
-#pragma unroll
-            for (int h = 1; h < kChains; ++h) v[i] += acc[h][nb][i];
-        }
-        *reinterpret_cast<float4*>(red[warp][nb][lane]) = make_float4(v[0], v[1], v[2], v[3]);
-    }
-    __syncthreads();
-    if (warp < NB) {
-        const int nb = warp;
-        float d[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int w2 = 0; w2 < nw; ++w2) {
-            const float4 v = *reinterpret_cast<const float4*>(red[w2][nb][lane]);
-            d[0] += v.x, d[1] += v.y, d[2] += v.z, d[3] += v.w;
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int m = g + (i >= 2 ? 8 : 0);
-            const int n = nb * 8 + 2 * t + (i & 1);
-            const int64_t j = static_cast<int64_t>(tile) * kTileCols + m;
-            if (j < a.cols && n < a.batch) a.y[static_cast<int64_t>(n) * a.cols + j] = a.scales[j] * d[i];
-        }
-    }
+}
+
+size_t stream_smem(int nb) {
+    return static_cast<size_t>(kRing) * kStageBlocks * 512 + 2 * kRing * 8 + sizeof(float) * 2 * kCW * nb * 32 * 4;
 }
 
 // Outlier term: y[n, j] += sum_{e in column j} x[n, row_e] * v_e. One warp
@@ -408,9 +529,12 @@ struct ezq_gemv_plan {
     uint32_t* out_row;
     float* out_val;
     int64_t n_out;
-    int warps;            // warps per CTA
     int dev;
     float* xt;            // batch > 1 with outliers: x transposed [rows][16] f32 (owned)
+    int grid;             // persistent CTAs of k_gemv_stream (block ranges)
+    int maxsplit;         // most ranges one tile is cut into
+    float* ws;            // split-tile partials (owned)
+    int* tickets;         // per tile (owned, self-resetting)
 };
 
 extern "C" {
@@ -464,9 +588,25 @@ int ezq_gemv_prepare(const ezq_qweight* q, void* stream, ezq_gemv_plan** plan) {
     if (q->n_outliers > 0) EZQ_CK(cudaMalloc(&p->xt, sizeof(float) * 16 * static_cast<size_t>(q->rows)));
     EZQ_CK(cudaMalloc(&p->out_row, sizeof(uint32_t) * std::max<int64_t>(q->n_outliers, 1)));
     EZQ_CK(cudaMalloc(&p->out_val, sizeof(float) * std::max<int64_t>(q->n_outliers, 1)));
-    // Warps per CTA (one CTA per 16-column tile): about 16 resident warps
-    // per SM in one wave -- 4 when there are many tiles, 16 for long K.
-    p->warps = p->tiles >= 512 ? 4 : (p->kq >= 128 ? 16 : 8);
+    // Persistent ranges: kStreamCtasPerSm CTAs per SM, each a contiguous
+    // range of 64-row blocks (never more ranges than blocks).
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t nblk = p->tiles * p->kq;
+    p->grid = static_cast<int>(std::min<int64_t>(nblk, static_cast<int64_t>(sms) * kStreamCtasPerSm));
+    p->maxsplit = 1;
+    for (int64_t tl = 0; tl < p->tiles; ++tl) {  // ranges cutting each tile (host mirror of range_of)
+        auto rng = [&](int64_t b) {
+            int64_t c = (b * p->grid) / nblk;
+            while (c > 0 && range_begin(c, nblk, p->grid) > b) --c;
+            while (c + 1 < p->grid && range_begin(c + 1, nblk, p->grid) <= b) ++c;
+            return c;
+        };
+        p->maxsplit = std::max<int>(p->maxsplit, static_cast<int>(rng((tl + 1) * p->kq - 1) - rng(tl * p->kq) + 1));
+    }
+    EZQ_CK(cudaMalloc(&p->ws, sizeof(float) * 256 * static_cast<size_t>(p->tiles) * p->maxsplit));
+    EZQ_CK(cudaMalloc(&p->tickets, sizeof(int) * static_cast<size_t>(p->tiles)));
+    EZQ_CK(cudaMemsetAsync(p->tickets, 0, sizeof(int) * static_cast<size_t>(p->tiles), st));
     const int64_t nw = p->tiles * p->kq * 32;
     k_gemv_repack<<<static_cast<unsigned>((nw + 255) / 256), 256, 0, st>>>(q->packed, q->rows, q->cols,
                                                                          q->bits, p->kq, p->lmin, p->T);
@@ -495,8 +635,12 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
     const int pt = prof_begin("gemv", st);
     GemvArgs a{};
     a.T = p->T;
-    a.kq = static_cast<int>(p->kq);
-    a.tiles = static_cast<int>(p->tiles);
+    a.kq = p->kq;
+    a.nblk = p->tiles * p->kq;
+    a.grid = p->grid;
+    a.ws = p->ws;
+    a.tickets = p->tickets;
+    a.maxsplit = p->maxsplit;
     a.rows = p->rows;
     a.cols = p->cols;
     a.lmin = p->lmin;
@@ -515,17 +659,15 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
                                                                                   p->xt);
             count_launch();
         }
-        const unsigned grid = static_cast<unsigned>(p->tiles);
-        // two n8 tiles hold twice the accumulators: at most 8 warps per CTA so
-        // that two CTAs share an SM and a 16-warp plan stays one wave
-        const unsigned threads = static_cast<unsigned>((two ? std::min(p->warps, 8) : p->warps) * 32);
+        const unsigned grid = static_cast<unsigned>(p->grid);
+        const size_t smem = stream_smem(two ? 2 : 1);
         switch (x_dtype * 2 + (two ? 1 : 0)) {
-            case 0: k_gemv_mma<1, kF32><<<grid, threads, 0, st>>>(a); break;
-            case 1: k_gemv_mma<2, kF32><<<grid, threads, 0, st>>>(a); break;
-            case 2: k_gemv_mma<1, kBF16><<<grid, threads, 0, st>>>(a); break;
-            case 3: k_gemv_mma<2, kBF16><<<grid, threads, 0, st>>>(a); break;
-            case 4: k_gemv_mma<1, kF16><<<grid, threads, 0, st>>>(a); break;
-            default: k_gemv_mma<2, kF16><<<grid, threads, 0, st>>>(a); break;
+            case 0: k_gemv_stream<1, kF32><<<grid, kStreamThreads, smem, st>>>(a); break;
+            case 1: k_gemv_stream<2, kF32><<<grid, kStreamThreads, smem, st>>>(a); break;
+            case 2: k_gemv_stream<1, kBF16><<<grid, kStreamThreads, smem, st>>>(a); break;
+            case 3: k_gemv_stream<2, kBF16><<<grid, kStreamThreads, smem, st>>>(a); break;
+            case 4: k_gemv_stream<1, kF16><<<grid, kStreamThreads, smem, st>>>(a); break;
+            default: k_gemv_stream<2, kF16><<<grid, kStreamThreads, smem, st>>>(a); break;
         }
         count_launch();
         if (p->n_out) {
@@ -575,6 +717,8 @@ void ezq_gemv_plan_free(ezq_gemv_plan* p) {
     if (p->xt) cudaFree(p->xt);
     cudaFree(p->out_row);
     cudaFree(p->out_val);
+    cudaFree(p->ws);
+    cudaFree(p->tickets);
     delete p;
 }
 

@@ -432,24 +432,6 @@ __global__ void __launch_bounds__(kWarpsK3b * 32) k_seq_errors(const TDesc* __re
 }
 
 // ---- near-tie resolution ------------------------------------
-// Reference-order error of one column at scale s (eval_dense's err,
-// optimize.cpp:36-49, isolated outliers skipped as normal_mask_apply does),
-// strided reads. Used for the candidate scales the K3s loop could not certify.
-__device__ double column_seq_err(const float* col, int64_t R, int64_t C, double s, float olo, float ohi,
-                                 const CfgDev& cfg) {
-    const double inv = __ddiv_rn(1.0, s);
-    const double dmin = cfg.lmin, dmax = cfg.lmax;
-    double e = 0.0;
-    for (int64_t r = 0; r < R; ++r) {
-        const float x = __ldg(col + r * C);
-        if (is_outlier_f(x, olo, ohi)) continue;
-        const double xd = static_cast<double>(x);
-        const double d = fma(s, level_exact(xd, inv, dmin, dmax), -xd);  // exact: s*q is
-        e = __dadd_rn(e, __dmul_rn(d, d));
-    }
-    return e;
-}
-
 // The reference's whole q_range loop for one column in its own order
 // (optimize_channel_range, optimize.cpp:118-184): the fallback for a column
 // whose candidates overflowed the slots. The gradient sum is exact in any
@@ -480,55 +462,140 @@ __device__ double column_ref_optimize(const float* col, int64_t R, int64_t C, do
     return best_s;
 }
 
-// One warp = one K3b tile (32 adjacent columns); a lane resolves its column
-// when the K3s loop left candidates: filter them against the final best
-// (bound as in k_qsort.cu tie_gamma, with rows >= normals), drop repeated
-// scales, evaluate each in reference order and apply the reference's rule
-// (strict-< earliest minimum; fixed step: fixed_err <= e0). Warps without a
-// flagged column return at once.
+// Near-tie resolution before K3b. One warp = one K3b tile
+// (32 adjacent columns, lane = column); warps whose columns carry no
+// candidate list return at once (all of them at 4 bits in practice). A
+// column's candidates (sc.tie_*, step order) are filtered against the final
+// best and de-duplicated; every kept candidate becomes a "pair" (owner lane,
+// scale) handed to a lane of the warp, and the pairs' reference-order errors
+// (eval_dense's sequential fp64 sum over the column's normals in row order,
+// optimize.cpp:36-49) run over one coalesced stream of the tile's rows, each
+// pair lane taking its owner's value by shuffle. The owner then applies the
+// reference's rule (strict-< earliest minimum, optimize.cpp:158; fixed step:
+// fixed_err <= e0, :169-178) and stores the winner in s_fin. More than 32
+// pairs in a warp: further passes over the rows (rare). A column whose slots
+// overflowed runs the reference's whole loop itself (column_ref_optimize).
+struct TiePairs {
+    int src[32];     // owner lane of the pair
+    double s[32];    // candidate scale
+    double err[32];  // reference-order error at s
+};
+
 __global__ void __launch_bounds__(kWarpsK3b * 32) k_resolve_ties(const TDesc* __restrict__ td,
                                                                 const int2* __restrict__ tiles, int ntiles,
                                                                 Scratch sc, CfgDev cfg) {
+    __shared__ TiePairs tp_all[kWarpsK3b];
     const int lane = threadIdx.x & 31;
     const int ti = blockIdx.x * kWarpsK3b + (threadIdx.x >> 5);
     if (ti >= ntiles) return;
+    TiePairs& tp = tp_all[threadIdx.x >> 5];
     const int2 tile = tiles[ti];
     const TDesc& d = td[tile.x];
-    const int64_t c = tile.y + lane, R = d.rows, C = d.cols;
-    const int tn = c < C ? sc.tie_n[d.col_base + c] : 0;
-    if (tn == 0) return;
-    const int64_t gc = d.col_base + c;
-    const int cnt = tn & (kTieFixed - 1);
-    const bool fixed = (tn & kTieFixed) != 0;
-    const float* col = d.W + c;
+    const int64_t c0 = tile.y, R = d.rows, C = d.cols;
+    const int64_t c = c0 + lane;
+    const bool act = c < C;
+    const int64_t gc = d.col_base + (act ? c : c0);
+    const int tn = act ? sc.tie_n[gc] : 0;
+    if (!__any_sync(0xffffffffu, tn != 0)) return;
     const float olo = d.st->olo, ohi = d.st->ohi;
-    atomicAdd(&d.st->ties, 1);
-    if (cnt > cfg.tie_cap) {  // slots overflowed: the reference loop itself
+    const float* col = d.W + (act ? c : c0);
+    const int cnt = tn & (kTieFixed - 1);
+    const bool tfixed = (tn & kTieFixed) != 0;
+    const bool overflow = cnt > cfg.tie_cap;
+    if (overflow) {  // divergent, rare: the reference's loop on this column
+        atomicAdd(&d.st->ties, 1);
         atomicAdd(&d.st->tie_fallback, 1);
         sc.s_fin[gc] = column_ref_optimize(col, R, C, sc.s_rtn[gc], olo, ohi, cfg);
-        return;
     }
+    __syncwarp();
     const double* ts = sc.tie_s + gc * kTieMax;
     const double* te = sc.tie_e + gc * kTieMax;
-    double e1 = te[0];
-    for (int i = 1; i < cnt; ++i) e1 = fmin(e1, te[i]);
-    const double gam = (static_cast<double>(R) + 8.0) * 1.1102230246251565e-16 * 1.02;
-    double best_s = 0.0, best_e = 0.0;
-    int k = 0;
-    for (int i = 0; i < cnt; ++i) {
-        const double s = ts[i];
-        if (!fixed && te[i] - e1 > gam * (te[i] + e1)) continue;
-        bool dup = false;
-        for (int j = 0; j < i; ++j) dup |= ts[j] == s;
-        if (dup) continue;
-        const double e = column_seq_err(col, R, C, s, olo, ohi, cfg);
-        if (k == 0 || (fixed ? e <= best_e : e < best_e)) {  // fixed: [s0, s_fixed]
-            best_e = e;
-            best_s = s;
+    unsigned keep = 0;  // bit i: candidate i kept (within the bound, first of its scale)
+    if (cnt >= 2 && !overflow) {
+        double e1 = te[0];
+        for (int i = 1; i < cnt; ++i) e1 = te[i] < e1 ? te[i] : e1;
+        const double gam = (static_cast<double>(R) + 8.0) * 1.1102230246251565e-16 * 1.02;  // rows >= normals
+        for (int i = 0; i < cnt; ++i) {
+            const double si = ts[i];
+            if (!tfixed && te[i] - e1 > gam * (te[i] + e1)) continue;
+            bool dup = false;
+            for (int j = 0; j < i; ++j) dup |= ((keep >> j) & 1u) && ts[j] == si;
+            if (!dup) keep |= 1u << i;
         }
-        ++k;
+        if (__popc(keep) < 2) keep = 0;  // one distinct candidate: certified after all
     }
-    if (k > 1) sc.s_fin[gc] = best_s;
+    const int mine_n = __popc(keep);
+    int base = mine_n;  // exclusive warp scan of the pair counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, base, o);
+        if (lane >= o) base += v;
+    }
+    const int npairs = __shfl_sync(0xffffffffu, base, 31);
+    base -= mine_n;
+    const float fmin = static_cast<float>(cfg.lmin), fmax = static_cast<float>(cfg.lmax);
+    const double dmin = cfg.lmin, dmax = cfg.lmax;
+    double mine[kTieMax];
+    for (int pb = 0; pb < npairs; pb += 32) {  // warp-uniform
+        __syncwarp();
+        for (int i = 0, k = base; i < cnt && keep; ++i) {
+            if (!((keep >> i) & 1u)) continue;
+            if (k >= pb && k < pb + 32) {
+                tp.src[k - pb] = lane;
+                tp.s[k - pb] = ts[i];
+            }
+            ++k;
+        }
+        __syncwarp();
+        const bool pown = lane < npairs - pb;
+        const int psrc = pown ? tp.src[lane] : 0;
+        const double ps = pown ? tp.s[lane] : 1.0;
+        const double pinv = __ddiv_rn(1.0, ps);
+        const float pinvf = __double2float_rn(pinv);
+        double pe = 0.0;
+        int64_t r = 0;
+        for (; r + kRowsK3b <= R; r += kRowsK3b) {
+            float x[kRowsK3b];
+#pragma unroll
+            for (int j = 0; j < kRowsK3b; ++j) x[j] = __ldg(col + (r + j) * C);
+#pragma unroll
+            for (int j = 0; j < kRowsK3b; ++j) {
+                const float xv = __shfl_sync(0xffffffffu, x[j], psrc);
+                if (pown && !is_outlier_f(xv, olo, ohi))
+                    pe = __dadd_rn(pe, seq_sq(xv, static_cast<double>(xv), ps, pinvf, pinv, fmin, fmax, dmin, dmax,
+                                              cfg.guard));
+            }
+        }
+        for (; r < R; ++r) {
+            const float xv = __shfl_sync(0xffffffffu, __ldg(col + r * C), psrc);
+            if (pown && !is_outlier_f(xv, olo, ohi))
+                pe = __dadd_rn(pe, seq_sq(xv, static_cast<double>(xv), ps, pinvf, pinv, fmin, fmax, dmin, dmax,
+                                          cfg.guard));
+        }
+        tp.err[lane] = pe;
+        __syncwarp();
+        for (int k = 0; k < mine_n; ++k) {
+            const int slot = base + k - pb;
+            if (slot >= 0 && slot < 32) mine[k] = tp.err[slot];
+        }
+    }
+    if (!keep) return;
+    int k = 0, first = 1;
+    double be = 0.0, bs = 0.0, e_s0 = 0.0, s_s0 = 0.0, e_fx = 0.0, s_fx = 0.0;
+    for (int i = 0; i < cnt; ++i) {
+        if (!((keep >> i) & 1u)) continue;
+        const double si = ts[i], ei = mine[k++];
+        if (tfixed) {  // [s0, s_fixed]
+            if (first) e_s0 = ei, s_s0 = si;
+            else e_fx = ei, s_fx = si;
+        } else if (first || ei < be) {  // strict: earliest minimum wins
+            be = ei;
+            bs = si;
+        }
+        first = 0;
+    }
+    sc.s_fin[gc] = tfixed ? (e_fx <= e_s0 ? s_fx : s_s0) : bs;
+    atomicAdd(&d.st->ties, 1);
 }
 
 // Fix-up of the fused pack: columns flagged by K3b (stored scale s_rtn, codes

@@ -96,27 +96,50 @@ __device__ __forceinline__ DD err_minus_c(double Ad, double q, double s) {
 __device__ __forceinline__ float tie_gamma(int n) {
     return (static_cast<float>(n) + 8.0f) * 1.1102230246251565e-16f * 1.01f;
 }
-// Candidate bookkeeping of one column (state identical on every lane; `writer`
-// stores). best/err are err - C; cfull = C (estimate) converts to full errors.
+// Pre-filter of the per-step check: an error above best + gamma (2 best + 2 C)
+// (with slack) can be neither a new best nor near one, so the hot loop pays
+// one compare per step; TieTrack::step runs only below it.
+__device__ __forceinline__ double tie_threshold(double best, double cfull, float gam) {
+    return __dadd_rn(best, static_cast<double>(gam) * 2.0002 * __dadd_rn(best, cfull));
+}
+// Candidate bookkeeping of one column, kept by its writer lane only (other
+// lanes return at once). best/err are err - C; cfull = C (an estimate)
+// converts to full errors. The list (sc.tie_s / tie_e, step order) holds the
+// distinct scales whose exact errors lie within the bound of the running
+// best: a new best drops the entries now beyond it (the filter reads back the
+// writer's own stores), a far new best empties it. nc > cap: a candidate was
+// lost (the column takes the whole-loop fallback).
 struct TieTrack {
     int nc;
-    __device__ __forceinline__ void push(bool writer, const Scratch& sc, int64_t gcol, int cap, double s,
-                                         double efull) {
-        if (writer && nc < cap) {
+    __device__ __forceinline__ void push(const Scratch& sc, int64_t gcol, int cap, double s, double efull) {
+        if (nc < cap) {
             sc.tie_s[gcol * kTieMax + nc] = s;
             sc.tie_e[gcol * kTieMax + nc] = efull;
         }
         ++nc;
     }
     // Called for t >= 1 before the best is updated; lt = err < best.
-    __device__ __forceinline__ void step(bool writer, const Scratch& sc, int64_t gcol, int cap, bool lt,
-                                         DD err, DD best, double s, double best_s, float gam, double cfull) {
-        if (!lt && s == best_s) return;  // same scale, same error in both orders
+    __device__ __forceinline__ void step(bool writer, const Scratch& sc, int64_t gcol, int cap, bool lt, DD err,
+                                         DD best, double s, double best_s, float gam, double cfull) {
+        if (!writer || (!lt && s == best_s)) return;  // same scale: same error in both orders
         const double gap = fabs(__dadd_rn(__dsub_rn(err.hi, best.hi), __dsub_rn(err.lo, best.lo)));
         const double ef = __dadd_rn(err.hi, cfull), bf = __dadd_rn(best.hi, cfull);
         if (gap <= static_cast<double>(gam) * __dadd_rn(ef, bf)) {
-            if (nc == 0) push(writer, sc, gcol, cap, best_s, bf);
-            push(writer, sc, gcol, cap, s, ef);
+            if (nc == 0) {
+                push(sc, gcol, cap, best_s, bf);
+            } else if (lt && nc <= cap) {  // keep the entries still within the bound of the new best
+                int k = 0;
+                for (int j = 0; j < nc; ++j) {
+                    const double e = sc.tie_e[gcol * kTieMax + j];
+                    if (__dsub_rn(e, ef) <= static_cast<double>(gam) * __dadd_rn(e, ef)) {
+                        sc.tie_s[gcol * kTieMax + k] = sc.tie_s[gcol * kTieMax + j];
+                        sc.tie_e[gcol * kTieMax + k] = e;
+                        ++k;
+                    }
+                }
+                nc = k;
+            }
+            push(sc, gcol, cap, s, ef);
         } else if (lt) {
             nc = 0;  // every earlier candidate is now beyond the bound
         }
@@ -125,12 +148,12 @@ struct TieTrack {
     __device__ __forceinline__ void fixed(bool writer, const Scratch& sc, int64_t gcol, int cap, DD fe, DD e0,
                                           double fs, double s0, float gam, double cfull) {
         nc = 0;
-        if (fs == s0) return;
+        if (!writer || fs == s0) return;
         const double gap = fabs(__dadd_rn(__dsub_rn(fe.hi, e0.hi), __dsub_rn(fe.lo, e0.lo)));
         const double ef = __dadd_rn(fe.hi, cfull), bf = __dadd_rn(e0.hi, cfull);
         if (gap <= static_cast<double>(gam) * __dadd_rn(ef, bf)) {
-            push(writer, sc, gcol, cap, s0, bf);
-            push(writer, sc, gcol, cap, fs, ef);
+            push(sc, gcol, cap, s0, bf);
+            push(sc, gcol, cap, fs, ef);
             nc |= kTieFixed;
         }
     }
@@ -619,6 +642,7 @@ __global__ void __launch_bounds__(256, 4) k_qrange_tables(const TDesc* __restric
         double best_s = s, fixed_s = s;
         const float gam = tie_gamma(n);
         const bool track = cfg.tie_cap > 0 && cfg.select != EZQ_SELECT_FIXED;
+        double tie_thr = 0.0;
         bool own[TPL];
         int jl[TPL], wA[TPL], ib[TPL];
         float Xp[TPL], span[TPL];  // previous threshold; x[k0+7] - x[k0] near it
@@ -672,9 +696,14 @@ __global__ void __launch_bounds__(256, 4) k_qrange_tables(const TDesc* __restric
                 e0 = err;
                 best_err = err;
                 fixed_err = err;
+                tie_thr = tie_threshold(err.hi, ci.chi, gam);
             } else {
                 const bool lt = dd_lt(err, best_err);  // strict: earliest minimum wins (optimize.cpp:158)
-                if (track) tie.step(live && gl == 0, sc, gcol, cfg.tie_cap, lt, err, best_err, s, best_s, gam, ci.chi);
+                if (track && (lt || err.hi <= tie_thr)) {  // rare: a new best or a near one
+                    const double cf = ci.chi;
+                    tie.step(live && gl == 0, sc, gcol, cfg.tie_cap, lt, err, best_err, s, best_s, gam, cf);
+                    if (lt) tie_thr = tie_threshold(err.hi, cf, gam);
+                }
                 if (lt) {
                     best_err = err;
                     best_s = s;
@@ -699,7 +728,7 @@ __global__ void __launch_bounds__(256, 4) k_qrange_tables(const TDesc* __restric
     if (live && gl == 0) {
         sc.s_rtn[gcol] = s_rtn;
         sc.s_fin[gcol] = s_fin;
-        sc.tie_n[gcol] = tie.nc;
+        sc.tie_n[gcol] = (tie.nc & (kTieFixed - 1)) >= 2 ? tie.nc : 0;  // one entry: the best itself
     }
 }
 
@@ -756,6 +785,7 @@ __global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__
         double best_s = s, fixed_s = s;
         const float gam = tie_gamma(nall);
         const bool track = cfg.tie_cap > 0 && cfg.select != EZQ_SELECT_FIXED;
+        double tie_thr = 0.0;
         bool own[PPL];
         int jl[PPL], np[PPL], ib[PPL];
         ColTab ct[PPL];
@@ -809,9 +839,13 @@ __global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__
                 e0 = err;
                 best_err = err;
                 fixed_err = err;
+                tie_thr = tie_threshold(err.hi, call, gam);
             } else {
                 const bool lt = dd_lt(err, best_err);  // strict: earliest minimum wins (optimize.cpp:158)
-                if (track) tie.step(lane == 0, sc, gcol, cfg.tie_cap, lt, err, best_err, s, best_s, gam, call);
+                if (track && (lt || err.hi <= tie_thr)) {  // rare: a new best or a near one
+                    tie.step(lane == 0, sc, gcol, cfg.tie_cap, lt, err, best_err, s, best_s, gam, call);
+                    if (lt) tie_thr = tie_threshold(err.hi, call, gam);
+                }
                 if (lt) {
                     best_err = err;
                     best_s = s;
@@ -836,7 +870,7 @@ __global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__
     if (lane == 0) {
         sc.s_rtn[gcol] = s_rtn;
         sc.s_fin[gcol] = s_fin;
-        sc.tie_n[gcol] = tie.nc;
+        sc.tie_n[gcol] = (tie.nc & (kTieFixed - 1)) >= 2 ? tie.nc : 0;  // one entry: the best itself
     }
 }
 

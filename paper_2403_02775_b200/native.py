@@ -121,6 +121,30 @@ class QuantizedWeight:
     final_error: Optional[float] = None
     _owner: object = field(default=None, repr=False, compare=False)
 
+    def __getstate__(self):
+        """Pickles as plain arrays: zero-copy views of library memory are
+        copied and the owner handle (a ctypes pointer) is dropped."""
+        d = dict(self.__dict__)
+        for k in ("packed", "scales", "outliers"):
+            d[k] = np.array(d[k], copy=True)
+        d["_owner"] = None
+        return d
+
+
+class _OwnedBuffer:
+    """Exposes `nbytes` of library memory at `addr` through the array
+    interface and holds the owner: numpy arrays built on it keep the owner
+    (and so the memory) alive for as long as any view exists."""
+
+    def __init__(self, addr: int, nbytes: int, owner):
+        self.__array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (addr, False), "version": 3}
+        self._owner = owner
+
+
+def _owned_view(addr: int, count: int, dtype, owner) -> np.ndarray:
+    dt = np.dtype(dtype)
+    return np.asarray(_OwnedBuffer(addr, count * dt.itemsize, owner)).view(dt)
+
 
 class _COwner:
     """Keeps a library-owned host ezq_qweight alive while numpy views of its
@@ -216,6 +240,19 @@ def check(code: int):
         _raise(code)
 
 
+def _as_f32(W):
+    """A float32 row-major matrix the C-ABI can read: numpy inputs are made
+    contiguous float32 (a copy when needed); torch inputs must be float32 and
+    contiguous (a transposed view or a 16-bit tensor would be read as the
+    wrong bytes) and are converted with .contiguous().float() otherwise."""
+    if isinstance(W, np.ndarray):
+        return np.ascontiguousarray(W, dtype=np.float32)
+    import torch
+    if W.dtype != torch.float32 or not W.is_contiguous():
+        W = W.contiguous().to(torch.float32)
+    return W
+
+
 def _ptr(a) -> Optional[int]:
     """Address of a numpy array or torch tensor (None for None)."""
     if a is None:
@@ -288,6 +325,7 @@ def config_validate(cfg: Config):
 # ---- tensor-scale ---------------------------------------------------------
 def tensor_stats(W, stream=None) -> dict:
     """stats.hpp:14 -> {mean, stddev, max_abs, count}."""
+    W = _as_f32(W)
     rows, cols = W.shape
     st = CStats()
     check(lib().ezq_tensor_stats(_ptr(W), rows, cols, _mem(W), _stream(stream, W), C.byref(st)))
@@ -296,6 +334,7 @@ def tensor_stats(W, stream=None) -> dict:
 
 def detect_outliers(W, cfg: Config, stream=None):
     """outliers.hpp:15 -> (entries[OUTLIER_DTYPE], mean, stddev)."""
+    W = _as_f32(W)
     rows, cols = W.shape
     c = cfg.to_c()
     e = C.POINTER(COutlier)()
@@ -315,14 +354,18 @@ def _from_c(q: CQWeight, owner=None) -> QuantizedWeight:
     struct) the arrays are zero-copy views kept alive by the owner; without it
     they are copied."""
     assert q.mem == MEM_HOST
-    cp = (lambda a: a) if owner is not None else (lambda a: a.copy())
-    packed = cp(np.ctypeslib.as_array(q.packed, shape=(q.packed_bytes,))) if q.packed_bytes else np.zeros(0, np.uint8)
-    scales = cp(np.ctypeslib.as_array(q.scales, shape=(q.cols,)))
-    if q.n_outliers:
-        raw = np.ctypeslib.as_array(C.cast(q.outliers, C.POINTER(C.c_uint8)), shape=(q.n_outliers * 12,))
-        outl = cp(raw.view(OUTLIER_DTYPE))
-    else:
-        outl = np.zeros(0, dtype=OUTLIER_DTYPE)
+
+    def arr(ptr, count, dtype):
+        if not count:
+            return np.zeros(0, dtype)
+        addr = C.cast(ptr, C.c_void_p).value
+        if owner is not None:
+            return _owned_view(addr, count, dtype, owner)
+        return _owned_view(addr, count, dtype, None).copy()
+
+    packed = arr(q.packed, q.packed_bytes, np.uint8)
+    scales = arr(q.scales, q.cols, np.float32)
+    outl = arr(q.outliers, q.n_outliers, OUTLIER_DTYPE)
     return QuantizedWeight(q.rows, q.cols, q.bits, packed, scales, outl, q.mean, q.stddev,
                            q.sigma_n, q.rtn_error if q.has_errors else None,
                            q.final_error if q.has_errors else None, owner)
@@ -330,6 +373,7 @@ def _from_c(q: CQWeight, owner=None) -> QuantizedWeight:
 
 def quantize_tensor(W, cfg: Config, mode: str = "easyquant", stream=None) -> QuantizedWeight:
     """pipeline.hpp:33 -- host copy of the artifact (device work inside)."""
+    W = _as_f32(W)
     rows, cols = W.shape
     c = cfg.to_c()
     q = C.POINTER(CQWeight)()
@@ -382,7 +426,10 @@ class DeviceBatch:
 def quantize_batch(Ws: Sequence, cfg: Config, mode: str = "easyquant", out_mem: int = MEM_HOST,
                    stream=None):
     """ezq_quantize_batch: list of QuantizedWeight (host) or a DeviceBatch."""
+    Ws = [_as_f32(w) for w in Ws]
     n = len(Ws)
+    if n and len({_mem(w) for w in Ws}) != 1:
+        raise ValueError("quantize_batch: every tensor must live in the same memory (all host or all device)")
     ptrs = (C.c_void_p * n)(*[_ptr(w) for w in Ws])
     rows = (C.c_int64 * n)(*[w.shape[0] for w in Ws])
     cols = (C.c_int64 * n)(*[w.shape[1] for w in Ws])
@@ -477,6 +524,7 @@ def decode_quantized(data: bytes) -> QuantizedWeight:
 
 
 def reconstruction_error(a, b, skip: Optional[np.ndarray] = None) -> float:
+    a, b = _as_f32(a), _as_f32(b)
     rows, cols = a.shape
     r = c = None
     n = 0
@@ -542,6 +590,7 @@ def grid_oracle_batch(Ws: Sequence, cfg: Config, grid_points: int = 2000, stream
     """ezq_grid_oracle_batch: the reference's brute-force grid optimum
     (optimize.cpp:186-229) for every column of every tensor, on the device.
     Returns a list of (best_scale, best_error) float64 arrays, one per tensor."""
+    Ws = [_as_f32(w) for w in Ws]
     n = len(Ws)
     ptrs = (C.c_void_p * n)(*[_ptr(w) for w in Ws])
     rows = (C.c_int64 * n)(*[w.shape[0] for w in Ws])

@@ -166,3 +166,25 @@ def test_decode_errors_match_compiled_reference(N, O, R):
         if ref[0] == "err" and ref[1] == 9:
             ref = ("err", 9, None)  # std::exception (not io_error): offset not reported
         assert ours == ref, (b.hex(), ours, ref)
+
+
+def test_zero_copy_views_keep_their_owner_alive(N, O):
+    """decode_quantized returns zero-copy views of library memory: a kept
+    array must stay valid after its QuantizedWeight is dropped, even when the
+    next decode of the same size reuses the allocator's free block."""
+    import gc
+    import pickle
+    a = _artifact(N, O, 64, 32, 4, 11, n_out=5)
+    b = _artifact(N, O, 64, 32, 4, 12, n_out=5)
+    q = N.decode_quantized(N.encode_quantized(a))
+    kept_packed, kept_scales, kept_out = q.packed, q.scales, q.outliers
+    ref = (kept_packed.copy(), kept_scales.copy(), kept_out.copy())
+    del q
+    gc.collect()
+    others = [N.decode_quantized(N.encode_quantized(b)) for _ in range(4)]
+    assert np.array_equal(kept_packed, ref[0])
+    assert np.array_equal(kept_scales, ref[1])
+    assert np.array_equal(kept_out, ref[2])
+    # artifacts pickle as plain arrays (the multi-process driver ships them)
+    back = pickle.loads(pickle.dumps(others[0]))
+    assert np.array_equal(back.packed, others[0].packed) and back._owner is None
