@@ -10,10 +10,15 @@ ezq_quantize_batch with inputs already resident in HBM (`value`), and through
 the same C-ABI call with pinned HOST buffers, H2D/D2H inside the timed region
 (`e2e`). configs[2]'s other points (4-/3-bit x sigma_n 3.2905 / 2.8070 /
 2.5758, i.e. 0.1 / 0.5 / 1 % Gaussian outliers) are timed the same way and
-reported as `sweep` rows of the same line. Multi-GPU (torchrun): every rank
-quantizes its own weight set (the tensors are independent; no data-path
-collective) -> weak scaling; `--shard` instead LPT-partitions ONE weight set
-over the ranks through the whole-model driver (strong scaling).
+reported as `sweep` rows of the same line. Multi-GPU (torchrun): ONE weight
+set is LPT-partitioned over the ranks by the whole-model driver's rule
+(driver.lpt_partition, rows x cols per tensor; every tensor seeded by its
+index, so the set is the same for any N); each rank quantizes its share
+with no data-path collective, and the step time is the slowest rank's
+(strong scaling). `--scaling weak` gives every rank a whole set instead.
+`--workload opt-175b` (configs[3]) runs the full OPT-175B-shaped set (96
+layers, 174 B weights) once: layers are generated on the device in batches
+(the fp32 model is 696 GB) and only the quantizer calls are timed.
 
 `--impl reference` times the reference's own CPU implementation
 (oracle/_ref/libezq_ref.so, compiled from /root/reference's sources; else
@@ -38,6 +43,7 @@ WORKLOADS = {
     "opt-1.3b": (2048, 24, 8192, "OPT-1.3B-shaped weight set (configs[1])"),
     "llama-7b": (4096, 32, 11008, "LLaMA-7B-shaped weight set (configs[2])"),
     "opt-175b-layer": (12288, 1, 49152, "one OPT-175B layer (configs[3] per-layer unit)"),
+    "opt-175b": (12288, 96, 49152, "OPT-175B-shaped weight set, 96 layers (configs[3])"),
     "c1": (4096, 1, 0, "single 4096x4096 tensor (configs[0])"),
 }
 
@@ -161,8 +167,12 @@ def cpu_reference_time(shapes, cfg, seed=7):
     return time.perf_counter() - t0, "port", threads
 
 
-def base_line(args, cfg, shapes, params, world):
+def base_line(args, cfg, shapes, params, world, mine=None):
+    """`shapes`/`params`: the whole weight set; `mine`: rank 0's tensor
+    indices (strong scaling), None when every rank holds a whole set."""
     h, L, ffn, desc = WORKLOADS[args.workload]
+    strong = mine is not None
+    p0 = sum(shapes[i][0] * shapes[i][1] for i in mine) if strong else params
     return {
         "metric": "weights quantized/sec",
         "unit": "weights/s",
@@ -170,20 +180,24 @@ def base_line(args, cfg, shapes, params, world):
         "steps": args.steps,
         "warmup": args.warmup,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (N(0,0.02^2) random-init weights of the named shapes, seeded per rank)",
+        "data": "synthetic (N(0,0.02^2) random-init weights of the named shapes, each tensor seeded by its index)",
         "config": {
             "workload": f"{args.workload}: {desc}",
-            "tensors_per_gpu": len(shapes),
-            "weights_per_gpu": params,
+            "tensors": len(shapes),
+            "weights": params if strong else params * world,
+            "tensors_rank0": len(mine) if strong else len(shapes),
+            "weights_rank0": p0,
             "shapes": sorted({f"{r}x{c}" for r, c in shapes}),
             "bits": cfg.bits, "sigma_n": cfg.sigma_n, "steps": cfg.steps, "lr": cfg.lr,
             "select": cfg.select,
-            "l2_policy": "inputs larger than L2 (%.2f GB resident per GPU > 126 MB)" % (4 * params / 1e9)
-            if 4 * params > 2e8 else "single tensor; L2 not flushed (compute-bound kernel)",
-            "parallelism": f"tensor-sharded dp{world} (independent weight sets, no collective)",
+            "l2_policy": "inputs larger than L2 (%.2f GB resident on rank 0 > 126 MB)" % (4 * p0 / 1e9)
+            if 4 * p0 > 2e8 else "single tensor; L2 not flushed (compute-bound kernel)",
+            "parallelism": (f"lpt-sharded over {world} GPU(s): one weight set, tensors partitioned by "
+                            f"driver.lpt_partition (rows x cols), no collective on the data path") if strong
+            else f"tensor-sharded dp{world} (independent weight sets, no collective)",
         },
     }
 
@@ -341,6 +355,98 @@ def k3_roofline(args, prof, fp64_peak, clocks):
     }
 
 
+def run_opt175b(args, cfg, shapes, rank, local, world):
+    """configs[3]: the whole OPT-175B-shaped set (576 tensors, 174 B weights)
+    at ~1% outliers (sigma_n 2.5758), LPT-sharded over the ranks. The fp32
+    model (696 GB) does not fit in HBM, so every rank generates its share on
+    the device in batches of <= 8 GB and only the quantizer calls are timed
+    (CUDA events around each ezq_quantize_batch, inputs resident, outputs
+    device-resident); the step is one pass over the model."""
+    import torch
+    import torch.distributed as dist
+    from paper_2403_02775_b200 import native as N
+    from paper_2403_02775_b200.driver import lpt_partition
+    from paper_2403_02775_b200.native import Config
+    cfg = Config(sigma_n=2.5758)
+    params = sum(r * c for r, c in shapes)
+    bins = lpt_partition([r * c for r, c in shapes], world)
+    mine = bins[rank]
+    batches, cur, cur_b = [], [], 0
+    for i in mine:
+        b = 4 * shapes[i][0] * shapes[i][1]
+        if cur and cur_b + b > (8 << 30):
+            batches.append(cur)
+            cur, cur_b = [], 0
+        cur.append(i)
+        cur_b += b
+    if cur:
+        batches.append(cur)
+
+    def gen(idx):
+        out = []
+        for i in idx:
+            g = torch.Generator(device="cuda").manual_seed(1234 + i)
+            out.append(torch.randn(shapes[i], generator=g, device="cuda", dtype=torch.float32) * 0.02)
+        return out
+
+    Ws = gen(batches[0])
+    for _ in range(args.warmup):
+        N.quantize_batch(Ws, cfg, out_mem=N.MEM_DEVICE).close()
+    del Ws
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    N.profile_enable(True)
+    launches0 = N.kernel_launches()
+    dev_ms, n_out, worst = 0.0, 0, 0.0
+    t0 = time.perf_counter()
+    with ClockSampler(local) as clocks:
+        for bt in batches:
+            Ws = gen(bt)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            b = N.quantize_batch(Ws, cfg, out_mem=N.MEM_DEVICE)
+            e1.record()
+            torch.cuda.synchronize()
+            dev_ms += e0.elapsed_time(e1)
+            for k in range(len(bt)):
+                q = b[k]
+                n_out += q.n_outliers
+                assert q.final_error <= q.rtn_error
+                worst = max(worst, q.final_error / q.rtn_error if q.rtn_error else 0.0)
+            b.close()
+            del Ws
+    wall = time.perf_counter() - t0
+    launches = N.kernel_launches() - launches0
+    prof = {f: N.profile_read(f) for f in ("stats", "detect", "qsort", "qrange", "qrange_stream", "seqerr", "pack")}
+    N.profile_enable(False)
+    t = torch.tensor([dev_ms, wall], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms, wall = float(t[0].item()), float(t[1].item())
+    if rank == 0:
+        fp64_peak = N.measure_fp64_peak()
+        args.steps = 1
+        line = base_line(args, cfg, shapes, params, world, bins[0])
+        rp = sum(shapes[i][0] * shapes[i][1] for i in mine)
+        line.update({
+            "value": params / (dev_ms * 1e-3), "ms_per_step": dev_ms, "wall_s_rank_max": wall,
+            "e2e": None, "e2e_note": "not measured for this workload: the 696 GB fp32 model fits neither "
+                                     "host nor device memory; inputs are generated on the device per batch",
+            "gpu_launches": launches, "clocks": clocks.summary(),
+            "roofline": k3_roofline(args, prof, fp64_peak, clocks.summary()),
+            "kernel_share": {f: prof[f]["ms"] / dev_ms for f in prof if prof[f]["launches"]},
+            "outlier_pct_rank0": 100.0 * n_out / rp, "worst_final_over_rtn_rank0": worst,
+            "ties": dict(zip(("resolved_columns", "fallback_columns"), N.tie_stats())),
+            "paper_claim": "< 10 min on 8 GPUs (EasyQuant, arXiv 2403.02775, PAPER.md:188)",
+        })
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -352,6 +458,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-gemv", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: one weight set LPT-sharded over the ranks; weak: a whole set per rank")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -371,8 +479,19 @@ def main():
     cfg = Config()
     shapes = layer_shapes(args.workload)
     params = sum(r * c for r, c in shapes)
-    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
-    Ws = [torch.randn(s, generator=gen, device="cuda", dtype=torch.float32) * 0.02 for s in shapes]
+    if args.workload == "opt-175b":
+        return run_opt175b(args, cfg, shapes, rank, local, world)
+    from paper_2403_02775_b200.driver import lpt_partition
+    strong = args.scaling == "strong"
+    mine = lpt_partition([r * c for r, c in shapes], world)[rank] if strong else list(range(len(shapes)))
+    mine0 = lpt_partition([r * c for r, c in shapes], world)[0] if strong else None
+    total = params if strong else params * world  # weights quantized per step by the whole job
+
+    def gen_tensor(i, salt=0):
+        g = torch.Generator(device="cuda").manual_seed(1234 + i + (0 if strong else 100003 * rank) + salt)
+        return torch.randn(shapes[i], generator=g, device="cuda", dtype=torch.float32) * 0.02
+
+    Ws = [gen_tensor(i) for i in mine]
     torch.cuda.synchronize()
 
     def barrier():
@@ -414,7 +533,7 @@ def main():
         t = torch.tensor([step_s], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         step_s = float(t.item())
-    value = world * params / step_s
+    value = total / step_s
 
     # ---- configs[2] sweep points (device-resident, same timing) ----------
     sweep = []
@@ -437,9 +556,10 @@ def main():
                     t = torch.tensor([ms], device="cuda", dtype=torch.float64)
                     dist.all_reduce(t, op=dist.ReduceOp.MAX)
                     ms = float(t.item())
+                my = sum(w.numel() for w in Ws)
                 sweep.append({"bits": bits, "sigma_n": sig, "target_outlier_pct": pct,
-                              "outlier_pct": 100.0 * n_out_pt / params, "ms_per_step": ms,
-                              "value": world * params / (ms * 1e-3), "unit": "weights/s"})
+                              "outlier_pct_rank0": 100.0 * n_out_pt / my, "ms_per_step": ms,
+                              "value": total / (ms * 1e-3), "unit": "weights/s"})
 
     # ---- e2e: the public C-ABI with pinned host buffers ----------------------
     e2e = None
@@ -465,7 +585,7 @@ def main():
             t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
-        e2e = {"value": world * params / e2e_s, "unit": "weights/s", "h2d_bytes_per_step": h2d,
+        e2e = {"value": total / e2e_s, "unit": "weights/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_s,
                "timer": "host wall clock around the synchronous ezq_quantize_batch call "
                         "(pinned host W in, host artifacts out)"}
@@ -478,12 +598,15 @@ def main():
 
     roof = k3_roofline(args, prof, fp64_peak, clocks.summary())
     # work-based view: the reference's eval_dense does 7 flop per
-    # normal element per evaluation, steps + 1 evaluations per column
-    cols_total = sum(c for _, c in shapes)
-    elem_steps = (params - n_out) * (cfg.steps + 1)
+    # normal element per evaluation, steps + 1 evaluations per column (rank
+    # 0's share: the kernels timed above)
+    rshapes = [shapes[i] for i in mine]
+    rparams = sum(r * c for r, c in rshapes)
+    cols_total = sum(c for _, c in rshapes)
+    elem_steps = (rparams - n_out) * (cfg.steps + 1)
     flop = 7.0 * elem_steps
     loop_ms = prof["qrange"]["ms"] / args.steps if prof["qrange"]["launches"] else None
-    packed = sum((r * c + 1) // 2 if cfg.bits == 4 else r * c for r, c in shapes)
+    packed = sum((r * c + 1) // 2 if cfg.bits == 4 else r * c for r, c in rshapes)
     roof["work"] = {
         "flop_per_normal_element_step": 7, "normal_element_steps_per_step": elem_steps,
         "fp64_peak_tflops": fp64_peak, "fp64_peak_source": "measured DFMA microkernel (this run)",
@@ -494,9 +617,9 @@ def main():
         "note": "the reference-algorithm flops this step replaces, per second, against the FP64 DFMA peak; "
                 ">1 is possible because K3s evaluates each step in O(levels) per column, not O(rows)",
     }
-    roof["algorithmic_bytes_per_step"] = 4 * params + packed + 12 * n_out + 4 * cols_total
+    roof["algorithmic_bytes_per_step"] = 4 * rparams + packed + 12 * n_out + 4 * cols_total
     roof["dram_bytes_per_step"] = (roof.get("ncu") or {}).get("step_dram_bytes")
-    line = base_line(args, cfg, shapes, params, world)
+    line = base_line(args, cfg, shapes, params, world, mine0)
     line.update({
         "value": value,
         "ms_per_step": step_s * 1e3,
@@ -506,7 +629,8 @@ def main():
         "clocks": clocks.summary(),
         "roofline": roof,
         "kernel_share": {f: prof[f]["ms"] / args.steps / (step_s * 1e3) for f in prof if prof[f]["launches"]},
-        "outlier_pct": 100.0 * n_out / params,
+        "outlier_pct": 100.0 * n_out / rparams,
+        "ties": dict(zip(("resolved_columns", "fallback_columns"), N.tie_stats())),
     })
     if sweep:
         line["sweep"] = sweep

@@ -165,50 +165,55 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const unsigned (&a)[4], 
             : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
 }
 
-// ---- K6 main kernel: persistent, TMA-fed ------------------------------------
-// The codes of a tile are contiguous (T[tile][q][lane]), so the whole
-// artifact is one array of 512-byte blocks in (tile, q) order. Each CTA owns
-// a contiguous range of ~nblk/grid blocks and streams it through a ring of
-// kRing stages x kStageBlocks blocks with cp.async.bulk (one elected producer
-// lane, mbarrier full/empty pairs): ~100 KB of codes in flight per SM, which
-// is what an HBM-latency-bound stream needs (Little's law: ~5 MB in flight
-// GPU-wide at 6.5 TB/s), without holding them in registers. kCW consumer
-// warps take the range's blocks round-robin (LDS.128 from the ring, x
-// fragments from L1/L2 one block ahead), dequantize to exact levels and run
-// the MMAs. At every tile boundary the warps' fragments meet in shared memory
-// (fixed order); a tile cut by a range boundary is split across CTAs: each
+// ---- K6 main kernel: column-block skinny GEMM, persistent, TMA-fed ----------
+// Output columns go in blocks of kBM = 128 (8 MMA tiles); the artifact is
+// repacked as super-blocks (colblock, q) of 8 tiles x 64 rows = 4 KB, stored
+// T[cb][q][tile8][lane] so every run of super-blocks in (cb, q) order is one
+// contiguous byte range. Each CTA owns a contiguous range of ~nsb/grid
+// super-blocks and streams it through a ring of kRing stages of up to kS
+// super-blocks of ONE colblock: the codes by one cp.async.bulk (TMA) per
+// stage, the matching x slice (kS x 64 rows x batch) by cp.async 16-byte
+// copies from the producer warp's 32 lanes, both completing on the stage's
+// mbarrier. ~50-100 KB in flight per SM -- what an HBM-latency-bound stream
+// needs (Little's law: ~5 MB in flight GPU-wide at 6.5 TB/s) -- without
+// holding it in registers, and the x slice is loaded once per CTA per q for
+// all 128 columns. Each of the kCW = 4 consumer warps owns 2 of the 8 tiles
+// across the whole range (no cross-warp reduction): per super-block two
+// LDS.128 of codes, the x fragments from shared memory, dequantize to exact
+// levels, MMA. A colblock cut by a range boundary is split across CTAs: each
 // writes its partial to a workspace and the last to arrive (ticket) sums the
 // partials in CTA order -- deterministic, bit-identical across calls.
-constexpr int kCW = 4;            // consumer warps per CTA
-constexpr int kStageBlocks = 16;  // 64-row blocks per ring stage (8 KB)
-constexpr int kRing = 4;          // ring stages per CTA (32 KB)
+constexpr int kCW = 4;             // consumer warps per CTA
+constexpr int kBM = 128;           // columns per colblock
+constexpr int kTilesCB = kBM / kTileCols;  // 8
+constexpr int kSBBytes = kTilesCB * 512;   // 4 KB of codes per super-block
+constexpr int kS = 4;              // super-blocks per ring stage
+constexpr int kRing = 3;           // ring stages per CTA
 constexpr int kStreamThreads = (kCW + 1) * 32;
-constexpr int kStreamCtasPerSm = 3;
 
 struct GemvArgs {
     const uint4* T;
-    int64_t kq;    // 64-row blocks per tile
-    int64_t nblk;  // tiles * kq
+    int64_t kq;    // 64-row blocks (K)
+    int64_t nsb;   // colblocks * kq
     int grid;      // CTAs (ranges)
     int64_t rows, cols;
     int lmin;
     const float* scales;
-    const void* x;
-    int batch;  // rows of this group (1..16)
+    const void* x;     // [batch][rows], rows % 64 == 0 and 16-byte aligned rows (else a padded copy)
+    int64_t xstride;   // elements between batch rows of x
+    int batch;         // rows of this group (1..16)
     float* y;
-    float* ws;     // split-tile partials [tiles][maxsplit][16 batch][16 cols]
-    int* tickets;  // [tiles], self-resetting
+    float* ws;         // split-colblock partials [ncb][maxsplit][16 batch][128 cols]
+    int* tickets;      // [ncb], self-resetting
     int maxsplit;
 };
 
-__host__ __device__ __forceinline__ int64_t range_begin(int64_t c, int64_t nblk, int64_t grid) {
-    return c * nblk / grid;
-}
-// CTA whose range holds block b.
-__device__ __forceinline__ int64_t range_of(int64_t b, int64_t nblk, int64_t grid) {
-    int64_t c = (b * grid) / nblk;
-    while (c > 0 && range_begin(c, nblk, grid) > b) --c;
-    while (c + 1 < grid && range_begin(c + 1, nblk, grid) <= b) ++c;
+__host__ __device__ __forceinline__ int64_t range_begin(int64_t c, int64_t n, int64_t grid) { return c * n / grid; }
+// CTA whose range holds super-block b.
+__host__ __device__ __forceinline__ int64_t range_of(int64_t b, int64_t n, int64_t grid) {
+    int64_t c = (b * grid) / n;
+    while (c > 0 && range_begin(c, n, grid) > b) --c;
+    while (c + 1 < grid && range_begin(c + 1, n, grid) <= b) ++c;
     return c;
 }
 
@@ -225,24 +230,43 @@ __device__ __forceinline__ void named_sync(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+// Ring-stage geometry (the walk of a CTA's range; producer and consumers
+// compute the same sequence): stage = [sb, sb + cnt) inside one colblock.
+struct StageWalk {
+    int64_t sb, end, kq;
+    __device__ __forceinline__ int next_count() const {
+        const int64_t cb_end = (sb / kq + 1) * kq;
+        return static_cast<int>(min(min(static_cast<int64_t>(kS), end - sb), cb_end - sb));
+    }
+};
+
+// x slice row pitch in shared memory (elements): kS*64 + 16-byte pad
+// (conflict-free LDS.128 across the 8 batch rows of a fragment load).
+template <int XT>
+__host__ __device__ constexpr int xs_pitch() { return kS * 64 + (XT == kF32 ? 4 : 8); }
+template <int XT>
+__host__ __device__ constexpr int xs_bytes(int nbt) { return nbt * xs_pitch<XT>() * (XT == kF32 ? 4 : 2); }
+
 template <int NB, int XT>
-__global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) k_gemv_stream(const GemvArgs a) {
+__global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
     constexpr bool F16 = XT == kF16;
-    constexpr int kChains = NB == 1 ? 4 : 2;
+    constexpr int ES = XT == kF32 ? 4 : 2;       // x element bytes
+    constexpr int NBT = NB * 8;                  // batch rows staged
+    constexpr int XP = xs_pitch<XT>();
+    constexpr int XB = xs_bytes<XT>(NBT);        // x bytes per stage
     extern __shared__ __align__(128) unsigned char smem[];
-    uint4* ring = reinterpret_cast<uint4*>(smem);  // [kRing][kStageBlocks][32]
-    unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + kRing * kStageBlocks * 512);
-    float* red = reinterpret_cast<float*>(bars + 2 * kRing);  // [2][kCW][NB][32][4]
+    unsigned char* codes = smem;                                  // [kRing][kS][4 KB]
+    unsigned char* xsm = smem + kRing * kS * kSBBytes;            // [kRing][NBT][XP]
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(xsm + kRing * XB);
+    int* flag = reinterpret_cast<int*>(bars + 2 * kRing);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t cta = blockIdx.x;
-    const int64_t b0 = range_begin(cta, a.nblk, a.grid), b1 = range_begin(cta + 1, a.nblk, a.grid);
-    const int64_t nb = b1 - b0;
-    const int nst = static_cast<int>((nb + kStageBlocks - 1) / kStageBlocks);
+    const int64_t b0 = range_begin(cta, a.nsb, a.grid), b1 = range_begin(cta + 1, a.nsb, a.grid);
     const unsigned full0 = static_cast<unsigned>(__cvta_generic_to_shared(bars));
     const unsigned empty0 = full0 + 8 * kRing;
     if (threadIdx.x == 0) {
         for (int k = 0; k < kRing; ++k) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full0 + 8 * k));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 33;" ::"r"(full0 + 8 * k));  // tx + 32 cp.async lanes
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * k), "r"(kCW));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -250,155 +274,181 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamCtasPerSm) k_gemv_strea
     __syncthreads();
     asm volatile("griddepcontrol.launch_dependents;");
 
-    if (warp == kCW) {  // ---- producer: one elected lane streams the range
-        if (lane == 0) {
-            const uint4* src = a.T + b0 * 32;
-            for (int k = 0; k < nst; ++k) {
-                const int slot = k % kRing;
-                if (k >= kRing) bar_wait(empty0 + 8 * slot, ((k / kRing) - 1) & 1);
-                const unsigned bytes =
-                    static_cast<unsigned>(min(static_cast<int64_t>(kStageBlocks), nb - k * kStageBlocks)) * 512u;
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full0 + 8 * slot),
-                             "r"(bytes)
-                             : "memory");
+    if (warp == kCW) {  // ---- producer warp: codes by TMA (lane 0), x slices by cp.async (all lanes)
+        StageWalk wk{b0, b1, a.kq};
+        for (int k = 0; wk.sb < b1; ++k) {
+            const int cnt = wk.next_count();
+            const int slot = k % kRing;
+            if (k >= kRing) bar_wait(empty0 + 8 * slot, ((k / kRing) - 1) & 1);
+            const unsigned fb = full0 + 8 * slot;
+            if (lane == 0) {
+                const unsigned bytes = static_cast<unsigned>(cnt) * kSBBytes;
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(bytes) : "memory");
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        static_cast<unsigned>(__cvta_generic_to_shared(ring + slot * kStageBlocks * 32))),
-                    "l"(src + static_cast<int64_t>(k) * kStageBlocks * 32), "r"(bytes), "r"(full0 + 8 * slot)
+                        static_cast<unsigned>(__cvta_generic_to_shared(codes + slot * kS * kSBBytes))),
+                    "l"(a.T + wk.sb * (kSBBytes / 16)), "r"(bytes), "r"(fb)
                     : "memory");
             }
+            // x rows [64 q0, 64 (q0 + cnt)) of each staged batch row, 16-byte granules
+            const int64_t r0 = 64 * (wk.sb % a.kq);
+            const int gpr = cnt * 64 * ES / 16;  // granules per batch row
+            const unsigned xdst = static_cast<unsigned>(__cvta_generic_to_shared(xsm + slot * XB));
+            for (int gi = lane; gi < NBT * gpr; gi += 32) {
+                const int n = gi / gpr, k16 = gi % gpr;
+                const int nn = min(n, a.batch - 1);
+                const char* src = static_cast<const char*>(a.x) + (nn * a.xstride + r0) * ES + 16 * k16;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(xdst + n * XP * ES + 16 * k16), "l"(src)
+                             : "memory");
+            }
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(fb) : "memory");
+            wk.sb += cnt;
         }
         return;
     }
 
-    // ---- consumers
+    // ---- consumers: warp w owns tiles 2w, 2w+1 of every colblock
     const int g = lane >> 2, t = lane & 3;
     const unsigned magic = F16 ? 0x64006400u : 0x43004300u;
     const unsigned off2 = F16 ? static_cast<unsigned>(__half_as_ushort(__int2half_rn(1024 - a.lmin))) * 0x10001u
                               : static_cast<unsigned>(__bfloat16_as_ushort(__int2bfloat16_rn(128 - a.lmin))) * 0x10001u;
-    int nrow[NB];
+    float acc[2][NB][4];
 #pragma unroll
-    for (int n8 = 0; n8 < NB; ++n8) nrow[n8] = min(n8 * 8 + g, a.batch - 1);
-    const int64_t tile_first = b0 / a.kq, tile_last = nb > 0 ? (b1 - 1) / a.kq : tile_first - 1;
-    int tcount = 0;
-    for (int64_t tile = tile_first; tile <= tile_last; ++tile, ++tcount) {
-        const int64_t ta = max(b0, tile * a.kq), tb = min(b1, (tile + 1) * a.kq);  // this CTA's blocks of the tile
-        float acc[kChains][NB][4];
-#pragma unroll
-        for (int h = 0; h < kChains; ++h)
-#pragma unroll
-            for (int n8 = 0; n8 < NB; ++n8)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) acc[h][n8][i] = 0.f;
-        // my blocks: i in [ta, tb) with (i - b0) % kCW == warp
-        int64_t i = ta + ((warp - (ta - b0)) % kCW + kCW) % kCW;
-        XRaw<XT> xc[NB];
-        if (i < tb) {
-#pragma unroll
-            for (int n8 = 0; n8 < NB; ++n8)
-                x_load<XT>(a.x, a.rows, nrow[n8], kBlockRows * (i - tile * a.kq) + 16 * t, xc[n8]);
-        }
-        for (; i < tb; i += kCW) {
-            const int64_t j = i - b0;  // position in the range
-            const int k = static_cast<int>(j / kStageBlocks), slot = k % kRing;
-            bar_wait(full0 + 8 * slot, (k / kRing) & 1);
-            const uint4 w = ring[(slot * kStageBlocks + static_cast<int>(j % kStageBlocks)) * 32 + lane];
-            // release the stage after my last block in it (or my last block)
-            if (j % kStageBlocks >= kStageBlocks - kCW || i + kCW >= b1) {
-                __syncwarp();
-                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * slot) : "memory");
-            }
-            XRaw<XT> xn[NB];
-            if (i + kCW < tb) {
-#pragma unroll
-                for (int n8 = 0; n8 < NB; ++n8)
-                    x_load<XT>(a.x, a.rows, nrow[n8], kBlockRows * (i + kCW - tile * a.kq) + 16 * t, xn[n8]);
-            }
-            const unsigned ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-            for (int s = 0; s < 4; ++s) {
-                unsigned af[4];
-#pragma unroll
-                for (int r = 0; r < 4; ++r) af[r] = sub2<F16>(lop_pair(ws[s], r, magic), off2);
-#pragma unroll
-                for (int n8 = 0; n8 < NB; ++n8) {
-                    unsigned hi[2], lo[2];
-                    x_frag<XT>(xc[n8], s, hi, lo);
-                    mma16816<F16>(acc[s % kChains][n8], af, hi);
-                    if (XT == kF32) mma16816<F16>(acc[s % kChains][n8], af, lo);
-                }
-            }
-#pragma unroll
-            for (int n8 = 0; n8 < NB; ++n8) xc[n8] = xn[n8];
-        }
-        // ---- flush the tile: warps meet in shared memory (fixed order)
-        float* rb = red + (tcount & 1) * (kCW * NB * 32 * 4);
-#pragma unroll
-        for (int n8 = 0; n8 < NB; ++n8) {
-            float v[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                v[q] = acc[0][n8][q];
-#pragma unroll
-                for (int h = 1; h < kChains; ++h) v[q] += acc[h][n8][q];
-            }
-            *reinterpret_cast<float4*>(rb + ((warp * NB + n8) * 32 + lane) * 4) = make_float4(v[0], v[1], v[2], v[3]);
-        }
-        named_sync(1, kCW * 32);
-        if (warp != static_cast<int>(tile % kCW)) continue;
-        float d[NB][4];
-#pragma unroll
-        for (int n8 = 0; n8 < NB; ++n8) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) d[n8][q] = 0.f;
-            for (int w2 = 0; w2 < kCW; ++w2) {
-                const float4 v = *reinterpret_cast<const float4*>(rb + ((w2 * NB + n8) * 32 + lane) * 4);
-                d[n8][0] += v.x, d[n8][1] += v.y, d[n8][2] += v.z, d[n8][3] += v.w;
-            }
-        }
-        const bool whole = ta == tile * a.kq && tb == (tile + 1) * a.kq;
-        if (!whole) {
-            // split tile: partial to the workspace, the last CTA to arrive sums
-            const int64_t c_first = range_of(tile * a.kq, a.nblk, a.grid);
-            const int64_t c_last = range_of((tile + 1) * a.kq - 1, a.nblk, a.grid);
-            const int nsplit = static_cast<int>(c_last - c_first + 1);
-            float* wsl = a.ws + (tile * a.maxsplit + (cta - c_first)) * 256;
-#pragma unroll
-            for (int n8 = 0; n8 < NB; ++n8)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) wsl[(n8 * 32 + lane) * 4 + q] = d[n8][q];
-            __threadfence();
-            __syncwarp();
-            int last = 0;
-            if (lane == 0) last = atomicAdd(a.tickets + tile, 1) == nsplit - 1;
-            last = __shfl_sync(0xffffffffu, last, 0);
-            if (!last) continue;
-            __threadfence();
-            const float* wst = a.ws + tile * a.maxsplit * 256;
-#pragma unroll
-            for (int n8 = 0; n8 < NB; ++n8)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    float sum = 0.f;
-                    for (int sp = 0; sp < nsplit; ++sp) sum += __ldcg(wst + sp * 256 + (n8 * 32 + lane) * 4 + q);
-                    d[n8][q] = sum;
-                }
-            if (lane == 0) a.tickets[tile] = 0;  // ready for the next call
-        }
+    for (int u = 0; u < 2; ++u)
 #pragma unroll
         for (int n8 = 0; n8 < NB; ++n8)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int m = g + (q >= 2 ? 8 : 0);
-                const int n = n8 * 8 + 2 * t + (q & 1);
-                const int64_t jc = tile * kTileCols + m;
-                if (jc < a.cols && n < a.batch) a.y[static_cast<int64_t>(n) * a.cols + jc] = a.scales[jc] * d[n8][q];
+            for (int i = 0; i < 4; ++i) acc[u][n8][i] = 0.f;
+    StageWalk wk{b0, b1, a.kq};
+    int64_t cb_start = b0;  // first super-block of the current colblock in this range
+    for (int k = 0; wk.sb < b1; ++k) {
+        const int cnt = wk.next_count();
+        const int slot = k % kRing;
+        bar_wait(full0 + 8 * slot, (k / kRing) & 1);
+        const uint4* cw = reinterpret_cast<const uint4*>(codes + slot * kS * kSBBytes) + (2 * warp) * 32 + lane;
+        const unsigned char* xw = xsm + slot * XB;
+        for (int s = 0; s < cnt; ++s) {
+            const uint4 w0 = cw[s * (kSBBytes / 16)], w1 = cw[s * (kSBBytes / 16) + 32];
+            XRaw<XT> xr[NB];
+#pragma unroll
+            for (int n8 = 0; n8 < NB; ++n8) {
+                const uint4* xp = reinterpret_cast<const uint4*>(xw + ((n8 * 8 + g) * XP + s * 64 + 16 * t) * ES);
+#pragma unroll
+                for (int i = 0; i < XRaw<XT>::kWords / 4; ++i) {
+                    const uint4 u = xp[i];
+                    xr[n8].w[4 * i] = u.x, xr[n8].w[4 * i + 1] = u.y, xr[n8].w[4 * i + 2] = u.z, xr[n8].w[4 * i + 3] = u.w;
+                }
             }
+            const unsigned ws0[4] = {w0.x, w0.y, w0.z, w0.w}, ws1[4] = {w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+            for (int st = 0; st < 4; ++st) {
+                unsigned af0[4], af1[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    af0[r] = sub2<F16>(lop_pair(ws0[st], r, magic), off2);
+                    af1[r] = sub2<F16>(lop_pair(ws1[st], r, magic), off2);
+                }
+#pragma unroll
+                for (int n8 = 0; n8 < NB; ++n8) {
+                    unsigned hi[2], lo[2];
+                    x_frag<XT>(xr[n8], st, hi, lo);
+                    mma16816<F16>(acc[0][n8], af0, hi);
+                    mma16816<F16>(acc[1][n8], af1, hi);
+                    if (XT == kF32) {
+                        mma16816<F16>(acc[0][n8], af0, lo);
+                        mma16816<F16>(acc[1][n8], af1, lo);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * slot) : "memory");
+        wk.sb += cnt;
+        const int64_t cb = (wk.sb - 1) / a.kq;
+        if (wk.sb < b1 && wk.sb % a.kq != 0) continue;  // colblock continues in this range
+        // ---- flush colblock cb: this warp's 32 columns
+        const bool whole = cb_start == cb * a.kq && wk.sb == (cb + 1) * a.kq;
+        cb_start = wk.sb;
+        int last = 1, nsplit = 1;
+        int64_t c_first = cta;
+        if (!whole) {
+            c_first = range_of(cb * a.kq, a.nsb, a.grid);
+            nsplit = static_cast<int>(range_of((cb + 1) * a.kq - 1, a.nsb, a.grid) - c_first + 1);
+            float* wsl = a.ws + ((cb * a.maxsplit + (cta - c_first)) * 16) * kBM;
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int n8 = 0; n8 < NB; ++n8)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int m = (2 * warp + u) * kTileCols + g + (q >= 2 ? 8 : 0);
+                        const int n = n8 * 8 + 2 * t + (q & 1);
+                        wsl[n * kBM + m] = acc[u][n8][q];
+                    }
+            __threadfence();
+            named_sync(1, kCW * 32);
+            if (threadIdx.x == 0) *flag = atomicAdd(a.tickets + cb, 1) == nsplit - 1;
+            named_sync(1, kCW * 32);
+            last = *flag;
+            named_sync(1, kCW * 32);  // flag read by all before the next colblock reuses it
+            if (last) {
+                __threadfence();
+                const float* wst = a.ws + cb * a.maxsplit * 16 * kBM;
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                    for (int n8 = 0; n8 < NB; ++n8)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int m = (2 * warp + u) * kTileCols + g + (q >= 2 ? 8 : 0);
+                            const int n = n8 * 8 + 2 * t + (q & 1);
+                            float sum = 0.f;
+                            for (int sp = 0; sp < nsplit; ++sp) sum += __ldcg(wst + (sp * 16 + n) * kBM + m);
+                            acc[u][n8][q] = sum;
+                        }
+                if (threadIdx.x == 0) a.tickets[cb] = 0;  // ready for the next call
+            }
+        }
+        if (last) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int n8 = 0; n8 < NB; ++n8)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int64_t jc = cb * kBM + (2 * warp + u) * kTileCols + g + (q >= 2 ? 8 : 0);
+                        const int n = n8 * 8 + 2 * t + (q & 1);
+                        if (jc < a.cols && n < a.batch)
+                            a.y[static_cast<int64_t>(n) * a.cols + jc] = a.scales[jc] * acc[u][n8][q];
+                    }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int n8 = 0; n8 < NB; ++n8)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acc[u][n8][i] = 0.f;
     }
 }
 
-size_t stream_smem(int nb) {
-    return static_cast<size_t>(kRing) * kStageBlocks * 512 + 2 * kRing * 8 + sizeof(float) * 2 * kCW * nb * 32 * 4;
+template <int NB, int XT>
+size_t cb_smem() {
+    return static_cast<size_t>(kRing) * kS * kSBBytes + static_cast<size_t>(kRing) * xs_bytes<XT>(NB * 8) +
+           2 * kRing * 8 + 16;
+}
+
+// x [batch][rows] (any alignment / ragged K) -> xpad [batch][kq * 64] with
+// zeros past `rows`: the main kernel's 16-byte cp.async path needs 64-row
+// multiples and 16-byte aligned rows.
+__global__ void k_gemv_xpad(const void* __restrict__ x, int es, int64_t rows, int64_t prow, int batch,
+                            void* __restrict__ xp) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= prow * batch) return;
+    const int64_t n = i / prow, r = i % prow;
+    if (es == 4)
+        static_cast<float*>(xp)[i] = r < rows ? static_cast<const float*>(x)[n * rows + r] : 0.f;
+    else
+        static_cast<unsigned short*>(xp)[i] = r < rows ? static_cast<const unsigned short*>(x)[n * rows + r] : 0;
 }
 
 // Outlier term: y[n, j] += sum_{e in column j} x[n, row_e] * v_e. One warp
@@ -420,10 +470,19 @@ __global__ void __launch_bounds__(256) k_gemv_xt(const void* __restrict__ x, int
     if (r < rows) xt[r * 16 + n] = n < batch ? load_x(x, xt_type, static_cast<int64_t>(n) * rows + r) : 0.f;
 }
 
-template <int XT, int NBT>
+// Outlier values: f32 (exact), or f16 / bf16 (ezq_gemv_prepare_ex; 6 bytes
+// per outlier instead of 8, held to the GEMV's 1e-3 gate).
+template <int VT>
+__device__ __forceinline__ float load_val(const void* v, int64_t e) {
+    if (VT == 1) return __half2float(static_cast<const __half*>(v)[e]);
+    if (VT == 2) return __uint_as_float(static_cast<unsigned>(static_cast<const unsigned short*>(v)[e]) << 16);
+    return static_cast<const float*>(v)[e];
+}
+
+template <int XT, int NBT, int VT>
 __global__ void __launch_bounds__(256) k_gemv_outliers(int64_t rows, int64_t cols, const int64_t* __restrict__ col_ptr,
                                                        const uint32_t* __restrict__ out_row,
-                                                       const float* __restrict__ out_val, const void* __restrict__ x,
+                                                       const void* __restrict__ out_val, const void* __restrict__ x,
                                                        int batch, float* __restrict__ y,
                                                        const float* __restrict__ xt) {
     constexpr int kU = 4;
@@ -441,7 +500,7 @@ __global__ void __launch_bounds__(256) k_gemv_outliers(int64_t rows, int64_t col
         for (int u = 0; u < kU; ++u) {
             const int64_t e = eb + lane + 32 * u;
             r[u] = e < e1 ? __ldg(out_row + e) : 0u;
-            v[u] = e < e1 ? __ldg(out_val + e) : 0.f;
+            v[u] = e < e1 ? load_val<VT>(out_val, e) : 0.f;
         }
         if (NBT > 8) {  // transposed x: one 16-byte load per 4 batch rows
 #pragma unroll
@@ -481,15 +540,16 @@ __global__ void __launch_bounds__(256) k_gemv_outliers(int64_t rows, int64_t col
     }
 }
 
-// Repack the artifact's codes into the MMA fragment order (layout above).
-// Rows past the end (and columns past the end of the last tile) hold level 0.
+// Repack the artifact's codes into the MMA fragment order (layout above),
+// super-block major: T[cb][q][tile8][lane]. Rows past the end and columns
+// past the end (the last colblock's padding tiles) hold level 0.
 __global__ void k_gemv_repack(const uint8_t* __restrict__ packed, int64_t rows, int64_t cols, int bits,
-                              int64_t kq, int lmin, uint4* __restrict__ T) {
+                              int64_t kq, int64_t ncb, int lmin, uint4* __restrict__ T) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t tiles = (cols + kTileCols - 1) / kTileCols;
-    if (i >= tiles * kq * 32) return;
+    if (i >= ncb * kq * kTilesCB * 32) return;
     const int lane = static_cast<int>(i % 32);
-    const int64_t q = (i / 32) % kq, tile = i / (32 * kq);
+    const int64_t t8 = (i / 32) % kTilesCB, q = (i / (32 * kTilesCB)) % kq, cb = i / (32 * kTilesCB * kq);
+    const int64_t tile = cb * kTilesCB + t8;
     const int g = lane >> 2, t = lane & 3;
     // (column offset, row offset) of nibble slots at bits 0,16,4,20,8,24,12,28
     constexpr int mo[8] = {0, 0, 8, 8, 0, 0, 8, 8};
@@ -521,25 +581,62 @@ __global__ void k_gemv_repack(const uint8_t* __restrict__ packed, int64_t rows, 
 using namespace ezq;
 
 struct ezq_gemv_plan {
-    int64_t rows, cols, kq, tiles;
+    int64_t rows, cols, kq, tiles, ncb;
     int bits, lmin;
-    uint4* T;             // repacked codes (owned)
+    uint4* T;             // repacked codes, super-block major (owned)
     const float* scales;  // device (borrowed from the artifact)
     int64_t* col_ptr;     // CSC of the outliers (owned)
     uint32_t* out_row;
-    float* out_val;
+    void* out_val;        // f32 / f16 / bf16 (vdtype)
+    int vdtype;
     int64_t n_out;
     int dev;
     float* xt;            // batch > 1 with outliers: x transposed [rows][16] f32 (owned)
-    int grid;             // persistent CTAs of k_gemv_stream (block ranges)
-    int maxsplit;         // most ranges one tile is cut into
-    float* ws;            // split-tile partials (owned)
-    int* tickets;         // per tile (owned, self-resetting)
+    void* xpad;           // ragged / unaligned x: padded copy [16][kq * 64] (owned)
+    int grid[6];          // CTAs of k_gemv_cb per (x dtype, NB) variant
+    int maxsplit;         // most ranges one colblock is cut into (over the variants)
+    float* ws;            // split-colblock partials (owned)
+    int* tickets;         // per colblock (owned, self-resetting)
 };
+
+namespace {
+
+template <int NB, int XT>
+int cb_ctas_per_sm() {
+    auto k = k_gemv_cb<NB, XT>;
+    const int smem = static_cast<int>(cb_smem<NB, XT>());
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kStreamThreads, smem) != cudaSuccess || n < 1) n = 1;
+    return n;
+}
+
+template <int XT, int VT>
+cudaError_t launch_outliers_v(cudaLaunchConfig_t& lc, int bt, int64_t rows, int64_t cols, const int64_t* cp,
+                              const uint32_t* orow, const void* oval, const void* xg, float* yg, const float* xtg) {
+    if (bt == 1) return cudaLaunchKernelEx(&lc, k_gemv_outliers<XT, 1, VT>, rows, cols, cp, orow, oval, xg, bt, yg, xtg);
+    if (bt <= 8) return cudaLaunchKernelEx(&lc, k_gemv_outliers<XT, 8, VT>, rows, cols, cp, orow, oval, xg, bt, yg, xtg);
+    return cudaLaunchKernelEx(&lc, k_gemv_outliers<XT, 16, VT>, rows, cols, cp, orow, oval, xg, bt, yg, xtg);
+}
+
+template <int XT>
+cudaError_t launch_outliers(cudaLaunchConfig_t& lc, int vt, int bt, int64_t rows, int64_t cols, const int64_t* cp,
+                            const uint32_t* orow, const void* oval, const void* xg, float* yg, const float* xtg) {
+    if (vt == EZQ_GEMV_OUTLIER_F16) return launch_outliers_v<XT, 1>(lc, bt, rows, cols, cp, orow, oval, xg, yg, xtg);
+    if (vt == EZQ_GEMV_OUTLIER_BF16) return launch_outliers_v<XT, 2>(lc, bt, rows, cols, cp, orow, oval, xg, yg, xtg);
+    return launch_outliers_v<XT, 0>(lc, bt, rows, cols, cp, orow, oval, xg, yg, xtg);
+}
+
+template <int NB, int XT>
+void launch_cb(const GemvArgs& a, cudaStream_t st) {
+    k_gemv_cb<NB, XT><<<static_cast<unsigned>(a.grid), kStreamThreads, cb_smem<NB, XT>(), st>>>(a);
+}
+
+}  // namespace
 
 extern "C" {
 
-int ezq_gemv_prepare(const ezq_qweight* q, void* stream, ezq_gemv_plan** plan) {
+int ezq_gemv_prepare_ex(const ezq_qweight* q, int outlier_dtype, void* stream, ezq_gemv_plan** plan) {
     *plan = nullptr;
     if (q->mem != EZQ_MEM_DEVICE)
         return set_error(EZQ_ERR_INVALID_ARGUMENT, "ezq_gemv needs a device-resident artifact");
@@ -547,6 +644,8 @@ int ezq_gemv_prepare(const ezq_qweight* q, void* stream, ezq_gemv_plan** plan) {
         return set_error(EZQ_ERR_IO_FORMAT, "quantized tensor has empty shape");
     if (q->bits < 2 || q->bits > 4)
         return set_error(EZQ_ERR_INVALID_ARGUMENT, "ezq_gemv supports 2- to 4-bit artifacts");
+    if (outlier_dtype < EZQ_GEMV_OUTLIER_F32 || outlier_dtype > EZQ_GEMV_OUTLIER_BF16)
+        return set_error(EZQ_ERR_INVALID_ARGUMENT, "bad outlier value dtype");
     int dev;
     if (int s = bind_device(&dev)) return s;
     cudaStream_t st = pick_stream(stream, dev);
@@ -572,6 +671,20 @@ int ezq_gemv_prepare(const ezq_qweight* q, void* stream, ezq_gemv_plan** plan) {
             vv[pos[e.col]++] = e.value;
         }
     }
+    const size_t ves = outlier_dtype == EZQ_GEMV_OUTLIER_F32 ? 4 : 2;
+    std::vector<uint16_t> vh;
+    if (ves == 2) {  // round to nearest even, like the device conversions
+        vh.resize(vv.size());
+        for (size_t i = 0; i < vv.size(); ++i) {
+            if (outlier_dtype == EZQ_GEMV_OUTLIER_F16) {
+                const __half h = __float2half_rn(vv[i]);
+                vh[i] = __half_as_ushort(h);
+            } else {
+                const __nv_bfloat16 b = __float2bfloat16_rn(vv[i]);
+                vh[i] = __bfloat16_as_ushort(b);
+            }
+        }
+    }
     auto* p = new ezq_gemv_plan{};
     p->rows = q->rows;
     p->cols = q->cols;
@@ -579,49 +692,62 @@ int ezq_gemv_prepare(const ezq_qweight* q, void* stream, ezq_gemv_plan** plan) {
     p->lmin = -(1 << (q->bits - 1)) + 1;
     p->kq = (q->rows + kBlockRows - 1) / kBlockRows;
     p->tiles = (q->cols + kTileCols - 1) / kTileCols;
+    p->ncb = (p->tiles + kTilesCB - 1) / kTilesCB;
     p->scales = q->scales;
     p->n_out = q->n_outliers;
+    p->vdtype = outlier_dtype;
     p->dev = dev;
-    EZQ_CK(cudaMalloc(&p->T, sizeof(uint4) * p->tiles * p->kq * 32));
+    const int64_t nsb = p->ncb * p->kq;
+    EZQ_CK(cudaMalloc(&p->T, static_cast<size_t>(kSBBytes) * nsb));
     EZQ_CK(cudaMalloc(&p->col_ptr, sizeof(int64_t) * (q->cols + 1)));
     p->xt = nullptr;
     if (q->n_outliers > 0) EZQ_CK(cudaMalloc(&p->xt, sizeof(float) * 16 * static_cast<size_t>(q->rows)));
+    EZQ_CK(cudaMalloc(&p->xpad, sizeof(float) * 16 * static_cast<size_t>(p->kq) * kBlockRows));
     EZQ_CK(cudaMalloc(&p->out_row, sizeof(uint32_t) * std::max<int64_t>(q->n_outliers, 1)));
-    EZQ_CK(cudaMalloc(&p->out_val, sizeof(float) * std::max<int64_t>(q->n_outliers, 1)));
-    // Persistent ranges: kStreamCtasPerSm CTAs per SM, each a contiguous
-    // range of 64-row blocks (never more ranges than blocks).
+    EZQ_CK(cudaMalloc(&p->out_val, ves * std::max<int64_t>(q->n_outliers, 1)));
+    // Persistent ranges: as many CTAs as fit the SMs at once for each
+    // kernel variant (never more ranges than super-blocks).
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t nblk = p->tiles * p->kq;
-    p->grid = static_cast<int>(std::min<int64_t>(nblk, static_cast<int64_t>(sms) * kStreamCtasPerSm));
-    p->maxsplit = 1;
-    for (int64_t tl = 0; tl < p->tiles; ++tl) {  // ranges cutting each tile (host mirror of range_of)
-        auto rng = [&](int64_t b) {
-            int64_t c = (b * p->grid) / nblk;
-            while (c > 0 && range_begin(c, nblk, p->grid) > b) --c;
-            while (c + 1 < p->grid && range_begin(c + 1, nblk, p->grid) <= b) ++c;
-            return c;
-        };
-        p->maxsplit = std::max<int>(p->maxsplit, static_cast<int>(rng((tl + 1) * p->kq - 1) - rng(tl * p->kq) + 1));
+    static thread_local int occ[6] = {0, 0, 0, 0, 0, 0};
+    if (!occ[0]) {
+        occ[0] = cb_ctas_per_sm<1, kF32>();
+        occ[1] = cb_ctas_per_sm<2, kF32>();
+        occ[2] = cb_ctas_per_sm<1, kBF16>();
+        occ[3] = cb_ctas_per_sm<2, kBF16>();
+        occ[4] = cb_ctas_per_sm<1, kF16>();
+        occ[5] = cb_ctas_per_sm<2, kF16>();
     }
-    EZQ_CK(cudaMalloc(&p->ws, sizeof(float) * 256 * static_cast<size_t>(p->tiles) * p->maxsplit));
-    EZQ_CK(cudaMalloc(&p->tickets, sizeof(int) * static_cast<size_t>(p->tiles)));
-    EZQ_CK(cudaMemsetAsync(p->tickets, 0, sizeof(int) * static_cast<size_t>(p->tiles), st));
-    const int64_t nw = p->tiles * p->kq * 32;
-    k_gemv_repack<<<static_cast<unsigned>((nw + 255) / 256), 256, 0, st>>>(q->packed, q->rows, q->cols,
-                                                                         q->bits, p->kq, p->lmin, p->T);
+    p->maxsplit = 1;
+    for (int v = 0; v < 6; ++v) {
+        const int64_t G = std::min<int64_t>(nsb, static_cast<int64_t>(sms) * occ[v]);
+        p->grid[v] = static_cast<int>(G);
+        for (int64_t cb = 0; cb < p->ncb; ++cb)  // ranges cutting each colblock
+            p->maxsplit = std::max<int>(
+                p->maxsplit, static_cast<int>(range_of((cb + 1) * p->kq - 1, nsb, G) - range_of(cb * p->kq, nsb, G) + 1));
+    }
+    EZQ_CK(cudaMalloc(&p->ws, sizeof(float) * 16 * kBM * static_cast<size_t>(p->ncb) * p->maxsplit));
+    EZQ_CK(cudaMalloc(&p->tickets, sizeof(int) * static_cast<size_t>(p->ncb)));
+    EZQ_CK(cudaMemsetAsync(p->tickets, 0, sizeof(int) * static_cast<size_t>(p->ncb), st));
+    const int64_t nw = nsb * kTilesCB * 32;
+    k_gemv_repack<<<static_cast<unsigned>((nw + 255) / 256), 256, 0, st>>>(q->packed, q->rows, q->cols, q->bits,
+                                                                         p->kq, p->ncb, p->lmin, p->T);
     count_launch();
     EZQ_CK(cudaMemcpyAsync(p->col_ptr, ptr.data(), sizeof(int64_t) * (q->cols + 1),
                            cudaMemcpyHostToDevice, st));
     if (q->n_outliers) {
         EZQ_CK(cudaMemcpyAsync(p->out_row, rr.data(), sizeof(uint32_t) * q->n_outliers,
                                cudaMemcpyHostToDevice, st));
-        EZQ_CK(cudaMemcpyAsync(p->out_val, vv.data(), sizeof(float) * q->n_outliers,
-                               cudaMemcpyHostToDevice, st));
+        EZQ_CK(cudaMemcpyAsync(p->out_val, ves == 4 ? static_cast<const void*>(vv.data()) : vh.data(),
+                               ves * q->n_outliers, cudaMemcpyHostToDevice, st));
     }
     EZQ_CK(cudaStreamSynchronize(st));
     *plan = p;
     return clear_error();
+}
+
+int ezq_gemv_prepare(const ezq_qweight* q, void* stream, ezq_gemv_plan** plan) {
+    return ezq_gemv_prepare_ex(q, EZQ_GEMV_OUTLIER_F32, stream, plan);
 }
 
 int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, float* y,
@@ -636,8 +762,7 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
     GemvArgs a{};
     a.T = p->T;
     a.kq = p->kq;
-    a.nblk = p->tiles * p->kq;
-    a.grid = p->grid;
+    a.nsb = p->ncb * p->kq;
     a.ws = p->ws;
     a.tickets = p->tickets;
     a.maxsplit = p->maxsplit;
@@ -646,28 +771,43 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
     a.lmin = p->lmin;
     a.scales = p->scales;
     const size_t xes = x_dtype == kF32 ? 4 : 2;
+    // The main kernel stages x slices with 16-byte cp.async: 64-row multiples
+    // and 16-byte aligned rows, else a zero-padded copy first.
+    const bool direct = p->rows % kBlockRows == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
     // One launch per group of 16 batch rows (two n8 MMA tiles share the A
     // fragments); a group of <= 8 uses one n8 tile. The outlier pass is a
     // programmatic dependent launch (its gathers overlap the weight stream).
     for (int b0 = 0; b0 < batch; b0 += kMaxGroup) {
         a.batch = std::min(batch - b0, kMaxGroup);
-        a.x = static_cast<const char*>(x) + xes * static_cast<size_t>(b0) * p->rows;
+        const void* xg = static_cast<const char*>(x) + xes * static_cast<size_t>(b0) * p->rows;
         a.y = y + static_cast<int64_t>(b0) * p->cols;
+        if (direct) {
+            a.x = xg;
+            a.xstride = p->rows;
+        } else {
+            const int64_t prow = p->kq * kBlockRows;
+            const int64_t tot = prow * a.batch;
+            k_gemv_xpad<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(xg, static_cast<int>(xes), p->rows,
+                                                                               prow, a.batch, p->xpad);
+            count_launch();
+            a.x = p->xpad;
+            a.xstride = prow;
+        }
         const bool two = a.batch > 8;
         if (p->n_out && a.batch > 8) {  // transposed x for the outlier pass (pays off from 9 batch rows)
-            k_gemv_xt<<<static_cast<unsigned>((p->rows + 15) / 16), 256, 0, st>>>(a.x, x_dtype, p->rows, a.batch,
+            k_gemv_xt<<<static_cast<unsigned>((p->rows + 15) / 16), 256, 0, st>>>(xg, x_dtype, p->rows, a.batch,
                                                                                   p->xt);
             count_launch();
         }
-        const unsigned grid = static_cast<unsigned>(p->grid);
-        const size_t smem = stream_smem(two ? 2 : 1);
-        switch (x_dtype * 2 + (two ? 1 : 0)) {
-            case 0: k_gemv_stream<1, kF32><<<grid, kStreamThreads, smem, st>>>(a); break;
-            case 1: k_gemv_stream<2, kF32><<<grid, kStreamThreads, smem, st>>>(a); break;
-            case 2: k_gemv_stream<1, kBF16><<<grid, kStreamThreads, smem, st>>>(a); break;
-            case 3: k_gemv_stream<2, kBF16><<<grid, kStreamThreads, smem, st>>>(a); break;
-            case 4: k_gemv_stream<1, kF16><<<grid, kStreamThreads, smem, st>>>(a); break;
-            default: k_gemv_stream<2, kF16><<<grid, kStreamThreads, smem, st>>>(a); break;
+        const int v = x_dtype * 2 + (two ? 1 : 0);
+        a.grid = p->grid[v];
+        switch (v) {
+            case 0: launch_cb<1, kF32>(a, st); break;
+            case 1: launch_cb<2, kF32>(a, st); break;
+            case 2: launch_cb<1, kBF16>(a, st); break;
+            case 3: launch_cb<2, kBF16>(a, st); break;
+            case 4: launch_cb<1, kF16>(a, st); break;
+            default: launch_cb<2, kF16>(a, st); break;
         }
         count_launch();
         if (p->n_out) {
@@ -682,28 +822,23 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
             lc.numAttrs = 1;
             const int64_t* cp = p->col_ptr;
             const uint32_t* orow = p->out_row;
-            const float* oval = p->out_val;
-            const void* xg = a.x;
+            const void* oval = p->out_val;
             float* yg = a.y;
             const int bt = a.batch;
             const float* xtg = p->xt;
             cudaError_t e;
-#define EZQ_OUT(X)                                                                                     \
-    (bt == 1 ? cudaLaunchKernelEx(&lc, k_gemv_outliers<X, 1>, p->rows, p->cols, cp, orow, oval, xg, bt, yg, xtg) \
-     : bt <= 8 ? cudaLaunchKernelEx(&lc, k_gemv_outliers<X, 8>, p->rows, p->cols, cp, orow, oval, xg, bt, yg, xtg) \
-               : cudaLaunchKernelEx(&lc, k_gemv_outliers<X, 16>, p->rows, p->cols, cp, orow, oval, xg, bt, yg, xtg))
-            if (x_dtype == kF32) e = EZQ_OUT(kF32);
-            else if (x_dtype == kBF16) e = EZQ_OUT(kBF16);
-            else e = EZQ_OUT(kF16);
-#undef EZQ_OUT
+            if (x_dtype == kF32) e = launch_outliers<kF32>(lc, p->vdtype, bt, p->rows, p->cols, cp, orow, oval, xg, yg, xtg);
+            else if (x_dtype == kBF16) e = launch_outliers<kBF16>(lc, p->vdtype, bt, p->rows, p->cols, cp, orow, oval, xg, yg, xtg);
+            else e = launch_outliers<kF16>(lc, p->vdtype, bt, p->rows, p->cols, cp, orow, oval, xg, yg, xtg);
             EZQ_CK(e);
             count_launch();
         }
     }
     // Algorithmic bytes: the 4-bit codes (the repacked copy has the same
     // size as the artifact's nibbles), scales, CSC, x and y.
+    const double vbytes = p->vdtype == EZQ_GEMV_OUTLIER_F32 ? 4.0 : 2.0;
     const double bytes = static_cast<double>(p->rows * p->cols + 1) / 2 + 4.0 * p->cols +
-                         8.0 * p->n_out + 8.0 * (p->cols + 1) +
+                         (4.0 + vbytes) * p->n_out + 8.0 * (p->cols + 1) +
                          batch * p->rows * static_cast<double>(xes) + 4.0 * batch * p->cols;
     prof_end(pt, st, bytes);
     EZQ_CK(cudaGetLastError());
@@ -715,6 +850,7 @@ void ezq_gemv_plan_free(ezq_gemv_plan* p) {
     cudaFree(p->T);
     cudaFree(p->col_ptr);
     if (p->xt) cudaFree(p->xt);
+    cudaFree(p->xpad);
     cudaFree(p->out_row);
     cudaFree(p->out_val);
     cudaFree(p->ws);

@@ -213,6 +213,7 @@ def lib() -> C.CDLL:
         L.ezq_unpack_levels.argtypes = [P, I64, I64, I32, P]
         L.ezq_dequantize_channel.argtypes = [P, I64, D, P]
         L.ezq_gemv_prepare.argtypes = [C.POINTER(CQWeight), P, C.POINTER(P)]
+        L.ezq_gemv_prepare_ex.argtypes = [C.POINTER(CQWeight), I32, P, C.POINTER(P)]
         L.ezq_gemv.argtypes = [P, P, I32, I32, P, P]
         L.ezq_gemv_plan_free.argtypes = [P]
         L.ezq_profile_enable.argtypes = [I32]
@@ -448,12 +449,14 @@ class GemvPlan:
     DeviceBatch entry). x: torch CUDA tensor [batch, rows] (f32/bf16/f16)."""
 
     DTYPES = {"torch.float32": 0, "torch.bfloat16": 1, "torch.float16": 2}
+    OUTLIER_DTYPES = {"float32": 0, "float16": 1, "bfloat16": 2}
 
-    def __init__(self, batch: "DeviceBatch", i: int, stream=None):
+    def __init__(self, batch: "DeviceBatch", i: int, stream=None, outlier_dtype: str = "float32"):
         self._keep = batch
         self.rows, self.cols = batch[i].rows, batch[i].cols
         self.p = C.c_void_p()
-        check(lib().ezq_gemv_prepare(batch.ptrs[i], _stream(stream), C.byref(self.p)))
+        check(lib().ezq_gemv_prepare_ex(batch.ptrs[i], self.OUTLIER_DTYPES[outlier_dtype], _stream(stream),
+                                        C.byref(self.p)))
         self.stream = stream
 
     def __call__(self, x, y=None, stream=None):

@@ -12,12 +12,26 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("rows,cols,sigma,bits", [
     (4096, 4096, 3.0, 4), (512, 1024, 2.5758, 4), (1024, 264, 2.8070, 4),
+    (4096, 11008, 2.5758, 4), (11008, 4096, 2.5758, 4),  # the benched LLaMA-7B shapes
     (300, 77, 3.0, 4),      # generic path (odd cols)
     (256, 128, 3.0, 3),     # k=3 byte-per-level codes
 ])
 @pytest.mark.parametrize("batch", [1, 2, 5, 8, 16, 21])
 @pytest.mark.parametrize("dtype", ["float32", "bfloat16", "float16"])
 def test_gemv_matches_dequant_f64(gpu, O, rows, cols, sigma, bits, batch, dtype):
+    _gemv_case(gpu, O, rows, cols, sigma, bits, batch, dtype, "float32")
+
+
+@pytest.mark.parametrize("rows,cols", [(4096, 11008), (1000, 200), (2048, 520)])
+@pytest.mark.parametrize("batch", [1, 9])
+@pytest.mark.parametrize("odt", ["float16", "bfloat16"])
+def test_gemv_half_outlier_values(gpu, O, rows, cols, batch, odt):
+    """N1: outlier values stored as f16 / bf16 (6 bytes per outlier) stay
+    within the 1e-3 gate against dequantize + the fp64 GEMV."""
+    _gemv_case(gpu, O, rows, cols, 2.5758, 4, batch, "bfloat16", odt)
+
+
+def _gemv_case(gpu, O, rows, cols, sigma, bits, batch, dtype, odt):
     import torch
     W = O.gaussian(rows, cols, rows + cols, 0.02)
     O.plant_outliers(W, max(1, W.size // 200), 0.2, 1.0, 77)
@@ -25,7 +39,7 @@ def test_gemv_matches_dequant_f64(gpu, O, rows, cols, sigma, bits, batch, dtype)
     b = gpu.quantize_batch([Wd], Config(bits=bits, sigma_n=sigma, steps=20), out_mem=gpu.MEM_DEVICE)
     q = b.to_host(0)
     What = gpu.dequantize(q)
-    plan = gpu.GemvPlan(b, 0)
+    plan = gpu.GemvPlan(b, 0, outlier_dtype=odt)
     g = torch.Generator(device="cuda").manual_seed(batch)
     x = torch.randn(batch, rows, generator=g, device="cuda").to(getattr(torch, dtype))
     y = plan(x).cpu().numpy().astype(np.float64)

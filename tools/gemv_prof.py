@@ -26,13 +26,14 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--dtype", default="bfloat16")
     ap.add_argument("--plain", action="store_true", help="no graph: launch a few times (for ncu)")
+    ap.add_argument("--odt", default="float32", help="outlier value dtype (float32 / float16 / bfloat16)")
     a = ap.parse_args()
     gen = torch.Generator(device="cuda").manual_seed(99)
     r, c = a.rows, a.cols
     dense = [(torch.randn(r, c, generator=gen, device="cuda") * 0.02) for _ in range(a.copies)]
     for ratio in a.ratio:
         b = N.quantize_batch(dense, Config(sigma_n=SIG[ratio]), "outliers-only", out_mem=N.MEM_DEVICE)
-        plans = [N.GemvPlan(b, i) for i in range(a.copies)]
+        plans = [N.GemvPlan(b, i, outlier_dtype=a.odt) for i in range(a.copies)]
         n_out = sum(b[i].n_outliers for i in range(a.copies)) / a.copies
         for B in a.batch:
             x = torch.randn(B, r, generator=gen, device="cuda").to(getattr(torch, a.dtype))
@@ -62,7 +63,8 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             us = e0.elapsed_time(e1) / a.reps / a.copies * 1e3
-            nbytes = r * c / 2 + 4 * c + 8 * n_out + 8 * (c + 1) + x.element_size() * B * r + 4 * B * c
+            vb = 8 if a.odt == "float32" else 6
+            nbytes = r * c / 2 + 4 * c + vb * n_out + 8 * (c + 1) + x.element_size() * B * r + 4 * B * c
             print(f"{r}x{c} B={B} ratio={ratio} n_out={n_out:.0f}: {us:.2f} us  {nbytes / us / 1e3:.0f} GB/s")
         for p in plans:
             p.close()
