@@ -48,6 +48,8 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "runtime.hpp"
@@ -719,8 +721,13 @@ int ezq_gemv_prepare_ex(const ezq_qweight* q, int outlier_dtype, void* stream, e
         occ[5] = cb_ctas_per_sm<2, kF16>();
     }
     p->maxsplit = 1;
+    static const int cap = std::getenv("EZQ_GEMV_CTAS") ? std::atoi(std::getenv("EZQ_GEMV_CTAS")) : 0;  // tuning aid
+    static const bool dbg = std::getenv("EZQ_GEMV_DEBUG") != nullptr;
     for (int v = 0; v < 6; ++v) {
-        const int64_t G = std::min<int64_t>(nsb, static_cast<int64_t>(sms) * occ[v]);
+        const int per_sm = cap > 0 ? std::min(cap, occ[v]) : occ[v];
+        const int64_t G = std::min<int64_t>(nsb, static_cast<int64_t>(sms) * per_sm);
+        if (dbg) std::fprintf(stderr, "ezq_gemv_prepare: variant %d ctas/sm %d grid %lld nsb %lld\n", v, occ[v],
+                              static_cast<long long>(G), static_cast<long long>(nsb));
         p->grid[v] = static_cast<int>(G);
         for (int64_t cb = 0; cb < p->ncb; ++cb)  // ranges cutting each colblock
             p->maxsplit = std::max<int>(
