@@ -50,6 +50,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "runtime.hpp"
@@ -168,56 +169,38 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const unsigned (&a)[4], 
 }
 
 // ---- K6 main kernel: column-block skinny GEMM, persistent, TMA-fed ----------
-// Output columns go in blocks of kBM = 128 (8 MMA tiles); the artifact is
-// repacked as super-blocks (colblock, q) of 8 tiles x 64 rows = 4 KB, stored
-// T[cb][q][tile8][lane] so every run of super-blocks in (cb, q) order is one
-// contiguous byte range. Each CTA owns a contiguous range of ~nsb/grid
-// super-blocks and streams it through a ring of kRing stages of up to kS
-// super-blocks of ONE colblock: the codes by one cp.async.bulk (TMA) per
-// stage, the matching x slice (kS x 64 rows x batch) by cp.async 16-byte
-// copies from the producer warp's 32 lanes, both completing on the stage's
-// mbarrier. ~50-100 KB in flight per SM -- what an HBM-latency-bound stream
-// needs (Little's law: ~5 MB in flight GPU-wide at 6.5 TB/s) -- without
-// holding it in registers, and the x slice is loaded once per CTA per q for
-// all 128 columns. Each of the kCW = 4 consumer warps owns 2 of the 8 tiles
-// across the whole range (no cross-warp reduction): per super-block two
-// LDS.128 of codes, the x fragments from shared memory, dequantize to exact
-// levels, MMA. A colblock cut by a range boundary is split across CTAs: each
-// writes its partial to a workspace and the last to arrive (ticket) sums the
-// partials in CTA order -- deterministic, bit-identical across calls.
+// Output columns go in colblocks of TPC MMA tiles (16 x TPC columns; TPC in
+// {1, 2, 4, 8} chosen per shape by ezq_gemv_prepare so the colblocks fill
+// the SMs); the artifact is repacked T[cb][q][tile][lane] (uint4), so a
+// colblock's whole K is one contiguous byte range. A persistent CTA takes
+// colblocks cb = blockIdx.x, + gridDim.x, ... and streams each through a
+// ring of kRing stages of S q-blocks (8 KB of codes, one cp.async.bulk), the
+// stage's x slice (S x 64 rows x the batch rows) arriving by 16-byte cp.async
+// from the producer warp's lanes on the same mbarrier: tens of KB in flight
+// per CTA without holding them in registers, and every x slice is read once
+// per colblock. Each colblock's K is complete inside the CTA -- no
+// cross-CTA reduction. The kCW = 4 consumer warps split a stage's (q, tile)
+// blocks: with TPC >= 4 warp w owns tiles w, w + 4, ... over all of K (no
+// reduction at all); with TPC < 4 the 4 / TPC warps of a tile split its q
+// blocks and meet in shared memory at the end of the colblock (fixed order:
+// deterministic, bit-identical across calls).
 constexpr int kCW = 4;             // consumer warps per CTA
-constexpr int kBM = 128;           // columns per colblock
-constexpr int kTilesCB = kBM / kTileCols;  // 8
-constexpr int kSBBytes = kTilesCB * 512;   // 4 KB of codes per super-block
-constexpr int kS = 4;              // super-blocks per ring stage
 constexpr int kRing = 3;           // ring stages per CTA
+constexpr int kStageCode = 8192;   // code bytes per full stage
 constexpr int kStreamThreads = (kCW + 1) * 32;
 
 struct GemvArgs {
     const uint4* T;
     int64_t kq;    // 64-row blocks (K)
-    int64_t nsb;   // colblocks * kq
-    int grid;      // CTAs (ranges)
+    int64_t ncb;   // colblocks
     int64_t rows, cols;
     int lmin;
     const float* scales;
-    const void* x;     // [batch][rows], rows % 64 == 0 and 16-byte aligned rows (else a padded copy)
+    const void* x;     // [batch][xstride], 64-row multiples, 16-byte aligned rows (else a padded copy)
     int64_t xstride;   // elements between batch rows of x
     int batch;         // rows of this group (1..16)
     float* y;
-    float* ws;         // split-colblock partials [ncb][maxsplit][16 batch][128 cols]
-    int* tickets;      // [ncb], self-resetting
-    int maxsplit;
 };
-
-__host__ __device__ __forceinline__ int64_t range_begin(int64_t c, int64_t n, int64_t grid) { return c * n / grid; }
-// CTA whose range holds super-block b.
-__host__ __device__ __forceinline__ int64_t range_of(int64_t b, int64_t n, int64_t grid) {
-    int64_t c = (b * grid) / n;
-    while (c > 0 && range_begin(c, n, grid) > b) --c;
-    while (c + 1 < grid && range_begin(c + 1, n, grid) <= b) ++c;
-    return c;
-}
 
 __device__ __forceinline__ void bar_wait(unsigned bar, unsigned phase) {
     unsigned ok = 0;
@@ -232,38 +215,36 @@ __device__ __forceinline__ void named_sync(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-// Ring-stage geometry (the walk of a CTA's range; producer and consumers
-// compute the same sequence): stage = [sb, sb + cnt) inside one colblock.
-struct StageWalk {
-    int64_t sb, end, kq;
-    __device__ __forceinline__ int next_count() const {
-        const int64_t cb_end = (sb / kq + 1) * kq;
-        return static_cast<int>(min(min(static_cast<int64_t>(kS), end - sb), cb_end - sb));
+template <int TPC, int NB, int XT>
+struct CbGeom {
+    static constexpr int ES = XT == kF32 ? 4 : 2;                     // x element bytes
+    static constexpr int NBT = NB * 8;                                // batch rows staged
+    static constexpr int XQ = 64 * NBT * ES;                          // x bytes per q-block
+    static constexpr int S0 = kStageCode / (512 * TPC);               // q-blocks per stage (codes)
+    static constexpr int S = S0 < 16384 / XQ ? S0 : 16384 / XQ;       // ... capped by <= 16 KB of x
+    static constexpr int XP = S * 64 + (XT == kF32 ? 4 : 8);          // x row pitch (elements, padded)
+    static constexpr int XB = NBT * XP * ES;                          // x bytes per stage
+    static constexpr int CB = S * TPC * 512;                          // code bytes per stage
+    static constexpr int TW = TPC >= kCW ? TPC / kCW : 1;             // tiles per warp
+    static constexpr int QW = TPC >= kCW ? 1 : kCW / TPC;             // warps sharing a tile
+    static constexpr size_t smem() {
+        return static_cast<size_t>(kRing) * (CB + XB) + 2 * kRing * 8 +
+               (QW > 1 ? static_cast<size_t>(kCW) * NB * 32 * 4 * sizeof(float) : 0) + 16;
     }
 };
 
-// x slice row pitch in shared memory (elements): kS*64 + 16-byte pad
-// (conflict-free LDS.128 across the 8 batch rows of a fragment load).
-template <int XT>
-__host__ __device__ constexpr int xs_pitch() { return kS * 64 + (XT == kF32 ? 4 : 8); }
-template <int XT>
-__host__ __device__ constexpr int xs_bytes(int nbt) { return nbt * xs_pitch<XT>() * (XT == kF32 ? 4 : 2); }
-
-template <int NB, int XT>
+template <int TPC, int NB, int XT>
 __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
+    using Gm = CbGeom<TPC, NB, XT>;
     constexpr bool F16 = XT == kF16;
-    constexpr int ES = XT == kF32 ? 4 : 2;       // x element bytes
-    constexpr int NBT = NB * 8;                  // batch rows staged
-    constexpr int XP = xs_pitch<XT>();
-    constexpr int XB = xs_bytes<XT>(NBT);        // x bytes per stage
+    constexpr int ES = Gm::ES, NBT = Gm::NBT, S = Gm::S, XP = Gm::XP, XB = Gm::XB, CB = Gm::CB;
+    constexpr int TW = Gm::TW, QW = Gm::QW;
     extern __shared__ __align__(128) unsigned char smem[];
-    unsigned char* codes = smem;                                  // [kRing][kS][4 KB]
-    unsigned char* xsm = smem + kRing * kS * kSBBytes;            // [kRing][NBT][XP]
+    unsigned char* codes = smem;                     // [kRing][S][TPC][512]
+    unsigned char* xsm = smem + kRing * CB;          // [kRing][NBT][XP]
     unsigned long long* bars = reinterpret_cast<unsigned long long*>(xsm + kRing * XB);
-    int* flag = reinterpret_cast<int*>(bars + 2 * kRing);
+    float* red = reinterpret_cast<float*>(bars + 2 * kRing);  // [kCW][NB][32][4] (QW > 1)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t cta = blockIdx.x;
-    const int64_t b0 = range_begin(cta, a.nsb, a.grid), b1 = range_begin(cta + 1, a.nsb, a.grid);
     const unsigned full0 = static_cast<unsigned>(__cvta_generic_to_shared(bars));
     const unsigned empty0 = full0 + 8 * kRing;
     if (threadIdx.x == 0) {
@@ -275,168 +256,150 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
     }
     __syncthreads();
     asm volatile("griddepcontrol.launch_dependents;");
+    const int64_t nst_cb = (a.kq + S - 1) / S;  // stages per colblock
 
     if (warp == kCW) {  // ---- producer warp: codes by TMA (lane 0), x slices by cp.async (all lanes)
-        StageWalk wk{b0, b1, a.kq};
-        for (int k = 0; wk.sb < b1; ++k) {
-            const int cnt = wk.next_count();
-            const int slot = k % kRing;
-            if (k >= kRing) bar_wait(empty0 + 8 * slot, ((k / kRing) - 1) & 1);
-            const unsigned fb = full0 + 8 * slot;
-            if (lane == 0) {
-                const unsigned bytes = static_cast<unsigned>(cnt) * kSBBytes;
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(bytes) : "memory");
-                asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                        static_cast<unsigned>(__cvta_generic_to_shared(codes + slot * kS * kSBBytes))),
-                    "l"(a.T + wk.sb * (kSBBytes / 16)), "r"(bytes), "r"(fb)
-                    : "memory");
+        int k = 0;
+        for (int64_t cb = blockIdx.x; cb < a.ncb; cb += gridDim.x) {
+            for (int64_t sq = 0; sq < nst_cb; ++sq, ++k) {
+                const int64_t q0 = sq * S;
+                const int cnt = static_cast<int>(min(static_cast<int64_t>(S), a.kq - q0));
+                const int slot = k % kRing;
+                if (k >= kRing) bar_wait(empty0 + 8 * slot, ((k / kRing) - 1) & 1);
+                const unsigned fb = full0 + 8 * slot;
+                if (lane == 0) {
+                    const unsigned bytes = static_cast<unsigned>(cnt) * TPC * 512u;
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(bytes) : "memory");
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            static_cast<unsigned>(__cvta_generic_to_shared(codes + slot * CB))),
+                        "l"(a.T + (cb * a.kq + q0) * TPC * 32), "r"(bytes), "r"(fb)
+                        : "memory");
+                }
+                const int gpr = cnt * 64 * ES / 16;  // 16-byte granules per batch row
+                const unsigned xdst = static_cast<unsigned>(__cvta_generic_to_shared(xsm + slot * XB));
+                for (int gi = lane; gi < NBT * gpr; gi += 32) {
+                    const int n = gi / gpr, k16 = gi - n * gpr;
+                    const int nn = min(n, a.batch - 1);
+                    const char* src = static_cast<const char*>(a.x) + (nn * a.xstride + 64 * q0) * ES + 16 * k16;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(xdst + n * XP * ES + 16 * k16),
+                                 "l"(src)
+                                 : "memory");
+                }
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(fb) : "memory");
             }
-            // x rows [64 q0, 64 (q0 + cnt)) of each staged batch row, 16-byte granules
-            const int64_t r0 = 64 * (wk.sb % a.kq);
-            const int gpr = cnt * 64 * ES / 16;  // granules per batch row
-            const unsigned xdst = static_cast<unsigned>(__cvta_generic_to_shared(xsm + slot * XB));
-            for (int gi = lane; gi < NBT * gpr; gi += 32) {
-                const int n = gi / gpr, k16 = gi % gpr;
-                const int nn = min(n, a.batch - 1);
-                const char* src = static_cast<const char*>(a.x) + (nn * a.xstride + r0) * ES + 16 * k16;
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(xdst + n * XP * ES + 16 * k16), "l"(src)
-                             : "memory");
-            }
-            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(fb) : "memory");
-            wk.sb += cnt;
         }
         return;
     }
 
-    // ---- consumers: warp w owns tiles 2w, 2w+1 of every colblock
+    // ---- consumers
     const int g = lane >> 2, t = lane & 3;
     const unsigned magic = F16 ? 0x64006400u : 0x43004300u;
     const unsigned off2 = F16 ? static_cast<unsigned>(__half_as_ushort(__int2half_rn(1024 - a.lmin))) * 0x10001u
                               : static_cast<unsigned>(__bfloat16_as_ushort(__int2bfloat16_rn(128 - a.lmin))) * 0x10001u;
-    float acc[2][NB][4];
+    // my tiles: TPC >= 4: w, w + 4, ...; else tile w % TPC on q-blocks s = w / TPC (mod QW)
+    const int tile0 = TPC >= kCW ? warp : warp % TPC;
+    const int qoff = TPC >= kCW ? 0 : warp / TPC;
+    int k = 0;
+    for (int64_t cb = blockIdx.x; cb < a.ncb; cb += gridDim.x) {
+        float acc[TW][2][NB][4];  // two accumulator sets per tile (alternating q) break the MMA chain
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
+        for (int u = 0; u < TW; ++u)
 #pragma unroll
-        for (int n8 = 0; n8 < NB; ++n8)
+            for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) acc[u][n8][i] = 0.f;
-    StageWalk wk{b0, b1, a.kq};
-    int64_t cb_start = b0;  // first super-block of the current colblock in this range
-    for (int k = 0; wk.sb < b1; ++k) {
-        const int cnt = wk.next_count();
-        const int slot = k % kRing;
-        bar_wait(full0 + 8 * slot, (k / kRing) & 1);
-        const uint4* cw = reinterpret_cast<const uint4*>(codes + slot * kS * kSBBytes) + (2 * warp) * 32 + lane;
-        const unsigned char* xw = xsm + slot * XB;
-        for (int s = 0; s < cnt; ++s) {
-            const uint4 w0 = cw[s * (kSBBytes / 16)], w1 = cw[s * (kSBBytes / 16) + 32];
-            XRaw<XT> xr[NB];
+                for (int n8 = 0; n8 < NB; ++n8)
 #pragma unroll
-            for (int n8 = 0; n8 < NB; ++n8) {
-                const uint4* xp = reinterpret_cast<const uint4*>(xw + ((n8 * 8 + g) * XP + s * 64 + 16 * t) * ES);
-#pragma unroll
-                for (int i = 0; i < XRaw<XT>::kWords / 4; ++i) {
-                    const uint4 u = xp[i];
-                    xr[n8].w[4 * i] = u.x, xr[n8].w[4 * i + 1] = u.y, xr[n8].w[4 * i + 2] = u.z, xr[n8].w[4 * i + 3] = u.w;
-                }
-            }
-            const unsigned ws0[4] = {w0.x, w0.y, w0.z, w0.w}, ws1[4] = {w1.x, w1.y, w1.z, w1.w};
-#pragma unroll
-            for (int st = 0; st < 4; ++st) {
-                unsigned af0[4], af1[4];
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    af0[r] = sub2<F16>(lop_pair(ws0[st], r, magic), off2);
-                    af1[r] = sub2<F16>(lop_pair(ws1[st], r, magic), off2);
-                }
+                    for (int i = 0; i < 4; ++i) acc[u][h][n8][i] = 0.f;
+        for (int64_t sq = 0; sq < nst_cb; ++sq, ++k) {
+            const int cnt = static_cast<int>(min(static_cast<int64_t>(S), a.kq - sq * S));
+            const int slot = k % kRing;
+            bar_wait(full0 + 8 * slot, (k / kRing) & 1);
+            const uint4* cw = reinterpret_cast<const uint4*>(codes + slot * CB);
+            const unsigned char* xw = xsm + slot * XB;
+            for (int s = qoff; s < cnt; s += QW) {
+                XRaw<XT> xr[NB];
 #pragma unroll
                 for (int n8 = 0; n8 < NB; ++n8) {
-                    unsigned hi[2], lo[2];
-                    x_frag<XT>(xr[n8], st, hi, lo);
-                    mma16816<F16>(acc[0][n8], af0, hi);
-                    mma16816<F16>(acc[1][n8], af1, hi);
-                    if (XT == kF32) {
-                        mma16816<F16>(acc[0][n8], af0, lo);
-                        mma16816<F16>(acc[1][n8], af1, lo);
+                    const uint4* xp = reinterpret_cast<const uint4*>(xw + ((n8 * 8 + g) * XP + s * 64 + 16 * t) * ES);
+#pragma unroll
+                    for (int i = 0; i < XRaw<XT>::kWords / 4; ++i) {
+                        const uint4 u4 = xp[i];
+                        xr[n8].w[4 * i] = u4.x, xr[n8].w[4 * i + 1] = u4.y, xr[n8].w[4 * i + 2] = u4.z,
+                                      xr[n8].w[4 * i + 3] = u4.w;
+                    }
+                }
+                const int h = (s / QW) & 1;
+#pragma unroll
+                for (int u = 0; u < TW; ++u) {
+                    const uint4 w = cw[(s * TPC + tile0 + u * kCW) * 32 + lane];
+                    const unsigned ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                    for (int st = 0; st < 4; ++st) {
+                        unsigned af[4];
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) af[r] = sub2<F16>(lop_pair(ws[st], r, magic), off2);
+#pragma unroll
+                        for (int n8 = 0; n8 < NB; ++n8) {
+                            unsigned hi[2], lo[2];
+                            x_frag<XT>(xr[n8], st, hi, lo);
+                            if (h) {
+                                mma16816<F16>(acc[u][1][n8], af, hi);
+                                if (XT == kF32) mma16816<F16>(acc[u][1][n8], af, lo);
+                            } else {
+                                mma16816<F16>(acc[u][0][n8], af, hi);
+                                if (XT == kF32) mma16816<F16>(acc[u][0][n8], af, lo);
+                            }
+                        }
                     }
                 }
             }
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * slot) : "memory");
         }
-        __syncwarp();
-        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * slot) : "memory");
-        wk.sb += cnt;
-        const int64_t cb = (wk.sb - 1) / a.kq;
-        if (wk.sb < b1 && wk.sb % a.kq != 0) continue;  // colblock continues in this range
-        // ---- flush colblock cb: this warp's 32 columns
-        const bool whole = cb_start == cb * a.kq && wk.sb == (cb + 1) * a.kq;
-        cb_start = wk.sb;
-        int last = 1, nsplit = 1;
-        int64_t c_first = cta;
-        if (!whole) {
-            c_first = range_of(cb * a.kq, a.nsb, a.grid);
-            nsplit = static_cast<int>(range_of((cb + 1) * a.kq - 1, a.nsb, a.grid) - c_first + 1);
-            float* wsl = a.ws + ((cb * a.maxsplit + (cta - c_first)) * 16) * kBM;
+        // ---- colblock done: (QW > 1) the warps of a tile meet in shared memory
+        float d[TW][NB][4];
 #pragma unroll
-            for (int u = 0; u < 2; ++u)
-#pragma unroll
-                for (int n8 = 0; n8 < NB; ++n8)
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int m = (2 * warp + u) * kTileCols + g + (q >= 2 ? 8 : 0);
-                        const int n = n8 * 8 + 2 * t + (q & 1);
-                        wsl[n * kBM + m] = acc[u][n8][q];
-                    }
-            __threadfence();
-            named_sync(1, kCW * 32);
-            if (threadIdx.x == 0) *flag = atomicAdd(a.tickets + cb, 1) == nsplit - 1;
-            named_sync(1, kCW * 32);
-            last = *flag;
-            named_sync(1, kCW * 32);  // flag read by all before the next colblock reuses it
-            if (last) {
-                __threadfence();
-                const float* wst = a.ws + cb * a.maxsplit * 16 * kBM;
-#pragma unroll
-                for (int u = 0; u < 2; ++u)
-#pragma unroll
-                    for (int n8 = 0; n8 < NB; ++n8)
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const int m = (2 * warp + u) * kTileCols + g + (q >= 2 ? 8 : 0);
-                            const int n = n8 * 8 + 2 * t + (q & 1);
-                            float sum = 0.f;
-                            for (int sp = 0; sp < nsplit; ++sp) sum += __ldcg(wst + (sp * 16 + n) * kBM + m);
-                            acc[u][n8][q] = sum;
-                        }
-                if (threadIdx.x == 0) a.tickets[cb] = 0;  // ready for the next call
-            }
-        }
-        if (last) {
-#pragma unroll
-            for (int u = 0; u < 2; ++u)
-#pragma unroll
-                for (int n8 = 0; n8 < NB; ++n8)
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int64_t jc = cb * kBM + (2 * warp + u) * kTileCols + g + (q >= 2 ? 8 : 0);
-                        const int n = n8 * 8 + 2 * t + (q & 1);
-                        if (jc < a.cols && n < a.batch)
-                            a.y[static_cast<int64_t>(n) * a.cols + jc] = a.scales[jc] * acc[u][n8][q];
-                    }
-        }
-#pragma unroll
-        for (int u = 0; u < 2; ++u)
+        for (int u = 0; u < TW; ++u)
 #pragma unroll
             for (int n8 = 0; n8 < NB; ++n8)
 #pragma unroll
-                for (int i = 0; i < 4; ++i) acc[u][n8][i] = 0.f;
+                for (int i = 0; i < 4; ++i) d[u][n8][i] = acc[u][0][n8][i] + acc[u][1][n8][i];
+        bool writer = true;
+        if (QW > 1) {
+#pragma unroll
+            for (int n8 = 0; n8 < NB; ++n8)
+                *reinterpret_cast<float4*>(red + ((warp * NB + n8) * 32 + lane) * 4) =
+                    make_float4(d[0][n8][0], d[0][n8][1], d[0][n8][2], d[0][n8][3]);
+            named_sync(1, kCW * 32);
+            writer = warp < TPC;  // warp w < TPC sums the QW warps of tile w (warps w, w + TPC, ...)
+            if (writer) {
+#pragma unroll
+                for (int n8 = 0; n8 < NB; ++n8) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) d[0][n8][i] = 0.f;
+                    for (int j = 0; j < QW; ++j) {
+                        const float4 v = *reinterpret_cast<const float4*>(red + (((warp + j * TPC) * NB + n8) * 32 + lane) * 4);
+                        d[0][n8][0] += v.x, d[0][n8][1] += v.y, d[0][n8][2] += v.z, d[0][n8][3] += v.w;
+                    }
+                }
+            }
+            named_sync(1, kCW * 32);  // red is reused by the next colblock
+        }
+        if (writer) {
+#pragma unroll
+            for (int u = 0; u < TW; ++u)
+#pragma unroll
+                for (int n8 = 0; n8 < NB; ++n8)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int64_t jc = (cb * TPC + tile0 + u * kCW) * kTileCols + g + (q >= 2 ? 8 : 0);
+                        const int n = n8 * 8 + 2 * t + (q & 1);
+                        if (jc < a.cols && n < a.batch)
+                            a.y[static_cast<int64_t>(n) * a.cols + jc] = a.scales[jc] * d[u][n8][q];
+                    }
+        }
     }
-}
-
-template <int NB, int XT>
-size_t cb_smem() {
-    return static_cast<size_t>(kRing) * kS * kSBBytes + static_cast<size_t>(kRing) * xs_bytes<XT>(NB * 8) +
-           2 * kRing * 8 + 16;
 }
 
 // x [batch][rows] (any alignment / ragged K) -> xpad [batch][kq * 64] with
@@ -543,15 +506,15 @@ __global__ void __launch_bounds__(256) k_gemv_outliers(int64_t rows, int64_t col
 }
 
 // Repack the artifact's codes into the MMA fragment order (layout above),
-// super-block major: T[cb][q][tile8][lane]. Rows past the end and columns
+// colblock major: T[cb][q][tile(TPC)][lane]. Rows past the end and columns
 // past the end (the last colblock's padding tiles) hold level 0.
 __global__ void k_gemv_repack(const uint8_t* __restrict__ packed, int64_t rows, int64_t cols, int bits,
-                              int64_t kq, int64_t ncb, int lmin, uint4* __restrict__ T) {
+                              int64_t kq, int64_t ncb, int tpc, int lmin, uint4* __restrict__ T) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= ncb * kq * kTilesCB * 32) return;
+    if (i >= ncb * kq * tpc * 32) return;
     const int lane = static_cast<int>(i % 32);
-    const int64_t t8 = (i / 32) % kTilesCB, q = (i / (32 * kTilesCB)) % kq, cb = i / (32 * kTilesCB * kq);
-    const int64_t tile = cb * kTilesCB + t8;
+    const int64_t tt = (i / 32) % tpc, q = (i / (32 * tpc)) % kq, cb = i / (32 * tpc * kq);
+    const int64_t tile = cb * tpc + tt;
     const int g = lane >> 2, t = lane & 3;
     // (column offset, row offset) of nibble slots at bits 0,16,4,20,8,24,12,28
     constexpr int mo[8] = {0, 0, 8, 8, 0, 0, 8, 8};
@@ -585,7 +548,8 @@ using namespace ezq;
 struct ezq_gemv_plan {
     int64_t rows, cols, kq, tiles, ncb;
     int bits, lmin;
-    uint4* T;             // repacked codes, super-block major (owned)
+    int tpc;              // tiles per colblock (1, 2, 4, 8)
+    uint4* T;             // repacked codes, colblock major (owned)
     const float* scales;  // device (borrowed from the artifact)
     int64_t* col_ptr;     // CSC of the outliers (owned)
     uint32_t* out_row;
@@ -595,22 +559,68 @@ struct ezq_gemv_plan {
     int dev;
     float* xt;            // batch > 1 with outliers: x transposed [rows][16] f32 (owned)
     void* xpad;           // ragged / unaligned x: padded copy [16][kq * 64] (owned)
-    int grid[6];          // CTAs of k_gemv_cb per (x dtype, NB) variant
-    int maxsplit;         // most ranges one colblock is cut into (over the variants)
-    float* ws;            // split-colblock partials (owned)
-    int* tickets;         // per colblock (owned, self-resetting)
+    int grid[6];          // persistent CTAs of k_gemv_cb per (x dtype, NB) variant
 };
 
 namespace {
 
-template <int NB, int XT>
+template <int TPC, int NB, int XT>
 int cb_ctas_per_sm() {
-    auto k = k_gemv_cb<NB, XT>;
-    const int smem = static_cast<int>(cb_smem<NB, XT>());
+    auto k = k_gemv_cb<TPC, NB, XT>;
+    const int smem = static_cast<int>(CbGeom<TPC, NB, XT>::smem());
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kStreamThreads, smem) != cudaSuccess || n < 1) n = 1;
     return n;
+}
+
+template <int TPC>
+void occ_row(int* o) {  // variants in (x dtype, NB) order: f32/1, f32/2, bf16/1, bf16/2, f16/1, f16/2
+    o[0] = cb_ctas_per_sm<TPC, 1, kF32>();
+    o[1] = cb_ctas_per_sm<TPC, 2, kF32>();
+    o[2] = cb_ctas_per_sm<TPC, 1, kBF16>();
+    o[3] = cb_ctas_per_sm<TPC, 2, kBF16>();
+    o[4] = cb_ctas_per_sm<TPC, 1, kF16>();
+    o[5] = cb_ctas_per_sm<TPC, 2, kF16>();
+}
+
+// CTAs per SM of every (TPC, variant), measured once per process.
+const int* occupancy(int tpc) {
+    static int occ[4][6];
+    static std::once_flag once;
+    std::call_once(once, [] {
+        occ_row<1>(occ[0]);
+        occ_row<2>(occ[1]);
+        occ_row<4>(occ[2]);
+        occ_row<8>(occ[3]);
+    });
+    return occ[tpc == 1 ? 0 : tpc == 2 ? 1 : tpc == 4 ? 2 : 3];
+}
+
+template <int TPC, int NB, int XT>
+void launch_cb_t(const GemvArgs& a, int grid, cudaStream_t st) {
+    k_gemv_cb<TPC, NB, XT><<<static_cast<unsigned>(grid), kStreamThreads, CbGeom<TPC, NB, XT>::smem(), st>>>(a);
+}
+
+template <int TPC>
+void launch_cb_v(int v, const GemvArgs& a, int grid, cudaStream_t st) {
+    switch (v) {
+        case 0: launch_cb_t<TPC, 1, kF32>(a, grid, st); break;
+        case 1: launch_cb_t<TPC, 2, kF32>(a, grid, st); break;
+        case 2: launch_cb_t<TPC, 1, kBF16>(a, grid, st); break;
+        case 3: launch_cb_t<TPC, 2, kBF16>(a, grid, st); break;
+        case 4: launch_cb_t<TPC, 1, kF16>(a, grid, st); break;
+        default: launch_cb_t<TPC, 2, kF16>(a, grid, st); break;
+    }
+}
+
+void launch_cb(int tpc, int v, const GemvArgs& a, int grid, cudaStream_t st) {
+    switch (tpc) {
+        case 1: launch_cb_v<1>(v, a, grid, st); break;
+        case 2: launch_cb_v<2>(v, a, grid, st); break;
+        case 4: launch_cb_v<4>(v, a, grid, st); break;
+        default: launch_cb_v<8>(v, a, grid, st); break;
+    }
 }
 
 template <int XT, int VT>
@@ -627,11 +637,6 @@ cudaError_t launch_outliers(cudaLaunchConfig_t& lc, int vt, int bt, int64_t rows
     if (vt == EZQ_GEMV_OUTLIER_F16) return launch_outliers_v<XT, 1>(lc, bt, rows, cols, cp, orow, oval, xg, yg, xtg);
     if (vt == EZQ_GEMV_OUTLIER_BF16) return launch_outliers_v<XT, 2>(lc, bt, rows, cols, cp, orow, oval, xg, yg, xtg);
     return launch_outliers_v<XT, 0>(lc, bt, rows, cols, cp, orow, oval, xg, yg, xtg);
-}
-
-template <int NB, int XT>
-void launch_cb(const GemvArgs& a, cudaStream_t st) {
-    k_gemv_cb<NB, XT><<<static_cast<unsigned>(a.grid), kStreamThreads, cb_smem<NB, XT>(), st>>>(a);
 }
 
 }  // namespace
@@ -694,51 +699,39 @@ int ezq_gemv_prepare_ex(const ezq_qweight* q, int outlier_dtype, void* stream, e
     p->lmin = -(1 << (q->bits - 1)) + 1;
     p->kq = (q->rows + kBlockRows - 1) / kBlockRows;
     p->tiles = (q->cols + kTileCols - 1) / kTileCols;
-    p->ncb = (p->tiles + kTilesCB - 1) / kTilesCB;
-    p->scales = q->scales;
-    p->n_out = q->n_outliers;
-    p->vdtype = outlier_dtype;
-    p->dev = dev;
-    const int64_t nsb = p->ncb * p->kq;
-    EZQ_CK(cudaMalloc(&p->T, static_cast<size_t>(kSBBytes) * nsb));
+    // Colblock width: the TPC whose colblocks fill the resident CTAs best
+    // (ncb / (waves x resident CTAs), bf16 batch-1 occupancy), ties to the
+    // wider colblock (x slices read once per more columns).
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static const int force_tpc = std::getenv("EZQ_GEMV_TPC") ? std::atoi(std::getenv("EZQ_GEMV_TPC")) : 0;  // tuning aid
+    double best = -1.0;
+    for (int tpc : {8, 4, 2, 1}) {
+        const int64_t ncb = (p->tiles + tpc - 1) / tpc;
+        const int64_t res = static_cast<int64_t>(sms) * occupancy(tpc)[2];
+        const int64_t waves = (ncb + res - 1) / res;
+        const double eff = static_cast<double>(ncb) / static_cast<double>(waves * res);
+        if ((force_tpc ? tpc == force_tpc : eff > best + 1e-9)) best = eff, p->tpc = tpc;
+    }
+    p->ncb = (p->tiles + p->tpc - 1) / p->tpc;
+    const int* occ = occupancy(p->tpc);
+    static const bool dbg = std::getenv("EZQ_GEMV_DEBUG") != nullptr;
+    for (int v = 0; v < 6; ++v) {
+        p->grid[v] = static_cast<int>(std::min<int64_t>(p->ncb, static_cast<int64_t>(sms) * occ[v]));
+        if (dbg)
+            std::fprintf(stderr, "ezq_gemv_prepare: tpc %d ncb %lld variant %d ctas/sm %d grid %d\n", p->tpc,
+                         static_cast<long long>(p->ncb), v, occ[v], p->grid[v]);
+    }
+    const int64_t nw = p->ncb * p->kq * p->tpc * 32;
+    EZQ_CK(cudaMalloc(&p->T, sizeof(uint4) * nw));
     EZQ_CK(cudaMalloc(&p->col_ptr, sizeof(int64_t) * (q->cols + 1)));
     p->xt = nullptr;
     if (q->n_outliers > 0) EZQ_CK(cudaMalloc(&p->xt, sizeof(float) * 16 * static_cast<size_t>(q->rows)));
     EZQ_CK(cudaMalloc(&p->xpad, sizeof(float) * 16 * static_cast<size_t>(p->kq) * kBlockRows));
     EZQ_CK(cudaMalloc(&p->out_row, sizeof(uint32_t) * std::max<int64_t>(q->n_outliers, 1)));
     EZQ_CK(cudaMalloc(&p->out_val, ves * std::max<int64_t>(q->n_outliers, 1)));
-    // Persistent ranges: as many CTAs as fit the SMs at once for each
-    // kernel variant (never more ranges than super-blocks).
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    static thread_local int occ[6] = {0, 0, 0, 0, 0, 0};
-    if (!occ[0]) {
-        occ[0] = cb_ctas_per_sm<1, kF32>();
-        occ[1] = cb_ctas_per_sm<2, kF32>();
-        occ[2] = cb_ctas_per_sm<1, kBF16>();
-        occ[3] = cb_ctas_per_sm<2, kBF16>();
-        occ[4] = cb_ctas_per_sm<1, kF16>();
-        occ[5] = cb_ctas_per_sm<2, kF16>();
-    }
-    p->maxsplit = 1;
-    static const int cap = std::getenv("EZQ_GEMV_CTAS") ? std::atoi(std::getenv("EZQ_GEMV_CTAS")) : 0;  // tuning aid
-    static const bool dbg = std::getenv("EZQ_GEMV_DEBUG") != nullptr;
-    for (int v = 0; v < 6; ++v) {
-        const int per_sm = cap > 0 ? std::min(cap, occ[v]) : occ[v];
-        const int64_t G = std::min<int64_t>(nsb, static_cast<int64_t>(sms) * per_sm);
-        if (dbg) std::fprintf(stderr, "ezq_gemv_prepare: variant %d ctas/sm %d grid %lld nsb %lld\n", v, occ[v],
-                              static_cast<long long>(G), static_cast<long long>(nsb));
-        p->grid[v] = static_cast<int>(G);
-        for (int64_t cb = 0; cb < p->ncb; ++cb)  // ranges cutting each colblock
-            p->maxsplit = std::max<int>(
-                p->maxsplit, static_cast<int>(range_of((cb + 1) * p->kq - 1, nsb, G) - range_of(cb * p->kq, nsb, G) + 1));
-    }
-    EZQ_CK(cudaMalloc(&p->ws, sizeof(float) * 16 * kBM * static_cast<size_t>(p->ncb) * p->maxsplit));
-    EZQ_CK(cudaMalloc(&p->tickets, sizeof(int) * static_cast<size_t>(p->ncb)));
-    EZQ_CK(cudaMemsetAsync(p->tickets, 0, sizeof(int) * static_cast<size_t>(p->ncb), st));
-    const int64_t nw = nsb * kTilesCB * 32;
     k_gemv_repack<<<static_cast<unsigned>((nw + 255) / 256), 256, 0, st>>>(q->packed, q->rows, q->cols, q->bits,
-                                                                         p->kq, p->ncb, p->lmin, p->T);
+                                                                         p->kq, p->ncb, p->tpc, p->lmin, p->T);
     count_launch();
     EZQ_CK(cudaMemcpyAsync(p->col_ptr, ptr.data(), sizeof(int64_t) * (q->cols + 1),
                            cudaMemcpyHostToDevice, st));
@@ -769,10 +762,7 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
     GemvArgs a{};
     a.T = p->T;
     a.kq = p->kq;
-    a.nsb = p->ncb * p->kq;
-    a.ws = p->ws;
-    a.tickets = p->tickets;
-    a.maxsplit = p->maxsplit;
+    a.ncb = p->ncb;
     a.rows = p->rows;
     a.cols = p->cols;
     a.lmin = p->lmin;
@@ -807,15 +797,7 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
             count_launch();
         }
         const int v = x_dtype * 2 + (two ? 1 : 0);
-        a.grid = p->grid[v];
-        switch (v) {
-            case 0: launch_cb<1, kF32>(a, st); break;
-            case 1: launch_cb<2, kF32>(a, st); break;
-            case 2: launch_cb<1, kBF16>(a, st); break;
-            case 3: launch_cb<2, kBF16>(a, st); break;
-            case 4: launch_cb<1, kF16>(a, st); break;
-            default: launch_cb<2, kF16>(a, st); break;
-        }
+        launch_cb(p->tpc, v, a, p->grid[v], st);
         count_launch();
         if (p->n_out) {
             cudaLaunchConfig_t lc{};
@@ -860,8 +842,6 @@ void ezq_gemv_plan_free(ezq_gemv_plan* p) {
     cudaFree(p->xpad);
     cudaFree(p->out_row);
     cudaFree(p->out_val);
-    cudaFree(p->ws);
-    cudaFree(p->tickets);
     delete p;
 }
 
