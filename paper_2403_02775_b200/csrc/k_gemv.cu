@@ -699,6 +699,10 @@ int ezq_gemv_prepare_ex(const ezq_qweight* q, int outlier_dtype, void* stream, e
     p->lmin = -(1 << (q->bits - 1)) + 1;
     p->kq = (q->rows + kBlockRows - 1) / kBlockRows;
     p->tiles = (q->cols + kTileCols - 1) / kTileCols;
+    p->scales = q->scales;
+    p->n_out = q->n_outliers;
+    p->vdtype = outlier_dtype;
+    p->dev = dev;
     // Colblock width: the TPC whose colblocks fill the resident CTAs best
     // (ncb / (waves x resident CTAs), bf16 batch-1 occupancy), ties to the
     // wider colblock (x slices read once per more columns).
