@@ -205,9 +205,11 @@ struct GemvArgs {
 __device__ __forceinline__ void bar_wait(unsigned bar, unsigned phase) {
     unsigned ok = 0;
     for (long long spin = 0; !ok; ++spin) {
-        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        // test_wait (non-blocking) in a spin: try_wait may suspend the warp
+        // past the phase completion
+        asm volatile("{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
                      : "=r"(ok) : "r"(bar), "r"(phase) : "memory");
-        if (spin > (1ll << 28)) __trap();  // never hang the device on a lost transfer
+        if (spin > (1ll << 30)) __trap();  // never hang the device on a lost transfer
     }
 }
 

@@ -46,7 +46,8 @@ def _gemv_case(gpu, O, rows, cols, sigma, bits, batch, dtype, odt):
     xf = x.float().cpu().numpy()
     yref = O.gemv_f64(What, xf)
     err = np.abs(y - yref).max()
-    assert err <= 1e-3 * np.abs(yref).max(), (err, np.abs(yref).max())
+    if odt != "bfloat16":  # bf16 outlier values (8-bit mantissa) are a coarser format than the 1e-3 gate
+        assert err <= 1e-3 * np.abs(yref).max(), (err, np.abs(yref).max())
     if odt != "float32":
         # the kernel against the format it computes with: the outlier values
         # rounded to the storage dtype (the rounding itself is the format's
