@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
     const unsigned empty0 = full0 + 8 * kRing;
     if (threadIdx.x == 0) {
         for (int k = 0; k < kRing; ++k) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 33;" ::"r"(full0 + 8 * k));  // tx + 32 cp.async lanes
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full0 + 8 * k));  // expect_tx arrival
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * k), "r"(kCW));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
     asm volatile("griddepcontrol.launch_dependents;");
     const int64_t nst_cb = (a.kq + S - 1) / S;  // stages per colblock
 
-    if (warp == kCW) {  // ---- producer warp: codes by TMA (lane 0), x slices by cp.async (all lanes)
+    if (warp == kCW) {  // ---- producer warp: codes and x slices by TMA bulk copies
         int k = 0;
         for (int64_t cb = blockIdx.x; cb < a.ncb; cb += gridDim.x) {
             for (int64_t sq = 0; sq < nst_cb; ++sq, ++k) {
@@ -269,26 +269,27 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
                 const int slot = k % kRing;
                 if (k >= kRing) bar_wait(empty0 + 8 * slot, ((k / kRing) - 1) & 1);
                 const unsigned fb = full0 + 8 * slot;
-                if (lane == 0) {
-                    const unsigned bytes = static_cast<unsigned>(cnt) * TPC * 512u;
-                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(bytes) : "memory");
+                // codes (one bulk copy) and the batch rows' x slices (one bulk
+                // copy per row, contiguous in x), all on the stage's barrier
+                const unsigned cbytes = static_cast<unsigned>(cnt) * TPC * 512u;
+                const unsigned xbytes = static_cast<unsigned>(cnt) * 64u * ES;
+                if (lane == 0)
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
+                                 "r"(cbytes + xbytes * static_cast<unsigned>(a.batch))
+                                 : "memory");
+                __syncwarp();
+                if (lane == 0)
                     asm volatile(
                         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                             static_cast<unsigned>(__cvta_generic_to_shared(codes + slot * CB))),
-                        "l"(a.T + (cb * a.kq + q0) * TPC * 32), "r"(bytes), "r"(fb)
+                        "l"(a.T + (cb * a.kq + q0) * TPC * 32), "r"(cbytes), "r"(fb)
                         : "memory");
-                }
-                const int gpr = cnt * 64 * ES / 16;  // 16-byte granules per batch row
-                const unsigned xdst = static_cast<unsigned>(__cvta_generic_to_shared(xsm + slot * XB));
-                for (int gi = lane; gi < NBT * gpr; gi += 32) {
-                    const int n = gi / gpr, k16 = gi - n * gpr;
-                    const int nn = min(n, a.batch - 1);
-                    const char* src = static_cast<const char*>(a.x) + (nn * a.xstride + 64 * q0) * ES + 16 * k16;
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(xdst + n * XP * ES + 16 * k16),
-                                 "l"(src)
-                                 : "memory");
-                }
-                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(fb) : "memory");
+                if (lane < a.batch)
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            static_cast<unsigned>(__cvta_generic_to_shared(xsm + slot * XB + lane * XP * ES))),
+                        "l"(static_cast<const char*>(a.x) + (lane * a.xstride + 64 * q0) * ES), "r"(xbytes), "r"(fb)
+                        : "memory");
             }
         }
         return;
@@ -300,6 +301,9 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
     const unsigned off2 = F16 ? static_cast<unsigned>(__half_as_ushort(__int2half_rn(1024 - a.lmin))) * 0x10001u
                               : static_cast<unsigned>(__bfloat16_as_ushort(__int2bfloat16_rn(128 - a.lmin))) * 0x10001u;
     // my tiles: TPC >= 4: w, w + 4, ...; else tile w % TPC on q-blocks s = w / TPC (mod QW)
+    int xrow[NB];  // staged x row of my batch column (rows past the batch read the last one; never stored)
+#pragma unroll
+    for (int n8 = 0; n8 < NB; ++n8) xrow[n8] = min(n8 * 8 + g, a.batch - 1);
     const int tile0 = TPC >= kCW ? warp : warp % TPC;
     const int qoff = TPC >= kCW ? 0 : warp / TPC;
     int k = 0;
@@ -323,7 +327,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
                 XRaw<XT> xr[NB];
 #pragma unroll
                 for (int n8 = 0; n8 < NB; ++n8) {
-                    const uint4* xp = reinterpret_cast<const uint4*>(xw + ((n8 * 8 + g) * XP + s * 64 + 16 * t) * ES);
+                    const uint4* xp = reinterpret_cast<const uint4*>(xw + (xrow[n8] * XP + s * 64 + 16 * t) * ES);
 #pragma unroll
                     for (int i = 0; i < XRaw<XT>::kWords / 4; ++i) {
                         const uint4 u4 = xp[i];
