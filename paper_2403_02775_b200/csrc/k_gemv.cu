@@ -204,12 +204,12 @@ struct GemvArgs {
 
 __device__ __forceinline__ void bar_wait(unsigned bar, unsigned phase) {
     unsigned ok = 0;
-    for (long long spin = 0; !ok; ++spin) {
-        // test_wait (non-blocking) in a spin: try_wait may suspend the warp
-        // past the phase completion
-        asm volatile("{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+    for (int spin = 0; !ok; ++spin) {
+        // try_wait suspends the warp until the phase completes (or a time
+        // limit): waiting warps take no issue slots from the dequant
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
                      : "=r"(ok) : "r"(bar), "r"(phase) : "memory");
-        if (spin > (1ll << 30)) __trap();  // never hang the device on a lost transfer
+        if (spin > (1 << 28)) __trap();  // never hang the device on a lost transfer
     }
 }
 
@@ -229,11 +229,46 @@ struct CbGeom {
     static constexpr int CB = S * TPC * 512;                          // code bytes per stage
     static constexpr int TW = TPC >= kCW ? TPC / kCW : 1;             // tiles per warp
     static constexpr int QW = TPC >= kCW ? 1 : kCW / TPC;             // warps sharing a tile
+    // HSUB2-free dequant (bf16 / split-f32 x, batch <= 8): A' = level + C
+    // exactly (C = 128 - lmin), D' = D + C * sum(x) corrected at the end
+    static constexpr bool SUBFREE = XT != kF16 && NB == 1;
     static constexpr size_t smem() {
         return static_cast<size_t>(kRing) * (CB + XB) + 2 * kRing * 8 +
-               (QW > 1 ? static_cast<size_t>(kCW) * NB * 32 * 4 * sizeof(float) : 0) + 16;
+               (QW > 1 ? static_cast<size_t>(kCW) * NB * 32 * 4 * sizeof(float) : 0) + 16 * sizeof(float) + 16;
     }
 };
+
+// sum_i x[n][i] over all of K of every batch row, as the MMA sees the values
+// (bf16; f32 as bf16 hi + lo): fixed order (lane-strided 16-byte chunks, then
+// a fixed butterfly), into xsum[n]; then signals named barrier 2. One warp.
+template <int XT>
+__device__ void producer_xsum(const GemvArgs& a, float* xsum, int lane) {
+    constexpr int ES = XT == kF32 ? 4 : 2;
+    const int64_t chunks = a.kq * 64 * ES / 16;
+    for (int n = 0; n < a.batch; ++n) {
+        float acc = 0.f;
+        const uint4* row = reinterpret_cast<const uint4*>(static_cast<const char*>(a.x) + n * a.xstride * ES);
+        for (int64_t c16 = lane; c16 < chunks; c16 += 32) {
+            const uint4 u = __ldg(row + c16);
+            const unsigned w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (XT == kF32) {
+                    const float xv = __uint_as_float(w4[j]);
+                    const float hi = __bfloat162float(__float2bfloat16_rn(xv));
+                    acc += hi + __bfloat162float(__float2bfloat16_rn(xv - hi));
+                } else {
+                    acc += __uint_as_float(w4[j] << 16) + __uint_as_float(w4[j] & 0xffff0000u);
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) xsum[n] = acc;
+    }
+    __syncwarp();
+    asm volatile("bar.arrive 2, %0;" ::"r"(kStreamThreads) : "memory");
+}
 
 template <int TPC, int NB, int XT>
 __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
@@ -246,6 +281,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
     unsigned char* xsm = smem + kRing * CB;          // [kRing][NBT][XP]
     unsigned long long* bars = reinterpret_cast<unsigned long long*>(xsm + kRing * XB);
     float* red = reinterpret_cast<float*>(bars + 2 * kRing);  // [kCW][NB][32][4] (QW > 1)
+    float* xsum = red + (QW > 1 ? kCW * NB * 32 * 4 : 0);      // [16] sum_i x[n][i] (SUBFREE)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned full0 = static_cast<unsigned>(__cvta_generic_to_shared(bars));
     const unsigned empty0 = full0 + 8 * kRing;
@@ -262,8 +298,13 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
 
     if (warp == kCW) {  // ---- producer warp: codes and x slices by TMA bulk copies
         int k = 0;
+        bool xsum_done = !Gm::SUBFREE;
         for (int64_t cb = blockIdx.x; cb < a.ncb; cb += gridDim.x) {
             for (int64_t sq = 0; sq < nst_cb; ++sq, ++k) {
+                if (!xsum_done && k == kRing) {  // once per CTA, while the first stages are in flight
+                    producer_xsum<XT>(a, xsum, lane);
+                    xsum_done = true;
+                }
                 const int64_t q0 = sq * S;
                 const int cnt = static_cast<int>(min(static_cast<int64_t>(S), a.kq - q0));
                 const int slot = k % kRing;
@@ -292,6 +333,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
                         : "memory");
             }
         }
+        if (!xsum_done) producer_xsum<XT>(a, xsum, lane);  // fewer than kRing stages in this CTA
         return;
     }
 
@@ -323,7 +365,10 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
             bar_wait(full0 + 8 * slot, (k / kRing) & 1);
             const uint4* cw = reinterpret_cast<const uint4*>(codes + slot * CB);
             const unsigned char* xw = xsm + slot * XB;
-            for (int s = qoff; s < cnt; s += QW) {
+#pragma unroll
+            for (int si = 0; si < S / QW; ++si) {
+                const int s = qoff + si * QW;
+                if (s >= cnt) break;
                 XRaw<XT> xr[NB];
 #pragma unroll
                 for (int n8 = 0; n8 < NB; ++n8) {
@@ -335,7 +380,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
                                       xr[n8].w[4 * i + 3] = u4.w;
                     }
                 }
-                const int h = (s / QW) & 1;
+                const int h = si & 1;
 #pragma unroll
                 for (int u = 0; u < TW; ++u) {
                     const uint4 w = cw[(s * TPC + tile0 + u * kCW) * 32 + lane];
@@ -344,7 +389,8 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
                     for (int st = 0; st < 4; ++st) {
                         unsigned af[4];
 #pragma unroll
-                        for (int r = 0; r < 4; ++r) af[r] = sub2<F16>(lop_pair(ws[st], r, magic), off2);
+                        for (int r = 0; r < 4; ++r)
+                            af[r] = Gm::SUBFREE ? lop_pair(ws[st], r, magic) : sub2<F16>(lop_pair(ws[st], r, magic), off2);
 #pragma unroll
                         for (int n8 = 0; n8 < NB; ++n8) {
                             unsigned hi[2], lo[2];
@@ -371,6 +417,14 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
             for (int n8 = 0; n8 < NB; ++n8)
 #pragma unroll
                 for (int i = 0; i < 4; ++i) d[u][n8][i] = acc[u][0][n8][i] + acc[u][1][n8][i];
+        if (Gm::SUBFREE) {  // D' = D + C sum(x): remove the offset once per element
+            if (cb == blockIdx.x) named_sync(2, kStreamThreads);  // xsum published by the producer
+            const float C = static_cast<float>(128 - a.lmin);
+#pragma unroll
+            for (int u = 0; u < TW; ++u)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) d[u][0][q] -= C * xsum[min(2 * t + (q & 1), a.batch - 1)];
+        }
         bool writer = true;
         if (QW > 1) {
 #pragma unroll
