@@ -238,38 +238,6 @@ struct CbGeom {
     }
 };
 
-// sum_i x[n][i] over all of K of every batch row, as the MMA sees the values
-// (bf16; f32 as bf16 hi + lo): fixed order (lane-strided 16-byte chunks, then
-// a fixed butterfly), into xsum[n]; then signals named barrier 2. One warp.
-template <int XT>
-__device__ void producer_xsum(const GemvArgs& a, float* xsum, int lane) {
-    constexpr int ES = XT == kF32 ? 4 : 2;
-    const int64_t chunks = a.kq * 64 * ES / 16;
-    for (int n = 0; n < a.batch; ++n) {
-        float acc = 0.f;
-        const uint4* row = reinterpret_cast<const uint4*>(static_cast<const char*>(a.x) + n * a.xstride * ES);
-        for (int64_t c16 = lane; c16 < chunks; c16 += 32) {
-            const uint4 u = __ldg(row + c16);
-            const unsigned w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (XT == kF32) {
-                    const float xv = __uint_as_float(w4[j]);
-                    const float hi = __bfloat162float(__float2bfloat16_rn(xv));
-                    acc += hi + __bfloat162float(__float2bfloat16_rn(xv - hi));
-                } else {
-                    acc += __uint_as_float(w4[j] << 16) + __uint_as_float(w4[j] & 0xffff0000u);
-                }
-            }
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) xsum[n] = acc;
-    }
-    __syncwarp();
-    asm volatile("bar.arrive 2, %0;" ::"r"(kStreamThreads) : "memory");
-}
-
 template <int TPC, int NB, int XT>
 __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
     using Gm = CbGeom<TPC, NB, XT>;
@@ -288,7 +256,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
     if (threadIdx.x == 0) {
         for (int k = 0; k < kRing; ++k) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full0 + 8 * k));  // expect_tx arrival
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * k), "r"(kCW));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * k), "r"(kCW + 1));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -297,13 +265,57 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
     const int64_t nst_cb = (a.kq + S - 1) / S;  // stages per colblock
 
     if (warp == kCW) {  // ---- producer warp: codes and x slices by TMA bulk copies
+        // SUBFREE: while the CTA's first colblock streams, the producer also
+        // sums the staged x slices (sum_i x[n][i] over all of K, the values
+        // the MMA sees: bf16, or f32 as bf16 hi + lo; fixed lane assignment
+        // and butterfly -- deterministic), lagging kRing - 1 stages behind
+        // the copies; every other stage it releases at once. The sums go to
+        // xsum[] and named barrier 2 tells the consumers.
+        float xs_acc[Gm::NBT];
+#pragma unroll
+        for (int n = 0; n < Gm::NBT; ++n) xs_acc[n] = 0.f;
+        int done = 0;  // first-colblock stages summed and released
+        auto sum_stage = [&](int p) {
+            const int slot = p % kRing;
+            bar_wait(full0 + 8 * slot, (p / kRing) & 1);
+            const int cnt = static_cast<int>(min(static_cast<int64_t>(S), a.kq - static_cast<int64_t>(p) * S));
+            const unsigned char* xw = xsm + slot * XB;
+            for (int n = 0; n < a.batch; ++n) {
+                for (int c16 = lane; c16 < cnt * 64 * ES / 16; c16 += 32) {
+                    const uint4 u = *reinterpret_cast<const uint4*>(xw + n * XP * ES + 16 * c16);
+                    const unsigned w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (XT == kF32) {
+                            const float xv = __uint_as_float(w4[j]);
+                            const float hi = __bfloat162float(__float2bfloat16_rn(xv));
+                            xs_acc[n] += hi + __bfloat162float(__float2bfloat16_rn(xv - hi));
+                        } else {
+                            xs_acc[n] += __uint_as_float(w4[j] << 16) + __uint_as_float(w4[j] & 0xffff0000u);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * slot) : "memory");
+        };
+        auto publish = [&]() {
+            for (int n = 0; n < a.batch; ++n) {
+                float v = xs_acc[n];
+#pragma unroll
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) xsum[n] = v;
+            }
+            __syncwarp();
+            asm volatile("bar.arrive 2, %0;" ::"r"(kStreamThreads) : "memory");
+        };
+        const int first_n = static_cast<int>(nst_cb);  // stages of the first colblock
         int k = 0;
-        bool xsum_done = !Gm::SUBFREE;
         for (int64_t cb = blockIdx.x; cb < a.ncb; cb += gridDim.x) {
             for (int64_t sq = 0; sq < nst_cb; ++sq, ++k) {
-                if (!xsum_done && k == kRing) {  // once per CTA, while the first stages are in flight
-                    producer_xsum<XT>(a, xsum, lane);
-                    xsum_done = true;
+                if (Gm::SUBFREE && k == first_n) {  // leaving the first colblock: drain, publish
+                    while (done < first_n) sum_stage(done++);
+                    publish();
                 }
                 const int64_t q0 = sq * S;
                 const int cnt = static_cast<int>(min(static_cast<int64_t>(S), a.kq - q0));
@@ -331,9 +343,18 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
                             static_cast<unsigned>(__cvta_generic_to_shared(xsm + slot * XB + lane * XP * ES))),
                         "l"(static_cast<const char*>(a.x) + (lane * a.xstride + 64 * q0) * ES), "r"(xbytes), "r"(fb)
                         : "memory");
+                if (Gm::SUBFREE && k < first_n) {
+                    if (k >= kRing - 1) sum_stage(done++);  // the oldest stage in flight
+                } else {
+                    __syncwarp();
+                    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * slot) : "memory");
+                }
             }
         }
-        if (!xsum_done) producer_xsum<XT>(a, xsum, lane);  // fewer than kRing stages in this CTA
+        if (Gm::SUBFREE && k <= first_n) {  // the CTA had one colblock
+            while (done < first_n) sum_stage(done++);
+            publish();
+        }
         return;
     }
 
@@ -417,14 +438,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
             for (int n8 = 0; n8 < NB; ++n8)
 #pragma unroll
                 for (int i = 0; i < 4; ++i) d[u][n8][i] = acc[u][0][n8][i] + acc[u][1][n8][i];
-        if (Gm::SUBFREE) {  // D' = D + C sum(x): remove the offset once per element
-            if (cb == blockIdx.x) named_sync(2, kStreamThreads);  // xsum published by the producer
-            const float C = static_cast<float>(128 - a.lmin);
-#pragma unroll
-            for (int u = 0; u < TW; ++u)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) d[u][0][q] -= C * xsum[min(2 * t + (q & 1), a.batch - 1)];
-        }
+        if (Gm::SUBFREE && cb == blockIdx.x) named_sync(2, kStreamThreads);  // xsum published by the producer
         bool writer = true;
         if (QW > 1) {
 #pragma unroll
@@ -447,6 +461,13 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
             named_sync(1, kCW * 32);  // red is reused by the next colblock
         }
         if (writer) {
+            if (Gm::SUBFREE) {  // D' = D + C sum(x): remove the offset once per output element
+                const float C = static_cast<float>(128 - a.lmin);
+#pragma unroll
+                for (int u = 0; u < TW; ++u)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) d[u][0][q] -= C * xsum[min(2 * t + (q & 1), a.batch - 1)];
+            }
 #pragma unroll
             for (int u = 0; u < TW; ++u)
 #pragma unroll
