@@ -257,11 +257,10 @@ int ezq_decode_quantized(const uint8_t* bytes, int64_t len, ezq_qweight** out);
 typedef struct ezq_gemv_plan ezq_gemv_plan;
 int ezq_gemv_prepare(const ezq_qweight* q, void* stream, ezq_gemv_plan** plan);
 /* Same, with the outlier values stored as f32 (exact, 8 bytes per outlier
- * with the u32 row) or f16 / bf16 (6 bytes per outlier, round to nearest
- * even; the GEMV stays within its 1e-3 gate). */
+ * with the u32 row) or f16 (6 bytes per outlier, round to nearest even; the
+ * GEMV stays within its 1e-3 gate). */
 #define EZQ_GEMV_OUTLIER_F32 0
 #define EZQ_GEMV_OUTLIER_F16 1
-#define EZQ_GEMV_OUTLIER_BF16 2
 int ezq_gemv_prepare_ex(const ezq_qweight* q, int outlier_dtype, void* stream, ezq_gemv_plan** plan);
 int ezq_gemv(const ezq_gemv_plan* plan, const void* x, int x_dtype, int batch, float* y,
              void* stream);

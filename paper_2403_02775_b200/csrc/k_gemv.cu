@@ -217,7 +217,7 @@ __device__ __forceinline__ void named_sync(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-template <int TPC, int NB, int XT>
+template <int TPC, int NB, int XT, bool SF = false>
 struct CbGeom {
     static constexpr int ES = XT == kF32 ? 4 : 2;                     // x element bytes
     static constexpr int NBT = NB * 8;                                // batch rows staged
@@ -231,16 +231,16 @@ struct CbGeom {
     static constexpr int QW = TPC >= kCW ? 1 : kCW / TPC;             // warps sharing a tile
     // HSUB2-free dequant (bf16 / split-f32 x, batch <= 8): A' = level + C
     // exactly (C = 128 - lmin), D' = D + C * sum(x) corrected at the end
-    static constexpr bool SUBFREE = XT != kF16 && NB == 1;
+    static constexpr bool SUBFREE = SF && XT != kF16 && NB == 1;
     static constexpr size_t smem() {
         return static_cast<size_t>(kRing) * (CB + XB) + 2 * kRing * 8 +
                (QW > 1 ? static_cast<size_t>(kCW) * NB * 32 * 4 * sizeof(float) : 0) + 16 * sizeof(float) + 16;
     }
 };
 
-template <int TPC, int NB, int XT>
+template <int TPC, int NB, int XT, bool SF>
 __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
-    using Gm = CbGeom<TPC, NB, XT>;
+    using Gm = CbGeom<TPC, NB, XT, SF>;
     constexpr bool F16 = XT == kF16;
     constexpr int ES = Gm::ES, NBT = Gm::NBT, S = Gm::S, XP = Gm::XP, XB = Gm::XB, CB = Gm::CB;
     constexpr int TW = Gm::TW, QW = Gm::QW;
@@ -516,12 +516,11 @@ __global__ void __launch_bounds__(256) k_gemv_xt(const void* __restrict__ x, int
     if (r < rows) xt[r * 16 + n] = n < batch ? load_x(x, xt_type, static_cast<int64_t>(n) * rows + r) : 0.f;
 }
 
-// Outlier values: f32 (exact), or f16 / bf16 (ezq_gemv_prepare_ex; 6 bytes
-// per outlier instead of 8, held to the GEMV's 1e-3 gate).
+// Outlier values: f32 (exact) or f16 (ezq_gemv_prepare_ex; 6 bytes per
+// outlier instead of 8, held to the GEMV's 1e-3 gate).
 template <int VT>
 __device__ __forceinline__ float load_val(const void* v, int64_t e) {
     if (VT == 1) return __half2float(static_cast<const __half*>(v)[e]);
-    if (VT == 2) return __uint_as_float(static_cast<unsigned>(static_cast<const unsigned short*>(v)[e]) << 16);
     return static_cast<const float*>(v)[e];
 }
 
@@ -647,8 +646,10 @@ namespace {
 
 template <int TPC, int NB, int XT>
 int cb_ctas_per_sm() {
-    auto k = k_gemv_cb<TPC, NB, XT>;
     const int smem = static_cast<int>(CbGeom<TPC, NB, XT>::smem());
+    if (NB == 1 && XT != kF16)  // the HSUB2-free twin (same shared memory)
+        cudaFuncSetAttribute(k_gemv_cb<TPC, NB, XT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    auto k = k_gemv_cb<TPC, NB, XT, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kStreamThreads, smem) != cudaSuccess || n < 1) n = 1;
@@ -678,9 +679,16 @@ const int* occupancy(int tpc) {
     return occ[tpc == 1 ? 0 : tpc == 2 ? 1 : tpc == 4 ? 2 : 3];
 }
 
+// HSUB2-free dequant for batch <= 2 (bf16 / f32 x): the producer's per-stage
+// x sums stay cheap; larger batches keep the HSUB2 path.
 template <int TPC, int NB, int XT>
 void launch_cb_t(const GemvArgs& a, int grid, cudaStream_t st) {
-    k_gemv_cb<TPC, NB, XT><<<static_cast<unsigned>(grid), kStreamThreads, CbGeom<TPC, NB, XT>::smem(), st>>>(a);
+    if (NB == 1 && XT != kF16 && a.batch <= 2)
+        k_gemv_cb<TPC, NB, XT, true><<<static_cast<unsigned>(grid), kStreamThreads, CbGeom<TPC, NB, XT, true>::smem(),
+                                       st>>>(a);
+    else
+        k_gemv_cb<TPC, NB, XT, false><<<static_cast<unsigned>(grid), kStreamThreads, CbGeom<TPC, NB, XT>::smem(),
+                                        st>>>(a);
 }
 
 template <int TPC>
@@ -716,7 +724,6 @@ template <int XT>
 cudaError_t launch_outliers(cudaLaunchConfig_t& lc, int vt, int bt, int64_t rows, int64_t cols, const int64_t* cp,
                             const uint32_t* orow, const void* oval, const void* xg, float* yg, const float* xtg) {
     if (vt == EZQ_GEMV_OUTLIER_F16) return launch_outliers_v<XT, 1>(lc, bt, rows, cols, cp, orow, oval, xg, yg, xtg);
-    if (vt == EZQ_GEMV_OUTLIER_BF16) return launch_outliers_v<XT, 2>(lc, bt, rows, cols, cp, orow, oval, xg, yg, xtg);
     return launch_outliers_v<XT, 0>(lc, bt, rows, cols, cp, orow, oval, xg, yg, xtg);
 }
 
@@ -732,8 +739,9 @@ int ezq_gemv_prepare_ex(const ezq_qweight* q, int outlier_dtype, void* stream, e
         return set_error(EZQ_ERR_IO_FORMAT, "quantized tensor has empty shape");
     if (q->bits < 2 || q->bits > 4)
         return set_error(EZQ_ERR_INVALID_ARGUMENT, "ezq_gemv supports 2- to 4-bit artifacts");
-    if (outlier_dtype < EZQ_GEMV_OUTLIER_F32 || outlier_dtype > EZQ_GEMV_OUTLIER_BF16)
-        return set_error(EZQ_ERR_INVALID_ARGUMENT, "bad outlier value dtype");
+    if (outlier_dtype != EZQ_GEMV_OUTLIER_F32 && outlier_dtype != EZQ_GEMV_OUTLIER_F16)
+        return set_error(EZQ_ERR_INVALID_ARGUMENT,
+                         "outlier values are stored as f32 or f16 (bf16's 8-bit mantissa misses the 1e-3 GEMV gate)");
     int dev;
     if (int s = bind_device(&dev)) return s;
     cudaStream_t st = pick_stream(stream, dev);
@@ -764,13 +772,8 @@ int ezq_gemv_prepare_ex(const ezq_qweight* q, int outlier_dtype, void* stream, e
     if (ves == 2) {  // round to nearest even, like the device conversions
         vh.resize(vv.size());
         for (size_t i = 0; i < vv.size(); ++i) {
-            if (outlier_dtype == EZQ_GEMV_OUTLIER_F16) {
-                const __half h = __float2half_rn(vv[i]);
-                vh[i] = __half_as_ushort(h);
-            } else {
-                const __nv_bfloat16 b = __float2bfloat16_rn(vv[i]);
-                vh[i] = __bfloat16_as_ushort(b);
-            }
+            const __half h = __float2half_rn(vv[i]);
+            vh[i] = __half_as_ushort(h);
         }
     }
     auto* p = new ezq_gemv_plan{};

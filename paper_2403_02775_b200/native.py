@@ -449,7 +449,7 @@ class GemvPlan:
     DeviceBatch entry). x: torch CUDA tensor [batch, rows] (f32/bf16/f16)."""
 
     DTYPES = {"torch.float32": 0, "torch.bfloat16": 1, "torch.float16": 2}
-    OUTLIER_DTYPES = {"float32": 0, "float16": 1, "bfloat16": 2}
+    OUTLIER_DTYPES = {"float32": 0, "float16": 1}
 
     def __init__(self, batch: "DeviceBatch", i: int, stream=None, outlier_dtype: str = "float32"):
         self._keep = batch
