@@ -99,7 +99,7 @@ struct Scratch {
     double* tie_s;
     double* tie_e;
 };
-constexpr int kTieMax = 8;
+constexpr int kTieMax = 32;  // candidate slots per column (a bit mask in k_resolve_ties)
 constexpr int kTieFixed = 1 << 20;
 
 struct CfgDev {

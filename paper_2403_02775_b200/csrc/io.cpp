@@ -1,6 +1,13 @@
 // ezquant/io.hpp for the B200 engine (reference io.cpp:108-390): manifests
 // (nlohmann ordered_json, the reference's formatting), raw f32 tensor files,
 // and the .ezqt container over the C-ABI codec (codec.cpp).
+//
+// Derived from the reference's io.cpp: save_manifest, read_tensor_f32,
+// write_tensor_f32, write_quantized / read_quantized and tensor_file_stem
+// follow it closely on purpose -- their JSON key order, formatting and
+// exception texts are the byte-identical-output contract that
+// tests/test_model_driver.py enforces against the compiled reference. Off the
+// hot path; the codec itself (codec.cpp) is an independent C implementation.
 #include <bit>
 #include <cstring>
 #include <fstream>

@@ -102,62 +102,65 @@ __device__ __forceinline__ float tie_gamma(int n) {
 __device__ __forceinline__ double tie_threshold(double best, double cfull, float gam) {
     return __dadd_rn(best, static_cast<double>(gam) * 2.0002 * __dadd_rn(best, cfull));
 }
-// Candidate bookkeeping of one column, kept by its writer lane only (other
-// lanes return at once). best/err are err - C; cfull = C (an estimate)
-// converts to full errors. The list (sc.tie_s / tie_e, step order) holds the
-// distinct scales whose exact errors lie within the bound of the running
-// best: a new best drops the entries now beyond it (the filter reads back the
-// writer's own stores), a far new best empties it. nc > cap: a candidate was
-// lost (the column takes the whole-loop fallback).
-struct TieTrack {
-    int nc;
-    __device__ __forceinline__ void push(const Scratch& sc, int64_t gcol, int cap, double s, double efull) {
-        if (nc < cap) {
-            sc.tie_s[gcol * kTieMax + nc] = s;
-            sc.tie_e[gcol * kTieMax + nc] = efull;
-        }
+// Candidate bookkeeping of one column, kept by its writer lane in global
+// memory (sc.tie_n[gcol] is the running count), so the hot loop holds no
+// extra state beyond the pre-filter threshold. best/err are err - C; cfull
+// = C (an estimate) converts to full errors. The list (sc.tie_s / tie_e,
+// step order) holds the distinct scales whose exact errors lie within the
+// bound of the running best: a new best drops the entries now beyond it (the
+// filter reads back the writer's own stores), a far new best empties it.
+// count > cap: a candidate was lost (the column takes the whole-loop
+// fallback). Out of line: the slow path's registers stay out of the loop.
+__device__ __forceinline__ void tie_step(const Scratch& sc, int64_t gcol, int cap, bool lt, double err_hi, double err_lo,
+                                      double best_hi, double best_lo, double s, double best_s, float gam,
+                                      double cfull) {
+    if (!lt && s == best_s) return;  // same scale: same error in both orders
+    int nc = sc.tie_n[gcol];
+    double* ts = sc.tie_s + gcol * kTieMax;
+    double* te = sc.tie_e + gcol * kTieMax;
+    const double gap = fabs(__dadd_rn(__dsub_rn(err_hi, best_hi), __dsub_rn(err_lo, best_lo)));
+    const double ef = __dadd_rn(err_hi, cfull), bf = __dadd_rn(best_hi, cfull);
+    auto push = [&](double sv, double e) {
+        if (nc < cap) ts[nc] = sv, te[nc] = e;
         ++nc;
-    }
-    // Called for t >= 1 before the best is updated; lt = err < best.
-    __device__ __forceinline__ void step(bool writer, const Scratch& sc, int64_t gcol, int cap, bool lt, DD err,
-                                         DD best, double s, double best_s, float gam, double cfull) {
-        if (!writer || (!lt && s == best_s)) return;  // same scale: same error in both orders
-        const double gap = fabs(__dadd_rn(__dsub_rn(err.hi, best.hi), __dsub_rn(err.lo, best.lo)));
-        const double ef = __dadd_rn(err.hi, cfull), bf = __dadd_rn(best.hi, cfull);
-        if (gap <= static_cast<double>(gam) * __dadd_rn(ef, bf)) {
-            if (nc == 0) {
-                push(sc, gcol, cap, best_s, bf);
-            } else if (lt && nc <= cap) {  // keep the entries still within the bound of the new best
-                int k = 0;
-                for (int j = 0; j < nc; ++j) {
-                    const double e = sc.tie_e[gcol * kTieMax + j];
-                    if (__dsub_rn(e, ef) <= static_cast<double>(gam) * __dadd_rn(e, ef)) {
-                        sc.tie_s[gcol * kTieMax + k] = sc.tie_s[gcol * kTieMax + j];
-                        sc.tie_e[gcol * kTieMax + k] = e;
-                        ++k;
-                    }
+    };
+    if (gap <= static_cast<double>(gam) * __dadd_rn(ef, bf)) {
+        if (nc == 0) {
+            push(best_s, bf);
+        } else if (lt && nc <= cap) {  // keep the entries still within the bound of the new best
+            int k = 0;
+            for (int j = 0; j < nc; ++j) {
+                const double e = te[j];
+                if (__dsub_rn(e, ef) <= static_cast<double>(gam) * __dadd_rn(e, ef)) {
+                    ts[k] = ts[j];
+                    te[k] = e;
+                    ++k;
                 }
-                nc = k;
             }
-            push(sc, gcol, cap, s, ef);
-        } else if (lt) {
-            nc = 0;  // every earlier candidate is now beyond the bound
+            nc = k;
         }
+        push(s, ef);
+    } else if (lt) {
+        nc = 0;  // every earlier candidate is now beyond the bound
     }
-    // fixed-step selection (optimize.cpp:169-178): fixed_err <= e0
-    __device__ __forceinline__ void fixed(bool writer, const Scratch& sc, int64_t gcol, int cap, DD fe, DD e0,
-                                          double fs, double s0, float gam, double cfull) {
-        nc = 0;
-        if (!writer || fs == s0) return;
-        const double gap = fabs(__dadd_rn(__dsub_rn(fe.hi, e0.hi), __dsub_rn(fe.lo, e0.lo)));
-        const double ef = __dadd_rn(fe.hi, cfull), bf = __dadd_rn(e0.hi, cfull);
+    sc.tie_n[gcol] = nc;
+}
+
+// fixed-step selection (optimize.cpp:169-178): fixed_err <= e0 inside the bound
+__device__ __forceinline__ void tie_fixed(const Scratch& sc, int64_t gcol, double fe_hi, double fe_lo, double e0_hi,
+                                       double e0_lo, double fs, double s0, float gam, double cfull) {
+    int nc = 0;
+    if (fs != s0) {
+        const double gap = fabs(__dadd_rn(__dsub_rn(fe_hi, e0_hi), __dsub_rn(fe_lo, e0_lo)));
+        const double ef = __dadd_rn(fe_hi, cfull), bf = __dadd_rn(e0_hi, cfull);
         if (gap <= static_cast<double>(gam) * __dadd_rn(ef, bf)) {
-            push(sc, gcol, cap, s0, bf);
-            push(sc, gcol, cap, fs, ef);
-            nc |= kTieFixed;
+            sc.tie_s[gcol * kTieMax] = s0, sc.tie_e[gcol * kTieMax] = bf;
+            sc.tie_s[gcol * kTieMax + 1] = fs, sc.tie_e[gcol * kTieMax + 1] = ef;
+            nc = 2 | kTieFixed;
         }
     }
-};
+    sc.tie_n[gcol] = nc;
+}
 
 // Smallest float x with level(x) >= v at scale s: RN(x*inv) >= t (> t for
 // v <= 0), t = v - 1/2. Candidates start at RN32(t*s) (t*s is exact in
@@ -605,7 +608,7 @@ __global__ void __launch_bounds__(THREADS) k_qsort_tables(const TDesc* __restric
 // columns per warp divides it; the TPL searches of a lane are independent
 // (ILP). The tables are read through L1 (a step touches a few lines per
 // threshold), so occupancy is bounded by registers only.
-template <int G, int TPL>
+template <int G, int TPL, bool FIXED>
 __global__ void __launch_bounds__(256, 4) k_qrange_tables(const TDesc* __restrict__ td,
                                                        const K3Group* __restrict__ groups, int nslots, int cpb,
                                                        int dstride, int tstride, const double* __restrict__ tables,
@@ -633,15 +636,17 @@ __global__ void __launch_bounds__(256, 4) k_qrange_tables(const TDesc* __restric
     double s_rtn = static_cast<double>(__double2float_rn(s0_raw));
     double s_fin = s_rtn;
     const int64_t gcol = live ? td[g.tensor].col_base + g.col0 + cc : 0;
-    TieTrack tie{0};
+    if (live && gl == 0) sc.tie_n[gcol] = 0;
     if (cfg.mode == EZQ_MODE_EASYQUANT) {  // uniform across the warp
         double s = snap(s0_raw);
         const double s0 = s;
         double m = 0.0, vv = 0.0;
-        DD e0 = {0.0, 0.0}, best_err = {0.0, 0.0}, fixed_err = {0.0, 0.0};
+        // BEST: best_err / best_s is the running best (strict <); FIXED:
+        // best_err / best_s hold e0 / s0, fixed_err / fixed_s the chosen step
+        DD best_err = {0.0, 0.0}, fixed_err = {0.0, 0.0};
         double best_s = s, fixed_s = s;
         const float gam = tie_gamma(n);
-        const bool track = cfg.tie_cap > 0 && cfg.select != EZQ_SELECT_FIXED;
+        const bool track = !FIXED && cfg.tie_cap > 0;
         double tie_thr = 0.0;
         bool own[TPL];
         int jl[TPL], wA[TPL], ib[TPL];
@@ -693,33 +698,33 @@ __global__ void __launch_bounds__(256, 4) k_qrange_tables(const TDesc* __restric
             const DD err = err_minus_c(Ad, q, s);
             const double grad = 2.0 * __dsub_rn(__dmul_rn(Ad, s), q);  // A s exact
             if (t == 0) {
-                e0 = err;
                 best_err = err;
                 fixed_err = err;
-                tie_thr = tie_threshold(err.hi, ci.chi, gam);
-            } else {
+                if (track) tie_thr = tie_threshold(err.hi, infos[slot].chi, gam);
+            } else if (!FIXED) {
                 const bool lt = dd_lt(err, best_err);  // strict: earliest minimum wins (optimize.cpp:158)
                 if (track && (lt || err.hi <= tie_thr)) {  // rare: a new best or a near one
-                    const double cf = ci.chi;
-                    tie.step(live && gl == 0, sc, gcol, cfg.tie_cap, lt, err, best_err, s, best_s, gam, cf);
+                    const double cf = infos[slot].chi;
+                    if (live && gl == 0)
+                        tie_step(sc, gcol, cfg.tie_cap, lt, err.hi, err.lo, best_err.hi, best_err.lo, s, best_s, gam, cf);
                     if (lt) tie_thr = tie_threshold(err.hi, cf, gam);
                 }
                 if (lt) {
                     best_err = err;
                     best_s = s;
                 }
-                if (t == cfg.fixed_at) {
-                    fixed_s = s;
-                    fixed_err = err;
-                }
+            } else if (t == cfg.fixed_at) {
+                fixed_s = s;
+                fixed_err = err;
             }
             if (t == cfg.steps) break;
             s = snap(adam_update_tab(m, vv, s, grad, cfg.bc1[t + 1], cfg.bc2[t + 1], cfg.rbc1[t + 1],
                                      cfg.rbc2[t + 1], cfg.adam));
         }
-        if (cfg.select == EZQ_SELECT_FIXED) {
-            s_fin = dd_le(fixed_err, e0) ? fixed_s : s0;  // optimize.cpp:169-178
-            if (cfg.tie_cap > 0) tie.fixed(live && gl == 0, sc, gcol, cfg.tie_cap, fixed_err, e0, fixed_s, s0, gam, ci.chi);
+        if (FIXED) {
+            s_fin = dd_le(fixed_err, best_err) ? fixed_s : s0;  // optimize.cpp:169-178 (best_err = e0)
+            if (cfg.tie_cap > 0 && live && gl == 0)
+                tie_fixed(sc, gcol, fixed_err.hi, fixed_err.lo, best_err.hi, best_err.lo, fixed_s, s0, gam, infos[slot].chi);
         } else {
             s_fin = best_s;
         }
@@ -728,7 +733,8 @@ __global__ void __launch_bounds__(256, 4) k_qrange_tables(const TDesc* __restric
     if (live && gl == 0) {
         sc.s_rtn[gcol] = s_rtn;
         sc.s_fin[gcol] = s_fin;
-        sc.tie_n[gcol] = (tie.nc & (kTieFixed - 1)) >= 2 ? tie.nc : 0;  // one entry: the best itself
+        const int nc = sc.tie_n[gcol];
+        if ((nc & (kTieFixed - 1)) < 2) sc.tie_n[gcol] = 0;  // one entry: the best itself
     }
 }
 
@@ -740,8 +746,12 @@ void launch_loop_t(int64_t nslots64, int cpb, int dstride, int tstride, const TD
     const int nslots = static_cast<int>(nslots64);
     const int warps = (nslots + CPW - 1) / CPW;
     const int grid = (warps + 7) / 8;
-    k_qrange_tables<G, TPL><<<grid, 256, 0, st>>>(td, groups, nslots, cpb, dstride, tstride, tables, infos,
-                                                          sc, cfg);
+    if (cfg.select == EZQ_SELECT_FIXED)
+        k_qrange_tables<G, TPL, true><<<grid, 256, 0, st>>>(td, groups, nslots, cpb, dstride, tstride, tables, infos,
+                                                            sc, cfg);
+    else
+        k_qrange_tables<G, TPL, false><<<grid, 256, 0, st>>>(td, groups, nslots, cpb, dstride, tstride, tables, infos,
+                                                             sc, cfg);
 }
 
 // ---- K3s-b for row pieces / k = 5: one column per warp ------------------------
@@ -750,7 +760,7 @@ void launch_loop_t(int64_t nslots64, int cpb, int dstride, int tstride, const TD
 // l takes pairs l, l + 32, ... (PPL per lane) and the warp butterfly sums A
 // and Q -- exact, as every term is (same argument as above). Slots: column c
 // of column group g, piece p is slot (g * P + p) * cpb + c.
-template <int PPL>
+template <int PPL, bool FIXED>
 __global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__ td,
                                                        const K3Group* __restrict__ groups, int ncolgroups, int P,
                                                        int cpb, int dstride, int tstride,
@@ -776,15 +786,15 @@ __global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__
     double s_rtn = static_cast<double>(__double2float_rn(s0_raw));
     double s_fin = s_rtn;
     const int64_t gcol = td[G0.tensor].col_base + G0.col0 + cc;
-    TieTrack tie{0};
+    if (lane == 0) sc.tie_n[gcol] = 0;
     if (cfg.mode == EZQ_MODE_EASYQUANT) {  // uniform across the warp
         double s = snap(s0_raw);
         const double s0 = s;
         double m = 0.0, vv = 0.0;
-        DD e0 = {0.0, 0.0}, best_err = {0.0, 0.0}, fixed_err = {0.0, 0.0};
+        DD best_err = {0.0, 0.0}, fixed_err = {0.0, 0.0};  // FIXED: best_err holds e0
         double best_s = s, fixed_s = s;
         const float gam = tie_gamma(nall);
-        const bool track = cfg.tie_cap > 0 && cfg.select != EZQ_SELECT_FIXED;
+        const bool track = !FIXED && cfg.tie_cap > 0;
         double tie_thr = 0.0;
         bool own[PPL];
         int jl[PPL], np[PPL], ib[PPL];
@@ -836,32 +846,32 @@ __global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__
             const DD err = err_minus_c(Ad, q, s);
             const double grad = 2.0 * __dsub_rn(__dmul_rn(Ad, s), q);  // A s exact
             if (t == 0) {
-                e0 = err;
                 best_err = err;
                 fixed_err = err;
-                tie_thr = tie_threshold(err.hi, call, gam);
-            } else {
+                if (track) tie_thr = tie_threshold(err.hi, call, gam);
+            } else if (!FIXED) {
                 const bool lt = dd_lt(err, best_err);  // strict: earliest minimum wins (optimize.cpp:158)
                 if (track && (lt || err.hi <= tie_thr)) {  // rare: a new best or a near one
-                    tie.step(lane == 0, sc, gcol, cfg.tie_cap, lt, err, best_err, s, best_s, gam, call);
+                    if (lane == 0)
+                        tie_step(sc, gcol, cfg.tie_cap, lt, err.hi, err.lo, best_err.hi, best_err.lo, s, best_s, gam, call);
                     if (lt) tie_thr = tie_threshold(err.hi, call, gam);
                 }
                 if (lt) {
                     best_err = err;
                     best_s = s;
                 }
-                if (t == cfg.fixed_at) {
-                    fixed_s = s;
-                    fixed_err = err;
-                }
+            } else if (t == cfg.fixed_at) {
+                fixed_s = s;
+                fixed_err = err;
             }
             if (t == cfg.steps) break;
             s = snap(adam_update_tab(m, vv, s, grad, cfg.bc1[t + 1], cfg.bc2[t + 1], cfg.rbc1[t + 1],
                                      cfg.rbc2[t + 1], cfg.adam));
         }
-        if (cfg.select == EZQ_SELECT_FIXED) {
-            s_fin = dd_le(fixed_err, e0) ? fixed_s : s0;  // optimize.cpp:169-178
-            if (cfg.tie_cap > 0) tie.fixed(lane == 0, sc, gcol, cfg.tie_cap, fixed_err, e0, fixed_s, s0, gam, call);
+        if (FIXED) {
+            s_fin = dd_le(fixed_err, best_err) ? fixed_s : s0;  // optimize.cpp:169-178 (best_err = e0)
+            if (cfg.tie_cap > 0 && lane == 0)
+                tie_fixed(sc, gcol, fixed_err.hi, fixed_err.lo, best_err.hi, best_err.lo, fixed_s, s0, gam, call);
         } else {
             s_fin = best_s;
         }
@@ -870,7 +880,8 @@ __global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__
     if (lane == 0) {
         sc.s_rtn[gcol] = s_rtn;
         sc.s_fin[gcol] = s_fin;
-        sc.tie_n[gcol] = (tie.nc & (kTieFixed - 1)) >= 2 ? tie.nc : 0;  // one entry: the best itself
+        const int nc = sc.tie_n[gcol];
+        if ((nc & (kTieFixed - 1)) < 2) sc.tie_n[gcol] = 0;  // one entry: the best itself
     }
 }
 
@@ -880,8 +891,12 @@ void launch_pieces_t(int ncolgroups, int P, int cpb, int dstride, int tstride, c
                      const CfgDev& cfg, cudaStream_t st) {
     const int64_t cols = static_cast<int64_t>(ncolgroups) * cpb;  // one warp each
     const int grid = static_cast<int>((cols + 7) / 8);
-    k_qrange_pieces<PPL><<<grid, 256, 0, st>>>(td, groups, ncolgroups, P, cpb, dstride, tstride, tables, infos, sc,
-                                                cfg);
+    if (cfg.select == EZQ_SELECT_FIXED)
+        k_qrange_pieces<PPL, true><<<grid, 256, 0, st>>>(td, groups, ncolgroups, P, cpb, dstride, tstride, tables,
+                                                         infos, sc, cfg);
+    else
+        k_qrange_pieces<PPL, false><<<grid, 256, 0, st>>>(td, groups, ncolgroups, P, cpb, dstride, tstride, tables,
+                                                          infos, sc, cfg);
 }
 
 // ---- Grid oracle on the tables (brute_force_optimal_scale, optimize.cpp:186-229)
