@@ -102,20 +102,19 @@ __device__ __forceinline__ float tie_gamma(int n) {
 __device__ __forceinline__ double tie_threshold(double best, double cfull, float gam) {
     return __dadd_rn(best, static_cast<double>(gam) * 2.0002 * __dadd_rn(best, cfull));
 }
-// Candidate bookkeeping of one column, kept by its writer lane in global
-// memory (sc.tie_n[gcol] is the running count), so the hot loop holds no
-// extra state beyond the pre-filter threshold. best/err are err - C; cfull
+// Candidate bookkeeping of one column, kept by its writer lane (the running
+// count in a register; the list in global memory, touched only by near
+// steps). best/err are err - C; cfull
 // = C (an estimate) converts to full errors. The list (sc.tie_s / tie_e,
 // step order) holds the distinct scales whose exact errors lie within the
 // bound of the running best: a new best drops the entries now beyond it (the
 // filter reads back the writer's own stores), a far new best empties it.
 // count > cap: a candidate was lost (the column takes the whole-loop
 // fallback). Out of line: the slow path's registers stay out of the loop.
-__device__ __forceinline__ void tie_step(const Scratch& sc, int64_t gcol, int cap, bool lt, double err_hi, double err_lo,
-                                      double best_hi, double best_lo, double s, double best_s, float gam,
-                                      double cfull) {
+__device__ __forceinline__ void tie_step(int& nc, const Scratch& sc, int64_t gcol, int cap, bool lt, double err_hi,
+                                         double err_lo, double best_hi, double best_lo, double s, double best_s,
+                                         float gam, double cfull) {
     if (!lt && s == best_s) return;  // same scale: same error in both orders
-    int nc = sc.tie_n[gcol];
     double* ts = sc.tie_s + gcol * kTieMax;
     double* te = sc.tie_e + gcol * kTieMax;
     const double gap = fabs(__dadd_rn(__dsub_rn(err_hi, best_hi), __dsub_rn(err_lo, best_lo)));
@@ -143,7 +142,6 @@ __device__ __forceinline__ void tie_step(const Scratch& sc, int64_t gcol, int ca
     } else if (lt) {
         nc = 0;  // every earlier candidate is now beyond the bound
     }
-    sc.tie_n[gcol] = nc;
 }
 
 // fixed-step selection (optimize.cpp:169-178): fixed_err <= e0 inside the bound
@@ -637,6 +635,7 @@ __global__ void __launch_bounds__(256, 4) k_qrange_tables(const TDesc* __restric
     double s_fin = s_rtn;
     const int64_t gcol = live ? td[g.tensor].col_base + g.col0 + cc : 0;
     if (live && gl == 0) sc.tie_n[gcol] = 0;
+    int tie_nc_out = 0;
     if (cfg.mode == EZQ_MODE_EASYQUANT) {  // uniform across the warp
         double s = snap(s0_raw);
         const double s0 = s;
@@ -648,6 +647,7 @@ __global__ void __launch_bounds__(256, 4) k_qrange_tables(const TDesc* __restric
         const float gam = tie_gamma(n);
         const bool track = !FIXED && cfg.tie_cap > 0;
         double tie_thr = 0.0;
+        int tie_nc = 0;
         bool own[TPL];
         int jl[TPL], wA[TPL], ib[TPL];
         float Xp[TPL], span[TPL];  // previous threshold; x[k0+7] - x[k0] near it
@@ -706,7 +706,8 @@ __global__ void __launch_bounds__(256, 4) k_qrange_tables(const TDesc* __restric
                 if (track && (lt || err.hi <= tie_thr)) {  // rare: a new best or a near one
                     const double cf = infos[slot].chi;
                     if (live && gl == 0)
-                        tie_step(sc, gcol, cfg.tie_cap, lt, err.hi, err.lo, best_err.hi, best_err.lo, s, best_s, gam, cf);
+                        tie_step(tie_nc, sc, gcol, cfg.tie_cap, lt, err.hi, err.lo, best_err.hi, best_err.lo, s, best_s,
+                                 gam, cf);
                     if (lt) tie_thr = tie_threshold(err.hi, cf, gam);
                 }
                 if (lt) {
@@ -727,14 +728,14 @@ __global__ void __launch_bounds__(256, 4) k_qrange_tables(const TDesc* __restric
                 tie_fixed(sc, gcol, fixed_err.hi, fixed_err.lo, best_err.hi, best_err.lo, fixed_s, s0, gam, infos[slot].chi);
         } else {
             s_fin = best_s;
+            tie_nc_out = tie_nc;
         }
         s_rtn = s0;
     }
     if (live && gl == 0) {
         sc.s_rtn[gcol] = s_rtn;
         sc.s_fin[gcol] = s_fin;
-        const int nc = sc.tie_n[gcol];
-        if ((nc & (kTieFixed - 1)) < 2) sc.tie_n[gcol] = 0;  // one entry: the best itself
+        if (cfg.select != EZQ_SELECT_FIXED) sc.tie_n[gcol] = tie_nc_out >= 2 ? tie_nc_out : 0;  // 1: the best itself
     }
 }
 
@@ -787,6 +788,7 @@ __global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__
     double s_fin = s_rtn;
     const int64_t gcol = td[G0.tensor].col_base + G0.col0 + cc;
     if (lane == 0) sc.tie_n[gcol] = 0;
+    int tie_nc_out = 0;
     if (cfg.mode == EZQ_MODE_EASYQUANT) {  // uniform across the warp
         double s = snap(s0_raw);
         const double s0 = s;
@@ -796,6 +798,7 @@ __global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__
         const float gam = tie_gamma(nall);
         const bool track = !FIXED && cfg.tie_cap > 0;
         double tie_thr = 0.0;
+        int tie_nc = 0;
         bool own[PPL];
         int jl[PPL], np[PPL], ib[PPL];
         ColTab ct[PPL];
@@ -853,7 +856,8 @@ __global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__
                 const bool lt = dd_lt(err, best_err);  // strict: earliest minimum wins (optimize.cpp:158)
                 if (track && (lt || err.hi <= tie_thr)) {  // rare: a new best or a near one
                     if (lane == 0)
-                        tie_step(sc, gcol, cfg.tie_cap, lt, err.hi, err.lo, best_err.hi, best_err.lo, s, best_s, gam, call);
+                        tie_step(tie_nc, sc, gcol, cfg.tie_cap, lt, err.hi, err.lo, best_err.hi, best_err.lo, s, best_s,
+                                 gam, call);
                     if (lt) tie_thr = tie_threshold(err.hi, call, gam);
                 }
                 if (lt) {
@@ -874,14 +878,14 @@ __global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__
                 tie_fixed(sc, gcol, fixed_err.hi, fixed_err.lo, best_err.hi, best_err.lo, fixed_s, s0, gam, call);
         } else {
             s_fin = best_s;
+            tie_nc_out = tie_nc;
         }
         s_rtn = s0;
     }
     if (lane == 0) {
         sc.s_rtn[gcol] = s_rtn;
         sc.s_fin[gcol] = s_fin;
-        const int nc = sc.tie_n[gcol];
-        if ((nc & (kTieFixed - 1)) < 2) sc.tie_n[gcol] = 0;  // one entry: the best itself
+        if (cfg.select != EZQ_SELECT_FIXED) sc.tie_n[gcol] = tie_nc_out >= 2 ? tie_nc_out : 0;  // 1: the best itself
     }
 }
 

@@ -8,7 +8,8 @@ import json
 
 ap = argparse.ArgumentParser()
 ap.add_argument("csv")
-ap.add_argument("--colsteps", type=float, default=0)
+ap.add_argument("--colsteps", type=float, default=0, help="K3s loop column-steps over all calls in the list")
+ap.add_argument("--calls", type=int, default=1, help="quantize_batch calls in the list")
 a = ap.parse_args()
 lines = open(a.csv).read().splitlines()
 start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
@@ -36,7 +37,13 @@ for k, v in sorted(tot.items(), key=lambda x: -x[1]["gpu__time_duration.sum"]):
     print(f"{k:26s} n={v['n']:3d} {ms:8.3f} ms ({100 * ms / (allt / 1e6):5.1f}%) inst={v['smsp__inst_executed.sum']:.3e} "
           f"rd={v['dram__bytes_read.sum'] / 1e9:.2f} GB wr={v['dram__bytes_write.sum'] / 1e9:.2f} GB")
 print(f"total {allt / 1e6:.3f} ms")
-if a.colsteps and "k_qrange_tables" in out:
-    q = out["k_qrange_tables"]
-    print(json.dumps({"loop_inst_per_colstep": q["inst"] / a.colsteps,
-                      "loop_dram_bytes_per_launch": (q["dram_read"] + q["dram_write"]) / q["launches"]}))
+if a.colsteps:
+    loops = [out[k] for k in ("k_qrange_tables", "k_qrange_pieces") if k in out]
+    inst = sum(q["inst"] for q in loops)
+    launches = sum(q["launches"] for q in loops)
+    dram = sum(q["dram_read"] + q["dram_write"] for q in loops)
+    step_dram = sum(v["dram_read"] + v["dram_write"] for v in out.values()) / max(a.calls, 1)
+    print(json.dumps({"loop_inst_per_colstep": inst / a.colsteps,
+                      "loop_dram_bytes_per_launch": dram / max(launches, 1),
+                      "step_dram_bytes": step_dram,
+                      "column_steps": a.colsteps, "calls": a.calls}))
