@@ -96,11 +96,14 @@ __device__ __forceinline__ DD err_minus_c(double Ad, double q, double s) {
 __device__ __forceinline__ float tie_gamma(int n) {
     return (static_cast<float>(n) + 8.0f) * 1.1102230246251565e-16f * 1.01f;
 }
-// Pre-filter of the per-step check: an error above best + gamma (2 best + 2 C)
-// (with slack) can be neither a new best nor near one, so the hot loop pays
-// one compare per step; TieTrack::step runs only below it.
-__device__ __forceinline__ double tie_threshold(double best, double cfull, float gam) {
-    return __dadd_rn(best, static_cast<double>(gam) * 2.0002 * __dadd_rn(best, cfull));
+// Pre-filter of the per-step check: the window best -/+ gamma (2 best + 2 C)
+// (with slack) around the running best; a step outside it is certified
+// (a far new best only empties the list), so the hot loop pays one compare
+// per step and tie_step runs only inside it.
+__device__ __forceinline__ void tie_window(double best, double cfull, float gam, double& lo, double& hi) {
+    const double w = static_cast<double>(gam) * 2.0002 * __dadd_rn(best, cfull);
+    lo = __dsub_rn(best, w);  // a new best at or above lo is near the old one
+    hi = __dadd_rn(best, w);  // a later step at or below hi is near the best
 }
 // Candidate bookkeeping of one column, kept by its writer lane (the running
 // count in a register; the list in global memory, touched only by near
@@ -646,7 +649,8 @@ __global__ void __launch_bounds__(256, 4) k_qrange_tables(const TDesc* __restric
         double best_s = s, fixed_s = s;
         const float gam = tie_gamma(n);
         const bool track = !FIXED && cfg.tie_cap > 0;
-        double tie_thr = 0.0;
+        const double cfull = ci.chi;
+        double tie_thr = 0.0, tie_lo = 0.0;
         int tie_nc = 0;
         bool own[TPL];
         int jl[TPL], wA[TPL], ib[TPL];
@@ -700,19 +704,21 @@ __global__ void __launch_bounds__(256, 4) k_qrange_tables(const TDesc* __restric
             if (t == 0) {
                 best_err = err;
                 fixed_err = err;
-                if (track) tie_thr = tie_threshold(err.hi, infos[slot].chi, gam);
+                if (track) tie_window(err.hi, cfull, gam, tie_lo, tie_thr);
             } else if (!FIXED) {
                 const bool lt = dd_lt(err, best_err);  // strict: earliest minimum wins (optimize.cpp:158)
-                if (track && (lt || err.hi <= tie_thr)) {  // rare: a new best or a near one
-                    const double cf = infos[slot].chi;
+                // near the running best (from above or, as a new best, from below)?
+                if (track && (lt ? err.hi >= tie_lo : err.hi <= tie_thr)) {  // rare
                     if (live && gl == 0)
                         tie_step(tie_nc, sc, gcol, cfg.tie_cap, lt, err.hi, err.lo, best_err.hi, best_err.lo, s, best_s,
-                                 gam, cf);
-                    if (lt) tie_thr = tie_threshold(err.hi, cf, gam);
+                                 gam, infos[slot].chi);
+                } else if (lt) {
+                    tie_nc = 0;  // a far new best: every earlier candidate is beyond the bound
                 }
                 if (lt) {
                     best_err = err;
                     best_s = s;
+                    if (track) tie_window(err.hi, cfull, gam, tie_lo, tie_thr);
                 }
             } else if (t == cfg.fixed_at) {
                 fixed_s = s;
@@ -797,7 +803,7 @@ __global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__
         double best_s = s, fixed_s = s;
         const float gam = tie_gamma(nall);
         const bool track = !FIXED && cfg.tie_cap > 0;
-        double tie_thr = 0.0;
+        double tie_thr = 0.0, tie_lo = 0.0;
         int tie_nc = 0;
         bool own[PPL];
         int jl[PPL], np[PPL], ib[PPL];
@@ -851,18 +857,20 @@ __global__ void __launch_bounds__(256) k_qrange_pieces(const TDesc* __restrict__
             if (t == 0) {
                 best_err = err;
                 fixed_err = err;
-                if (track) tie_thr = tie_threshold(err.hi, call, gam);
+                if (track) tie_window(err.hi, call, gam, tie_lo, tie_thr);
             } else if (!FIXED) {
                 const bool lt = dd_lt(err, best_err);  // strict: earliest minimum wins (optimize.cpp:158)
-                if (track && (lt || err.hi <= tie_thr)) {  // rare: a new best or a near one
+                if (track && (lt ? err.hi >= tie_lo : err.hi <= tie_thr)) {  // rare: near the running best
                     if (lane == 0)
                         tie_step(tie_nc, sc, gcol, cfg.tie_cap, lt, err.hi, err.lo, best_err.hi, best_err.lo, s, best_s,
                                  gam, call);
-                    if (lt) tie_thr = tie_threshold(err.hi, call, gam);
+                } else if (lt) {
+                    tie_nc = 0;  // a far new best
                 }
                 if (lt) {
                     best_err = err;
                     best_s = s;
+                    if (track) tie_window(err.hi, call, gam, tie_lo, tie_thr);
                 }
             } else if (t == cfg.fixed_at) {
                 fixed_s = s;
