@@ -32,7 +32,7 @@
 // tile's 64-row blocks in turn with plain coalesced 16-byte loads,
 // software-pipelined one block ahead. The warps' fragments are reduced
 // through shared memory in fixed order (deterministic). The outlier term is
-// summed by a dedicated outlier warp of the same CTA (see k_gemv_cb) whose gathers
+// a second, programmatic-dependent launch (k_gemv_outliers) whose gathers
 // overlap the weight stream.
 //
 // Measured on B200 (tools/microbench/dequant_mma.cu): the dequant + MMA loop
@@ -187,16 +187,7 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const unsigned (&a)[4], 
 constexpr int kCW = 4;             // consumer warps per CTA
 constexpr int kRing = 3;           // ring stages per CTA
 constexpr int kStageCode = 8192;   // code bytes per full stage
-constexpr int kStreamThreads = (kCW + 1) * 32;   // consumers + the TMA producer
-constexpr int kOutThreads = (kCW + 2) * 32;      // + the outlier warp (plans with outliers)
-
-// Outlier values: f32 (exact) or f16 (ezq_gemv_prepare_ex; 6 bytes per
-// outlier instead of 8, held to the GEMV's 1e-3 gate).
-template <int VT>
-__device__ __forceinline__ float load_val(const void* v, int64_t e) {
-    if (VT == 1) return __half2float(static_cast<const __half*>(v)[e]);
-    return static_cast<const float*>(v)[e];
-}
+constexpr int kStreamThreads = (kCW + 1) * 32;
 
 struct GemvArgs {
     const uint4* T;
@@ -209,13 +200,6 @@ struct GemvArgs {
     int64_t xstride;   // elements between batch rows of x
     int batch;         // rows of this group (1..16)
     float* y;
-    // isolated outliers (CSC by column), applied by the outlier warp
-    int has_out;
-    int vt;                 // outlier value dtype: 0 f32, 1 f16
-    const int64_t* col_ptr;
-    const uint32_t* out_row;
-    const void* out_val;
-    const float* xt;        // batch > 1: x transposed [rows][16] f32
 };
 
 __device__ __forceinline__ void bar_wait(unsigned bar, unsigned phase) {
@@ -249,14 +233,13 @@ struct CbGeom {
     // exactly (C = 128 - lmin), D' = D + C * sum(x) corrected at the end
     static constexpr bool SUBFREE = SF && XT != kF16 && NB == 1;
     static constexpr size_t smem() {
-        return static_cast<size_t>(kRing) * (CB + XB) + (2 * kRing + 4) * 8 +
-               (QW > 1 ? static_cast<size_t>(kCW) * NB * 32 * 4 * sizeof(float) : 0) + 16 * sizeof(float) +
-               2 * static_cast<size_t>(16 * TPC) * NBT * sizeof(float) + 16;
+        return static_cast<size_t>(kRing) * (CB + XB) + 2 * kRing * 8 +
+               (QW > 1 ? static_cast<size_t>(kCW) * NB * 32 * 4 * sizeof(float) : 0) + 16 * sizeof(float) + 16;
     }
 };
 
 template <int TPC, int NB, int XT, bool SF>
-__global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
+__global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
     using Gm = CbGeom<TPC, NB, XT, SF>;
     constexpr bool F16 = XT == kF16;
     constexpr int ES = Gm::ES, NBT = Gm::NBT, S = Gm::S, XP = Gm::XP, XB = Gm::XB, CB = Gm::CB;
@@ -265,80 +248,21 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
     unsigned char* codes = smem;                     // [kRing][S][TPC][512]
     unsigned char* xsm = smem + kRing * CB;          // [kRing][NBT][XP]
     unsigned long long* bars = reinterpret_cast<unsigned long long*>(xsm + kRing * XB);
-    float* red = reinterpret_cast<float*>(bars + 2 * kRing + 4);  // [kCW][NB][32][4] (QW > 1)
+    float* red = reinterpret_cast<float*>(bars + 2 * kRing);  // [kCW][NB][32][4] (QW > 1)
     float* xsum = red + (QW > 1 ? kCW * NB * 32 * 4 : 0);      // [16] sum_i x[n][i] (SUBFREE)
-    float* oacc = xsum + 16;                                  // [2][16 TPC][NBT] outlier sums per colblock
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned full0 = static_cast<unsigned>(__cvta_generic_to_shared(bars));
     const unsigned empty0 = full0 + 8 * kRing;
-    const unsigned ofull0 = empty0 + 8 * kRing, oempty0 = ofull0 + 16;
     if (threadIdx.x == 0) {
         for (int k = 0; k < kRing; ++k) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full0 + 8 * k));  // expect_tx arrival
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * k), "r"(kCW + 1));
-        }
-        for (int b = 0; b < 2; ++b) {  // outlier-sum double buffer: full (outlier warp), empty (consumers)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;" ::"r"(empty0 + 8 * kRing + 8 * b));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * kRing + 16 + 8 * b), "r"(kCW * 32));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     asm volatile("griddepcontrol.launch_dependents;");
     const int64_t nst_cb = (a.kq + S - 1) / S;  // stages per colblock
-
-    constexpr int nthr = (kCW + 1) * 32;  // named barrier 2: consumers + producer
-    if (warp == kCW + 1) {  // ---- outlier warp (plans with isolated outliers)
-        // Per colblock: lane l sums its columns' CSC entries (fixed order:
-        // deterministic) y_o[c][n] = sum_e v_e x[n][r_e] into a shared
-        // double buffer, overlapped with the consumers' K loop; the
-        // consumers add it at their flush (barrier 3), and release the
-        // buffer (barrier 4) before it is rewritten two colblocks later.
-        constexpr int kE = 8;  // entries in flight per lane
-        int kk = 0;
-        for (int64_t cb = blockIdx.x; cb < a.ncb; cb += gridDim.x, ++kk) {
-            float* ob = oacc + (kk & 1) * (16 * TPC * NBT);
-            if (kk >= 2) bar_wait(oempty0 + 8 * (kk & 1), ((kk >> 1) - 1) & 1);
-            for (int cl = lane; cl < 16 * TPC; cl += 32) {
-                const int64_t c = cb * 16 * TPC + cl;
-                float acc[NBT];
-#pragma unroll
-                for (int n = 0; n < NBT; ++n) acc[n] = 0.f;
-                if (c < a.cols) {
-                    const int64_t e0 = __ldg(a.col_ptr + c), e1 = __ldg(a.col_ptr + c + 1);
-                    for (int64_t e = e0; e < e1; e += kE) {
-                        uint32_t r[kE];
-                        float v[kE];
-#pragma unroll
-                        for (int u = 0; u < kE; ++u) {
-                            const bool ok = e + u < e1;
-                            r[u] = ok ? __ldg(a.out_row + e + u) : 0u;
-                            v[u] = ok ? (a.vt ? load_val<1>(a.out_val, e + u) : load_val<0>(a.out_val, e + u)) : 0.f;
-                        }
-                        if (a.batch == 1) {
-#pragma unroll
-                            for (int u = 0; u < kE; ++u) acc[0] = fmaf(v[u], load_x(a.x, XT, r[u]), acc[0]);
-                        } else {
-#pragma unroll
-                            for (int u = 0; u < kE; ++u)
-#pragma unroll
-                                for (int n4 = 0; n4 < NBT / 4; ++n4) {
-                                    const float4 xv = __ldg(reinterpret_cast<const float4*>(a.xt + static_cast<int64_t>(r[u]) * 16) + n4);
-                                    acc[4 * n4] = fmaf(v[u], xv.x, acc[4 * n4]);
-                                    acc[4 * n4 + 1] = fmaf(v[u], xv.y, acc[4 * n4 + 1]);
-                                    acc[4 * n4 + 2] = fmaf(v[u], xv.z, acc[4 * n4 + 2]);
-                                    acc[4 * n4 + 3] = fmaf(v[u], xv.w, acc[4 * n4 + 3]);
-                                }
-                        }
-                    }
-                }
-#pragma unroll
-                for (int n = 0; n < NBT; ++n) ob[cl * NBT + n] = acc[n];
-            }
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ofull0 + 8 * (kk & 1)) : "memory");
-        }
-        return;
-    }
 
     if (warp == kCW) {  // ---- producer warp: codes and x slices by TMA bulk copies
         // SUBFREE: while the CTA's first colblock streams, the producer also
@@ -383,7 +307,7 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
                 if (lane == 0) xsum[n] = v;
             }
             __syncwarp();
-            asm volatile("bar.arrive 2, %0;" ::"r"(nthr) : "memory");
+            asm volatile("bar.arrive 2, %0;" ::"r"(kStreamThreads) : "memory");
         };
         const int first_n = static_cast<int>(nst_cb);  // stages of the first colblock
         int k = 0;
@@ -445,7 +369,7 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
     for (int n8 = 0; n8 < NB; ++n8) xrow[n8] = min(n8 * 8 + g, a.batch - 1);
     const int tile0 = TPC >= kCW ? warp : warp % TPC;
     const int qoff = TPC >= kCW ? 0 : warp / TPC;
-    int k = 0, kk_cb = 0;
+    int k = 0;
     for (int64_t cb = blockIdx.x; cb < a.ncb; cb += gridDim.x) {
         float acc[TW][2][NB][4];  // two accumulator sets per tile (alternating q) break the MMA chain
 #pragma unroll
@@ -514,7 +438,7 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
             for (int n8 = 0; n8 < NB; ++n8)
 #pragma unroll
                 for (int i = 0; i < 4; ++i) d[u][n8][i] = acc[u][0][n8][i] + acc[u][1][n8][i];
-        if (Gm::SUBFREE && cb == blockIdx.x) named_sync(2, nthr);  // xsum published by the producer
+        if (Gm::SUBFREE && cb == blockIdx.x) named_sync(2, kStreamThreads);  // xsum published by the producer
         bool writer = true;
         if (QW > 1) {
 #pragma unroll
@@ -536,8 +460,6 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
             }
             named_sync(1, kCW * 32);  // red is reused by the next colblock
         }
-        const float* ob = oacc + (kk_cb & 1) * (16 * TPC * NBT);
-        if (a.has_out) bar_wait(ofull0 + 8 * (kk_cb & 1), (kk_cb >> 1) & 1);  // the outlier warp's sums are in ob
         if (writer) {
             if (Gm::SUBFREE) {  // D' = D + C sum(x): remove the offset once per output element
                 const float C = static_cast<float>(128 - a.lmin);
@@ -554,15 +476,10 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
                     for (int q = 0; q < 4; ++q) {
                         const int64_t jc = (cb * TPC + tile0 + u * kCW) * kTileCols + g + (q >= 2 ? 8 : 0);
                         const int n = n8 * 8 + 2 * t + (q & 1);
-                        if (jc < a.cols && n < a.batch) {
-                            float yv = a.scales[jc] * d[u][n8][q];
-                            if (a.has_out) yv += ob[((tile0 + u * kCW) * kTileCols + g + (q >= 2 ? 8 : 0)) * NBT + n];
-                            a.y[static_cast<int64_t>(n) * a.cols + jc] = yv;
-                        }
+                        if (jc < a.cols && n < a.batch)
+                            a.y[static_cast<int64_t>(n) * a.cols + jc] = a.scales[jc] * d[u][n8][q];
                     }
         }
-        if (a.has_out) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(oempty0 + 8 * (kk_cb & 1)) : "memory");
-        ++kk_cb;
     }
 }
 
@@ -580,8 +497,17 @@ __global__ void k_gemv_xpad(const void* __restrict__ x, int es, int64_t rows, in
         static_cast<unsigned short*>(xp)[i] = r < rows ? static_cast<const unsigned short*>(x)[n * rows + r] : 0;
 }
 
+// Outlier term: y[n, j] += sum_{e in column j} x[n, row_e] * v_e. One warp
+// per column; the lanes take the column's CSC entries 32 apart, with kU
+// entries per lane loaded independently per round (one round covers 128
+// entries, i.e. a 1%-outlier column of up to 12.8k rows), and the partials
+// are combined by a fixed xor-butterfly (deterministic). NBT = batch rows
+// rounded up to 1, 8 or 16 (fully unrolled, predicated on `batch`).
+// Launched as a programmatic dependent of k_gemv_mma: the gathers overlap
+// the weight stream and griddepcontrol.wait orders the read-modify-write
+// of y after the main kernel's stores.
 // x [batch][rows] (any dtype) -> xt [rows][16] f32 (exact), so the outlier
-// warp reads a row's batch values with NBT/4 16-byte loads instead of NBT
+// pass reads a row's batch values with NBT/4 16-byte loads instead of NBT
 // scalar gathers.
 __global__ void __launch_bounds__(256) k_gemv_xt(const void* __restrict__ x, int xt_type, int64_t rows, int batch,
                                                  float* __restrict__ xt) {
@@ -590,7 +516,74 @@ __global__ void __launch_bounds__(256) k_gemv_xt(const void* __restrict__ x, int
     if (r < rows) xt[r * 16 + n] = n < batch ? load_x(x, xt_type, static_cast<int64_t>(n) * rows + r) : 0.f;
 }
 
+// Outlier values: f32 (exact) or f16 (ezq_gemv_prepare_ex; 6 bytes per
+// outlier instead of 8, held to the GEMV's 1e-3 gate).
+template <int VT>
+__device__ __forceinline__ float load_val(const void* v, int64_t e) {
+    if (VT == 1) return __half2float(static_cast<const __half*>(v)[e]);
+    return static_cast<const float*>(v)[e];
+}
 
+template <int XT, int NBT, int VT>
+__global__ void __launch_bounds__(256) k_gemv_outliers(int64_t rows, int64_t cols, const int64_t* __restrict__ col_ptr,
+                                                       const uint32_t* __restrict__ out_row,
+                                                       const void* __restrict__ out_val, const void* __restrict__ x,
+                                                       int batch, float* __restrict__ y,
+                                                       const float* __restrict__ xt) {
+    constexpr int kU = 4;
+    const int lane = threadIdx.x & 31;
+    const int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    float part[NBT];
+#pragma unroll
+    for (int n = 0; n < NBT; ++n) part[n] = 0.f;
+    int64_t e0 = 0, e1 = 0;
+    if (j < cols) e0 = __ldg(col_ptr + j), e1 = __ldg(col_ptr + j + 1);
+    for (int64_t eb = e0; eb < e1; eb += 32 * kU) {
+        uint32_t r[kU];
+        float v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int64_t e = eb + lane + 32 * u;
+            r[u] = e < e1 ? __ldg(out_row + e) : 0u;
+            v[u] = e < e1 ? load_val<VT>(out_val, e) : 0.f;
+        }
+        if (NBT > 8) {  // transposed x: one 16-byte load per 4 batch rows
+#pragma unroll
+            for (int u = 0; u < kU; ++u)
+#pragma unroll
+                for (int n4 = 0; n4 < NBT / 4; ++n4) {
+                    const float4 xv = __ldg(reinterpret_cast<const float4*>(xt + static_cast<int64_t>(r[u]) * 16) + n4);
+                    const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (4 * n4 + k < batch) part[4 * n4 + k] = fmaf(xs[k], v[u], part[4 * n4 + k]);
+                }
+        } else {
+#pragma unroll
+            for (int u = 0; u < kU; ++u)
+#pragma unroll
+                for (int n = 0; n < NBT; ++n)
+                    if (n < batch) part[n] = fmaf(load_x(x, XT, static_cast<int64_t>(n) * rows + r[u]), v[u], part[n]);
+        }
+    }
+    const bool any = e1 > e0;
+    if (any) {
+#pragma unroll
+        for (int n = 0; n < NBT; ++n) {
+            if (n >= batch) break;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) part[n] += __shfl_xor_sync(0xffffffffu, part[n], o);
+        }
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (any && lane < batch) {
+        float add = part[0];
+#pragma unroll
+        for (int k = 1; k < NBT; ++k)
+            if (k == lane) add = part[k];
+        y[static_cast<int64_t>(lane) * cols + j] += add;
+    }
+}
 
 // Repack the artifact's codes into the MMA fragment order (layout above),
 // colblock major: T[cb][q][tile(TPC)][lane]. Rows past the end and columns
@@ -690,11 +683,12 @@ const int* occupancy(int tpc) {
 // x sums stay cheap; larger batches keep the HSUB2 path.
 template <int TPC, int NB, int XT>
 void launch_cb_t(const GemvArgs& a, int grid, cudaStream_t st) {
-    const unsigned threads = a.has_out ? kOutThreads : kStreamThreads;
     if (NB == 1 && XT != kF16 && a.batch <= 2)
-        k_gemv_cb<TPC, NB, XT, true><<<static_cast<unsigned>(grid), threads, CbGeom<TPC, NB, XT, true>::smem(), st>>>(a);
+        k_gemv_cb<TPC, NB, XT, true><<<static_cast<unsigned>(grid), kStreamThreads, CbGeom<TPC, NB, XT, true>::smem(),
+                                       st>>>(a);
     else
-        k_gemv_cb<TPC, NB, XT, false><<<static_cast<unsigned>(grid), threads, CbGeom<TPC, NB, XT>::smem(), st>>>(a);
+        k_gemv_cb<TPC, NB, XT, false><<<static_cast<unsigned>(grid), kStreamThreads, CbGeom<TPC, NB, XT>::smem(),
+                                        st>>>(a);
 }
 
 template <int TPC>
@@ -716,6 +710,21 @@ void launch_cb(int tpc, int v, const GemvArgs& a, int grid, cudaStream_t st) {
         case 4: launch_cb_v<4>(v, a, grid, st); break;
         default: launch_cb_v<8>(v, a, grid, st); break;
     }
+}
+
+template <int XT, int VT>
+cudaError_t launch_outliers_v(cudaLaunchConfig_t& lc, int bt, int64_t rows, int64_t cols, const int64_t* cp,
+                              const uint32_t* orow, const void* oval, const void* xg, float* yg, const float* xtg) {
+    if (bt == 1) return cudaLaunchKernelEx(&lc, k_gemv_outliers<XT, 1, VT>, rows, cols, cp, orow, oval, xg, bt, yg, xtg);
+    if (bt <= 8) return cudaLaunchKernelEx(&lc, k_gemv_outliers<XT, 8, VT>, rows, cols, cp, orow, oval, xg, bt, yg, xtg);
+    return cudaLaunchKernelEx(&lc, k_gemv_outliers<XT, 16, VT>, rows, cols, cp, orow, oval, xg, bt, yg, xtg);
+}
+
+template <int XT>
+cudaError_t launch_outliers(cudaLaunchConfig_t& lc, int vt, int bt, int64_t rows, int64_t cols, const int64_t* cp,
+                            const uint32_t* orow, const void* oval, const void* xg, float* yg, const float* xtg) {
+    if (vt == EZQ_GEMV_OUTLIER_F16) return launch_outliers_v<XT, 1>(lc, bt, rows, cols, cp, orow, oval, xg, yg, xtg);
+    return launch_outliers_v<XT, 0>(lc, bt, rows, cols, cp, orow, oval, xg, yg, xtg);
 }
 
 }  // namespace
@@ -846,12 +855,6 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
     a.cols = p->cols;
     a.lmin = p->lmin;
     a.scales = p->scales;
-    a.has_out = p->n_out > 0;
-    a.vt = p->vdtype == EZQ_GEMV_OUTLIER_F16 ? 1 : 0;
-    a.col_ptr = p->col_ptr;
-    a.out_row = p->out_row;
-    a.out_val = p->out_val;
-    a.xt = p->xt;
     const size_t xes = x_dtype == kF32 ? 4 : 2;
     // The main kernel stages x slices with 16-byte cp.async: 64-row multiples
     // and 16-byte aligned rows, else a zero-padded copy first.
@@ -876,7 +879,7 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
             a.xstride = prow;
         }
         const bool two = a.batch > 8;
-        if (p->n_out && a.batch > 1) {  // transposed x for the outlier warp (one 16-byte load per 4 batch rows)
+        if (p->n_out && a.batch > 8) {  // transposed x for the outlier pass (pays off from 9 batch rows)
             k_gemv_xt<<<static_cast<unsigned>((p->rows + 15) / 16), 256, 0, st>>>(xg, x_dtype, p->rows, a.batch,
                                                                                   p->xt);
             count_launch();
@@ -884,6 +887,29 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
         const int v = x_dtype * 2 + (two ? 1 : 0);
         launch_cb(p->tpc, v, a, p->grid[v], st);
         count_launch();
+        if (p->n_out) {
+            cudaLaunchConfig_t lc{};
+            lc.gridDim = dim3(static_cast<unsigned>((p->cols + 7) / 8));  // one warp per column
+            lc.blockDim = dim3(256);
+            lc.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            const int64_t* cp = p->col_ptr;
+            const uint32_t* orow = p->out_row;
+            const void* oval = p->out_val;
+            float* yg = a.y;
+            const int bt = a.batch;
+            const float* xtg = p->xt;
+            cudaError_t e;
+            if (x_dtype == kF32) e = launch_outliers<kF32>(lc, p->vdtype, bt, p->rows, p->cols, cp, orow, oval, xg, yg, xtg);
+            else if (x_dtype == kBF16) e = launch_outliers<kBF16>(lc, p->vdtype, bt, p->rows, p->cols, cp, orow, oval, xg, yg, xtg);
+            else e = launch_outliers<kF16>(lc, p->vdtype, bt, p->rows, p->cols, cp, orow, oval, xg, yg, xtg);
+            EZQ_CK(e);
+            count_launch();
+        }
     }
     // Algorithmic bytes: the 4-bit codes (the repacked copy has the same
     // size as the artifact's nibbles), scales, CSC, x and y.
