@@ -530,58 +530,68 @@ __global__ void __launch_bounds__(256) k_gemv_outliers(int64_t rows, int64_t col
                                                        const void* __restrict__ out_val, const void* __restrict__ x,
                                                        int batch, float* __restrict__ y,
                                                        const float* __restrict__ xt) {
+    // A grid that fits on the SMs beside the main kernel's CTAs: each warp
+    // takes columns j = warp, + all warps, ... and computes ALL of them
+    // before griddepcontrol.wait (their gathers overlap the weight stream),
+    // keeping the sums in shared memory; then it applies them to y.
+    extern __shared__ float osum[];  // [8 warps][cpw][NBT]
     constexpr int kU = 4;
-    const int lane = threadIdx.x & 31;
-    const int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    float part[NBT];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    const int64_t w0 = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + wib;
+    const int cpw = static_cast<int>((cols + nwarps - 1) / nwarps);
+    float* my = osum + static_cast<int64_t>(wib) * cpw * NBT;
+    int ci = 0;
+    for (int64_t j = w0; j < cols; j += nwarps, ++ci) {
+        float part[NBT];
 #pragma unroll
-    for (int n = 0; n < NBT; ++n) part[n] = 0.f;
-    int64_t e0 = 0, e1 = 0;
-    if (j < cols) e0 = __ldg(col_ptr + j), e1 = __ldg(col_ptr + j + 1);
-    for (int64_t eb = e0; eb < e1; eb += 32 * kU) {
-        uint32_t r[kU];
-        float v[kU];
+        for (int n = 0; n < NBT; ++n) part[n] = 0.f;
+        const int64_t e0 = __ldg(col_ptr + j), e1 = __ldg(col_ptr + j + 1);
+        for (int64_t eb = e0; eb < e1; eb += 32 * kU) {
+            uint32_t r[kU];
+            float v[kU];
 #pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const int64_t e = eb + lane + 32 * u;
-            r[u] = e < e1 ? __ldg(out_row + e) : 0u;
-            v[u] = e < e1 ? load_val<VT>(out_val, e) : 0.f;
+            for (int u = 0; u < kU; ++u) {
+                const int64_t e = eb + lane + 32 * u;
+                r[u] = e < e1 ? __ldg(out_row + e) : 0u;
+                v[u] = e < e1 ? load_val<VT>(out_val, e) : 0.f;
+            }
+            if (NBT > 8) {  // transposed x: one 16-byte load per 4 batch rows
+#pragma unroll
+                for (int u = 0; u < kU; ++u)
+#pragma unroll
+                    for (int n4 = 0; n4 < NBT / 4; ++n4) {
+                        const float4 xv = __ldg(reinterpret_cast<const float4*>(xt + static_cast<int64_t>(r[u]) * 16) + n4);
+                        const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            if (4 * n4 + k < batch) part[4 * n4 + k] = fmaf(xs[k], v[u], part[4 * n4 + k]);
+                    }
+            } else {
+#pragma unroll
+                for (int u = 0; u < kU; ++u)
+#pragma unroll
+                    for (int n = 0; n < NBT; ++n)
+                        if (n < batch) part[n] = fmaf(load_x(x, XT, static_cast<int64_t>(n) * rows + r[u]), v[u], part[n]);
+            }
         }
-        if (NBT > 8) {  // transposed x: one 16-byte load per 4 batch rows
 #pragma unroll
-            for (int u = 0; u < kU; ++u)
-#pragma unroll
-                for (int n4 = 0; n4 < NBT / 4; ++n4) {
-                    const float4 xv = __ldg(reinterpret_cast<const float4*>(xt + static_cast<int64_t>(r[u]) * 16) + n4);
-                    const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (4 * n4 + k < batch) part[4 * n4 + k] = fmaf(xs[k], v[u], part[4 * n4 + k]);
-                }
-        } else {
-#pragma unroll
-            for (int u = 0; u < kU; ++u)
-#pragma unroll
-                for (int n = 0; n < NBT; ++n)
-                    if (n < batch) part[n] = fmaf(load_x(x, XT, static_cast<int64_t>(n) * rows + r[u]), v[u], part[n]);
-        }
-    }
-    const bool any = e1 > e0;
-    if (any) {
-#pragma unroll
-        for (int n = 0; n < NBT; ++n) {
+        for (int n = 0; n < NBT; ++n) {  // fixed butterfly: deterministic
             if (n >= batch) break;
 #pragma unroll
             for (int o = 16; o; o >>= 1) part[n] += __shfl_xor_sync(0xffffffffu, part[n], o);
         }
-    }
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (any && lane < batch) {
-        float add = part[0];
+        if (lane == 0) {
 #pragma unroll
-        for (int k = 1; k < NBT; ++k)
-            if (k == lane) add = part[k];
-        y[static_cast<int64_t>(lane) * cols + j] += add;
+            for (int n = 0; n < NBT; ++n) my[ci * NBT + n] = part[n];
+        }
+    }
+    __syncwarp();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    ci = 0;
+    for (int64_t j = w0; j < cols; j += nwarps, ++ci) {
+        const int64_t e0 = __ldg(col_ptr + j), e1 = __ldg(col_ptr + j + 1);
+        if (e1 > e0 && lane < batch) y[static_cast<int64_t>(lane) * cols + j] += my[ci * NBT + lane];
     }
 }
 
@@ -889,8 +899,15 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
         count_launch();
         if (p->n_out) {
             cudaLaunchConfig_t lc{};
-            lc.gridDim = dim3(static_cast<unsigned>((p->cols + 7) / 8));  // one warp per column
+            // two 8-warp CTAs per SM: resident beside the main kernel (see k_gemv_outliers)
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            const int64_t ctas = std::min<int64_t>((p->cols + 7) / 8,
+                                                   std::max<int64_t>(2 * static_cast<int64_t>(sms), (p->cols + 511) / 512));
+            const int64_t cpw = (p->cols + 8 * ctas - 1) / (8 * ctas);
+            lc.gridDim = dim3(static_cast<unsigned>(ctas));
             lc.blockDim = dim3(256);
+            lc.dynamicSmemBytes = static_cast<size_t>(8 * cpw * (a.batch > 8 ? 16 : (a.batch > 1 ? 8 : 1))) * sizeof(float);
             lc.stream = st;
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
