@@ -733,6 +733,16 @@ cudaError_t launch_outliers_v(cudaLaunchConfig_t& lc, int bt, int64_t rows, int6
 template <int XT>
 cudaError_t launch_outliers(cudaLaunchConfig_t& lc, int vt, int bt, int64_t rows, int64_t cols, const int64_t* cp,
                             const uint32_t* orow, const void* oval, const void* xg, float* yg, const float* xtg) {
+    if (vt == EZQ_GEMV_OUTLIER_F16 && bt > 8) {
+        // f16 values with the 16-row transposed-x variant fault (misaligned
+        // address, cause not found); the two 8-row halves use the direct path
+        const size_t es = XT == kF32 ? 4 : 2;
+        const cudaError_t e = launch_outliers_v<XT, 1>(lc, 8, rows, cols, cp, orow, oval, xg, yg, xtg);
+        if (e != cudaSuccess) return e;
+        return launch_outliers_v<XT, 1>(lc, bt - 8, rows, cols, cp, orow, oval,
+                                        static_cast<const char*>(xg) + es * 8 * static_cast<size_t>(rows),
+                                        yg + 8 * cols, xtg);
+    }
     if (vt == EZQ_GEMV_OUTLIER_F16) return launch_outliers_v<XT, 1>(lc, bt, rows, cols, cp, orow, oval, xg, yg, xtg);
     return launch_outliers_v<XT, 0>(lc, bt, rows, cols, cp, orow, oval, xg, yg, xtg);
 }
@@ -894,9 +904,18 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
                                                                                   p->xt);
             count_launch();
         }
+        static const bool dsync = std::getenv("EZQ_GEMV_SYNC") != nullptr;  // diagnosis: sync after every launch
+        if (dsync) {
+            const cudaError_t e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) return cuda_error(e, "gemv: before the main kernel");
+        }
         const int v = x_dtype * 2 + (two ? 1 : 0);
         launch_cb(p->tpc, v, a, p->grid[v], st);
         count_launch();
+        if (dsync) {
+            const cudaError_t e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) return cuda_error(e, "gemv: main kernel");
+        }
         if (p->n_out) {
             cudaLaunchConfig_t lc{};
             // two 8-warp CTAs per SM: resident beside the main kernel (see k_gemv_outliers)
