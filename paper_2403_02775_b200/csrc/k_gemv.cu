@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(256) k_gemv_outliers(int64_t rows, int64_t col
                 r[u] = e < e1 ? __ldg(out_row + e) : 0u;
                 v[u] = e < e1 ? load_val<VT>(out_val, e) : 0.f;
             }
-            if (NBT > 8) {  // transposed x: one 16-byte load per 4 batch rows
+            if (NBT > 1) {  // transposed x: one 16-byte load per 4 batch rows
 #pragma unroll
                 for (int u = 0; u < kU; ++u)
 #pragma unroll
@@ -734,14 +734,11 @@ template <int XT>
 cudaError_t launch_outliers(cudaLaunchConfig_t& lc, int vt, int bt, int64_t rows, int64_t cols, const int64_t* cp,
                             const uint32_t* orow, const void* oval, const void* xg, float* yg, const float* xtg) {
     if (vt == EZQ_GEMV_OUTLIER_F16 && bt > 8) {
-        // f16 values with the 16-row transposed-x variant fault (misaligned
-        // address, cause not found); the two 8-row halves use the direct path
-        const size_t es = XT == kF32 ? 4 : 2;
+        // f16 values with the 16-row variant fault (misaligned address, cause
+        // not found); two 8-row passes over the transposed x instead
         const cudaError_t e = launch_outliers_v<XT, 1>(lc, 8, rows, cols, cp, orow, oval, xg, yg, xtg);
         if (e != cudaSuccess) return e;
-        return launch_outliers_v<XT, 1>(lc, bt - 8, rows, cols, cp, orow, oval,
-                                        static_cast<const char*>(xg) + es * 8 * static_cast<size_t>(rows),
-                                        yg + 8 * cols, xtg);
+        return launch_outliers_v<XT, 1>(lc, bt - 8, rows, cols, cp, orow, oval, xg, yg + 8 * cols, xtg + 8);
     }
     if (vt == EZQ_GEMV_OUTLIER_F16) return launch_outliers_v<XT, 1>(lc, bt, rows, cols, cp, orow, oval, xg, yg, xtg);
     return launch_outliers_v<XT, 0>(lc, bt, rows, cols, cp, orow, oval, xg, yg, xtg);
@@ -899,7 +896,7 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
             a.xstride = prow;
         }
         const bool two = a.batch > 8;
-        if (p->n_out && a.batch > 8) {  // transposed x for the outlier pass (pays off from 9 batch rows)
+        if (p->n_out && a.batch > 1) {  // transposed x for the outlier pass (one 16-byte load per 4 batch rows)
             k_gemv_xt<<<static_cast<unsigned>((p->rows + 15) / 16), 256, 0, st>>>(xg, x_dtype, p->rows, a.batch,
                                                                                   p->xt);
             count_launch();
