@@ -738,7 +738,10 @@ cudaError_t launch_outliers(cudaLaunchConfig_t& lc, int vt, int bt, int64_t rows
         // not found); two 8-row passes over the transposed x instead
         const cudaError_t e = launch_outliers_v<XT, 1>(lc, 8, rows, cols, cp, orow, oval, xg, yg, xtg);
         if (e != cudaSuccess) return e;
-        return launch_outliers_v<XT, 1>(lc, bt - 8, rows, cols, cp, orow, oval, xg, yg + 8 * cols, xtg + 8);
+        const size_t es = XT == kF32 ? 4 : 2;  // rows 8.. of x (direct path, bt == 9) or of xt
+        return launch_outliers_v<XT, 1>(lc, bt - 8, rows, cols, cp, orow, oval,
+                                        static_cast<const char*>(xg) + es * 8 * static_cast<size_t>(rows),
+                                        yg + 8 * cols, xtg + 8);
     }
     if (vt == EZQ_GEMV_OUTLIER_F16) return launch_outliers_v<XT, 1>(lc, bt, rows, cols, cp, orow, oval, xg, yg, xtg);
     return launch_outliers_v<XT, 0>(lc, bt, rows, cols, cp, orow, oval, xg, yg, xtg);
