@@ -921,8 +921,11 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
             // two 8-warp CTAs per SM: resident beside the main kernel (see k_gemv_outliers)
             int sms = 148;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            const int64_t ctas = std::min<int64_t>((p->cols + 7) / 8,
-                                                   std::max<int64_t>(2 * static_cast<int64_t>(sms), (p->cols + 511) / 512));
+            // (up to 16k columns: one warp per column, measured faster at batch 1)
+            const int64_t ctas = p->cols <= 16384
+                                     ? (p->cols + 7) / 8
+                                     : std::min<int64_t>((p->cols + 7) / 8, std::max<int64_t>(2 * static_cast<int64_t>(sms),
+                                                                                            (p->cols + 511) / 512));
             const int64_t cpw = (p->cols + 8 * ctas - 1) / (8 * ctas);
             lc.gridDim = dim3(static_cast<unsigned>(ctas));
             lc.blockDim = dim3(256);
