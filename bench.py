@@ -224,7 +224,11 @@ def run_reference(args):
             times.append(t)
             ns.append(shp[0] * shp[1])
     value = sum(ns) / sum(times)
-    line = base_line(args, cfg, shapes, sum(r * c for r, c in shapes), world)
+    mine0 = None
+    if args.scaling == "strong":  # same config as our arm: one weight set, LPT-partitioned
+        from paper_2403_02775_b200.driver import lpt_partition
+        mine0 = lpt_partition([r * c for r, c in shapes], world)[0]
+    line = base_line(args, cfg, shapes, sum(r * c for r, c in shapes), world, mine0)
     line.update({
         "impl": "reference", "value": value, "ms_per_step": 1e3 * sum(times) / len(times),
         "n_gpus": world,
