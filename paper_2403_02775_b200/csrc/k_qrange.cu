@@ -315,46 +315,35 @@ __device__ __forceinline__ double seq_sq(float x, double xd, double s, float inv
     return __dmul_rn(d, d);
 }
 
-// Two warps per 32-column tile: role 0 runs the chain at s_rtn, role 1 the
-// chain at s_fin plus the fused pack (the two chains are independent, so a
-// tall tensor with few columns gets twice the warps in flight); they join in
-// shared memory and role 0 finalises the column.
-constexpr int kTilesK3b = 4;  // tiles per CTA (2 warps each)
-
-__global__ void __launch_bounds__(kTilesK3b * 64) k_seq_errors(const TDesc* __restrict__ td,
+__global__ void __launch_bounds__(kWarpsK3b * 32) k_seq_errors(const TDesc* __restrict__ td,
                                                               const int2* __restrict__ tiles, int ntiles,
                                                               Scratch sc, CfgDev cfg) {
-    __shared__ double ef_sh[kTilesK3b][32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int role = w & 1, slot = w >> 1;
-    const int ti = blockIdx.x * kTilesK3b + slot;
-    const bool valid = ti < ntiles;  // no early return: the CTA joins below
-    const int2 tile = tiles[valid ? ti : 0];
+    const int lane = threadIdx.x & 31;
+    const int ti = blockIdx.x * kWarpsK3b + (threadIdx.x >> 5);
+    if (ti >= ntiles) return;
+    const int2 tile = tiles[ti];
     const TDesc& d = td[tile.x];
     const int64_t c0 = tile.y, R = d.rows, C = d.cols;
     const int64_t c = c0 + lane;
-    const bool act = valid && c < C;  // idle lanes stay for the nibble-pair shuffles
-    const int64_t gc = d.col_base + (c < C ? c : c0);
+    const bool act = c < C;  // idle lanes stay for the nibble-pair shuffles
+    const int64_t gc = d.col_base + (act ? c : c0);
     const TStats* st = d.st;
     const float olo = st->olo, ohi = st->ohi;
     const double s_r = sc.s_rtn[gc], s_f = sc.s_fin[gc];
     // Fused K4: the codes at s_fin (pack_levels, rtn.cpp:123-149, outlier
-    // slots at level 0) are written by role 1; a column that ends up storing
-    // s_rtn is flagged and re-packed by k_repack.
+    // slots at level 0) are written here; a column that ends up storing s_rtn
+    // is flagged and re-packed by k_repack.
     const bool fused = d.pack_fused != 0;
     const unsigned lbase = __float_as_uint(kMagic) + static_cast<unsigned>(cfg.lmin);
     const unsigned lzero = static_cast<unsigned>(-cfg.lmin);
     const bool both = s_f != s_r;  // chosen == initial: one sum serves both
-    const double s_me = role ? s_f : s_r;
-    const double inv = __ddiv_rn(1.0, s_me);
-    const float invf = __double2float_rn(inv);
+    const double inv_r = __ddiv_rn(1.0, s_r), inv_f = __ddiv_rn(1.0, s_f);
+    const float invf_r = __double2float_rn(inv_r), invf_f = __double2float_rn(inv_f);
     const float fmin = static_cast<float>(cfg.lmin), fmax = static_cast<float>(cfg.lmax);
     const double dmin = cfg.lmin, dmax = cfg.lmax;
     const float guard = cfg.guard;
-    const float* col = d.W + (c < C ? c : c0);
-    const bool chain = valid && (role == 0 || both);  // warp-uniform
-    const bool pack = valid && role == 1 && fused;   // warp-uniform
-    double e = 0.0;
+    const float* col = d.W + (act ? c : c0);
+    double er = 0.0, ef = 0.0;
     int64_t r = 0;
     auto put = [&](int64_t row, unsigned tbits, bool out) {  // all lanes call it (shuffle)
         const unsigned off = out ? lzero : tbits - lbase;
@@ -365,61 +354,69 @@ __global__ void __launch_bounds__(kTilesK3b * 64) k_seq_errors(const TDesc* __re
             d.packed[row * C + c] = static_cast<uint8_t>(off);
         }
     };
-    if (chain || pack) {
-        for (; r + kRowsK3b <= R; r += kRowsK3b) {
-            float x[kRowsK3b];
+    for (; r + kRowsK3b <= R; r += kRowsK3b) {
+        float x[kRowsK3b];
 #pragma unroll
-            for (int j = 0; j < kRowsK3b; ++j) x[j] = __ldg(col + (r + j) * C);
-            // certified fp32 levels for the group, one guard test (exact fp64
-            // levels for the group when it trips)
-            float tq[kRowsK3b];
-            float rq = 0.f;
+        for (int j = 0; j < kRowsK3b; ++j) x[j] = __ldg(col + (r + j) * C);
+        // certified fp32 levels for the group at both scales, one guard test
+        // per scale (exact fp64 levels for the group when it trips)
+        float tr[kRowsK3b], tf[kRowsK3b];
+        float rr = 0.f, rf = 0.f;
 #pragma unroll
-            for (int j = 0; j < kRowsK3b; ++j) {
-                const float u = fminf(fmaxf(__fmul_rn(x[j], invf), fmin), fmax);
-                tq[j] = __fadd_rn(u, kMagic);
-                rq = fmaxf(rq, fabsf(__fsub_rn(u, __fsub_rn(tq[j], kMagic))));
-            }
-            if (rq >= guard) {
-#pragma unroll
-                for (int j = 0; j < kRowsK3b; ++j)
-                    tq[j] = __fadd_rn(static_cast<float>(level_exact(static_cast<double>(x[j]), inv, dmin, dmax)), kMagic);
-            }
-            if (pack) {  // warp-uniform
-#pragma unroll
-                for (int j = 0; j < kRowsK3b; ++j) put(r + j, __float_as_uint(tq[j]), is_outlier_f(x[j], olo, ohi));
-            }
-            if (chain) {
-#pragma unroll
-                for (int j = 0; j < kRowsK3b; ++j) {
-                    // normal_mask_apply: an isolated outlier adds exactly +0
-                    const bool out = is_outlier_f(x[j], olo, ohi);
-                    const double xd = static_cast<double>(x[j]);
-                    const double dq = fma(s_me, level_bits_to_double(tq[j]), -xd);  // exact: s*q is
-                    e = __dadd_rn(e, out ? 0.0 : __dmul_rn(dq, dq));
-                }
-            }
+        for (int j = 0; j < kRowsK3b; ++j) {
+            float u = fminf(fmaxf(__fmul_rn(x[j], invf_r), fmin), fmax);
+            tr[j] = __fadd_rn(u, kMagic);
+            rr = fmaxf(rr, fabsf(__fsub_rn(u, __fsub_rn(tr[j], kMagic))));
+            u = fminf(fmaxf(__fmul_rn(x[j], invf_f), fmin), fmax);
+            tf[j] = __fadd_rn(u, kMagic);
+            rf = fmaxf(rf, fabsf(__fsub_rn(u, __fsub_rn(tf[j], kMagic))));
         }
-        for (; r < R; ++r) {
-            const float x = __ldg(col + r * C);
-            const bool out = is_outlier_f(x, olo, ohi);
-            const double xd = static_cast<double>(x);
-            if (chain) e = __dadd_rn(e, out ? 0.0 : seq_sq(x, xd, s_me, invf, inv, fmin, fmax, dmin, dmax, guard));
-            if (pack) {
-                const double q = level_exact(xd, inv, dmin, dmax);
-                put(r, __float_as_uint(__fadd_rn(static_cast<float>(q), kMagic)), out);
+        if (rr >= guard) {
+#pragma unroll
+            for (int j = 0; j < kRowsK3b; ++j)
+                tr[j] = __fadd_rn(static_cast<float>(level_exact(static_cast<double>(x[j]), inv_r, dmin, dmax)), kMagic);
+        }
+        if (both && rf >= guard) {
+#pragma unroll
+            for (int j = 0; j < kRowsK3b; ++j)
+                tf[j] = __fadd_rn(static_cast<float>(level_exact(static_cast<double>(x[j]), inv_f, dmin, dmax)), kMagic);
+        }
+        if (fused) {  // warp-uniform
+#pragma unroll
+            for (int j = 0; j < kRowsK3b; ++j)
+                put(r + j, __float_as_uint(both ? tf[j] : tr[j]), is_outlier_f(x[j], olo, ohi));
+        }
+#pragma unroll
+        for (int j = 0; j < kRowsK3b; ++j) {
+            // normal_mask_apply: an isolated outlier adds exactly +0
+            const bool out = is_outlier_f(x[j], olo, ohi);
+            const double xd = static_cast<double>(x[j]);
+            const double dr = fma(s_r, level_bits_to_double(tr[j]), -xd);  // exact: s*q is
+            er = __dadd_rn(er, out ? 0.0 : __dmul_rn(dr, dr));
+            if (both) {
+                const double df = fma(s_f, level_bits_to_double(tf[j]), -xd);
+                ef = __dadd_rn(ef, out ? 0.0 : __dmul_rn(df, df));
             }
         }
     }
-    if (role == 1) ef_sh[slot][lane] = e;
-    __syncthreads();
-    if (role == 1 || !act) return;
-    const double er = e;
-    double ef = both ? ef_sh[slot][lane] : er;
+    for (; r < R; ++r) {
+        const float x = __ldg(col + r * C);
+        const bool out = is_outlier_f(x, olo, ohi);
+        const double xd = static_cast<double>(x);
+        er = __dadd_rn(er, out ? 0.0 : seq_sq(x, xd, s_r, invf_r, inv_r, fmin, fmax, dmin, dmax, guard));
+        if (both) ef = __dadd_rn(ef, out ? 0.0 : seq_sq(x, xd, s_f, invf_f, inv_f, fmin, fmax, dmin, dmax, guard));
+        if (fused) {
+            const double q = level_exact(xd, inv_f, dmin, dmax);
+            put(r, __float_as_uint(__fadd_rn(static_cast<float>(q), kMagic)), out);
+        }
+    }
+    if (!act) return;
     double s_store = s_f;
-    if (ef > er) {
-        // tree/sequential near-tie of the streaming K3: keep the initial
-        // scale so the per-column invariant final <= rtn holds (pipeline.cpp:107)
+    if (!both) {
+        ef = er;
+    } else if (ef > er) {
+        // tree/sequential near-tie: keep the initial scale so the per-column
+        // invariant final <= rtn holds (pipeline.cpp:107)
         s_store = s_r;
         ef = er;
     }
@@ -427,9 +424,9 @@ __global__ void __launch_bounds__(kTilesK3b * 64) k_seq_errors(const TDesc* __re
     const float scale = __double2float_rn(s_store);
     if (!(scale > 0.f)) d.st->scale_zero = 1;  // check_scale (rtn.cpp:19-22)
     d.scales[c] = scale;
-    const double inv_s = scale > 0.f ? __ddiv_rn(1.0, static_cast<double>(scale)) : 1.0;
-    sc.inv[gc] = inv_s;
-    sc.invf[gc] = __double2float_rn(inv_s);
+    const double inv = scale > 0.f ? __ddiv_rn(1.0, static_cast<double>(scale)) : 1.0;
+    sc.inv[gc] = inv;
+    sc.invf[gc] = __double2float_rn(inv);
     sc.err_rtn[gc] = er;
     sc.err_fin[gc] = ef;
 }
@@ -769,7 +766,7 @@ void launch_k3(const K3Launch& kl, const TDesc* td, const K3Group* groups, int n
 void launch_seq_errors(const TDesc* td, const int2* tiles, int ntiles, Scratch sc, CfgDev cfg,
                        cudaStream_t st) {
     if (ntiles == 0) return;
-    k_seq_errors<<<(ntiles + kTilesK3b - 1) / kTilesK3b, kTilesK3b * 64, 0, st>>>(td, tiles, ntiles, sc, cfg);
+    k_seq_errors<<<(ntiles + kWarpsK3b - 1) / kWarpsK3b, kWarpsK3b * 32, 0, st>>>(td, tiles, ntiles, sc, cfg);
     count_launch();
 }
 
