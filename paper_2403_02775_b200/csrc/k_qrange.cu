@@ -297,6 +297,7 @@ __global__ void __launch_bounds__(512, 1) k_qrange(const TDesc* __restrict__ td,
 // registers. The per-column finalisation (stored float scale, per-column
 // invariant, 1/scale for K4) follows in the same lane.
 constexpr int kRowsK3b = 8;
+constexpr int kPipeK3b = 3;  // row groups in flight per lane (K3b, near-tie resolution)
 constexpr int kWarpsK3b = 4;
 
 // Squared residual of one normal element at scale s in reference semantics
@@ -354,10 +355,30 @@ __global__ void __launch_bounds__(kWarpsK3b * 32) k_seq_errors(const TDesc* __re
             d.packed[row * C + c] = static_cast<uint8_t>(off);
         }
     };
+    // Row groups are software-pipelined kPipeK3b deep: the loads of the next
+    // groups are in flight while one is computed (a tall tensor has few
+    // columns, i.e. few warps, so each must keep many rows in flight).
+    float xb[kPipeK3b][kRowsK3b];
+#pragma unroll
+    for (int p = 0; p < kPipeK3b; ++p)
+#pragma unroll
+        for (int j = 0; j < kRowsK3b; ++j) {
+            const int64_t rr0 = p * kRowsK3b + j;
+            xb[p][j] = rr0 < R ? __ldg(col + rr0 * C) : 0.f;
+        }
     for (; r + kRowsK3b <= R; r += kRowsK3b) {
         float x[kRowsK3b];
 #pragma unroll
-        for (int j = 0; j < kRowsK3b; ++j) x[j] = __ldg(col + (r + j) * C);
+        for (int j = 0; j < kRowsK3b; ++j) x[j] = xb[0][j];
+#pragma unroll
+        for (int p = 0; p + 1 < kPipeK3b; ++p)
+#pragma unroll
+            for (int j = 0; j < kRowsK3b; ++j) xb[p][j] = xb[p + 1][j];
+#pragma unroll
+        for (int j = 0; j < kRowsK3b; ++j) {
+            const int64_t rn = r + kPipeK3b * kRowsK3b + j;
+            xb[kPipeK3b - 1][j] = rn < R ? __ldg(col + rn * C) : 0.f;
+        }
         // certified fp32 levels for the group at both scales, one guard test
         // per scale (exact fp64 levels for the group when it trips)
         float tr[kRowsK3b], tf[kRowsK3b];
@@ -554,10 +575,27 @@ __global__ void __launch_bounds__(kWarpsK3b * 32) k_resolve_ties(const TDesc* __
         const float pinvf = __double2float_rn(pinv);
         double pe = 0.0;
         int64_t r = 0;
+        float xb[kPipeK3b][kRowsK3b];  // software pipeline, as in k_seq_errors
+#pragma unroll
+        for (int p = 0; p < kPipeK3b; ++p)
+#pragma unroll
+            for (int j = 0; j < kRowsK3b; ++j) {
+                const int64_t rr0 = p * kRowsK3b + j;
+                xb[p][j] = rr0 < R ? __ldg(col + rr0 * C) : 0.f;
+            }
         for (; r + kRowsK3b <= R; r += kRowsK3b) {
             float x[kRowsK3b];
 #pragma unroll
-            for (int j = 0; j < kRowsK3b; ++j) x[j] = __ldg(col + (r + j) * C);
+            for (int j = 0; j < kRowsK3b; ++j) x[j] = xb[0][j];
+#pragma unroll
+            for (int p = 0; p + 1 < kPipeK3b; ++p)
+#pragma unroll
+                for (int j = 0; j < kRowsK3b; ++j) xb[p][j] = xb[p + 1][j];
+#pragma unroll
+            for (int j = 0; j < kRowsK3b; ++j) {
+                const int64_t rn = r + kPipeK3b * kRowsK3b + j;
+                xb[kPipeK3b - 1][j] = rn < R ? __ldg(col + rn * C) : 0.f;
+            }
 #pragma unroll
             for (int j = 0; j < kRowsK3b; ++j) {
                 const float xv = __shfl_sync(0xffffffffu, x[j], psrc);
