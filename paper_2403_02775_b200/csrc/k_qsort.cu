@@ -199,6 +199,25 @@ __device__ __forceinline__ float level_threshold(int v, double s, double inv) {
     return c;
 }
 
+// The common case of level_threshold, branch-free: RN32(t s) or one of its
+// float neighbours is the threshold (ok = false otherwise: call
+// level_threshold). Keeps the hot loop free of divergent early returns.
+__device__ __forceinline__ float level_threshold_fast(int v, double s, double inv, bool& ok) {
+    const double t = static_cast<double>(v) - 0.5;
+    const bool strict = v <= 0;
+    auto pred = [&](float x) {
+        const double u = __dmul_rn(static_cast<double>(x), inv);
+        return strict ? (u > t) : (u >= t);
+    };
+    const float c = __double2float_rn(__dmul_rn(t, s));
+    const int b = __float_as_int(c), dn = c > 0.f ? -1 : 1;
+    const float pv = __int_as_float(b + dn), nx = __int_as_float(b - dn);
+    const bool pp = pred(pv), pc = pred(c), pn = pred(nx);
+    const bool a1 = !pp && pc, a2 = !pc && pn;
+    ok = c != 0.f && fabsf(c) < 3.0e38f && (a1 || a2);
+    return a1 ? c : nx;
+}
+
 // Column table: D[k] = P(k) for k <= kz (kz = count of x < 0), D[k + 1] =
 // S(k) for kz <= k <= n. x_k = D[k+1] - D[k] (k < kz), D[k+1] - D[k+2]
 // (kz <= k < n): exact wherever a threshold can fall.
@@ -276,6 +295,19 @@ __device__ __forceinline__ int search_near(const ColTab& c, int guess, float X, 
     }
     span = 0.f;
     return search_from(c, k0, X);
+}
+
+// One aligned 16-float window around the predicted index (the common case
+// of search_near, branch-free); ok = false when the answer lies outside it.
+__device__ __forceinline__ int search_window(const ColTab& c, int guess, float X, float& span, bool& ok) {
+    const int k0 = max(guess - 6, 0) & ~3;
+    const float4* w = reinterpret_cast<const float4*>(c.xs + k0);
+    const float4 a = __ldg(w), b = __ldg(w + 1), e = __ldg(w + 2), f = __ldg(w + 3);
+    const int cnt = (a.x < X) + (a.y < X) + (a.z < X) + (a.w < X) + (b.x < X) + (b.y < X) + (b.z < X) + (b.w < X) +
+                    (e.x < X) + (e.y < X) + (e.z < X) + (e.w < X) + (f.x < X) + (f.y < X) + (f.z < X) + (f.w < X);
+    ok = cnt < 16 && (cnt > 0 || k0 == 0);
+    span = f.w - a.x;
+    return k0 + cnt;
 }
 
 constexpr int kSortRadixBits = 6;
@@ -652,60 +684,63 @@ __global__ void __launch_bounds__(256, 4) k_qrange_tables(const TDesc* __restric
         const double cfull = ci.chi;
         double tie_thr = 0.0, tie_lo = 0.0;
         int tie_nc = 0;
-        bool own[TPL];
-        int jl[TPL], wA[TPL], ib[TPL];
-        float Xp[TPL], span[TPL];  // previous threshold; x[k0+7] - x[k0] near it
-#pragma unroll
-        for (int u = 0; u < TPL; ++u) {
-            const int idx = u * G + gl;
-            own[u] = live && idx < nb;
-            jl[u] = cfg.lmin + 1 + idx;
-            wA[u] = jl[u] >= 1 ? 2 * jl[u] - 1 : 1 - 2 * jl[u];
-            ib[u] = n >> 1;
-            Xp[u] = 0.f;
-            span[u] = 0.f;
-        }
-        for (int t = 0;; ++t) {
-            int a = 0;
-            double q = 0.0;
-            const double inv = __drcp_rn(s);  // RN(1/s), as the reference's 1.0 / s
-#pragma unroll
-            for (int u = 0; u < TPL; ++u) {
-                if (!own[u]) continue;
-                const int j = jl[u];
-                const float X = level_threshold(j, s, inv);
-                if (t == 0) {
-                    ib[u] = search_from(ct, ib[u], X);
-                    span[u] = 0.f;
-                    if (ib[u] + 8 <= n && ib[u] >= 8) span[u] = __ldg(ct.xs + ib[u] + 7) - __ldg(ct.xs + ib[u] - 8);
-                } else {
-                    // predict the shift from the threshold's move and the
-                    // spacing seen around the old position
-                    const float sp = span[u];
-                    const float dk = (sp > 0.f && sp < 3.0e38f) ? __fdividef(15.f * (X - Xp[u]), sp) : 0.f;
-                    const int guess = ib[u] + static_cast<int>(rintf(fminf(fmaxf(dk, -256.f), 256.f)));
-                    ib[u] = search_near(ct, min(max(guess, 0), n), X, span[u]);
-                }
-                Xp[u] = X;
-                const bool pos = j >= 1;
-                a += wA[u] * (pos ? n - ib[u] : ib[u]);
-                q = __dadd_rn(q, pos ? __ldg(ct.D + ib[u] + 1) : -__ldg(ct.D + ib[u]));
-            }
+        static_assert(TPL == 1, "one threshold per lane");
+        // lane gl owns threshold level j = lmin + 1 + gl; a lane without one
+        // (gl >= nb, or a dead slot) searches a valid threshold with weight 0
+        // and contributes nothing -- the step stays free of divergence
+        const bool own = live && gl < nb;
+        const int j = own ? cfg.lmin + 1 + gl : cfg.lmax;
+        const bool pos = j >= 1;
+        const int wA = own ? (pos ? 2 * j - 1 : 1 - 2 * j) : 0;
+        int ib = n >> 1;
+        float Xp = 0.f, span = 0.f;  // previous threshold; x[k0+15] - x[k0] near it
+        auto threshold = [&](double inv) {
+            bool ok;
+            float X = level_threshold_fast(j, s, inv, ok);
+            if (!ok) X = level_threshold(j, s, inv);  // rare
+            return X;
+        };
+        // A s^2 - 2 Q s (+ C) and the gradient from this lane's threshold
+        auto reduce = [&](DD& err, double& grad) {
+            int a = wA * (pos ? n - ib : ib);
+            const double dv = __ldg(ct.D + ib + (pos ? 1 : 0));
+            double q = own ? (pos ? dv : -dv) : 0.0;
 #pragma unroll
             for (int o = G / 2; o; o >>= 1) {  // exact in any order
                 a += __shfl_xor_sync(0xffffffffu, a, o, G);
                 q = __dadd_rn(q, __shfl_xor_sync(0xffffffffu, q, o, G));
             }
             const double Ad = static_cast<double>(a);
-            // A s^2 - 2 Q s + C: both products exact as pairs; the three
-            // leading parts summed exactly, the tails added after
-            const DD err = err_minus_c(Ad, q, s);
-            const double grad = 2.0 * __dsub_rn(__dmul_rn(Ad, s), q);  // A s exact
-            if (t == 0) {
-                best_err = err;
-                fixed_err = err;
-                if (track) tie_window(err.hi, cfull, gam, tie_lo, tie_thr);
-            } else if (!FIXED) {
+            // both products exact as pairs; the leading parts summed exactly,
+            // the tails added after
+            err = err_minus_c(Ad, q, s);
+            grad = 2.0 * __dsub_rn(__dmul_rn(Ad, s), q);  // A s exact
+        };
+        DD err;
+        double grad;
+        {  // step 0 (optimize.cpp:138-145): galloping search from the middle
+            const float X = threshold(__drcp_rn(s));  // RN(1/s), as the reference's 1.0 / s
+            ib = search_from(ct, ib, X);
+            if (ib + 8 <= n && ib >= 8) span = __ldg(ct.xs + ib + 7) - __ldg(ct.xs + ib - 8);
+            Xp = X;
+            reduce(err, grad);
+            best_err = err;
+            fixed_err = err;
+            if (track) tie_window(err.hi, cfull, gam, tie_lo, tie_thr);
+        }
+        for (int t = 1; t <= cfg.steps; ++t) {
+            s = snap(adam_update_tab(m, vv, s, grad, cfg.bc1[t], cfg.bc2[t], cfg.rbc1[t], cfg.rbc2[t], cfg.adam));
+            const float X = threshold(__drcp_rn(s));
+            // predict the shift from the threshold's move and the spacing seen
+            // around the old position; one aligned window usually holds it
+            const float dk = (span > 0.f && span < 3.0e38f) ? __fdividef(15.f * (X - Xp), span) : 0.f;
+            const int guess = min(max(ib + static_cast<int>(rintf(fminf(fmaxf(dk, -256.f), 256.f))), 0), n);
+            bool ok;
+            ib = search_window(ct, guess, X, span, ok);
+            if (!ok) ib = search_near(ct, guess, X, span);  // rare
+            Xp = X;
+            reduce(err, grad);
+            if (!FIXED) {
                 const bool lt = dd_lt(err, best_err);  // strict: earliest minimum wins (optimize.cpp:158)
                 // near the running best (from above or, as a new best, from below)?
                 if (track && (lt ? err.hi >= tie_lo : err.hi <= tie_thr)) {  // rare
@@ -724,9 +759,6 @@ __global__ void __launch_bounds__(256, 4) k_qrange_tables(const TDesc* __restric
                 fixed_s = s;
                 fixed_err = err;
             }
-            if (t == cfg.steps) break;
-            s = snap(adam_update_tab(m, vv, s, grad, cfg.bc1[t + 1], cfg.bc2[t + 1], cfg.rbc1[t + 1],
-                                     cfg.rbc2[t + 1], cfg.adam));
         }
         if (FIXED) {
             s_fin = dd_le(fixed_err, best_err) ? fixed_s : s0;  // optimize.cpp:169-178 (best_err = e0)
