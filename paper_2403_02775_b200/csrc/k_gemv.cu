@@ -921,8 +921,10 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
             // two 8-warp CTAs per SM: resident beside the main kernel (see k_gemv_outliers)
             int sms = 148;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            // (up to 16k columns: one warp per column, measured faster at batch 1)
-            const int64_t ctas = p->cols <= 16384
+            // (up to 16k columns, or without PDL: one warp per column)
+            static const int pdl_max = std::getenv("EZQ_GEMV_PDL_MAX") ? std::atoi(std::getenv("EZQ_GEMV_PDL_MAX")) : 1;
+            const bool pdl = a.batch <= pdl_max;
+            const int64_t ctas = (p->cols <= 16384 || !pdl)
                                      ? (p->cols + 7) / 8
                                      : std::min<int64_t>((p->cols + 7) / 8, std::max<int64_t>(2 * static_cast<int64_t>(sms),
                                                                                             (p->cols + 511) / 512));
@@ -933,7 +935,10 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
             lc.stream = st;
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            at[0].val.programmaticStreamSerializationAllowed = 1;
+            // programmatic dependent launch (gathers overlap the weight stream)
+            // at batch 1; plain stream order above (measured: overlapping the
+            // multi-row gathers with the stream slowed both)
+            at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
             lc.attrs = at;
             lc.numAttrs = 1;
             const int64_t* cp = p->col_ptr;
