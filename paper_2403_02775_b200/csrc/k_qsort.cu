@@ -470,7 +470,7 @@ struct ColumnSorter {
 // sorted in registers with a block radix sort, and its table D (rows + 2
 // doubles) and ColInfo go to global memory for the loop kernel.
 template <int THREADS, int IPT>
-__global__ void __launch_bounds__(THREADS) k_qsort_tables(const TDesc* __restrict__ td,
+__global__ void __launch_bounds__(THREADS, 3072 / THREADS / 4) k_qsort_tables(const TDesc* __restrict__ td,
                                                           const K3Group* __restrict__ groups, int cpb, int prows,
                                                           int dstride, int xstride, int tstride, int need_c,
                                                           double* __restrict__ tables,
