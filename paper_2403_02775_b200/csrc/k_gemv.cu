@@ -185,8 +185,7 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const unsigned (&a)[4], 
 // blocks and meet in shared memory at the end of the colblock (fixed order:
 // deterministic, bit-identical across calls).
 constexpr int kCW = 4;             // consumer warps per CTA
-constexpr int kRing = 3;           // ring stages per CTA (streaming many colblocks per CTA)
-constexpr int kRingDeep = 8;       // ... when every colblock has its own resident CTA (whole K in flight)
+constexpr int kRing = 3;           // ring stages per CTA
 constexpr int kStageCode = 8192;   // code bytes per full stage
 constexpr int kStreamThreads = (kCW + 1) * 32;
 
@@ -201,7 +200,6 @@ struct GemvArgs {
     int64_t xstride;   // elements between batch rows of x
     int batch;         // rows of this group (1..16)
     float* y;
-    int ring;          // ring stages (kRing or kRingDeep)
 };
 
 __device__ __forceinline__ void bar_wait(unsigned bar, unsigned phase) {
@@ -234,8 +232,8 @@ struct CbGeom {
     // HSUB2-free dequant (bf16 / split-f32 x, batch <= 8): A' = level + C
     // exactly (C = 128 - lmin), D' = D + C * sum(x) corrected at the end
     static constexpr bool SUBFREE = SF && XT != kF16 && NB == 1;
-    static constexpr size_t smem(int ring = kRing) {
-        return static_cast<size_t>(ring) * (CB + XB) + 2 * kRingDeep * 8 +
+    static constexpr size_t smem() {
+        return static_cast<size_t>(kRing) * (CB + XB) + 2 * kRing * 8 +
                (QW > 1 ? static_cast<size_t>(kCW) * NB * 32 * 4 * sizeof(float) : 0) + 16 * sizeof(float) + 16;
     }
 };
@@ -247,17 +245,16 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
     constexpr int ES = Gm::ES, NBT = Gm::NBT, S = Gm::S, XP = Gm::XP, XB = Gm::XB, CB = Gm::CB;
     constexpr int TW = Gm::TW, QW = Gm::QW;
     extern __shared__ __align__(128) unsigned char smem[];
-    const int ring = a.ring;
-    unsigned char* codes = smem;                     // [ring][S][TPC][512]
-    unsigned char* xsm = smem + ring * CB;           // [ring][NBT][XP]
-    unsigned long long* bars = reinterpret_cast<unsigned long long*>(xsm + ring * XB);
-    float* red = reinterpret_cast<float*>(bars + 2 * kRingDeep);  // [kCW][NB][32][4] (QW > 1)
+    unsigned char* codes = smem;                     // [kRing][S][TPC][512]
+    unsigned char* xsm = smem + kRing * CB;          // [kRing][NBT][XP]
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(xsm + kRing * XB);
+    float* red = reinterpret_cast<float*>(bars + 2 * kRing);  // [kCW][NB][32][4] (QW > 1)
     float* xsum = red + (QW > 1 ? kCW * NB * 32 * 4 : 0);      // [16] sum_i x[n][i] (SUBFREE)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned full0 = static_cast<unsigned>(__cvta_generic_to_shared(bars));
-    const unsigned empty0 = full0 + 8 * kRingDeep;
+    const unsigned empty0 = full0 + 8 * kRing;
     if (threadIdx.x == 0) {
-        for (int k = 0; k < ring; ++k) {
+        for (int k = 0; k < kRing; ++k) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full0 + 8 * k));  // expect_tx arrival
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * k), "r"(kCW + 1));
         }
@@ -271,7 +268,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
         // SUBFREE: while the CTA's first colblock streams, the producer also
         // sums the staged x slices (sum_i x[n][i] over all of K, the values
         // the MMA sees: bf16, or f32 as bf16 hi + lo; fixed lane assignment
-        // and butterfly -- deterministic), lagging ring - 1 stages behind
+        // and butterfly -- deterministic), lagging kRing - 1 stages behind
         // the copies; every other stage it releases at once. The sums go to
         // xsum[] and named barrier 2 tells the consumers.
         float xs_acc[Gm::NBT];
@@ -279,8 +276,8 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
         for (int n = 0; n < Gm::NBT; ++n) xs_acc[n] = 0.f;
         int done = 0;  // first-colblock stages summed and released
         auto sum_stage = [&](int p) {
-            const int slot = p % ring;
-            bar_wait(full0 + 8 * slot, (p / ring) & 1);
+            const int slot = p % kRing;
+            bar_wait(full0 + 8 * slot, (p / kRing) & 1);
             const int cnt = static_cast<int>(min(static_cast<int64_t>(S), a.kq - static_cast<int64_t>(p) * S));
             const unsigned char* xw = xsm + slot * XB;
             for (int n = 0; n < a.batch; ++n) {
@@ -322,8 +319,8 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
                 }
                 const int64_t q0 = sq * S;
                 const int cnt = static_cast<int>(min(static_cast<int64_t>(S), a.kq - q0));
-                const int slot = k % ring;
-                if (k >= ring) bar_wait(empty0 + 8 * slot, ((k / ring) - 1) & 1);
+                const int slot = k % kRing;
+                if (k >= kRing) bar_wait(empty0 + 8 * slot, ((k / kRing) - 1) & 1);
                 const unsigned fb = full0 + 8 * slot;
                 // codes (one bulk copy) and the batch rows' x slices (one bulk
                 // copy per row, contiguous in x), all on the stage's barrier
@@ -347,7 +344,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
                         "l"(static_cast<const char*>(a.x) + (lane * a.xstride + 64 * q0) * ES), "r"(xbytes), "r"(fb)
                         : "memory");
                 if (Gm::SUBFREE && k < first_n) {
-                    if (k >= ring - 1) sum_stage(done++);  // the oldest stage in flight
+                    if (k >= kRing - 1) sum_stage(done++);  // the oldest stage in flight
                 } else {
                     __syncwarp();
                     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * slot) : "memory");
@@ -385,8 +382,8 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
                     for (int i = 0; i < 4; ++i) acc[u][h][n8][i] = 0.f;
         for (int64_t sq = 0; sq < nst_cb; ++sq, ++k) {
             const int cnt = static_cast<int>(min(static_cast<int64_t>(S), a.kq - sq * S));
-            const int slot = k % ring;
-            bar_wait(full0 + 8 * slot, (k / ring) & 1);
+            const int slot = k % kRing;
+            bar_wait(full0 + 8 * slot, (k / kRing) & 1);
             const uint4* cw = reinterpret_cast<const uint4*>(codes + slot * CB);
             const unsigned char* xw = xsm + slot * XB;
 #pragma unroll
@@ -653,50 +650,43 @@ struct ezq_gemv_plan {
     float* xt;            // batch > 1 with outliers: x transposed [rows][16] f32 (owned)
     void* xpad;           // ragged / unaligned x: padded copy [16][kq * 64] (owned)
     int grid[6];          // persistent CTAs of k_gemv_cb per (x dtype, NB) variant
-    int ring[6];          // its ring depth
 };
 
 namespace {
 
 template <int TPC, int NB, int XT>
-int cb_ctas_per_sm(int ring) {
-    const int smem = static_cast<int>(CbGeom<TPC, NB, XT>::smem(kRingDeep));  // the attribute covers both depths
+int cb_ctas_per_sm() {
+    const int smem = static_cast<int>(CbGeom<TPC, NB, XT>::smem());
     if (NB == 1 && XT != kF16)  // the HSUB2-free twin (same shared memory)
         cudaFuncSetAttribute(k_gemv_cb<TPC, NB, XT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     auto k = k_gemv_cb<TPC, NB, XT, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kStreamThreads, CbGeom<TPC, NB, XT>::smem(ring)) !=
-            cudaSuccess ||
-        n < 1)
-        n = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kStreamThreads, smem) != cudaSuccess || n < 1) n = 1;
     return n;
 }
 
 template <int TPC>
-void occ_row(int* o, int ring) {  // variants in (x dtype, NB) order: f32/1, f32/2, bf16/1, bf16/2, f16/1, f16/2
-    o[0] = cb_ctas_per_sm<TPC, 1, kF32>(ring);
-    o[1] = cb_ctas_per_sm<TPC, 2, kF32>(ring);
-    o[2] = cb_ctas_per_sm<TPC, 1, kBF16>(ring);
-    o[3] = cb_ctas_per_sm<TPC, 2, kBF16>(ring);
-    o[4] = cb_ctas_per_sm<TPC, 1, kF16>(ring);
-    o[5] = cb_ctas_per_sm<TPC, 2, kF16>(ring);
+void occ_row(int* o) {  // variants in (x dtype, NB) order: f32/1, f32/2, bf16/1, bf16/2, f16/1, f16/2
+    o[0] = cb_ctas_per_sm<TPC, 1, kF32>();
+    o[1] = cb_ctas_per_sm<TPC, 2, kF32>();
+    o[2] = cb_ctas_per_sm<TPC, 1, kBF16>();
+    o[3] = cb_ctas_per_sm<TPC, 2, kBF16>();
+    o[4] = cb_ctas_per_sm<TPC, 1, kF16>();
+    o[5] = cb_ctas_per_sm<TPC, 2, kF16>();
 }
 
-// CTAs per SM of every (ring depth, TPC, variant), measured once per process.
-const int* occupancy(int tpc, bool deep = false) {
-    static int occ[2][4][6];
+// CTAs per SM of every (TPC, variant), measured once per process.
+const int* occupancy(int tpc) {
+    static int occ[4][6];
     static std::once_flag once;
     std::call_once(once, [] {
-        for (int d = 0; d < 2; ++d) {
-            const int ring = d ? kRingDeep : kRing;
-            occ_row<1>(occ[d][0], ring);
-            occ_row<2>(occ[d][1], ring);
-            occ_row<4>(occ[d][2], ring);
-            occ_row<8>(occ[d][3], ring);
-        }
+        occ_row<1>(occ[0]);
+        occ_row<2>(occ[1]);
+        occ_row<4>(occ[2]);
+        occ_row<8>(occ[3]);
     });
-    return occ[deep ? 1 : 0][tpc == 1 ? 0 : tpc == 2 ? 1 : tpc == 4 ? 2 : 3];
+    return occ[tpc == 1 ? 0 : tpc == 2 ? 1 : tpc == 4 ? 2 : 3];
 }
 
 // HSUB2-free dequant for batch <= 2 (bf16 / f32 x): the producer's per-stage
@@ -704,10 +694,10 @@ const int* occupancy(int tpc, bool deep = false) {
 template <int TPC, int NB, int XT>
 void launch_cb_t(const GemvArgs& a, int grid, cudaStream_t st) {
     if (NB == 1 && XT != kF16 && a.batch <= 2)
-        k_gemv_cb<TPC, NB, XT, true><<<static_cast<unsigned>(grid), kStreamThreads,
-                                       CbGeom<TPC, NB, XT, true>::smem(a.ring), st>>>(a);
+        k_gemv_cb<TPC, NB, XT, true><<<static_cast<unsigned>(grid), kStreamThreads, CbGeom<TPC, NB, XT, true>::smem(),
+                                       st>>>(a);
     else
-        k_gemv_cb<TPC, NB, XT, false><<<static_cast<unsigned>(grid), kStreamThreads, CbGeom<TPC, NB, XT>::smem(a.ring),
+        k_gemv_cb<TPC, NB, XT, false><<<static_cast<unsigned>(grid), kStreamThreads, CbGeom<TPC, NB, XT>::smem(),
                                         st>>>(a);
 }
 
@@ -833,20 +823,12 @@ int ezq_gemv_prepare_ex(const ezq_qweight* q, int outlier_dtype, void* stream, e
     }
     p->ncb = (p->tiles + p->tpc - 1) / p->tpc;
     const int* occ = occupancy(p->tpc);
-    const int* occ_deep = occupancy(p->tpc, true);
     static const bool dbg = std::getenv("EZQ_GEMV_DEBUG") != nullptr;
-    static const int force_ring = std::getenv("EZQ_GEMV_RING") ? std::atoi(std::getenv("EZQ_GEMV_RING")) : 0;
     for (int v = 0; v < 6; ++v) {
-        // every colblock its own resident CTA even with the deep ring: put
-        // the colblock's whole K in flight at once (short, latency-bound
-        // GEMVs); else stream colblocks through the shallow ring
-        const bool deep = force_ring ? force_ring == kRingDeep
-                                     : p->ncb <= static_cast<int64_t>(sms) * occ_deep[v];
-        p->ring[v] = deep ? kRingDeep : kRing;
-        p->grid[v] = static_cast<int>(std::min<int64_t>(p->ncb, static_cast<int64_t>(sms) * (deep ? occ_deep[v] : occ[v])));
+        p->grid[v] = static_cast<int>(std::min<int64_t>(p->ncb, static_cast<int64_t>(sms) * occ[v]));
         if (dbg)
-            std::fprintf(stderr, "ezq_gemv_prepare: tpc %d ncb %lld variant %d ring %d ctas/sm %d grid %d\n", p->tpc,
-                         static_cast<long long>(p->ncb), v, p->ring[v], deep ? occ_deep[v] : occ[v], p->grid[v]);
+            std::fprintf(stderr, "ezq_gemv_prepare: tpc %d ncb %lld variant %d ctas/sm %d grid %d\n", p->tpc,
+                         static_cast<long long>(p->ncb), v, occ[v], p->grid[v]);
     }
     const int64_t nw = p->ncb * p->kq * p->tpc * 32;
     EZQ_CK(cudaMalloc(&p->T, sizeof(uint4) * nw));
@@ -928,7 +910,6 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
             if (e != cudaSuccess) return cuda_error(e, "gemv: before the main kernel");
         }
         const int v = x_dtype * 2 + (two ? 1 : 0);
-        a.ring = p->ring[v];
         launch_cb(p->tpc, v, a, p->grid[v], st);
         count_launch();
         if (dsync) {
