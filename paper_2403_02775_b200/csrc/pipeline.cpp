@@ -617,12 +617,13 @@ int quantize_batch_host(const float* const* Ws, const int64_t* rows, const int64
                         ezq_qweight** outs, int* failed) {
     // Chunk sizes (overridable for tuning: EZQ_CHUNK_MB / EZQ_FIRST_MB).
     static const int64_t kChunkBytes =
-        std::getenv("EZQ_CHUNK_MB") ? (std::atoll(std::getenv("EZQ_CHUNK_MB")) << 20) : (384ll << 20);
+        std::getenv("EZQ_CHUNK_MB") ? (std::atoll(std::getenv("EZQ_CHUNK_MB")) << 20) : (768ll << 20);
     std::vector<std::pair<int, int>> chunks;  // [first, last)
     int64_t max_bytes = 0;
     // The first chunk is small so compute starts after a short ingest; the
-    // later ones are 384 MB (OPT-1.3B host->host: 1024 MB chunks 104 ms,
-    // 384 MB 100 ms, + 128 MB first chunk 99 ms; 256 MB 105 ms).
+    // later ones are 768 MB (LLaMA-7B set host->host on B200: 384 MB chunks
+    // 542 ms, 768 MB 489 ms, 1536 MB 498 ms; the pure 25.9 GB H2D copy takes
+    // 467 ms, tools/h2d_ceiling.py).
     static const int64_t kFirstBytes = std::getenv("EZQ_FIRST_MB") ? (std::atoll(std::getenv("EZQ_FIRST_MB")) << 20)
                                                                     : (128ll << 20);
     // ... and so is the last: its compute and D2H are the exposed tail.
