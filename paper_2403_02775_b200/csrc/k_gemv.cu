@@ -185,8 +185,8 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const unsigned (&a)[4], 
 // blocks and meet in shared memory at the end of the colblock (fixed order:
 // deterministic, bit-identical across calls).
 constexpr int kCW = 4;             // consumer warps per CTA
-constexpr int kRing = 3;           // ring stages per CTA
-constexpr int kStageCode = 8192;   // code bytes per full stage
+constexpr int kRing = 2;           // ring stages per CTA
+constexpr int kStageCode = 32768;  // code bytes per full stage (sweep on B200: 8-32 KB x 2-6 stages)
 constexpr int kStreamThreads = (kCW + 1) * 32;
 
 struct GemvArgs {
