@@ -524,36 +524,6 @@ __device__ __forceinline__ float load_val(const void* v, int64_t e) {
     return static_cast<const float*>(v)[e];
 }
 
-// Batch 1: one COLUMN per lane (its CSC entries summed in order: fixed,
-// deterministic), kE entries in flight per lane, every gather issued before
-// griddepcontrol.wait; lanes of a warp walk 32 adjacent columns, so the
-// column pointers and the y update are coalesced.
-template <int XT, int VT>
-__global__ void __launch_bounds__(256) k_gemv_outliers_b1(int64_t cols, const int64_t* __restrict__ col_ptr,
-                                                          const uint32_t* __restrict__ out_row,
-                                                          const void* __restrict__ out_val, const void* __restrict__ x,
-                                                          float* __restrict__ y) {
-    constexpr int kE = 8;
-    const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    float acc = 0.f;
-    int64_t e0 = 0, e1 = 0;
-    if (j < cols) e0 = __ldg(col_ptr + j), e1 = __ldg(col_ptr + j + 1);
-    for (int64_t e = e0; e < e1; e += kE) {
-        uint32_t r[kE];
-        float v[kE];
-#pragma unroll
-        for (int u = 0; u < kE; ++u) {
-            const bool ok = e + u < e1;
-            r[u] = ok ? __ldg(out_row + e + u) : 0u;
-            v[u] = ok ? load_val<VT>(out_val, e + u) : 0.f;
-        }
-#pragma unroll
-        for (int u = 0; u < kE; ++u) acc = fmaf(load_x(x, XT, r[u]), v[u], acc);
-    }
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (e1 > e0) y[j] += acc;
-}
-
 template <int XT, int NBT, int VT>
 __global__ void __launch_bounds__(256) k_gemv_outliers(int64_t rows, int64_t cols, const int64_t* __restrict__ col_ptr,
                                                        const uint32_t* __restrict__ out_row,
@@ -755,12 +725,7 @@ void launch_cb(int tpc, int v, const GemvArgs& a, int grid, cudaStream_t st) {
 template <int XT, int VT>
 cudaError_t launch_outliers_v(cudaLaunchConfig_t& lc, int bt, int64_t rows, int64_t cols, const int64_t* cp,
                               const uint32_t* orow, const void* oval, const void* xg, float* yg, const float* xtg) {
-    if (bt == 1) {  // one column per lane
-        cudaLaunchConfig_t l1 = lc;
-        l1.gridDim = dim3(static_cast<unsigned>((cols + 255) / 256));
-        l1.dynamicSmemBytes = 0;
-        return cudaLaunchKernelEx(&l1, k_gemv_outliers_b1<XT, VT>, cols, cp, orow, oval, xg, yg);
-    }
+    if (bt == 1) return cudaLaunchKernelEx(&lc, k_gemv_outliers<XT, 1, VT>, rows, cols, cp, orow, oval, xg, bt, yg, xtg);
     if (bt <= 8) return cudaLaunchKernelEx(&lc, k_gemv_outliers<XT, 8, VT>, rows, cols, cp, orow, oval, xg, bt, yg, xtg);
     return cudaLaunchKernelEx(&lc, k_gemv_outliers<XT, 16, VT>, rows, cols, cp, orow, oval, xg, bt, yg, xtg);
 }
