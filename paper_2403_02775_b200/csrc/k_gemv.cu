@@ -921,13 +921,14 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
             // two 8-warp CTAs per SM: resident beside the main kernel (see k_gemv_outliers)
             int sms = 148;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            // (up to 16k columns, or without PDL: one warp per column)
+            // A programmatic dependent launch (gathers overlap the weight
+            // stream) pays at batch 1 on up to 16k columns; above that, plain
+            // stream order (measured on B200: the overlap slowed both kernels:
+            // BLOOM shape batch 1, 135 vs 110 us; batch 16, 494 vs 321 us).
+            // One warp per column either way.
             static const int pdl_max = std::getenv("EZQ_GEMV_PDL_MAX") ? std::atoi(std::getenv("EZQ_GEMV_PDL_MAX")) : 1;
-            const bool pdl = a.batch <= pdl_max;
-            const int64_t ctas = (p->cols <= 16384 || !pdl)
-                                     ? (p->cols + 7) / 8
-                                     : std::min<int64_t>((p->cols + 7) / 8, std::max<int64_t>(2 * static_cast<int64_t>(sms),
-                                                                                            (p->cols + 511) / 512));
+            const bool pdl = a.batch <= pdl_max && p->cols <= 16384;
+            const int64_t ctas = (p->cols + 7) / 8;
             const int64_t cpw = (p->cols + 8 * ctas - 1) / (8 * ctas);
             lc.gridDim = dim3(static_cast<unsigned>(ctas));
             lc.blockDim = dim3(256);
