@@ -50,6 +50,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <vector>
 
@@ -188,6 +189,8 @@ constexpr int kCW = 4;             // consumer warps per CTA
 constexpr int kRing = 2;           // ring stages per CTA
 constexpr int kStageCode = 32768;  // code bytes per full stage (sweep on B200: 8-32 KB x 2-6 stages)
 constexpr int kStreamThreads = (kCW + 1) * 32;
+constexpr int kOutWarpsMax = 4;                                  // outlier warps (fused outliers): 1 or 4
+constexpr int kOutThreads = kStreamThreads + 32 * kOutWarpsMax;
 
 struct GemvArgs {
     const uint4* T;
@@ -200,7 +203,24 @@ struct GemvArgs {
     int64_t xstride;   // elements between batch rows of x
     int batch;         // rows of this group (1..16)
     float* y;
+    // Fused outlier term (ezq_gemv_prepare; null: the separate pass): per
+    // colblock, the outliers of every 512-row segment as {header, entries},
+    // streamed into the ring beside the stage's codes.
+    const unsigned char* oseg;
+    const int64_t* obnd;  // [ncb * nseg + 1] byte offsets of the segments in oseg
+    int64_t nseg;         // segments per colblock
+    int ob;               // shared-memory bytes per ring stage for the segments
+    int oes;              // entry bytes: 8 = {u32 row, f32 value}, 4 = {u16 row | f16 value << 16}
 };
+
+// Fused outliers: segment = 512 rows (8 q-blocks; every stage of the variants
+// that fuse holds 1 or 2 whole segments) x one colblock. Layout (16-byte
+// aligned, sizes multiples of 16): u32 total bytes; u16 start[TPC * 16 + 1]
+// (entry index of each column's first outlier; rows ascending inside a
+// column); pad; entries.
+constexpr int kSegRows = 512;
+constexpr int kSegQ = kSegRows / kBlockRows;
+__host__ __device__ constexpr int seg_hdr_bytes(int tpc) { return (4 + 2 * (tpc * kTileCols + 1) + 15) & ~15; }
 
 __device__ __forceinline__ void bar_wait(unsigned bar, unsigned phase) {
     unsigned ok = 0;
@@ -232,14 +252,136 @@ struct CbGeom {
     // HSUB2-free dequant (bf16 / split-f32 x, batch <= 8): A' = level + C
     // exactly (C = 128 - lmin), D' = D + C * sum(x) corrected at the end
     static constexpr bool SUBFREE = SF && XT != kF16 && NB == 1;
-    static constexpr size_t smem() {
-        return static_cast<size_t>(kRing) * (CB + XB) + 2 * kRing * 8 +
-               (QW > 1 ? static_cast<size_t>(kCW) * NB * 32 * 4 * sizeof(float) : 0) + 16 * sizeof(float) + 16;
-    }
+    static constexpr size_t RED = QW > 1 ? static_cast<size_t>(kCW) * NB * 32 * 4 * sizeof(float) : 0;
+    static constexpr size_t smem() { return static_cast<size_t>(kRing) * (CB + XB) + 2 * kRing * 8 + RED + 16 * sizeof(float) + 16; }
+    // fused outliers: 2 mbarriers (outlier sums ready / read), the sums
+    // [TPC * 16][NBT], then the segment ring
+    static constexpr size_t OBAR = static_cast<size_t>(kRing) * (CB + XB) + 2 * kRing * 8 + RED + 16 * sizeof(float);
+    static constexpr size_t OSUM = (OBAR + 16 + 15) & ~static_cast<size_t>(15);
+    static constexpr size_t osm_off() { return OSUM + static_cast<size_t>(TPC) * kTileCols * NBT * sizeof(float); }
 };
 
-template <int TPC, int NB, int XT, bool SF>
-__global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
+// x value of batch row n at staged row r (exact f32)
+template <int XT>
+__device__ __forceinline__ float xs_val(const unsigned char* xs, int pitch, int n, unsigned r) {
+    if (XT == kF32) return reinterpret_cast<const float*>(xs)[n * pitch + r];
+    const unsigned short u = reinterpret_cast<const unsigned short*>(xs)[n * pitch + r];
+    if (XT == kBF16) return __uint_as_float(static_cast<unsigned>(u) << 16);
+    return __half2float(__ushort_as_half(u));
+}
+
+__device__ __forceinline__ void seg_entry(const unsigned char* ent, int oes, int e, unsigned& r, float& v) {
+    if (oes == 8) {
+        const uint2 w = *reinterpret_cast<const uint2*>(ent + 8 * e);
+        r = w.x;
+        v = __uint_as_float(w.y);
+    } else {
+        const unsigned w = *reinterpret_cast<const unsigned*>(ent + 4 * e);
+        r = w & 0xffffu;
+        v = __half2float(__ushort_as_half(static_cast<unsigned short>(w >> 16)));
+    }
+}
+
+// The outlier warps (fused outliers; OW = 1 for batch groups of <= 2 rows,
+// else 4): extra consumers of every ring stage. Warp ow owns C / OW of the
+// colblock's C = 16 TPC columns; its lanes own them (CW / 32 columns per
+// lane, or 32 / CW lanes per column splitting the entries), walk each stage's
+// segment lists in rounds -- every round loads the next entry of all L
+// lists at once, L independent shared-memory chains in flight -- and
+// accumulate NBO batch rows in registers (fixed order: deterministic). At
+// the end of a colblock it hands the sums to the writers through shared
+// memory (one buffer, mbarriers both ways).
+template <int TPC, int S, int XT, int XP, int XB, int NBT, int NBO, int OW>
+__device__ __forceinline__ void outlier_warp(const GemvArgs& a, int64_t nst_cb, unsigned full0, unsigned empty0,
+                                             const unsigned char* osm, const unsigned char* xsm, float* osum,
+                                             unsigned obar0, unsigned rbar0, int lane, int ow) {
+    constexpr int C = TPC * kTileCols;
+    constexpr int CW = C / OW;                   // columns per outlier warp
+    constexpr int CPL = CW >= 32 ? CW / 32 : 1;  // columns per lane
+    constexpr int LPC = CW >= 32 ? 1 : 32 / CW;  // lanes per column
+    constexpr int SPG = S >= kSegQ ? S / kSegQ : 1;
+    constexpr int L = CPL * SPG;
+    constexpr int ES = XT == kF32 ? 4 : 2;
+    const int sub = lane % LPC;
+    int k = 0, it = 0;
+    for (int64_t cb = blockIdx.x; cb < a.ncb; cb += gridDim.x, ++it) {
+        float o[CPL][NBO];
+#pragma unroll
+        for (int i = 0; i < CPL; ++i)
+#pragma unroll
+            for (int n = 0; n < NBO; ++n) o[i][n] = 0.f;
+        for (int64_t sq = 0; sq < nst_cb; ++sq, ++k) {
+            const int slot = k % kRing;
+            bar_wait(full0 + 8 * slot, (k / kRing) & 1);
+            const unsigned char* ob = osm + slot * a.ob;
+            const unsigned char* xw = xsm + slot * XB;
+            const int64_t sg0 = sq * SPG;
+            const unsigned char* ent[SPG];
+            int e[L], e1[L];
+#pragma unroll
+            for (int sg = 0; sg < SPG; ++sg) {
+                const bool ok = sg0 + sg < a.nseg;
+                const unsigned short* hs = reinterpret_cast<const unsigned short*>(ob + 4);
+                ent[sg] = ob + seg_hdr_bytes(TPC);
+#pragma unroll
+                for (int i = 0; i < CPL; ++i) {
+                    const int c = ow * CW + (LPC > 1 ? lane / LPC : lane + 32 * i);
+                    e[sg * CPL + i] = ok ? hs[c] + sub : 0;
+                    e1[sg * CPL + i] = ok ? hs[c + 1] : 0;
+                }
+                if (sg + 1 < SPG && ok) ob += *reinterpret_cast<const unsigned*>(ob);
+            }
+            bool more = false;
+#pragma unroll
+            for (int i = 0; i < L; ++i) more |= e[i] < e1[i];
+#pragma unroll 1
+            while (more) {
+                unsigned r[L];
+                float v[L];
+#pragma unroll
+                for (int i = 0; i < L; ++i) {
+                    r[i] = 0;
+                    v[i] = 0.f;
+                    if (e[i] < e1[i]) seg_entry(ent[i / CPL], a.oes, e[i], r[i], v[i]);
+                }
+#pragma unroll
+                for (int i = 0; i < L; ++i)
+                    if (e[i] < e1[i]) {
+                        const unsigned char* xs = xw + (i / CPL) * kSegRows * ES;
+#pragma unroll
+                        for (int n = 0; n < NBO; ++n) o[i % CPL][n] = fmaf(v[i], xs_val<XT>(xs, XP, n, r[i]), o[i % CPL][n]);
+                    }
+                more = false;
+#pragma unroll
+                for (int i = 0; i < L; ++i) {
+                    e[i] += LPC;
+                    more |= e[i] < e1[i];
+                }
+            }
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8 * slot) : "memory");
+        }
+        // hand the colblock's sums to the writers
+        if (it >= 1) bar_wait(rbar0, (it - 1) & 1);  // the buffer was read by the writers of it - 1
+#pragma unroll
+        for (int off = 1; off < LPC; off <<= 1)  // lanes of a column: fixed butterfly
+#pragma unroll
+            for (int n = 0; n < NBO; ++n) o[0][n] += __shfl_xor_sync(0xffffffffu, o[0][n], off);
+        float* os = osum;
+        if (sub == 0) {
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) {
+                const int c = ow * CW + (LPC > 1 ? lane / LPC : lane + 32 * i);
+#pragma unroll
+                for (int n = 0; n < NBO; ++n) os[c * NBT + n] = o[i][n];
+            }
+        }
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(obar0) : "memory");
+    }
+}
+
+template <int TPC, int NB, int XT, bool SF, bool OUT>
+__global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
     using Gm = CbGeom<TPC, NB, XT, SF>;
     constexpr bool F16 = XT == kF16;
     constexpr int ES = Gm::ES, NBT = Gm::NBT, S = Gm::S, XP = Gm::XP, XB = Gm::XB, CB = Gm::CB;
@@ -250,13 +392,22 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
     unsigned long long* bars = reinterpret_cast<unsigned long long*>(xsm + kRing * XB);
     float* red = reinterpret_cast<float*>(bars + 2 * kRing);  // [kCW][NB][32][4] (QW > 1)
     float* xsum = red + (QW > 1 ? kCW * NB * 32 * 4 : 0);      // [16] sum_i x[n][i] (SUBFREE)
+    // OUT: outlier sums ready (obar: every outlier lane) / read (rbar: every consumer lane)
+    const unsigned obar0 = static_cast<unsigned>(__cvta_generic_to_shared(smem + Gm::OBAR)), rbar0 = obar0 + 8;
+    float* osum = reinterpret_cast<float*>(smem + Gm::OSUM);  // [TPC * 16][NBT] (OUT)
+    unsigned char* osm = smem + Gm::osm_off();                 // [kRing][a.ob] outlier segments (OUT)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nout = static_cast<int>(blockDim.x >> 5) - kCW - 1;  // outlier warps (OUT)
     const unsigned full0 = static_cast<unsigned>(__cvta_generic_to_shared(bars));
     const unsigned empty0 = full0 + 8 * kRing;
     if (threadIdx.x == 0) {
         for (int k = 0; k < kRing; ++k) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full0 + 8 * k));  // expect_tx arrival
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * k), "r"(kCW + 1));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8 * k), "r"(kCW + 1 + (OUT ? nout : 0)));
+        }
+        if (OUT) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(obar0), "r"(32 * nout));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(rbar0), "r"(kCW * 32));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -264,6 +415,16 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
     asm volatile("griddepcontrol.launch_dependents;");
     const int64_t nst_cb = (a.kq + S - 1) / S;  // stages per colblock
 
+    if (OUT && warp > kCW) {  // ---- outlier warps (1 or 4: out_warps(batch))
+        using G = CbGeom<TPC, NB, XT, SF>;
+        const int ow = warp - kCW - 1;
+        if (NB == 2) outlier_warp<TPC, S, XT, XP, XB, G::NBT, 16, 4>(a, nst_cb, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
+        else if (a.batch == 1) outlier_warp<TPC, S, XT, XP, XB, G::NBT, 1, 1>(a, nst_cb, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
+        else if (a.batch == 2) outlier_warp<TPC, S, XT, XP, XB, G::NBT, 2, 1>(a, nst_cb, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
+        else if (a.batch <= 4) outlier_warp<TPC, S, XT, XP, XB, G::NBT, 4, 4>(a, nst_cb, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
+        else outlier_warp<TPC, S, XT, XP, XB, G::NBT, 8, 4>(a, nst_cb, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
+        return;
+    }
     if (warp == kCW) {  // ---- producer warp: codes and x slices by TMA bulk copies
         // SUBFREE: while the CTA's first colblock streams, the producer also
         // sums the staged x slices (sum_i x[n][i] over all of K, the values
@@ -307,9 +468,20 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
                 if (lane == 0) xsum[n] = v;
             }
             __syncwarp();
-            asm volatile("bar.arrive 2, %0;" ::"r"(kStreamThreads) : "memory");
+            asm volatile("bar.arrive 2, %0;" ::"r"(kStreamThreads) : "memory");  // consumers + producer
         };
         const int first_n = static_cast<int>(nst_cb);  // stages of the first colblock
+        // OUT: byte range of a stage's segments, loaded one stage ahead (lane 0)
+        constexpr int SPG = S >= kSegQ ? S / kSegQ : 1;
+        int64_t o_lo = 0, o_hi = 0;
+        auto seg_range = [&](int64_t cb, int64_t sq) {
+            if (OUT && lane == 0 && cb < a.ncb) {
+                const int64_t s0 = sq * SPG, s1 = min(s0 + SPG, a.nseg);
+                o_lo = __ldg(a.obnd + cb * a.nseg + s0);
+                o_hi = __ldg(a.obnd + cb * a.nseg + s1);
+            }
+        };
+        seg_range(blockIdx.x, 0);
         int k = 0;
         for (int64_t cb = blockIdx.x; cb < a.ncb; cb += gridDim.x) {
             for (int64_t sq = 0; sq < nst_cb; ++sq, ++k) {
@@ -326,17 +498,30 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
                 // copy per row, contiguous in x), all on the stage's barrier
                 const unsigned cbytes = static_cast<unsigned>(cnt) * TPC * 512u;
                 const unsigned xbytes = static_cast<unsigned>(cnt) * 64u * ES;
+                const int64_t seg_lo = o_lo;
+                const unsigned obytes = OUT ? static_cast<unsigned>(o_hi - o_lo) : 0u;
                 if (lane == 0)
                     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
-                                 "r"(cbytes + xbytes * static_cast<unsigned>(a.batch))
+                                 "r"(cbytes + xbytes * static_cast<unsigned>(a.batch) + obytes)
                                  : "memory");
                 __syncwarp();
-                if (lane == 0)
+                if (lane == 0) {
                     asm volatile(
                         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                             static_cast<unsigned>(__cvta_generic_to_shared(codes + slot * CB))),
                         "l"(a.T + (cb * a.kq + q0) * TPC * 32), "r"(cbytes), "r"(fb)
                         : "memory");
+                    if (OUT && obytes)
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                static_cast<unsigned>(__cvta_generic_to_shared(osm + slot * a.ob))),
+                            "l"(a.oseg + seg_lo), "r"(obytes), "r"(fb)
+                            : "memory");
+                }
+                if (OUT) {  // the next stage of this CTA
+                    if (sq + 1 < nst_cb) seg_range(cb, sq + 1);
+                    else seg_range(cb + gridDim.x, 0);
+                }
                 if (lane < a.batch)
                     asm volatile(
                         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -369,8 +554,8 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
     for (int n8 = 0; n8 < NB; ++n8) xrow[n8] = min(n8 * 8 + g, a.batch - 1);
     const int tile0 = TPC >= kCW ? warp : warp % TPC;
     const int qoff = TPC >= kCW ? 0 : warp / TPC;
-    int k = 0;
-    for (int64_t cb = blockIdx.x; cb < a.ncb; cb += gridDim.x) {
+    int k = 0, it = 0;
+    for (int64_t cb = blockIdx.x; cb < a.ncb; cb += gridDim.x, ++it) {
         float acc[TW][2][NB][4];  // two accumulator sets per tile (alternating q) break the MMA chain
 #pragma unroll
         for (int u = 0; u < TW; ++u)
@@ -460,6 +645,8 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
             }
             named_sync(1, kCW * 32);  // red is reused by the next colblock
         }
+        const float* os = osum;  // OUT: this colblock's outlier sums
+        if (OUT && writer) bar_wait(obar0, it & 1);
         if (writer) {
             if (Gm::SUBFREE) {  // D' = D + C sum(x): remove the offset once per output element
                 const float C = static_cast<float>(128 - a.lmin);
@@ -476,10 +663,14 @@ __global__ void __launch_bounds__(kStreamThreads) k_gemv_cb(const GemvArgs a) {
                     for (int q = 0; q < 4; ++q) {
                         const int64_t jc = (cb * TPC + tile0 + u * kCW) * kTileCols + g + (q >= 2 ? 8 : 0);
                         const int n = n8 * 8 + 2 * t + (q & 1);
-                        if (jc < a.cols && n < a.batch)
-                            a.y[static_cast<int64_t>(n) * a.cols + jc] = a.scales[jc] * d[u][n8][q];
+                        if (jc < a.cols && n < a.batch) {
+                            float yv = a.scales[jc] * d[u][n8][q];
+                            if (OUT) yv += os[((tile0 + u * kCW) * kTileCols + g + (q >= 2 ? 8 : 0)) * Gm::NBT + n];
+                            a.y[static_cast<int64_t>(n) * a.cols + jc] = yv;
+                        }
                     }
         }
+        if (OUT) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(rbar0) : "memory");
     }
 }
 
@@ -650,16 +841,34 @@ struct ezq_gemv_plan {
     float* xt;            // batch > 1 with outliers: x transposed [rows][16] f32 (owned)
     void* xpad;           // ragged / unaligned x: padded copy [16][kq * 64] (owned)
     int grid[6];          // persistent CTAs of k_gemv_cb per (x dtype, NB) variant
+    // fused outlier term (k_gemv_cb<..., OUT>): 512-row segments per colblock
+    unsigned char* oseg;  // (owned)
+    int64_t* obnd;        // [ncb * nseg + 1] (owned)
+    int64_t nseg;
+    int oes;              // entry bytes (8: f32 values, 4: f16)
+    int ob[6];            // segment bytes per ring stage, per variant
+    int gridf[6][2];      // persistent CTAs of the fused kernel, per variant and outlier warps (1, 4)
+    size_t fsmem[6];      // its dynamic shared memory; 0: the separate pass
 };
 
 namespace {
+
+int max_optin_smem() {
+    static int v = [] {
+        int dev = 0, m = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&m, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) m = 227 * 1024;
+        return m;
+    }();
+    return v;
+}
 
 template <int TPC, int NB, int XT>
 int cb_ctas_per_sm() {
     const int smem = static_cast<int>(CbGeom<TPC, NB, XT>::smem());
     if (NB == 1 && XT != kF16)  // the HSUB2-free twin (same shared memory)
-        cudaFuncSetAttribute(k_gemv_cb<TPC, NB, XT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    auto k = k_gemv_cb<TPC, NB, XT, false>;
+        cudaFuncSetAttribute(k_gemv_cb<TPC, NB, XT, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    auto k = k_gemv_cb<TPC, NB, XT, false, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kStreamThreads, smem) != cudaSuccess || n < 1) n = 1;
@@ -689,36 +898,95 @@ const int* occupancy(int tpc) {
     return occ[tpc == 1 ? 0 : tpc == 2 ? 1 : tpc == 4 ? 2 : 3];
 }
 
-// HSUB2-free dequant for batch <= 2 (bf16 / f32 x): the producer's per-stage
-// x sums stay cheap; larger batches keep the HSUB2 path.
+// Fused-outlier geometry of variant v: q-blocks per stage, segment ring
+// offset, and CTAs per SM with `ob` segment bytes per stage (0: no fit).
+struct FusedGeom {
+    int S;
+    size_t osm_off;
+};
+
 template <int TPC, int NB, int XT>
-void launch_cb_t(const GemvArgs& a, int grid, cudaStream_t st) {
-    if (NB == 1 && XT != kF16 && a.batch <= 2)
-        k_gemv_cb<TPC, NB, XT, true><<<static_cast<unsigned>(grid), kStreamThreads, CbGeom<TPC, NB, XT, true>::smem(),
-                                       st>>>(a);
-    else
-        k_gemv_cb<TPC, NB, XT, false><<<static_cast<unsigned>(grid), kStreamThreads, CbGeom<TPC, NB, XT>::smem(),
-                                        st>>>(a);
+FusedGeom fused_geom() {
+    using G = CbGeom<TPC, NB, XT>;
+    return {G::S, G::osm_off()};
+}
+
+// outlier warps of a fused launch (see outlier_warp)
+int out_warps(int batch) { return batch <= 2 ? 1 : kOutWarpsMax; }
+
+template <int TPC, int NB, int XT>
+int fused_ctas_per_sm(size_t smem, int threads) {
+    if (smem > static_cast<size_t>(max_optin_smem())) return 0;
+    const int cap = max_optin_smem();
+    if (NB == 1 && XT != kF16)
+        cudaFuncSetAttribute(k_gemv_cb<TPC, NB, XT, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+    auto k = k_gemv_cb<TPC, NB, XT, false, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, threads, smem) != cudaSuccess) n = 0;
+    return n;
 }
 
 template <int TPC>
-void launch_cb_v(int v, const GemvArgs& a, int grid, cudaStream_t st) {
+void fused_info(int v, size_t ob, int threads, FusedGeom* g, int* ctas) {
+    auto pick = [&](FusedGeom fg, auto occ_fn) {
+        *g = fg;
+        if (ctas) *ctas = occ_fn(fg.osm_off + static_cast<size_t>(kRing) * ob, threads);
+    };
     switch (v) {
-        case 0: launch_cb_t<TPC, 1, kF32>(a, grid, st); break;
-        case 1: launch_cb_t<TPC, 2, kF32>(a, grid, st); break;
-        case 2: launch_cb_t<TPC, 1, kBF16>(a, grid, st); break;
-        case 3: launch_cb_t<TPC, 2, kBF16>(a, grid, st); break;
-        case 4: launch_cb_t<TPC, 1, kF16>(a, grid, st); break;
-        default: launch_cb_t<TPC, 2, kF16>(a, grid, st); break;
+        case 0: pick(fused_geom<TPC, 1, kF32>(), fused_ctas_per_sm<TPC, 1, kF32>); break;
+        case 1: pick(fused_geom<TPC, 2, kF32>(), fused_ctas_per_sm<TPC, 2, kF32>); break;
+        case 2: pick(fused_geom<TPC, 1, kBF16>(), fused_ctas_per_sm<TPC, 1, kBF16>); break;
+        case 3: pick(fused_geom<TPC, 2, kBF16>(), fused_ctas_per_sm<TPC, 2, kBF16>); break;
+        case 4: pick(fused_geom<TPC, 1, kF16>(), fused_ctas_per_sm<TPC, 1, kF16>); break;
+        default: pick(fused_geom<TPC, 2, kF16>(), fused_ctas_per_sm<TPC, 2, kF16>); break;
     }
 }
 
-void launch_cb(int tpc, int v, const GemvArgs& a, int grid, cudaStream_t st) {
+void fused_variant(int tpc, int v, size_t ob, int threads, FusedGeom* g, int* ctas) {
     switch (tpc) {
-        case 1: launch_cb_v<1>(v, a, grid, st); break;
-        case 2: launch_cb_v<2>(v, a, grid, st); break;
-        case 4: launch_cb_v<4>(v, a, grid, st); break;
-        default: launch_cb_v<8>(v, a, grid, st); break;
+        case 1: fused_info<1>(v, ob, threads, g, ctas); break;
+        case 2: fused_info<2>(v, ob, threads, g, ctas); break;
+        case 4: fused_info<4>(v, ob, threads, g, ctas); break;
+        default: fused_info<8>(v, ob, threads, g, ctas); break;
+    }
+}
+
+// HSUB2-free dequant for batch <= 2 (bf16 / f32 x): the producer's per-stage
+// x sums stay cheap; larger batches keep the HSUB2 path. `smem` > 0: the
+// fused-outlier kernel with that much dynamic shared memory.
+template <int TPC, int NB, int XT>
+void launch_cb_t(const GemvArgs& a, int grid, size_t smem, cudaStream_t st) {
+    const unsigned gd = static_cast<unsigned>(grid);
+    const bool sf = NB == 1 && XT != kF16 && a.batch <= 2;
+    if (smem) {
+        const unsigned nt = static_cast<unsigned>(kStreamThreads + 32 * out_warps(a.batch));
+        if (sf) k_gemv_cb<TPC, NB, XT, true, true><<<gd, nt, smem, st>>>(a);
+        else k_gemv_cb<TPC, NB, XT, false, true><<<gd, nt, smem, st>>>(a);
+    } else {
+        if (sf) k_gemv_cb<TPC, NB, XT, true, false><<<gd, kStreamThreads, CbGeom<TPC, NB, XT, true>::smem(), st>>>(a);
+        else k_gemv_cb<TPC, NB, XT, false, false><<<gd, kStreamThreads, CbGeom<TPC, NB, XT>::smem(), st>>>(a);
+    }
+}
+
+template <int TPC>
+void launch_cb_v(int v, const GemvArgs& a, int grid, size_t smem, cudaStream_t st) {
+    switch (v) {
+        case 0: launch_cb_t<TPC, 1, kF32>(a, grid, smem, st); break;
+        case 1: launch_cb_t<TPC, 2, kF32>(a, grid, smem, st); break;
+        case 2: launch_cb_t<TPC, 1, kBF16>(a, grid, smem, st); break;
+        case 3: launch_cb_t<TPC, 2, kBF16>(a, grid, smem, st); break;
+        case 4: launch_cb_t<TPC, 1, kF16>(a, grid, smem, st); break;
+        default: launch_cb_t<TPC, 2, kF16>(a, grid, smem, st); break;
+    }
+}
+
+void launch_cb(int tpc, int v, const GemvArgs& a, int grid, size_t smem, cudaStream_t st) {
+    switch (tpc) {
+        case 1: launch_cb_v<1>(v, a, grid, smem, st); break;
+        case 2: launch_cb_v<2>(v, a, grid, smem, st); break;
+        case 4: launch_cb_v<4>(v, a, grid, smem, st); break;
+        default: launch_cb_v<8>(v, a, grid, smem, st); break;
     }
 }
 
@@ -830,6 +1098,98 @@ int ezq_gemv_prepare_ex(const ezq_qweight* q, int outlier_dtype, void* stream, e
             std::fprintf(stderr, "ezq_gemv_prepare: tpc %d ncb %lld variant %d ctas/sm %d grid %d\n", p->tpc,
                          static_cast<long long>(p->ncb), v, occ[v], p->grid[v]);
     }
+    // Fused outliers: for every colblock and 512-row segment, the header
+    // (u32 bytes, u16 column starts) and the entries, rows ascending per
+    // column; each variant whose stage holds whole segments and whose ring
+    // still fits in shared memory (with >= 1 CTA per SM) runs the outlier
+    // term inside the main kernel. EZQ_GEMV_FUSED=0 keeps the separate pass.
+    std::vector<unsigned char> seg;
+    std::vector<int64_t> bnd;
+    const char* fz = std::getenv("EZQ_GEMV_FUSED");
+    bool fuse = q->n_outliers > 0 && !(fz && std::atoi(fz) == 0);
+    if (fuse) {
+        const int C = p->tpc * kTileCols, hdr = seg_hdr_bytes(p->tpc), es = ves == 4 ? 8 : 4;
+        p->nseg = (q->rows + kSegRows - 1) / kSegRows;
+        p->oes = es;
+        bnd.resize(static_cast<size_t>(p->ncb * p->nseg + 1));
+        seg.reserve(static_cast<size_t>(q->n_outliers) * es + static_cast<size_t>(p->ncb * p->nseg) * (hdr + 16));
+        std::vector<int64_t> cur(ptr.begin(), ptr.end() - 1);
+        std::vector<uint16_t> st(C + 1);
+        for (int64_t cb = 0; cb < p->ncb && fuse; ++cb)
+            for (int64_t sg = 0; sg < p->nseg; ++sg) {
+                const size_t base = seg.size();
+                bnd[cb * p->nseg + sg] = static_cast<int64_t>(base);
+                const uint32_t rend = static_cast<uint32_t>(std::min<int64_t>((sg + 1) * kSegRows, q->rows));
+                int64_t n = 0;
+                for (int c = 0; c < C; ++c) {
+                    st[c] = static_cast<uint16_t>(n);
+                    const int64_t j = cb * C + c;
+                    if (j >= q->cols) continue;
+                    int64_t e = cur[j];
+                    while (e < ptr[j + 1] && rr[e] < rend) ++e;
+                    n += e - cur[j];
+                    if (n > 65535) break;
+                }
+                if (n > 65535) {  // denser than the u16 header can index: keep the separate pass
+                    fuse = false;
+                    break;
+                }
+                st[C] = static_cast<uint16_t>(n);
+                const size_t ebytes = (static_cast<size_t>(n) * es + 15) & ~static_cast<size_t>(15);
+                seg.resize(base + hdr + ebytes, 0);
+                const uint32_t tot = static_cast<uint32_t>(hdr + ebytes);
+                std::memcpy(seg.data() + base, &tot, 4);
+                std::memcpy(seg.data() + base + 4, st.data(), 2 * (C + 1));
+                unsigned char* ent = seg.data() + base + hdr;
+                int64_t i = 0;
+                for (int c = 0; c < C; ++c) {
+                    const int64_t j = cb * C + c;
+                    if (j >= q->cols) continue;
+                    for (; cur[j] < ptr[j + 1] && rr[cur[j]] < rend; ++cur[j], ++i) {
+                        const uint32_t rl = rr[cur[j]] - static_cast<uint32_t>(sg * kSegRows);
+                        if (es == 8) {
+                            std::memcpy(ent + 8 * i, &rl, 4);
+                            std::memcpy(ent + 8 * i + 4, &vv[cur[j]], 4);
+                        } else {
+                            const uint32_t w = rl | (static_cast<uint32_t>(vh[cur[j]]) << 16);
+                            std::memcpy(ent + 4 * i, &w, 4);
+                        }
+                    }
+                }
+            }
+        if (fuse) bnd[p->ncb * p->nseg] = static_cast<int64_t>(seg.size());
+    }
+    for (int v = 0; v < 6; ++v) {
+        p->fsmem[v] = 0;
+        p->ob[v] = 0;
+        p->gridf[v][0] = p->gridf[v][1] = 0;
+        if (!fuse) continue;
+        FusedGeom fg{};
+        fused_variant(p->tpc, v, 0, 0, &fg, nullptr);
+        if (fg.S % kSegQ) continue;  // stage smaller than a segment (f32 x, 9..16 rows)
+        const int64_t spg = fg.S / kSegQ;
+        int64_t mx = 0;
+        for (int64_t cb = 0; cb < p->ncb; ++cb)
+            for (int64_t s0 = 0; s0 < p->nseg; s0 += spg)
+                mx = std::max(mx, bnd[cb * p->nseg + std::min(s0 + spg, p->nseg)] - bnd[cb * p->nseg + s0]);
+        int c1 = 0, c4 = 0;
+        fused_variant(p->tpc, v, static_cast<size_t>(mx), kStreamThreads + 32, &fg, &c1);
+        fused_variant(p->tpc, v, static_cast<size_t>(mx), kStreamThreads + 32 * kOutWarpsMax, &fg, &c4);
+        if (c1 < 1 || c4 < 1) continue;
+        p->ob[v] = static_cast<int>(mx);
+        p->fsmem[v] = fg.osm_off + static_cast<size_t>(kRing) * mx;
+        p->gridf[v][0] = static_cast<int>(std::min<int64_t>(p->ncb, static_cast<int64_t>(sms) * c1));
+        p->gridf[v][1] = static_cast<int>(std::min<int64_t>(p->ncb, static_cast<int64_t>(sms) * c4));
+        if (dbg)
+            std::fprintf(stderr, "ezq_gemv_prepare: fused variant %d: %lld B/stage, smem %zu, ctas/sm %d / %d\n", v,
+                         static_cast<long long>(mx), p->fsmem[v], c1, c4);
+    }
+    p->oseg = nullptr;
+    p->obnd = nullptr;
+    if (fuse) {
+        EZQ_CK(cudaMalloc(&p->oseg, std::max<size_t>(seg.size(), 16)));
+        EZQ_CK(cudaMalloc(&p->obnd, sizeof(int64_t) * bnd.size()));
+    }
     const int64_t nw = p->ncb * p->kq * p->tpc * 32;
     EZQ_CK(cudaMalloc(&p->T, sizeof(uint4) * nw));
     EZQ_CK(cudaMalloc(&p->col_ptr, sizeof(int64_t) * (q->cols + 1)));
@@ -848,6 +1208,10 @@ int ezq_gemv_prepare_ex(const ezq_qweight* q, int outlier_dtype, void* stream, e
                                cudaMemcpyHostToDevice, st));
         EZQ_CK(cudaMemcpyAsync(p->out_val, ves == 4 ? static_cast<const void*>(vv.data()) : vh.data(),
                                ves * q->n_outliers, cudaMemcpyHostToDevice, st));
+    }
+    if (p->oseg) {
+        EZQ_CK(cudaMemcpyAsync(p->oseg, seg.data(), seg.size(), cudaMemcpyHostToDevice, st));
+        EZQ_CK(cudaMemcpyAsync(p->obnd, bnd.data(), sizeof(int64_t) * bnd.size(), cudaMemcpyHostToDevice, st));
     }
     EZQ_CK(cudaStreamSynchronize(st));
     *plan = p;
@@ -899,7 +1263,7 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
             a.xstride = prow;
         }
         const bool two = a.batch > 8;
-        if (p->n_out && a.batch > 1) {  // transposed x for the outlier pass (one 16-byte load per 4 batch rows)
+        if (p->n_out && a.batch > 1 && !p->fsmem[x_dtype * 2 + (a.batch > 8 ? 1 : 0)]) {  // transposed x for the outlier pass (one 16-byte load per 4 batch rows)
             k_gemv_xt<<<static_cast<unsigned>((p->rows + 15) / 16), 256, 0, st>>>(xg, x_dtype, p->rows, a.batch,
                                                                                   p->xt);
             count_launch();
@@ -910,13 +1274,21 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
             if (e != cudaSuccess) return cuda_error(e, "gemv: before the main kernel");
         }
         const int v = x_dtype * 2 + (two ? 1 : 0);
-        launch_cb(p->tpc, v, a, p->grid[v], st);
+        const bool fused = p->n_out && p->fsmem[v];
+        if (fused) {
+            a.oseg = p->oseg;
+            a.obnd = p->obnd;
+            a.nseg = p->nseg;
+            a.ob = p->ob[v];
+            a.oes = p->oes;
+        }
+        launch_cb(p->tpc, v, a, fused ? p->gridf[v][out_warps(a.batch) > 1] : p->grid[v], fused ? p->fsmem[v] : 0, st);
         count_launch();
         if (dsync) {
             const cudaError_t e = cudaStreamSynchronize(st);
             if (e != cudaSuccess) return cuda_error(e, "gemv: main kernel");
         }
-        if (p->n_out) {
+        if (p->n_out && !fused) {
             cudaLaunchConfig_t lc{};
             // two 8-warp CTAs per SM: resident beside the main kernel (see k_gemv_outliers)
             int sms = 148;
@@ -975,6 +1347,8 @@ void ezq_gemv_plan_free(ezq_gemv_plan* p) {
     cudaFree(p->xpad);
     cudaFree(p->out_row);
     cudaFree(p->out_val);
+    if (p->oseg) cudaFree(p->oseg);
+    if (p->obnd) cudaFree(p->obnd);
     delete p;
 }
 
