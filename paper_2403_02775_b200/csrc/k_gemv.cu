@@ -189,7 +189,7 @@ constexpr int kCW = 4;             // consumer warps per CTA
 constexpr int kRing = 2;           // ring stages per CTA
 constexpr int kStageCode = 32768;  // code bytes per full stage (sweep on B200: 8-32 KB x 2-6 stages)
 constexpr int kStreamThreads = (kCW + 1) * 32;
-constexpr int kOutWarpsMax = 4;                                  // outlier warps (fused outliers): 1 or 4
+constexpr int kOutWarpsSmall = 2, kOutWarpsMax = 4;              // outlier warps (fused outliers)
 constexpr int kOutThreads = kStreamThreads + 32 * kOutWarpsMax;
 
 struct GemvArgs {
@@ -210,14 +210,15 @@ struct GemvArgs {
     const int64_t* obnd;  // [ncb * nseg + 1] byte offsets of the segments in oseg
     int64_t nseg;         // segments per colblock
     int ob;               // shared-memory bytes per ring stage for the segments
-    int oes;              // entry bytes: 8 = {u32 row, f32 value}, 4 = {u16 row | f16 value << 16}
+    int oes;              // value bytes: 4 = f32, 2 = f16
 };
 
 // Fused outliers: segment = 512 rows (8 q-blocks; every stage of the variants
 // that fuse holds 1 or 2 whole segments) x one colblock. Layout (16-byte
 // aligned, sizes multiples of 16): u32 total bytes; u16 start[TPC * 16 + 1]
 // (entry index of each column's first outlier; rows ascending inside a
-// column); pad; entries.
+// column); pad; the E = start[TPC * 16] values (f32 or f16); their rows
+// inside the segment (u16); pad. 6 (f32) or 4 (f16) bytes per outlier.
 constexpr int kSegRows = 512;
 constexpr int kSegQ = kSegRows / kBlockRows;
 __host__ __device__ constexpr int seg_hdr_bytes(int tpc) { return (4 + 2 * (tpc * kTileCols + 1) + 15) & ~15; }
@@ -270,19 +271,14 @@ __device__ __forceinline__ float xs_val(const unsigned char* xs, int pitch, int 
     return __half2float(__ushort_as_half(u));
 }
 
-__device__ __forceinline__ void seg_entry(const unsigned char* ent, int oes, int e, unsigned& r, float& v) {
-    if (oes == 8) {
-        const uint2 w = *reinterpret_cast<const uint2*>(ent + 8 * e);
-        r = w.x;
-        v = __uint_as_float(w.y);
-    } else {
-        const unsigned w = *reinterpret_cast<const unsigned*>(ent + 4 * e);
-        r = w & 0xffffu;
-        v = __half2float(__ushort_as_half(static_cast<unsigned short>(w >> 16)));
-    }
+__device__ __forceinline__ void seg_entry(const unsigned char* vals, const unsigned short* rows, int oes, int e,
+                                          unsigned& r, float& v) {
+    r = rows[e];
+    v = oes == 4 ? reinterpret_cast<const float*>(vals)[e]
+                 : __half2float(reinterpret_cast<const __half*>(vals)[e]);
 }
 
-// The outlier warps (fused outliers; OW = 1 for batch groups of <= 2 rows,
+// The outlier warps (fused outliers; OW = 2 for batch groups of <= 2 rows,
 // else 4): extra consumers of every ring stage. Warp ow owns C / OW of the
 // colblock's C = 16 TPC columns; its lanes own them (CW / 32 columns per
 // lane, or 32 / CW lanes per column splitting the entries), walk each stage's
@@ -316,13 +312,15 @@ __device__ __forceinline__ void outlier_warp(const GemvArgs& a, int64_t nst_cb, 
             const unsigned char* ob = osm + slot * a.ob;
             const unsigned char* xw = xsm + slot * XB;
             const int64_t sg0 = sq * SPG;
-            const unsigned char* ent[SPG];
+            const unsigned char* ent[SPG];   // values
+            const unsigned short* rws[SPG];  // rows
             int e[L], e1[L];
 #pragma unroll
             for (int sg = 0; sg < SPG; ++sg) {
                 const bool ok = sg0 + sg < a.nseg;
                 const unsigned short* hs = reinterpret_cast<const unsigned short*>(ob + 4);
                 ent[sg] = ob + seg_hdr_bytes(TPC);
+                rws[sg] = reinterpret_cast<const unsigned short*>(ent[sg] + a.oes * (ok ? hs[C] : 0));
 #pragma unroll
                 for (int i = 0; i < CPL; ++i) {
                     const int c = ow * CW + (LPC > 1 ? lane / LPC : lane + 32 * i);
@@ -342,7 +340,7 @@ __device__ __forceinline__ void outlier_warp(const GemvArgs& a, int64_t nst_cb, 
                 for (int i = 0; i < L; ++i) {
                     r[i] = 0;
                     v[i] = 0.f;
-                    if (e[i] < e1[i]) seg_entry(ent[i / CPL], a.oes, e[i], r[i], v[i]);
+                    if (e[i] < e1[i]) seg_entry(ent[i / CPL], rws[i / CPL], a.oes, e[i], r[i], v[i]);
                 }
 #pragma unroll
                 for (int i = 0; i < L; ++i)
@@ -415,12 +413,12 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
     asm volatile("griddepcontrol.launch_dependents;");
     const int64_t nst_cb = (a.kq + S - 1) / S;  // stages per colblock
 
-    if (OUT && warp > kCW) {  // ---- outlier warps (1 or 4: out_warps(batch))
+    if (OUT && warp > kCW) {  // ---- outlier warps (2 or 4: out_warps(batch))
         using G = CbGeom<TPC, NB, XT, SF>;
         const int ow = warp - kCW - 1;
         if (NB == 2) outlier_warp<TPC, S, XT, XP, XB, G::NBT, 16, 4>(a, nst_cb, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
-        else if (a.batch == 1) outlier_warp<TPC, S, XT, XP, XB, G::NBT, 1, 1>(a, nst_cb, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
-        else if (a.batch == 2) outlier_warp<TPC, S, XT, XP, XB, G::NBT, 2, 1>(a, nst_cb, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
+        else if (a.batch == 1) outlier_warp<TPC, S, XT, XP, XB, G::NBT, 1, kOutWarpsSmall>(a, nst_cb, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
+        else if (a.batch == 2) outlier_warp<TPC, S, XT, XP, XB, G::NBT, 2, kOutWarpsSmall>(a, nst_cb, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
         else if (a.batch <= 4) outlier_warp<TPC, S, XT, XP, XB, G::NBT, 4, 4>(a, nst_cb, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
         else outlier_warp<TPC, S, XT, XP, XB, G::NBT, 8, 4>(a, nst_cb, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
         return;
@@ -845,9 +843,9 @@ struct ezq_gemv_plan {
     unsigned char* oseg;  // (owned)
     int64_t* obnd;        // [ncb * nseg + 1] (owned)
     int64_t nseg;
-    int oes;              // entry bytes (8: f32 values, 4: f16)
+    int oes;              // value bytes (4: f32, 2: f16)
     int ob[6];            // segment bytes per ring stage, per variant
-    int gridf[6][2];      // persistent CTAs of the fused kernel, per variant and outlier warps (1, 4)
+    int gridf[6][2];      // persistent CTAs of the fused kernel, per variant and outlier warps (small, max)
     size_t fsmem[6];      // its dynamic shared memory; 0: the separate pass
 };
 
@@ -912,7 +910,7 @@ FusedGeom fused_geom() {
 }
 
 // outlier warps of a fused launch (see outlier_warp)
-int out_warps(int batch) { return batch <= 2 ? 1 : kOutWarpsMax; }
+int out_warps(int batch) { return batch <= 2 ? kOutWarpsSmall : kOutWarpsMax; }
 
 template <int TPC, int NB, int XT>
 int fused_ctas_per_sm(size_t smem, int threads) {
@@ -1108,9 +1106,9 @@ int ezq_gemv_prepare_ex(const ezq_qweight* q, int outlier_dtype, void* stream, e
     const char* fz = std::getenv("EZQ_GEMV_FUSED");
     bool fuse = q->n_outliers > 0 && !(fz && std::atoi(fz) == 0);
     if (fuse) {
-        const int C = p->tpc * kTileCols, hdr = seg_hdr_bytes(p->tpc), es = ves == 4 ? 8 : 4;
+        const int C = p->tpc * kTileCols, hdr = seg_hdr_bytes(p->tpc), es = static_cast<int>(ves) + 2;
         p->nseg = (q->rows + kSegRows - 1) / kSegRows;
-        p->oes = es;
+        p->oes = static_cast<int>(ves);
         bnd.resize(static_cast<size_t>(p->ncb * p->nseg + 1));
         seg.reserve(static_cast<size_t>(q->n_outliers) * es + static_cast<size_t>(p->ncb * p->nseg) * (hdr + 16));
         std::vector<int64_t> cur(ptr.begin(), ptr.end() - 1);
@@ -1141,19 +1139,16 @@ int ezq_gemv_prepare_ex(const ezq_qweight* q, int outlier_dtype, void* stream, e
                 std::memcpy(seg.data() + base, &tot, 4);
                 std::memcpy(seg.data() + base + 4, st.data(), 2 * (C + 1));
                 unsigned char* ent = seg.data() + base + hdr;
+                unsigned char* erow = ent + ves * n;
                 int64_t i = 0;
                 for (int c = 0; c < C; ++c) {
                     const int64_t j = cb * C + c;
                     if (j >= q->cols) continue;
                     for (; cur[j] < ptr[j + 1] && rr[cur[j]] < rend; ++cur[j], ++i) {
-                        const uint32_t rl = rr[cur[j]] - static_cast<uint32_t>(sg * kSegRows);
-                        if (es == 8) {
-                            std::memcpy(ent + 8 * i, &rl, 4);
-                            std::memcpy(ent + 8 * i + 4, &vv[cur[j]], 4);
-                        } else {
-                            const uint32_t w = rl | (static_cast<uint32_t>(vh[cur[j]]) << 16);
-                            std::memcpy(ent + 4 * i, &w, 4);
-                        }
+                        const uint16_t rl = static_cast<uint16_t>(rr[cur[j]] - static_cast<uint32_t>(sg * kSegRows));
+                        std::memcpy(erow + 2 * i, &rl, 2);
+                        if (ves == 4) std::memcpy(ent + 4 * i, &vv[cur[j]], 4);
+                        else std::memcpy(ent + 2 * i, &vh[cur[j]], 2);
                     }
                 }
             }
@@ -1173,7 +1168,7 @@ int ezq_gemv_prepare_ex(const ezq_qweight* q, int outlier_dtype, void* stream, e
             for (int64_t s0 = 0; s0 < p->nseg; s0 += spg)
                 mx = std::max(mx, bnd[cb * p->nseg + std::min(s0 + spg, p->nseg)] - bnd[cb * p->nseg + s0]);
         int c1 = 0, c4 = 0;
-        fused_variant(p->tpc, v, static_cast<size_t>(mx), kStreamThreads + 32, &fg, &c1);
+        fused_variant(p->tpc, v, static_cast<size_t>(mx), kStreamThreads + 32 * kOutWarpsSmall, &fg, &c1);
         fused_variant(p->tpc, v, static_cast<size_t>(mx), kStreamThreads + 32 * kOutWarpsMax, &fg, &c4);
         if (c1 < 1 || c4 < 1) continue;
         p->ob[v] = static_cast<int>(mx);
