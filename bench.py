@@ -287,7 +287,7 @@ def gemv_bench(N, torch, copies=8, batches=(1, 4, 8, 16), reps=20):
                 x = torch.randn(B, r, generator=gen, device="cuda").to(torch.bfloat16)
                 y = torch.empty(B, c, device="cuda", dtype=torch.float32)
                 us = timed(lambda: [p(x, y) for p in plans])
-                nbytes = (r * c) / 2 + 4 * c + 8 * n_out + 8 * (c + 1) + 2 * B * r + 4 * B * c
+                nbytes = (r * c) / 2 + 4 * c + 6 * n_out + 2 * B * r + 4 * B * c  # 6 B: f32 value + u16 row
                 rec = {"shape": f"{r}x{c}", "batch": B, "outlier_pct": 100 * ratio, "us": us,
                        "gbps": nbytes / (us * 1e-6) / 1e9, "frac": nbytes / (us * 1e-6) / 1e9 / hbm}
                 if ratio == 0.0:
@@ -312,8 +312,8 @@ def gemv_bench(N, torch, copies=8, batches=(1, 4, 8, 16), reps=20):
                 x = torch.randn(B, r, generator=gen, device="cuda").to(torch.bfloat16)
                 y = torch.empty(B, c, device="cuda", dtype=torch.float32)
                 us = timed(lambda: plan(x, y)) * copies  # one matrix per replay
-                vb = 8 if odt == "float32" else 6
-                nbytes = (r * c) / 2 + 4 * c + vb * n_out + 8 * (c + 1) + 2 * B * r + 4 * B * c
+                vb = 6 if odt == "float32" else 4  # value + u16 row
+                nbytes = (r * c) / 2 + 4 * c + vb * n_out + 2 * B * r + 4 * B * c
                 rows_out.append({"shape": f"{r}x{c}", "batch": B, "outlier_pct": 100 * ratio, "outlier_dtype": odt,
                                  "us": us, "gbps": nbytes / (us * 1e-6) / 1e9,
                                  "frac": nbytes / (us * 1e-6) / 1e9 / hbm})

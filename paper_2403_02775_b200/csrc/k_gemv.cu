@@ -27,23 +27,19 @@
 // Words are stored T[tile][q][lane] as uint4 (4 k-steps): one fully
 // coalesced 512-byte load per warp per 64 rows.
 //
-// Work split: one CTA per 16-column tile (4, 8 or 16 warps, chosen so that
-// about 16 warps per SM are resident in a single wave); its warps take the
-// tile's 64-row blocks in turn with plain coalesced 16-byte loads,
-// software-pipelined one block ahead. The warps' fragments are reduced
-// through shared memory in fixed order (deterministic). The outlier term is
-// a second, programmatic-dependent launch (k_gemv_outliers) whose gathers
-// overlap the weight stream.
+// Work split (k_gemv_cb below): persistent CTAs stream colblocks of TPC
+// tiles over all of K through a TMA ring (codes, x slices and the outlier
+// segments of each stage on one mbarrier); 4 consumer warps run the MMAs,
+// outlier warps apply the isolated outliers from the staged x slice, and
+// the writers add both (fixed order: deterministic). k_gemv_outliers is the
+// separate CSC pass kept for the variants that do not fuse.
 //
-// Measured on B200 (tools/microbench/dequant_mma.cu): the dequant + MMA loop
-// costs ~25 SM-cycles per 64-row block at 16 warps/SM (ALU-bound: 3 SHF + 4
-// LOP3 + 4 HSUB2 per 8 codes), i.e. ~6 TB/s of int4 codes per GPU -- about
-// the HBM rate, so the kernel sits on both limits at once. A persistent
-// variant streaming the codes through a TMA bulk-copy/mbarrier ring was
-// built and measured (git history) and was not faster at these sizes.
+// Measured on B200: the dequant + MMA loop is ALU-heavy
+// (SHF + LOP3 (+ HSUB2) per A register), ~0.72 of the HBM copy rate at the
+// BLOOM-176B FFN shape at batch 1.
 //
-// HBM-bound: algorithmic bytes = N/2 (codes) + 4 cols (scales) + 8 n_out
-// (outlier row + value) + 8 (cols+1) (CSC pointers) + B rows |x| + 4 B cols.
+// HBM-bound: algorithmic bytes = N/2 (codes) + 4 cols (scales) + 6 (f32) or
+// 4 (f16) n_out (outlier value + row) + B rows |x| + 4 B cols.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -1324,11 +1320,12 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
         }
     }
     // Algorithmic bytes: the 4-bit codes (the repacked copy has the same
-    // size as the artifact's nibbles), scales, CSC, x and y.
+    // size as the artifact's nibbles), scales, outlier values + u16 rows, x
+    // and y.
     const double vbytes = p->vdtype == EZQ_GEMV_OUTLIER_F32 ? 4.0 : 2.0;
     const double bytes = static_cast<double>(p->rows * p->cols + 1) / 2 + 4.0 * p->cols +
-                         (4.0 + vbytes) * p->n_out + 8.0 * (p->cols + 1) +
-                         batch * p->rows * static_cast<double>(xes) + 4.0 * batch * p->cols;
+                         (2.0 + vbytes) * p->n_out + batch * p->rows * static_cast<double>(xes) +
+                         4.0 * batch * p->cols;
     prof_end(pt, st, bytes);
     EZQ_CK(cudaGetLastError());
     return clear_error();

@@ -96,3 +96,57 @@ def test_gemv_split_and_ragged(gpu, O, rows, cols, batch):
         assert np.array_equal(plan(x).cpu().numpy().view(np.uint32), y.view(np.uint32))
     plan.close()
     b.close()
+
+
+@pytest.mark.parametrize("rows,cols", [(1000, 700), (2048, 136), (4096, 2048)])
+@pytest.mark.parametrize("batch", [1, 2, 5, 16])
+@pytest.mark.parametrize("dtype", ["bfloat16", "float16", "float32"])
+@pytest.mark.parametrize("odt", ["float32", "float16"])
+def test_gemv_fused_vs_separate_outliers(gpu, O, monkeypatch, rows, cols, batch, dtype, odt):
+    """The outlier term fused into the main kernel (512-row segments in the
+    TMA ring, outlier warps) and the separate CSC pass (EZQ_GEMV_FUSED=0,
+    also the path of f32 x at 9..16 rows and of segments too dense for the
+    u16 header) both hold the 1e-3 gate, agree with each other to fp32
+    rounding, and repeat bit for bit."""
+    import torch
+    W = O.gaussian(rows, cols, rows + 3 * cols, 0.02)
+    O.plant_outliers(W, max(1, W.size // 50), 0.2, 1.0, 11)
+    b = gpu.quantize_batch([torch.from_numpy(W).cuda()], Config(sigma_n=2.5758, steps=10), out_mem=gpu.MEM_DEVICE)
+    x = torch.randn(batch, rows, generator=torch.Generator(device="cuda").manual_seed(5), device="cuda")
+    x = x.to(getattr(torch, dtype))
+    ys = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("EZQ_GEMV_FUSED", fused)
+        plan = gpu.GemvPlan(b, 0, outlier_dtype=odt)
+        ys[fused] = plan(x).cpu().numpy()
+        for _ in range(2):
+            assert np.array_equal(plan(x).cpu().numpy().view(np.uint32), ys[fused].view(np.uint32))
+        plan.close()
+    q = b.to_host(0)
+    Wq = gpu.dequantize(q)
+    o = q.outliers
+    Wq[o["row"], o["col"]] = torch.from_numpy(o["value"].copy()).to(getattr(torch, odt)).float().numpy()
+    yref = O.gemv_f64(Wq, x.float().cpu().numpy())
+    scale = np.abs(yref).max()
+    for y in ys.values():
+        assert np.abs(y.astype(np.float64) - yref).max() <= 1e-3 * scale
+    assert np.abs(ys["1"].astype(np.float64) - ys["0"]).max() <= 1e-5 * scale
+    b.close()
+
+
+def test_gemv_dense_outliers(gpu, O):
+    """Most entries outliers (sigma_n 0.5): large segments (fused when the ring
+    still fits in shared memory, else the separate pass) stay exact."""
+    import torch
+    W = O.gaussian(1024, 256, 17, 0.02)
+    b = gpu.quantize_batch([torch.from_numpy(W).cuda()], Config(sigma_n=0.5, steps=5), out_mem=gpu.MEM_DEVICE)
+    q = b.to_host(0)
+    assert q.outliers.size > W.size // 2
+    plan = gpu.GemvPlan(b, 0)
+    for batch in (1, 3, 12):
+        x = torch.randn(batch, 1024, generator=torch.Generator(device="cuda").manual_seed(batch), device="cuda")
+        y = plan(x.to(torch.bfloat16)).cpu().numpy().astype(np.float64)
+        yref = O.gemv_f64(gpu.dequantize(q), x.to(torch.bfloat16).float().cpu().numpy())
+        assert np.abs(y - yref).max() <= 1e-3 * np.abs(yref).max()
+    plan.close()
+    b.close()
