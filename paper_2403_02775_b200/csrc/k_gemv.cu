@@ -1273,7 +1273,7 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
             a.ob = p->ob[v];
             a.oes = p->oes;
         }
-        launch_cb(p->tpc, v, a, fused ? p->gridf[v][out_warps(a.batch) > 1] : p->grid[v], fused ? p->fsmem[v] : 0, st);
+        launch_cb(p->tpc, v, a, fused ? p->gridf[v][out_warps(a.batch) == kOutWarpsMax] : p->grid[v], fused ? p->fsmem[v] : 0, st);
         count_launch();
         if (dsync) {
             const cudaError_t e = cudaStreamSynchronize(st);
