@@ -24,6 +24,7 @@
 namespace ezq {
 
 constexpr int kDetectBlock = 16384;  // elements per detect CTA (256 thr x 64)
+constexpr int kDetectSeg = 2048;     // elements per detect warp (contiguous)
 constexpr int kPackPerThread = 16;   // elements per pack/dequant thread
 constexpr int kPackThreads = 256;
 constexpr int64_t kPackBlock = (int64_t)kPackPerThread * kPackThreads;
@@ -82,6 +83,7 @@ struct Scratch {
     // K2
     long long* blk_count;
     long long* blk_offset;
+    int32_t* seg_off;  // [block][kDetectBlock / kDetectSeg]: outliers of the block's earlier segments
     // per-column (global column index)
     double* s_rtn;    // initial scale per column (snapped / float(s0))
     double* s_fin;    // scale chosen by K3 per column

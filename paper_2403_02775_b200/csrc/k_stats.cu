@@ -433,30 +433,52 @@ __device__ __forceinline__ unsigned pred4(const float4& v, int64_t f, int64_t n,
     return m;
 }
 
+// One CTA per 16384-element block, one warp per contiguous 2048-element
+// segment (4 float4 per lane in flight): the block's outlier count, and each
+// segment's offset inside the block for k_detect_write.
 __global__ void __launch_bounds__(kDT) k_detect_count(const TDesc* __restrict__ td,
                                                       const int64_t* __restrict__ dblk_base,
                                                       int ntens, int64_t total, Scratch sc) {
+    constexpr int kV = kDetectSeg / 128;  // float4 per lane
+    constexpr int kB = 4;                 // in flight
+    constexpr int NW = kDT / 32;
+    static_assert(kDetectBlock == NW * kDetectSeg, "one segment per warp");
     const int64_t g = blockIdx.x;
     if (g >= total) return;
     const int t = find_tensor(dblk_base, ntens, g);
     const TDesc& d = td[t];
     const TStats* st = d.st;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int cnt = 0;
     if (st->mask) {
         const float olo = st->olo, ohi = st->ohi;
-        const int64_t b0 = (g - d.dblk_base) * (int64_t)kDetectBlock;
+        const int64_t s0 = (g - d.dblk_base) * (int64_t)kDetectBlock + (int64_t)warp * kDetectSeg;
         const bool al = (reinterpret_cast<uintptr_t>(d.W) & 15) == 0;
-#pragma unroll 4
-        for (int r = 0; r < kDRounds; ++r) {
-            const int64_t f = b0 + 4 * ((int64_t)r * kDT + threadIdx.x);
-            if (f >= d.n) break;
-            cnt += __popc(pred4(load4(d.W, d.n, f, al), f, d.n, olo, ohi));
+        for (int i0 = 0; i0 < kV; i0 += kB) {
+            float4 v[kB];
+#pragma unroll
+            for (int b = 0; b < kB; ++b) {
+                const int64_t f = s0 + 4 * ((i0 + b) * 32 + lane);
+                v[b] = f < d.n ? load4(d.W, d.n, f, al) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int b = 0; b < kB; ++b) {
+                const int64_t f = s0 + 4 * ((i0 + b) * 32 + lane);
+                cnt += f < d.n ? __popc(pred4(v[b], f, d.n, olo, ohi)) : 0;
+            }
         }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     }
-    typedef cub::BlockReduce<int, kDT> BR;
-    __shared__ typename BR::TempStorage tmp;
-    const int tot = BR(tmp).Sum(cnt);
-    if (threadIdx.x == 0) sc.blk_count[g] = tot;
+    __shared__ int wcnt[NW];
+    if (lane == 0) wcnt[warp] = cnt;
+    __syncthreads();
+    if (threadIdx.x < NW) {
+        int off = 0;
+        for (int w = 0; w < static_cast<int>(threadIdx.x); ++w) off += wcnt[w];
+        sc.seg_off[g * NW + threadIdx.x] = off;
+        if (threadIdx.x == NW - 1) sc.blk_count[g] = off + wcnt[NW - 1];
+    }
 }
 
 // One CTA per tensor: exclusive scan of its block counts.
@@ -480,28 +502,31 @@ __global__ void __launch_bounds__(1024) k_detect_scan(const TDesc* __restrict__ 
     if (threadIdx.x == 0) d.st->n_out = carry;
 }
 
-// One CTA per 16384-element block, one warp per 2048-element segment: the
-// warp counts its segment's outliers (4 float4 per lane in flight at a
-// time), one CTA barrier turns the 8 warp counts into offsets, then each warp
-// re-reads its segment (L1/L2 hits) and writes its outliers in flat order
-// with ballot ranks -- no per-round block scans.
+// Same geometry as k_detect_count: each warp writes its segment's outliers
+// in flat order from its offset (block offset + k_detect_count's segment
+// offset) with ballot ranks, reading W once; warps without outliers skip.
 __global__ void __launch_bounds__(kDT) k_detect_write(const TDesc* __restrict__ td,
                                                       const int64_t* __restrict__ dblk_base,
                                                       int ntens, int64_t total, Scratch sc) {
-    constexpr int kSeg = kDetectBlock / (kDT / 32);  // elements per warp
-    constexpr int kV = kSeg / 128;                   // float4 per lane
-    constexpr int kB = 4;                            // float4 per lane in flight
+    constexpr int kV = kDetectSeg / 128;  // float4 per lane
+    constexpr int kB = 4;                 // in flight
+    constexpr int NW = kDT / 32;
     const int64_t g = blockIdx.x;
     if (g >= total) return;
     const int t = find_tensor(dblk_base, ntens, g);
     const TDesc& d = td[t];
     const TStats* st = d.st;
-    if (!st->mask || sc.blk_count[g] == 0) return;
-    const float olo = st->olo, ohi = st->ohi;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t s0 = (g - d.dblk_base) * (int64_t)kDetectBlock + (int64_t)warp * kSeg;
+    if (!st->mask) return;
+    const int off = sc.seg_off[g * NW + warp];
+    const int end = warp + 1 < NW ? sc.seg_off[g * NW + warp + 1] : static_cast<int>(sc.blk_count[g]);
+    if (end == off) return;  // warp-uniform: no outliers in this segment
+    const float olo = st->olo, ohi = st->ohi;
+    const int64_t s0 = (g - d.dblk_base) * (int64_t)kDetectBlock + (int64_t)warp * kDetectSeg;
     const bool al = (reinterpret_cast<uintptr_t>(d.W) & 15) == 0;
-    int cnt = 0;
+    long long pos = sc.blk_offset[g] + off;
+    const unsigned below = (1u << lane) - 1u;
+    const uint64_t C = static_cast<uint64_t>(d.cols);
     for (int i0 = 0; i0 < kV; i0 += kB) {
         float4 v[kB];
 #pragma unroll
@@ -512,45 +537,30 @@ __global__ void __launch_bounds__(kDT) k_detect_write(const TDesc* __restrict__ 
 #pragma unroll
         for (int b = 0; b < kB; ++b) {
             const int64_t f = s0 + 4 * ((i0 + b) * 32 + lane);
-            cnt += f < d.n ? __popc(pred4(v[b], f, d.n, olo, ohi)) : 0;
-        }
-    }
+            const unsigned m = f < d.n ? pred4(v[b], f, d.n, olo, ohi) : 0u;
+            if (!__ballot_sync(0xffffffffu, m != 0u)) continue;  // warp-uniform
+            int before = 0, total_i = 0;  // outliers of lower lanes / of the whole row of 128
 #pragma unroll
-    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    __shared__ int wcnt[kDT / 32];
-    if (lane == 0) wcnt[warp] = cnt;
-    __syncthreads();
-    if (cnt == 0) return;  // warp-uniform
-    long long pos = sc.blk_offset[g];
-    for (int w = 0; w < warp; ++w) pos += wcnt[w];
-    const unsigned below = (1u << lane) - 1u;
-    const uint64_t C = static_cast<uint64_t>(d.cols);
-    for (int i = 0; i < kV; ++i) {
-        const int64_t f = s0 + 4 * (i * 32 + lane);
-        const float4 v = f < d.n ? load4(d.W, d.n, f, al) : make_float4(0.f, 0.f, 0.f, 0.f);
-        const unsigned m = f < d.n ? pred4(v, f, d.n, olo, ohi) : 0u;
-        if (!__ballot_sync(0xffffffffu, m != 0u)) continue;  // warp-uniform
-        int before = 0, total_i = 0;  // outliers of lower lanes / of the whole row of 128
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const unsigned b = __ballot_sync(0xffffffffu, (m >> k) & 1u);
-            before += __popc(b & below);
-            total_i += __popc(b);
-        }
-        long long p = pos + before;
-        const float vals[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if ((m >> k) & 1u) {
-                const uint64_t flat = static_cast<uint64_t>(f + k);
-                ezq_outlier e;
-                e.row = static_cast<uint32_t>(flat / C);
-                e.col = static_cast<uint32_t>(flat % C);
-                e.value = vals[k];
-                d.outliers[p++] = e;
+            for (int k = 0; k < 4; ++k) {
+                const unsigned bb = __ballot_sync(0xffffffffu, (m >> k) & 1u);
+                before += __popc(bb & below);
+                total_i += __popc(bb);
             }
+            long long p = pos + before;
+            const float vals[4] = {v[b].x, v[b].y, v[b].z, v[b].w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if ((m >> k) & 1u) {
+                    const uint64_t flat = static_cast<uint64_t>(f + k);
+                    ezq_outlier e;
+                    e.row = static_cast<uint32_t>(flat / C);
+                    e.col = static_cast<uint32_t>(flat % C);
+                    e.value = vals[k];
+                    d.outliers[p++] = e;
+                }
+            }
+            pos += total_i;
         }
-        pos += total_i;
     }
 }
 

@@ -288,6 +288,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     for (int k = 0; k < 3; ++k) ar.reserve_n<double>(tot_chunks);
     for (int k = 0; k < 2; ++k) ar.reserve_n<float>(tot_chunks);
     for (int k = 0; k < 2; ++k) ar.reserve_n<long long>(tot_dblk);
+    ar.reserve_n<int32_t>(tot_dblk * (kDetectBlock / kDetectSeg));
     for (int k = 0; k < 5; ++k) ar.reserve_n<double>(tot_cols);
     ar.reserve_n<float>(tot_cols);
     ar.reserve_n<uint8_t>(tot_cols);
@@ -313,6 +314,7 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     sc.p_mx = ar.take<float>(tot_chunks);
     sc.blk_count = ar.take<long long>(tot_dblk);
     sc.blk_offset = ar.take<long long>(tot_dblk);
+    sc.seg_off = ar.take<int32_t>(tot_dblk * (kDetectBlock / kDetectSeg));
     sc.s_rtn = ar.take<double>(tot_cols);
     sc.s_fin = ar.take<double>(tot_cols);
     sc.err_rtn = ar.take<double>(tot_cols);
@@ -924,6 +926,7 @@ int ezq_detect_outliers(const float* W, int64_t rows, int64_t cols, const ezq_co
     for (int k = 0; k < 3; ++k) ar.reserve_n<double>(hd.n_chunks);
     for (int k = 0; k < 2; ++k) ar.reserve_n<float>(hd.n_chunks);
     for (int k = 0; k < 2; ++k) ar.reserve_n<long long>(hd.n_dblk);
+    ar.reserve_n<int32_t>(hd.n_dblk * (kDetectBlock / kDetectSeg));
     if (mem == EZQ_MEM_HOST) ar.reserve(sizeof(float) * N);
     if (int s = ar.allocate(st)) return s;
     TStats* d_st = ar.take<TStats>(1);
@@ -938,6 +941,7 @@ int ezq_detect_outliers(const float* W, int64_t rows, int64_t cols, const ezq_co
     sc.p_mx = ar.take<float>(hd.n_chunks);
     sc.blk_count = ar.take<long long>(hd.n_dblk);
     sc.blk_offset = ar.take<long long>(hd.n_dblk);
+    sc.seg_off = ar.take<int32_t>(hd.n_dblk * (kDetectBlock / kDetectSeg));
     if (mem == EZQ_MEM_HOST) {
         float* dW = ar.take<float>(N);
         EZQ_CK(cudaMemcpyAsync(dW, W, sizeof(float) * N, cudaMemcpyHostToDevice, st));
