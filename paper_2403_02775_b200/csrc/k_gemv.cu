@@ -406,7 +406,6 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    asm volatile("griddepcontrol.launch_dependents;");
     const int64_t nst_cb = (a.kq + S - 1) / S;  // stages per colblock
 
     if (OUT && warp > kCW) {  // ---- outlier warps (2 or 4: out_warps(batch))
@@ -516,6 +515,11 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
                     if (sq + 1 < nst_cb) seg_range(cb, sq + 1);
                     else seg_range(cb + gridDim.x, 0);
                 }
+                // Launched as a programmatic dependent of the previous kernel
+                // (a chain of GEMVs): the codes and outlier segments are
+                // weights and stream before the wait; x may be the previous
+                // kernel's output.
+                if (k == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
                 if (lane < a.batch)
                     asm volatile(
                         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -534,6 +538,11 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
             while (done < first_n) sum_stage(done++);
             publish();
         }
+        // every copy of this CTA is issued: the next kernel in the stream (a
+        // programmatic dependent) may launch and start its own weight stream
+        // as the CTAs drain -- late enough that its CTAs are placed as ours
+        // retire rather than beside them
+        asm volatile("griddepcontrol.launch_dependents;");
         return;
     }
 
@@ -642,6 +651,7 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
         const float* os = osum;  // OUT: this colblock's outlier sums
         if (OUT && writer) bar_wait(obar0, it & 1);
         if (writer) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");  // y: after the previous kernel (no-op once passed)
             if (Gm::SUBFREE) {  // D' = D + C sum(x): remove the offset once per output element
                 const float C = static_cast<float>(128 - a.lmin);
 #pragma unroll
@@ -946,6 +956,24 @@ void fused_variant(int tpc, int v, size_t ob, int threads, FusedGeom* g, int* ct
     }
 }
 
+template <typename K>
+void launch_pdl(K kernel, unsigned grid, unsigned threads, size_t smem, cudaStream_t st, const GemvArgs& a) {
+    // programmatic dependent launch: the weight stream of this GEMV starts
+    // while the previous kernel drains (EZQ_GEMV_CHAIN=0: plain stream order)
+    static const bool chain = !(std::getenv("EZQ_GEMV_CHAIN") && std::atoi(std::getenv("EZQ_GEMV_CHAIN")) == 0);
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(threads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = chain ? 1 : 0;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    cudaLaunchKernelEx(&lc, kernel, a);
+}
+
 // HSUB2-free dequant for batch <= 2 (bf16 / f32 x): the producer's per-stage
 // x sums stay cheap; larger batches keep the HSUB2 path. `smem` > 0: the
 // fused-outlier kernel with that much dynamic shared memory.
@@ -955,11 +983,11 @@ void launch_cb_t(const GemvArgs& a, int grid, size_t smem, cudaStream_t st) {
     const bool sf = NB == 1 && XT != kF16 && a.batch <= 2;
     if (smem) {
         const unsigned nt = static_cast<unsigned>(kStreamThreads + 32 * out_warps(a.batch));
-        if (sf) k_gemv_cb<TPC, NB, XT, true, true><<<gd, nt, smem, st>>>(a);
-        else k_gemv_cb<TPC, NB, XT, false, true><<<gd, nt, smem, st>>>(a);
+        if (sf) launch_pdl(k_gemv_cb<TPC, NB, XT, true, true>, gd, nt, smem, st, a);
+        else launch_pdl(k_gemv_cb<TPC, NB, XT, false, true>, gd, nt, smem, st, a);
     } else {
-        if (sf) k_gemv_cb<TPC, NB, XT, true, false><<<gd, kStreamThreads, CbGeom<TPC, NB, XT, true>::smem(), st>>>(a);
-        else k_gemv_cb<TPC, NB, XT, false, false><<<gd, kStreamThreads, CbGeom<TPC, NB, XT>::smem(), st>>>(a);
+        if (sf) launch_pdl(k_gemv_cb<TPC, NB, XT, true, false>, gd, kStreamThreads, CbGeom<TPC, NB, XT, true>::smem(), st, a);
+        else launch_pdl(k_gemv_cb<TPC, NB, XT, false, false>, gd, kStreamThreads, CbGeom<TPC, NB, XT>::smem(), st, a);
     }
 }
 
