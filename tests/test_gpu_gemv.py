@@ -150,3 +150,69 @@ def test_gemv_dense_outliers(gpu, O):
         assert np.abs(y - yref).max() <= 1e-3 * np.abs(yref).max()
     plan.close()
     b.close()
+
+
+@pytest.mark.parametrize("graph", [False, True])
+@pytest.mark.parametrize("dims,batch", [((1024, 2048, 512, 768), 1), ((512, 4096, 1000, 300), 16),
+                                        ((2048, 2048, 2048, 2048), 5)])
+def test_gemv_chained_layers(gpu, O, graph, dims, batch):
+    """A chain of GEMVs on one stream (each a programmatic dependent launch
+    of the previous kernel): every layer's x is the previous layer's y, and
+    every layer of a second pass writes one shared y -- the weight stream may
+    start early, but x is read and y written only after the previous kernel
+    (griddepcontrol.wait). Also inside a CUDA graph."""
+    import torch
+    Ws, plans, bs = [], [], []
+    for i in range(len(dims) - 1):
+        W = O.gaussian(dims[i], dims[i + 1], 31 + i, 0.02)
+        O.plant_outliers(W, max(1, W.size // 100), 0.2, 1.0, 40 + i)
+        b = gpu.quantize_batch([torch.from_numpy(W).cuda()], Config(steps=5), out_mem=gpu.MEM_DEVICE)
+        Ws.append(gpu.dequantize(b.to_host(0)).astype(np.float64))
+        plans.append(gpu.GemvPlan(b, 0))
+        bs.append(b)
+    x0 = torch.randn(batch, dims[0], generator=torch.Generator(device="cuda").manual_seed(8), device="cuda")
+    ys = [torch.empty(batch, d, device="cuda") for d in dims[1:]]
+    shared = torch.empty(batch * max(dims[1:]), device="cuda")
+
+    def out(d):  # contiguous [batch, d] view of the shared output buffer
+        return shared[: batch * d].view(batch, d)
+
+    zin = {d: torch.zeros(batch, d, device="cuda") for d in dims}
+
+    def run():
+        x = x0
+        for p, y in zip(plans, ys):
+            p(x, y)
+            x = y
+        for p, d in zip(plans, dims[1:]):  # WAW: the shared output keeps the last layer's result
+            p(x0 if p is plans[0] else zin[p.rows], out(d))
+        plans[0](x0, out(dims[1]))
+
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            run()
+        torch.cuda.current_stream().wait_stream(s)
+        with torch.cuda.graph(g):
+            run()
+        for y in ys:
+            y.zero_()
+        g.replay()
+    else:
+        run()
+    torch.cuda.synchronize()
+    ref = x0.cpu().numpy().astype(np.float64)
+    for W, y in zip(Ws, ys):
+        ref = ref @ W
+        got = y.cpu().numpy().astype(np.float64)
+        assert np.abs(got - ref).max() <= 2e-3 * np.abs(ref).max()
+        ref = got  # each layer against its own input (the chain's errors do not compound in the check)
+    first = x0.cpu().numpy().astype(np.float64) @ Ws[0]
+    got = out(dims[1]).cpu().numpy().astype(np.float64)
+    assert np.abs(got - first).max() <= 1e-3 * np.abs(first).max()
+    for p in plans:
+        p.close()
+    for b in bs:
+        b.close()
