@@ -1102,7 +1102,7 @@ int ezq_gemv_prepare_ex(const ezq_qweight* q, int outlier_dtype, void* stream, e
     // wider colblock (x slices read once per more columns).
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    static const int force_tpc = std::getenv("EZQ_GEMV_TPC") ? std::atoi(std::getenv("EZQ_GEMV_TPC")) : 0;  // tuning aid
+    const int force_tpc = std::getenv("EZQ_GEMV_TPC") ? std::atoi(std::getenv("EZQ_GEMV_TPC")) : 0;  // tuning / test aid
     double best = -1.0;
     for (int tpc : {8, 4, 2, 1}) {
         const int64_t ncb = (p->tiles + tpc - 1) / tpc;

@@ -216,3 +216,28 @@ def test_gemv_chained_layers(gpu, O, graph, dims, batch):
         p.close()
     for b in bs:
         b.close()
+
+
+@pytest.mark.parametrize("tpc", [1, 2, 4, 8])
+@pytest.mark.parametrize("batch,dtype", [(1, "bfloat16"), (2, "float32"), (5, "float16"), (16, "bfloat16"),
+                                         (12, "float32")])
+def test_gemv_every_colblock_width(gpu, O, monkeypatch, tpc, batch, dtype):
+    """Every colblock width (EZQ_GEMV_TPC) with fused and separate outlier
+    passes: QW > 1 reductions (TPC < 4), two tiles per warp (TPC = 8), the
+    2-segment stages of batch groups <= 8 and the 1-segment ones of 9..16."""
+    import torch
+    W = O.gaussian(1536, 1000, 5 * tpc + batch, 0.02)
+    O.plant_outliers(W, W.size // 80, 0.2, 1.0, 3)
+    b = gpu.quantize_batch([torch.from_numpy(W).cuda()], Config(sigma_n=2.5758, steps=5), out_mem=gpu.MEM_DEVICE)
+    Wd = gpu.dequantize(b.to_host(0)).astype(np.float64)
+    x = torch.randn(batch, 1536, generator=torch.Generator(device="cuda").manual_seed(tpc), device="cuda")
+    x = x.to(getattr(torch, dtype))
+    yref = x.float().cpu().numpy().astype(np.float64) @ Wd
+    monkeypatch.setenv("EZQ_GEMV_TPC", str(tpc))
+    for fused in ("1", "0"):
+        monkeypatch.setenv("EZQ_GEMV_FUSED", fused)
+        plan = gpu.GemvPlan(b, 0)
+        y = plan(x).cpu().numpy().astype(np.float64)
+        assert np.abs(y - yref).max() <= 1e-3 * np.abs(yref).max(), (tpc, fused)
+        plan.close()
+    b.close()
