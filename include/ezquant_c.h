@@ -174,6 +174,15 @@ int ezq_quantize_tensor(const float* W, int64_t rows, int64_t cols, const ezq_co
 int ezq_quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* cols, int n,
                        const ezq_config* cfg, int mode, int in_mem, int out_mem, void* stream,
                        ezq_qweight** outs, int* failed_index);
+/* sigma_sweep's device loop (report.cpp:241-284): one EASYQUANT batch per
+ * sigma_n over the same tensors; per point and tensor (point-major,
+ * [nsig][n]) the outlier count, rtn_error and final_error (0 for tensors
+ * without errors, as the reference's rows). With device-resident inputs the
+ * tensor stats (K1) are computed by the first point only -- they do not
+ * depend on sigma_n -- and reused, bit-identically, by the others. */
+int ezq_sigma_sweep_batch(const float* const* Ws, const int64_t* rows, const int64_t* cols, int n,
+                          const ezq_config* cfg, int in_mem, void* stream, const float* sigmas, int nsig,
+                          int64_t* n_outliers, double* rtn_error, double* final_error, int* failed_index);
 /* brute_force_optimal_scale (optimize.cpp:186-229) for every column of a
  * batch, on the device: the reference's grid (grid_points scales in
  * [s0/8, 1.25 s0] plus s0) over each column's normals (outliers isolated

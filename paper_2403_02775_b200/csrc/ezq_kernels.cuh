@@ -144,6 +144,7 @@ void launch_stats_pass1(const TDesc* td, const int64_t* chunk_base, int ntens,
 void launch_stats_fin1(const TDesc* td, int ntens, Scratch sc, cudaStream_t st);
 void launch_stats_pass2(const TDesc* td, const int64_t* chunk_base, int ntens,
                         int64_t total_chunks, Scratch sc, cudaStream_t st, bool aligned);
+void launch_stats_rethreshold(const TDesc* td, int ntens, float sigma_n, int mask_mode, cudaStream_t st);
 void launch_stats_fin2(const TDesc* td, int ntens, Scratch sc, float sigma_n, int mask_mode,
                        cudaStream_t st);
 void launch_detect_count(const TDesc* td, const int64_t* dblk_base, int ntens,

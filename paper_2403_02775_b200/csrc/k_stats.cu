@@ -244,6 +244,25 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) k_stats_pipe(const TDesc* _
     }
 }
 
+// The sigma_n-dependent part of the stats (outliers.cpp:18-27): the mask and
+// the exact float bounds of the outlier predicate from mean and stddev.
+__device__ __forceinline__ void set_outlier_threshold(TStats* st, float sigma_n, int mask_mode) {
+    st->mask = (mask_mode && st->stddev != 0.0) ? 1 : 0;
+    st->thr = st->mask ? __dmul_rn(static_cast<double>(sigma_n), st->stddev)
+                       : __longlong_as_double(0x7ff0000000000000ll);
+    st->olo = st->mask ? outlier_lo_bound(st->mean, st->thr) : -__int_as_float(0x7f800000);
+    st->ohi = st->mask ? outlier_hi_bound(st->mean, st->thr) : __int_as_float(0x7f800000);
+    st->n_out = 0;
+}
+
+__device__ __forceinline__ void set_constant_threshold(TStats* st) {
+    st->mask = 0;
+    st->thr = __longlong_as_double(0x7ff0000000000000ll);
+    st->olo = -__int_as_float(0x7f800000);
+    st->ohi = __int_as_float(0x7f800000);
+    st->n_out = 0;
+}
+
 // One CTA per tensor. Order-free merges (max|x|, min, max) run as block
 // reductions; the two sums are merged in chunk order by thread 0 from
 // registers-prefetched SMEM (stats.cpp:66-76 / 96-98). Constant-tensor rule
@@ -257,13 +276,7 @@ __global__ void __launch_bounds__(256) k_stats_merge(const TDesc* __restrict__ t
     TStats* st = d.st;
     __shared__ double bs[2048];
     if (PASS2 && st->constant) {
-        if (threadIdx.x == 0) {
-            st->mask = 0;
-            st->thr = __longlong_as_double(0x7ff0000000000000ll);
-            st->olo = -__int_as_float(0x7f800000);
-            st->ohi = __int_as_float(0x7f800000);
-            st->n_out = 0;
-        }
+        if (threadIdx.x == 0) set_constant_threshold(st);
         return;
     }
     double sum = 0.0;
@@ -306,12 +319,7 @@ __global__ void __launch_bounds__(256) k_stats_merge(const TDesc* __restrict__ t
     if (PASS2) {
         st->ss = sum;
         st->stddev = __dsqrt_rn(__ddiv_rn(sum, static_cast<double>(d.n)));
-        st->mask = (mask_mode && st->stddev != 0.0) ? 1 : 0;
-        st->thr = st->mask ? __dmul_rn(static_cast<double>(sigma_n), st->stddev)
-                           : __longlong_as_double(0x7ff0000000000000ll);
-        st->olo = st->mask ? outlier_lo_bound(st->mean, st->thr) : -__int_as_float(0x7f800000);
-        st->ohi = st->mask ? outlier_hi_bound(st->mean, st->thr) : __int_as_float(0x7f800000);
-        st->n_out = 0;
+        set_outlier_threshold(st, sigma_n, mask_mode);
     } else {
         st->sum = sum;
         st->max_abs = static_cast<double>(amax);
@@ -612,6 +620,21 @@ void launch_stats_pass2(const TDesc* td, const int64_t* chunk_base, int ntens,
 void launch_stats_fin2(const TDesc* td, int ntens, Scratch sc, float sigma_n, int mask_mode,
                        cudaStream_t st) {
     k_stats_merge<true><<<ntens, 256, 0, st>>>(td, sc, sigma_n, mask_mode);
+    count_launch();
+}
+
+// Batched sigma sweep: the stats of an earlier call are reused and only the
+// sigma_n-dependent threshold is recomputed (same device code as k_stats_merge).
+__global__ void k_stats_rethreshold(const TDesc* __restrict__ td, int ntens, float sigma_n, int mask_mode) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ntens) return;
+    TStats* st = td[i].st;
+    if (st->constant) set_constant_threshold(st);
+    else set_outlier_threshold(st, sigma_n, mask_mode);
+}
+
+void launch_stats_rethreshold(const TDesc* td, int ntens, float sigma_n, int mask_mode, cudaStream_t st) {
+    k_stats_rethreshold<<<(ntens + 127) / 128, 128, 0, st>>>(td, ntens, sigma_n, mask_mode);
     count_launch();
 }
 

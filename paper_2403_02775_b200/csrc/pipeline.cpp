@@ -144,9 +144,13 @@ struct GridReq {
     double* error;
 };
 
+// reuse / stats_out (batched sigma sweep): the per-tensor stats of an
+// earlier call over the same tensors are taken as given and only the
+// sigma_n-dependent threshold is recomputed; stats_out receives this call's.
 int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* cols, int n,
                    const ezq_config* cfg, int mode, int in_mem, int out_mem, void* user_stream,
-                   ezq_qweight** outs, int* failed, cudaStream_t d2h = nullptr, const GridReq* grid = nullptr) {
+                   ezq_qweight** outs, int* failed, cudaStream_t d2h = nullptr, const GridReq* grid = nullptr,
+                   const TStats* reuse = nullptr, TStats* stats_out = nullptr) {
     if (failed) *failed = -1;
     if (n <= 0) return clear_error();
     for (int i = 0; i < n; ++i) outs[i] = nullptr;
@@ -356,6 +360,17 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
         t_stage.reset(need);
     }
     std::vector<TStats> hs(n, fresh_stats());
+    if (reuse)
+        for (int i = 0; i < n; ++i) {  // the sigma-independent stats; per-call fields fresh
+            hs[i].sum = reuse[i].sum;
+            hs[i].max_abs = reuse[i].max_abs;
+            hs[i].mean = reuse[i].mean;
+            hs[i].stddev = reuse[i].stddev;
+            hs[i].ss = reuse[i].ss;
+            hs[i].mn = reuse[i].mn;
+            hs[i].mx = reuse[i].mx;
+            hs[i].constant = reuse[i].constant;
+        }
     if (int s = upload(d_stats, hs, st)) return s;
     if (int s = upload(d_desc, hd, st)) return s;
     if (int s = upload(d_chunk_base, chunk_base, st)) return s;
@@ -373,12 +388,18 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
     int64_t tot_elems = 0;
     for (int i = 0; i < n; ++i) tot_elems += hd[i].n;
     int pt = prof_begin("stats", st);
-    launch_stats_pass1(d_desc, d_chunk_base, n, tot_chunks, sc, st, all_aligned);
-    launch_stats_fin1(d_desc, n, sc, st);
+    if (reuse && cfg_status == EZQ_OK) {
+        launch_stats_rethreshold(d_desc, n, cfg->sigma_n, mode != EZQ_MODE_RTN, st);
+    } else {
+        launch_stats_pass1(d_desc, d_chunk_base, n, tot_chunks, sc, st, all_aligned);
+        launch_stats_fin1(d_desc, n, sc, st);
+    }
     if (cfg_status == EZQ_OK) {
-        launch_stats_pass2(d_desc, d_chunk_base, n, tot_chunks, sc, st, all_aligned);
-        launch_stats_fin2(d_desc, n, sc, cfg->sigma_n, mode != EZQ_MODE_RTN, st);
-        prof_end(pt, st, 8.0 * tot_elems);  // two reads of W
+        if (!reuse) {
+            launch_stats_pass2(d_desc, d_chunk_base, n, tot_chunks, sc, st, all_aligned);
+            launch_stats_fin2(d_desc, n, sc, cfg->sigma_n, mode != EZQ_MODE_RTN, st);
+        }
+        prof_end(pt, st, reuse ? 0.0 : 8.0 * tot_elems);  // two reads of W
         if (mode != EZQ_MODE_RTN) {
             pt = prof_begin("detect", st);
             launch_detect_count(d_desc, d_dblk_base, n, tot_dblk, sc, st);
@@ -402,6 +423,8 @@ int quantize_batch(const float* const* Ws, const int64_t* rows, const int64_t* c
         }
     }
     if (cfg_status != EZQ_OK) return set_error(cfg_status, cfg_msg);
+    if (stats_out)
+        for (int i = 0; i < n; ++i) stats_out[i] = hs[i];
     if (mode != EZQ_MODE_RTN) {
         for (int i = 0; i < n; ++i)
             if (rows[i] > UINT32_MAX || cols[i] > UINT32_MAX) {  // outliers.cpp:30-31
@@ -763,6 +786,39 @@ int ezq_quantize_batch(const float* const* Ws, const int64_t* rows, const int64_
     }
     return quantize_batch(Ws, rows, cols, n, cfg, mode, in_mem, out_mem, stream, outs,
                           failed_index);
+}
+
+int ezq_sigma_sweep_batch(const float* const* Ws, const int64_t* rows, const int64_t* cols, int n,
+                          const ezq_config* cfg, int in_mem, void* stream, const float* sigmas, int nsig,
+                          int64_t* n_outliers, double* rtn_error, double* final_error, int* failed_index) {
+    if (failed_index) *failed_index = -1;
+    if (nsig < 0 || (nsig > 0 && (!sigmas || !n_outliers || !rtn_error || !final_error)))
+        return set_error(EZQ_ERR_INVALID_ARGUMENT, "sigma sweep: bad sigma list or null output");
+    if (n <= 0 || nsig == 0) return clear_error();
+    std::vector<ezq_qweight*> q(static_cast<size_t>(n), nullptr);
+    std::vector<TStats> saved(static_cast<size_t>(n));
+    for (int k = 0; k < nsig; ++k) {
+        ezq_config c = *cfg;
+        c.sigma_n = sigmas[k];
+        // device-resident inputs: the first point computes the stats, the
+        // others reuse them (K1 once per sweep); host inputs stream per point
+        const bool dev = in_mem == EZQ_MEM_DEVICE;
+        const int s = dev ? quantize_batch(Ws, rows, cols, n, &c, EZQ_MODE_EASYQUANT, in_mem, EZQ_MEM_DEVICE, stream,
+                                           q.data(), failed_index, nullptr, nullptr, k ? saved.data() : nullptr,
+                                           k ? nullptr : saved.data())
+                          : ezq_quantize_batch(Ws, rows, cols, n, &c, EZQ_MODE_EASYQUANT, in_mem, EZQ_MEM_DEVICE,
+                                               stream, q.data(), failed_index);
+        if (s != EZQ_OK) return s;
+        for (int i = 0; i < n; ++i) {
+            const int64_t o = static_cast<int64_t>(k) * n + i;
+            n_outliers[o] = q[i]->n_outliers;
+            rtn_error[o] = q[i]->has_errors ? q[i]->rtn_error : 0.0;
+            final_error[o] = q[i]->has_errors ? q[i]->final_error : 0.0;
+            ezq_qweight_free(q[i]);
+            q[i] = nullptr;
+        }
+    }
+    return clear_error();
 }
 
 int ezq_grid_oracle_batch(const float* const* Ws, const int64_t* rows, const int64_t* cols, int n,

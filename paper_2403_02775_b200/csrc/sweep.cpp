@@ -4,8 +4,9 @@
 // worker threads), uploaded to HBM once when they fit, and each sigma_n is
 // one ezq_quantize_batch over all of them with device-resident outputs:
 // only the per-tensor scalars (outlier count, rtn_error, final_error) are
-// read back. Sums run in manifest order exactly like the reference, so the
-// rows are bit-identical to it.
+// read back, and the tensor stats (sigma-independent) are computed by the
+// first point only (ezq_sigma_sweep_batch). Sums run in manifest order
+// exactly like the reference, so the rows are bit-identical to it.
 #include <atomic>
 #include <cstdio>
 #include <ostream>
@@ -117,34 +118,38 @@ std::vector<SweepRow> sigma_sweep(const ModelManifest& manifest, const QuantConf
         src[k] = in_mem == EZQ_MEM_DEVICE ? dev.ptr[k] : W[k].data.data();
     }
 
-    std::vector<SweepRow> out;
-    std::vector<ezq_qweight*> q(static_cast<size_t>(m), nullptr);
+    // one device loop over the sigma list (ezq_sigma_sweep_batch: the stats
+    // are computed once for device-resident inputs), then the rows in
+    // manifest order exactly like the reference
+    const int64_t ns = static_cast<int64_t>(sigmas.size());
     for (float sn : sigmas) {
         QuantConfig cfg = base;
         cfg.sigma_n = sn;
         cfg.validate();
-        const ezq_config c = to_c(cfg);
-        std::vector<int64_t> outl(static_cast<size_t>(n), 0);
+    }
+    std::vector<int64_t> s_out(static_cast<size_t>(ns * m));
+    std::vector<double> s_rtn(static_cast<size_t>(ns * m)), s_fin(static_cast<size_t>(ns * m));
+    if (m > 0 && ns > 0) {
+        const ezq_config c = to_c(base);
+        int failed = -1;
+        const int s = ezq_sigma_sweep_batch(src.data(), rows.data(), cols.data(), static_cast<int>(m), &c, in_mem,
+                                            nullptr, sigmas.data(), static_cast<int>(ns), s_out.data(), s_rtn.data(),
+                                            s_fin.data(), &failed);
+        if (s != EZQ_OK) raise_status(s);
+    }
+    std::vector<SweepRow> out;
+    for (int64_t k = 0; k < ns; ++k) {
+        std::vector<int64_t> outl(static_cast<size_t>(n), 0), params(static_cast<size_t>(n), 0);
         std::vector<double> rtn(static_cast<size_t>(n), 0.0), fin(static_cast<size_t>(n), 0.0);
-        std::vector<int64_t> params(static_cast<size_t>(n), 0);
-        if (m > 0) {
-            int failed = -1;
-            const int s = ezq_quantize_batch(src.data(), rows.data(), cols.data(), static_cast<int>(m), &c,
-                                             EZQ_MODE_EASYQUANT, in_mem, EZQ_MEM_DEVICE, nullptr, q.data(),
-                                             &failed);
-            if (s != EZQ_OK) raise_status(s);
-            for (int64_t k = 0; k < m; ++k) {
-                const int64_t i = mat[k];
-                outl[i] = q[k]->n_outliers;
-                rtn[i] = q[k]->has_errors ? q[k]->rtn_error : 0.0;
-                fin[i] = q[k]->has_errors ? q[k]->final_error : 0.0;
-                params[i] = rows[k] * cols[k];
-                ezq_qweight_free(q[k]);
-                q[k] = nullptr;
-            }
+        for (int64_t j = 0; j < m; ++j) {
+            const int64_t i = mat[j];
+            outl[i] = s_out[k * m + j];
+            rtn[i] = s_rtn[k * m + j];
+            fin[i] = s_fin[k * m + j];
+            params[i] = rows[j] * cols[j];
         }
         SweepRow row;
-        row.sigma_n = sn;
+        row.sigma_n = sigmas[k];
         int64_t total_params = 0;
         for (int64_t i = 0; i < n; ++i) {  // manifest order, like the reference
             row.outliers += outl[i];

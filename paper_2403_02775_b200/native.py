@@ -189,6 +189,8 @@ def lib() -> C.CDLL:
                                          C.POINTER(C.POINTER(CQWeight)), C.POINTER(C.c_int)]
         L.ezq_grid_oracle_batch.argtypes = [C.POINTER(P), C.POINTER(I64), C.POINTER(I64), I32,
                                             C.POINTER(CConfig), I32, I32, P, P, P, C.POINTER(C.c_int)]
+        L.ezq_sigma_sweep_batch.argtypes = [C.POINTER(P), C.POINTER(I64), C.POINTER(I64), I32,
+                                            C.POINTER(CConfig), I32, P, P, I32, P, P, P, C.POINTER(C.c_int)]
         L.ezq_dequantize_tensor.argtypes = [C.POINTER(CQWeight), P, I32, P]
         L.ezq_qweight_wrap.argtypes = [I64, I64, I32, P, I64, P, I64, P, I64, D, D, C.c_float,
                                        I32, C.POINTER(C.POINTER(CQWeight))]
@@ -610,6 +612,25 @@ def grid_oracle_batch(Ws: Sequence, cfg: Config, grid_points: int = 2000, stream
         out.append((sc[o:o + k], er[o:o + k]))
         o += k
     return out
+
+
+def sigma_sweep_batch(Ws: Sequence, cfg: Config, sigmas: Sequence[float], stream=None):
+    """ezq_sigma_sweep_batch: one EASYQUANT batch per sigma_n (the tensor
+    stats computed once for device-resident inputs). Returns (n_outliers,
+    rtn_error, final_error), each [len(sigmas), len(Ws)]."""
+    Ws = [_as_f32(w) for w in Ws]
+    n, k = len(Ws), len(sigmas)
+    ptrs = (C.c_void_p * n)(*[_ptr(w) for w in Ws])
+    rows = (C.c_int64 * n)(*[w.shape[0] for w in Ws])
+    cols = (C.c_int64 * n)(*[w.shape[1] for w in Ws])
+    sg = np.asarray(sigmas, np.float32)
+    no = np.zeros((k, n), np.int64)
+    rt, fi = np.zeros((k, n), np.float64), np.zeros((k, n), np.float64)
+    failed = C.c_int(-1)
+    c = cfg.to_c()
+    check(lib().ezq_sigma_sweep_batch(ptrs, rows, cols, n, C.byref(c), _mem(Ws[0]), _stream(stream, Ws[0]),
+                                      _ptr(sg), k, _ptr(no), _ptr(rt), _ptr(fi), C.byref(failed)))
+    return no, rt, fi
 
 
 def quantize_channel(x, scale: float, cfg: Config) -> np.ndarray:

@@ -554,3 +554,28 @@ def test_near_tie_column_channel_api(gpu):
     g = load_golden("near_tie_col.npz")
     r = gpu.optimize_channel(g["x"], None, Config())
     assert np.float32(r["scale"]) == np.float32(g["scales"][1]) and r["best_step"] == 133
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bits", [4, 3])
+def test_sigma_sweep_batch_reuses_stats(gpu, O, bits):
+    """ezq_sigma_sweep_batch (the sweep's device loop: K1 stats computed by
+    the first point, reused by the others) gives exactly the per-point
+    results of independent quantize_batch calls -- outlier counts and both
+    error totals, bit for bit -- including a constant tensor and a tensor
+    with planted outliers."""
+    import torch
+    Ws = [O.gaussian(512, 300, 1, 0.02), O.gaussian(1024, 128, 2, 0.5), np.full((64, 96), 0.25, np.float32)]
+    O.plant_outliers(Ws[1], 500, 2.0, 5.0, 9)
+    Wd = [torch.from_numpy(w).cuda() for w in Ws]
+    sigmas = [1.5, 2.5758, 3.0, 6.0]
+    cfg = Config(bits=bits, steps=20)
+    no, rt, fi = gpu.sigma_sweep_batch(Wd, cfg, sigmas)
+    for k, sg in enumerate(sigmas):
+        b = gpu.quantize_batch(Wd, Config(bits=bits, steps=20, sigma_n=sg), out_mem=gpu.MEM_DEVICE)
+        for i in range(len(Ws)):
+            q = b[i]
+            assert no[k, i] == q.n_outliers, (sg, i)
+            if q.has_errors:
+                assert rt[k, i] == q.rtn_error and fi[k, i] == q.final_error, (sg, i)
+        b.close()
