@@ -16,7 +16,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(_HERE, "_lib")
-LIB_PATH = os.path.join(LIB_DIR, "libezq_b200.so")
+LIB_PATH = os.environ.get("EZQ_LIB") or os.path.join(LIB_DIR, "libezq_b200.so")  # EZQ_LIB: A/B builds (dev aid)
 
 OK, INVALID_ARGUMENT, INVARIANT, IO_FAILURE, IO_FORMAT, IO_VERSION = 0, 1, 2, 3, 4, 5
 CUDA_ERROR, NO_DEVICE, OOM = 10, 11, 12
