@@ -503,6 +503,9 @@ def main():
     torch.cuda.set_device(local)
     N.set_device(local)
     if world > 1:
+        # NCCL's init log (stderr) names every rank and device of the job
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     cfg = Config()
