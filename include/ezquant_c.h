@@ -275,6 +275,28 @@ int ezq_gemv(const ezq_gemv_plan* plan, const void* x, int x_dtype, int batch, f
              void* stream);
 void ezq_gemv_plan_free(ezq_gemv_plan* plan);
 
+/* ---- dense 3-bit codes (new -- the reference stores k = 3
+ * one offset byte per level, rtn.cpp:119-147) ------------------------------ */
+/* Layout: the level offsets (level - lmin, 0..7) in flat row-major order as
+ * one little-endian bit stream, element e at bits 3e..3e+2: 8 levels per 3
+ * bytes, 3 * ceil(count / 8) bytes, zero tail bits. Buffers are all host or
+ * all device memory (`mem`). */
+int64_t ezq_dense3_size(int64_t count);
+/* The reference's k = 3 payload (one offset byte per level, as pack_levels
+ * writes it) -> dense stream. A byte > 7 fails like unpack_levels
+ * (EZQ_ERR_INVALID_ARGUMENT, the element index in ezq_last_error). */
+int ezq_pack_dense3(const uint8_t* levels, int64_t count, uint8_t* out, int mem, void* stream);
+/* Dense stream -> one offset byte per level (the reference's k = 3 payload). */
+int ezq_unpack_dense3(const uint8_t* dense, int64_t count, uint8_t* out, int mem, void* stream);
+/* dequantize_tensor (pipeline.cpp:117-142) of a 3-bit artifact whose codes
+ * are given as a dense stream (`dense`, in q->mem; q->packed is not read):
+ * bit-identical to ezq_dequantize_tensor on the byte-per-level codes. */
+int ezq_dequantize_dense3(const ezq_qweight* q, const uint8_t* dense, float* out, int out_mem, void* stream);
+/* ezq_gemv_prepare_ex for a device-resident 3-bit artifact whose codes are a
+ * dense stream (device memory); the plan is the one the byte codes give. */
+int ezq_gemv_prepare_dense3(const ezq_qweight* q, const uint8_t* dense, int outlier_dtype, void* stream,
+                            ezq_gemv_plan** plan);
+
 #ifdef __cplusplus
 }
 #endif

@@ -227,3 +227,33 @@ def gemv_f64(What, x):
     y = np.zeros((batch, What.shape[1]), np.float64)
     lib().ezqo_gemv_f64(_p(What), What.shape[0], What.shape[1], _p(x), batch, _p(y))
     return y
+
+
+# ---- dense 3-bit stream (test restatement of include/ezquant_c.h's layout) --
+# The reference has no dense 3-bit format (it stores k = 3 one offset byte per
+# level, rtn.cpp:119-147); this is the plain definition the device codec is
+# checked against: offset e at bits 3e..3e+2 of a little-endian bit stream.
+def dense3_size(count):
+    return 0 if count <= 0 else 3 * ((count + 7) // 8)
+
+
+def dense3_pack(offsets):
+    o = np.ascontiguousarray(offsets, np.uint8).ravel()
+    if o.size and int(o.max()) > 7:
+        raise ValueError("offset exceeds level span 7")
+    n = o.size
+    g = np.zeros(((n + 7) // 8) * 8, np.uint32)
+    g[:n] = o
+    g = g.reshape(-1, 8)
+    word = np.zeros(g.shape[0], np.uint32)
+    for i in range(8):
+        word |= g[:, i] << np.uint32(3 * i)
+    out = np.stack([(word >> np.uint32(8 * b)) & np.uint32(0xFF) for b in range(3)], axis=1)
+    return out.astype(np.uint8).ravel()
+
+
+def dense3_unpack(stream, count):
+    s = np.ascontiguousarray(stream, np.uint8).ravel()[: dense3_size(count)].reshape(-1, 3).astype(np.uint32)
+    word = s[:, 0] | (s[:, 1] << np.uint32(8)) | (s[:, 2] << np.uint32(16))
+    out = np.stack([(word >> np.uint32(3 * i)) & np.uint32(7) for i in range(8)], axis=1)
+    return out.astype(np.uint8).ravel()[:count]

@@ -173,67 +173,71 @@ __global__ void __launch_bounds__(kPackThreads) k_pack(const TDesc* __restrict__
     }
 }
 
+// A CTA's kPackBlock elements go as quads: thread t writes elements
+// 4 (t + kPackThreads k) .. + 3 with one float4 each (consecutive lanes,
+// consecutive 16-byte stores; the codes are read as one u16 (k = 4) or u32
+// per quad, also coalesced).
 __global__ void __launch_bounds__(kPackThreads) k_dequant(int64_t rows, int64_t cols, int bits,
                                                           const uint8_t* __restrict__ packed,
                                                           const float* __restrict__ scales,
                                                           float* __restrict__ out,
                                                           unsigned long long* bad_byte) {
     const int64_t n = rows * cols;
-    const int64_t e0 = (static_cast<int64_t>(blockIdx.x) * kPackThreads + threadIdx.x) *
-                       kPackPerThread;
-    if (e0 >= n) return;
-    const int64_t cnt = min(static_cast<int64_t>(kPackPerThread), n - e0);
+    const int64_t b0 = static_cast<int64_t>(blockIdx.x) * kPackBlock;
+    const int cnt = static_cast<int>(min(kPackBlock, n - b0));
     const int lmin = -(1 << (bits - 1)) + 1;
     const int span = (1 << (bits - 1)) - lmin;
-    uint8_t off[kPackPerThread];
-    if (bits == 4) {
-        uint8_t b[kPackPerThread / 2];
-        if (cnt == kPackPerThread) {
-            const uint2 w = *reinterpret_cast<const uint2*>(packed + e0 / 2);
+    // vector paths need aligned bases (b0 is a multiple of 4096)
+    const bool vout = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+    const bool vin = (reinterpret_cast<uintptr_t>(packed) & (bits == 4 ? 1 : 3)) == 0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                b[k] = (w.x >> (8 * k)) & 0xff;
-                b[4 + k] = (w.y >> (8 * k)) & 0xff;
+    for (int k = 0; k < kPackPerThread / 4; ++k) {
+        const int l = 4 * (threadIdx.x + kPackThreads * k);
+        if (l >= cnt) break;
+        const int64_t e = b0 + l;
+        const int m = min(4, cnt - l);
+        uint8_t off[4];
+        if (bits == 4) {
+            if (vin && m == 4) {
+                const unsigned w = __ldg(reinterpret_cast<const unsigned short*>(packed + e / 2));
+                off[0] = w & 0xf, off[1] = (w >> 4) & 0xf, off[2] = (w >> 8) & 0xf, off[3] = (w >> 12) & 0xf;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint8_t b = j < m ? packed[(e + j) / 2] : 0;
+                    off[j] = ((e + j) & 1) ? (b >> 4) : (b & 0x0f);
+                }
             }
         } else {
+            if (vin && m == 4) {
+                const unsigned w = __ldg(reinterpret_cast<const unsigned*>(packed + e));
 #pragma unroll
-            for (int k = 0; k < kPackPerThread / 2; ++k)
-                b[k] = (2 * k < cnt) ? packed[e0 / 2 + k] : 0;
+                for (int j = 0; j < 4; ++j) off[j] = (w >> (8 * j)) & 0xff;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) off[j] = j < m ? packed[e + j] : 0;
+            }
+            // unpack_levels rejects offsets beyond the level span (rtn.cpp:173-178).
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (j < m && off[j] > span) atomicMin(bad_byte, static_cast<unsigned long long>(e + j));
         }
+        // 32-bit modulo when the tensor has < 2^32 elements (a 64-bit IMOD per quad costs more than the quad)
+        int64_t col = n < (int64_t(1) << 32) ? static_cast<int64_t>(static_cast<uint32_t>(e) % static_cast<uint32_t>(cols))
+                                             : e % cols;
+        float v[4];
 #pragma unroll
-        for (int k = 0; k < kPackPerThread / 2; ++k) {
-            off[2 * k] = b[k] & 0x0f;
-            off[2 * k + 1] = b[k] >> 4;
+        for (int j = 0; j < 4; ++j) {
+            v[j] = __fmul_rn(__ldg(scales + col), static_cast<float>(lmin + off[j]));
+            if (++col == cols) col = 0;
         }
-    } else {
-        if (cnt == kPackPerThread) {
-            const uint4 w = *reinterpret_cast<const uint4*>(packed + e0);
-            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-            for (int k = 0; k < kPackPerThread; ++k) off[k] = (ws[k / 4] >> (8 * (k % 4))) & 0xff;
+        if (vout && m == 4) {
+            *reinterpret_cast<float4*>(out + e) = make_float4(v[0], v[1], v[2], v[3]);
         } else {
 #pragma unroll
-            for (int k = 0; k < kPackPerThread; ++k) off[k] = (k < cnt) ? packed[e0 + k] : 0;
+            for (int j = 0; j < 4; ++j)
+                if (j < m) out[e + j] = v[j];
         }
-        // unpack_levels rejects offsets beyond the level span (rtn.cpp:173-178).
-#pragma unroll
-        for (int k = 0; k < kPackPerThread; ++k)
-            if (k < cnt && off[k] > span) atomicMin(bad_byte, static_cast<unsigned long long>(e0 + k));
-    }
-    int64_t col = e0 % cols;
-    float v[kPackPerThread];
-#pragma unroll
-    for (int k = 0; k < kPackPerThread; ++k) {
-        v[k] = __fmul_rn(scales[col], static_cast<float>(lmin + off[k]));
-        if (++col == cols) col = 0;
-    }
-    if (cnt == kPackPerThread && (reinterpret_cast<uintptr_t>(out + e0) & 15) == 0) {
-        float4* o4 = reinterpret_cast<float4*>(out + e0);
-#pragma unroll
-        for (int k = 0; k < kPackPerThread / 4; ++k)
-            o4[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-    } else {
-        for (int64_t k = 0; k < cnt; ++k) out[e0 + k] = v[k];
     }
 }
 

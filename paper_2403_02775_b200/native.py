@@ -218,6 +218,12 @@ def lib() -> C.CDLL:
         L.ezq_gemv_prepare_ex.argtypes = [C.POINTER(CQWeight), I32, P, C.POINTER(P)]
         L.ezq_gemv.argtypes = [P, P, I32, I32, P, P]
         L.ezq_gemv_plan_free.argtypes = [P]
+        L.ezq_dense3_size.argtypes = [I64]
+        L.ezq_dense3_size.restype = I64
+        L.ezq_pack_dense3.argtypes = [P, I64, P, I32, P]
+        L.ezq_unpack_dense3.argtypes = [P, I64, P, I32, P]
+        L.ezq_dequantize_dense3.argtypes = [C.POINTER(CQWeight), P, P, I32, P]
+        L.ezq_gemv_prepare_dense3.argtypes = [C.POINTER(CQWeight), P, I32, P, C.POINTER(P)]
         L.ezq_profile_enable.argtypes = [I32]
         L.ezq_profile_read.argtypes = [C.c_char_p, C.POINTER(D), C.POINTER(I64), C.POINTER(D)]
         L.ezq_measure_fp64_peak.argtypes = [C.POINTER(D)]
@@ -411,6 +417,11 @@ class DeviceBatch:
     def dequantize_into(self, i, out, stream=None):
         """ezq_dequantize_tensor of entry i into `out` (torch CUDA tensor or numpy)."""
         check(lib().ezq_dequantize_tensor(self.ptrs[i], _ptr(out), _mem(out), _stream(stream, out)))
+        return out
+
+    def dequantize_dense3_into(self, i, dense, out, stream=None):
+        """ezq_dequantize_dense3 of entry i (3-bit) from a device dense stream."""
+        check(lib().ezq_dequantize_dense3(self.ptrs[i], _ptr(dense), _ptr(out), _mem(out), _stream(stream, out)))
         return out
 
     def close(self):
@@ -679,3 +690,74 @@ def dequantize_channel(levels, scale: float) -> np.ndarray:
     out = np.zeros(lv.size, np.float32)
     check(lib().ezq_dequantize_channel(_ptr(lv), lv.size, scale, _ptr(out)))
     return out
+
+
+# ---- dense 3-bit codes (include/ezquant_c.h: ezq_*_dense3) -------------------
+def dense3_size(count: int) -> int:
+    return int(lib().ezq_dense3_size(count))
+
+
+def _u8(a):
+    if isinstance(a, np.ndarray):
+        return np.ascontiguousarray(a, dtype=np.uint8)
+    import torch
+    if a.dtype != torch.uint8 or not a.is_contiguous():
+        raise ValueError("dense3: expected a contiguous uint8 tensor")
+    return a
+
+
+def pack_dense3(levels, stream=None):
+    """The k = 3 payload (one offset byte per level; numpy or torch uint8, all
+    host or all device) -> dense 3-bit stream in the same memory."""
+    lv = _u8(levels)
+    n = int(lv.size if isinstance(lv, np.ndarray) else lv.numel())
+    if isinstance(lv, np.ndarray):
+        out = np.zeros(dense3_size(n), np.uint8)
+    else:
+        import torch
+        out = torch.empty(dense3_size(n), dtype=torch.uint8, device=lv.device)
+    check(lib().ezq_pack_dense3(_ptr(lv), n, _ptr(out), _mem(lv), _stream(stream, lv)))
+    return out
+
+
+def unpack_dense3(dense, count: int, stream=None):
+    """Dense 3-bit stream -> one offset byte per level (same memory kind)."""
+    d = _u8(dense)
+    if isinstance(d, np.ndarray):
+        out = np.zeros(max(count, 0), np.uint8)
+    else:
+        import torch
+        out = torch.empty(max(count, 0), dtype=torch.uint8, device=d.device)
+    check(lib().ezq_unpack_dense3(_ptr(d), count, _ptr(out), _mem(d), _stream(stream, d)))
+    return out
+
+
+def dequantize_dense3(q: "QuantizedWeight", dense, out=None, stream=None) -> np.ndarray:
+    """dequantize_tensor of a host 3-bit artifact whose codes are the dense
+    stream `dense` (numpy uint8)."""
+    outl = np.ascontiguousarray(q.outliers, dtype=OUTLIER_DTYPE)
+    scales = np.ascontiguousarray(q.scales, dtype=np.float32)
+    d = np.ascontiguousarray(dense, dtype=np.uint8)
+    w = C.POINTER(CQWeight)()
+    check(lib().ezq_qweight_wrap(q.rows, q.cols, q.bits, None, 0, _ptr(scales), scales.size, _ptr(outl),
+                                 outl.size, q.mean, q.stddev, q.sigma_n, MEM_HOST, C.byref(w)))
+    if out is None:
+        out = np.zeros((max(q.rows, 0), max(q.cols, 0)), dtype=np.float32)
+    try:
+        check(lib().ezq_dequantize_dense3(w, _ptr(d), _ptr(out), _mem(out), _stream(stream, out)))
+    finally:
+        lib().ezq_qweight_free(w)
+    return out
+
+
+class GemvPlanDense3(GemvPlan):
+    """GemvPlan of a device-resident 3-bit DeviceBatch entry whose codes are
+    given as a dense 3-bit stream on the device (torch uint8)."""
+
+    def __init__(self, batch: "DeviceBatch", i: int, dense, stream=None, outlier_dtype: str = "float32"):
+        self._keep = (batch, dense)
+        self.rows, self.cols = batch[i].rows, batch[i].cols
+        self.p = C.c_void_p()
+        check(lib().ezq_gemv_prepare_dense3(batch.ptrs[i], _ptr(_u8(dense)), self.OUTLIER_DTYPES[outlier_dtype],
+                                            _stream(stream, dense), C.byref(self.p)))
+        self.stream = stream
