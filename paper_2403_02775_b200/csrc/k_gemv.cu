@@ -207,6 +207,12 @@ struct GemvArgs {
     int64_t nseg;         // segments per colblock
     int ob;               // shared-memory bytes per ring stage for the segments
     int oes;              // value bytes: 4 = f32, 2 = f16
+    // Split K (ks > 1): a thread-block cluster of ks CTAs shares each
+    // colblock, rank r streaming stages [nst r / ks, nst (r + 1) / ks); the
+    // ranks' partial outputs meet in rank 0's shared memory (DSMEM, fixed
+    // rank order: deterministic) -- more bytes in flight per colblock for
+    // shapes with fewer colblocks than resident CTAs.
+    int ks;
 };
 
 // Fused outliers: segment = 512 rows (8 q-blocks; every stage of the variants
@@ -227,6 +233,16 @@ __device__ __forceinline__ void bar_wait(unsigned bar, unsigned phase) {
         asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
                      : "=r"(ok) : "r"(bar), "r"(phase) : "memory");
         if (spin > (1 << 28)) __trap();  // never hang the device on a lost transfer
+    }
+}
+
+// Same, acquiring at cluster scope (split-K partials written by other CTAs).
+__device__ __forceinline__ void bar_wait_cluster(unsigned bar, unsigned phase) {
+    unsigned ok = 0;
+    for (int spin = 0; !ok; ++spin) {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(ok) : "r"(bar), "r"(phase) : "memory");
+        if (spin > (1 << 28)) __trap();
     }
 }
 
@@ -284,7 +300,8 @@ __device__ __forceinline__ void seg_entry(const unsigned char* vals, const unsig
 // the end of a colblock it hands the sums to the writers through shared
 // memory (one buffer, mbarriers both ways).
 template <int TPC, int S, int XT, int XP, int XB, int NBT, int NBO, int OW>
-__device__ __forceinline__ void outlier_warp(const GemvArgs& a, int64_t nst_cb, unsigned full0, unsigned empty0,
+__device__ __forceinline__ void outlier_warp(const GemvArgs& a, int64_t s_lo, int64_t s_hi, int64_t cb0, int64_t cbstep,
+                                             unsigned full0, unsigned empty0,
                                              const unsigned char* osm, const unsigned char* xsm, float* osum,
                                              unsigned obar0, unsigned rbar0, int lane, int ow) {
     constexpr int C = TPC * kTileCols;
@@ -296,13 +313,13 @@ __device__ __forceinline__ void outlier_warp(const GemvArgs& a, int64_t nst_cb, 
     constexpr int ES = XT == kF32 ? 4 : 2;
     const int sub = lane % LPC;
     int k = 0, it = 0;
-    for (int64_t cb = blockIdx.x; cb < a.ncb; cb += gridDim.x, ++it) {
+    for (int64_t cb = cb0; cb < a.ncb; cb += cbstep, ++it) {
         float o[CPL][NBO];
 #pragma unroll
         for (int i = 0; i < CPL; ++i)
 #pragma unroll
             for (int n = 0; n < NBO; ++n) o[i][n] = 0.f;
-        for (int64_t sq = 0; sq < nst_cb; ++sq, ++k) {
+        for (int64_t sq = s_lo; sq < s_hi; ++sq, ++k) {
             const int slot = k % kRing;
             bar_wait(full0 + 8 * slot, (k / kRing) & 1);
             const unsigned char* ob = osm + slot * a.ob;
@@ -374,7 +391,7 @@ __device__ __forceinline__ void outlier_warp(const GemvArgs& a, int64_t nst_cb, 
     }
 }
 
-template <int TPC, int NB, int XT, bool SF, bool OUT>
+template <int TPC, int NB, int XT, bool SF, bool OUT, int KS = 1>
 __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
     using Gm = CbGeom<TPC, NB, XT, SF>;
     constexpr bool F16 = XT == kF16;
@@ -405,17 +422,44 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncthreads();
-    const int64_t nst_cb = (a.kq + S - 1) / S;  // stages per colblock
+    // split K: this CTA's rank in its cluster, colblock walk and stage range
+    const int64_t nst_all = (a.kq + S - 1) / S;
+    unsigned rank = 0;
+    int64_t cb0 = blockIdx.x, cbstep = gridDim.x, s_lo = 0, s_hi = nst_all;
+    if (KS > 1) {
+        asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+        cb0 = blockIdx.x / KS, cbstep = gridDim.x / KS;
+        s_lo = nst_all * rank / KS, s_hi = nst_all * (rank + 1) / KS;
+    }
+    const int64_t nst_cb = s_hi - s_lo;  // stages per colblock of this CTA
+    // split-K reduction area at the end of dynamic shared memory: [full, free
+    // mbarriers][(ks - 1) slots of the writers' partial outputs]
+    constexpr int NWR = QW > 1 ? TPC : kCW;             // writer warps
+    constexpr int RV = TW * NB * 4;                     // values per writer lane
+    unsigned dsz;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsz));
+    const unsigned kred = KS > 1 ? (dsz - 16u - static_cast<unsigned>((KS - 1) * NWR * 32 * RV * 4)) & ~15u : 0u;
+    const unsigned cfull = static_cast<unsigned>(__cvta_generic_to_shared(smem)) + kred, cfree = cfull + 8;
+    float* kbuf = reinterpret_cast<float*>(smem + kred + 16);  // [ks - 1][NWR * 32][RV]
+    if (KS > 1) {
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cfull), "r"(KS - 1));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cfree));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        // every CTA of the cluster has its barriers before any remote arrive
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
 
     if (OUT && warp > kCW) {  // ---- outlier warps (2 or 4: out_warps(batch))
         using G = CbGeom<TPC, NB, XT, SF>;
         const int ow = warp - kCW - 1;
-        if (NB == 2) outlier_warp<TPC, S, XT, XP, XB, G::NBT, 16, 4>(a, nst_cb, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
-        else if (a.batch == 1) outlier_warp<TPC, S, XT, XP, XB, G::NBT, 1, kOutWarpsSmall>(a, nst_cb, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
-        else if (a.batch == 2) outlier_warp<TPC, S, XT, XP, XB, G::NBT, 2, kOutWarpsSmall>(a, nst_cb, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
-        else if (a.batch <= 4) outlier_warp<TPC, S, XT, XP, XB, G::NBT, 4, 4>(a, nst_cb, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
-        else outlier_warp<TPC, S, XT, XP, XB, G::NBT, 8, 4>(a, nst_cb, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
+        if (NB == 2) outlier_warp<TPC, S, XT, XP, XB, G::NBT, 16, 4>(a, s_lo, s_hi, cb0, cbstep, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
+        else if (a.batch == 1) outlier_warp<TPC, S, XT, XP, XB, G::NBT, 1, kOutWarpsSmall>(a, s_lo, s_hi, cb0, cbstep, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
+        else if (a.batch == 2) outlier_warp<TPC, S, XT, XP, XB, G::NBT, 2, kOutWarpsSmall>(a, s_lo, s_hi, cb0, cbstep, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
+        else if (a.batch <= 4) outlier_warp<TPC, S, XT, XP, XB, G::NBT, 4, 4>(a, s_lo, s_hi, cb0, cbstep, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
+        else outlier_warp<TPC, S, XT, XP, XB, G::NBT, 8, 4>(a, s_lo, s_hi, cb0, cbstep, full0, empty0, osm, xsm, osum, obar0, rbar0, lane, ow);
         return;
     }
     if (warp == kCW) {  // ---- producer warp: codes and x slices by TMA bulk copies
@@ -432,7 +476,7 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
         auto sum_stage = [&](int p) {
             const int slot = p % kRing;
             bar_wait(full0 + 8 * slot, (p / kRing) & 1);
-            const int cnt = static_cast<int>(min(static_cast<int64_t>(S), a.kq - static_cast<int64_t>(p) * S));
+            const int cnt = static_cast<int>(min(static_cast<int64_t>(S), a.kq - (s_lo + p) * S));
             const unsigned char* xw = xsm + slot * XB;
             for (int n = 0; n < a.batch; ++n) {
                 for (int c16 = lane; c16 < cnt * 64 * ES / 16; c16 += 32) {
@@ -474,10 +518,10 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
                 o_hi = __ldg(a.obnd + cb * a.nseg + s1);
             }
         };
-        seg_range(blockIdx.x, 0);
+        seg_range(cb0, s_lo);
         int k = 0;
-        for (int64_t cb = blockIdx.x; cb < a.ncb; cb += gridDim.x) {
-            for (int64_t sq = 0; sq < nst_cb; ++sq, ++k) {
+        for (int64_t cb = cb0; cb < a.ncb; cb += cbstep) {
+            for (int64_t sq = s_lo; sq < s_hi; ++sq, ++k) {
                 if (Gm::SUBFREE && k == first_n) {  // leaving the first colblock: drain, publish
                     while (done < first_n) sum_stage(done++);
                     publish();
@@ -512,8 +556,8 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
                             : "memory");
                 }
                 if (OUT) {  // the next stage of this CTA
-                    if (sq + 1 < nst_cb) seg_range(cb, sq + 1);
-                    else seg_range(cb + gridDim.x, 0);
+                    if (sq + 1 < s_hi) seg_range(cb, sq + 1);
+                    else seg_range(cb + cbstep, s_lo);
                 }
                 // Launched as a programmatic dependent of the previous kernel
                 // (a chain of GEMVs): the codes and outlier segments are
@@ -558,7 +602,7 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
     const int tile0 = TPC >= kCW ? warp : warp % TPC;
     const int qoff = TPC >= kCW ? 0 : warp / TPC;
     int k = 0, it = 0;
-    for (int64_t cb = blockIdx.x; cb < a.ncb; cb += gridDim.x, ++it) {
+    for (int64_t cb = cb0; cb < a.ncb; cb += cbstep, ++it) {
         float acc[TW][2][NB][4];  // two accumulator sets per tile (alternating q) break the MMA chain
 #pragma unroll
         for (int u = 0; u < TW; ++u)
@@ -568,7 +612,7 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
                 for (int n8 = 0; n8 < NB; ++n8)
 #pragma unroll
                     for (int i = 0; i < 4; ++i) acc[u][h][n8][i] = 0.f;
-        for (int64_t sq = 0; sq < nst_cb; ++sq, ++k) {
+        for (int64_t sq = s_lo; sq < s_hi; ++sq, ++k) {
             const int cnt = static_cast<int>(min(static_cast<int64_t>(S), a.kq - sq * S));
             const int slot = k % kRing;
             bar_wait(full0 + 8 * slot, (k / kRing) & 1);
@@ -626,7 +670,7 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
             for (int n8 = 0; n8 < NB; ++n8)
 #pragma unroll
                 for (int i = 0; i < 4; ++i) d[u][n8][i] = acc[u][0][n8][i] + acc[u][1][n8][i];
-        if (Gm::SUBFREE && cb == blockIdx.x) named_sync(2, kStreamThreads);  // xsum published by the producer
+        if (Gm::SUBFREE && cb == cb0) named_sync(2, kStreamThreads);  // xsum published by the producer
         bool writer = true;
         if (QW > 1) {
 #pragma unroll
@@ -659,6 +703,23 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
 #pragma unroll
                     for (int q = 0; q < 4; ++q) d[u][0][q] -= C * xsum[min(2 * t + (q & 1), a.batch - 1)];
             }
+            if (KS == 1) {  // one CTA per colblock: straight to y
+#pragma unroll
+                for (int u = 0; u < TW; ++u)
+#pragma unroll
+                    for (int n8 = 0; n8 < NB; ++n8)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int64_t jc = (cb * TPC + tile0 + u * kCW) * kTileCols + g + (q >= 2 ? 8 : 0);
+                            const int n = n8 * 8 + 2 * t + (q & 1);
+                            if (jc < a.cols && n < a.batch) {
+                                float yv = a.scales[jc] * d[u][n8][q];
+                                if (OUT) yv += os[((tile0 + u * kCW) * kTileCols + g + (q >= 2 ? 8 : 0)) * Gm::NBT + n];
+                                a.y[static_cast<int64_t>(n) * a.cols + jc] = yv;
+                            }
+                        }
+            } else {
+            float yv[TW][NB][4];
 #pragma unroll
             for (int u = 0; u < TW; ++u)
 #pragma unroll
@@ -667,12 +728,61 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
                     for (int q = 0; q < 4; ++q) {
                         const int64_t jc = (cb * TPC + tile0 + u * kCW) * kTileCols + g + (q >= 2 ? 8 : 0);
                         const int n = n8 * 8 + 2 * t + (q & 1);
+                        float v = 0.f;
                         if (jc < a.cols && n < a.batch) {
-                            float yv = a.scales[jc] * d[u][n8][q];
-                            if (OUT) yv += os[((tile0 + u * kCW) * kTileCols + g + (q >= 2 ? 8 : 0)) * Gm::NBT + n];
-                            a.y[static_cast<int64_t>(n) * a.cols + jc] = yv;
+                            v = a.scales[jc] * d[u][n8][q];
+                            if (OUT) v += os[((tile0 + u * kCW) * kTileCols + g + (q >= 2 ? 8 : 0)) * Gm::NBT + n];
                         }
+                        yv[u][n8][q] = v;
                     }
+            {  // split K: the ranks' partial outputs meet in rank 0 (DSMEM)
+                const int wl = warp * 32 + lane;  // writers are warps 0 .. NWR - 1
+#define YV(i) yv[(i) / (NB * 4)][((i) / 4) % NB][(i) % 4]
+                if (rank != 0) {
+                    if (it >= 1) bar_wait_cluster(cfree, (it - 1) & 1);  // rank 0 has read the previous colblock
+                    const unsigned la = static_cast<unsigned>(__cvta_generic_to_shared(kbuf + ((rank - 1) * NWR * 32 + wl) * RV));
+                    unsigned ra;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(ra) : "r"(la));
+#pragma unroll
+                    for (int i = 0; i < RV; ++i)
+                        asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(ra + 4 * i), "f"(YV(i)) : "memory");
+                    named_sync(3, NWR * 32);
+                    if (wl == 0) {
+                        unsigned rb;
+                        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rb) : "r"(cfull));
+                        asm volatile("fence.acq_rel.cluster;\nmbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb)
+                                     : "memory");
+                    }
+                } else {
+                    bar_wait_cluster(cfull, it & 1);
+                    for (int r = 1; r < KS; ++r) {  // fixed rank order: deterministic
+                        const float* src = kbuf + ((r - 1) * NWR * 32 + wl) * RV;
+#pragma unroll
+                        for (int i = 0; i < RV; ++i) YV(i) += src[i];
+                    }
+                    named_sync(3, NWR * 32);  // every writer has read the slots
+                    if (wl == 0 && cb + cbstep < a.ncb)  // (no signal after the last colblock: the ranks may have exited)
+                        for (int r = 1; r < KS; ++r) {
+                            unsigned rb;
+                            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(cfree), "r"(r));
+                            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
+                        }
+                }
+#undef YV
+            }
+            if (rank == 0) {
+#pragma unroll
+                for (int u = 0; u < TW; ++u)
+#pragma unroll
+                    for (int n8 = 0; n8 < NB; ++n8)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int64_t jc = (cb * TPC + tile0 + u * kCW) * kTileCols + g + (q >= 2 ? 8 : 0);
+                            const int n = n8 * 8 + 2 * t + (q & 1);
+                            if (jc < a.cols && n < a.batch) a.y[static_cast<int64_t>(n) * a.cols + jc] = yv[u][n8][q];
+                        }
+            }
+            }
         }
         if (OUT) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(rbar0) : "memory");
     }
@@ -853,6 +963,7 @@ struct ezq_gemv_plan {
     int ob[6];            // segment bytes per ring stage, per variant
     int gridf[6][2];      // persistent CTAs of the fused kernel, per variant and outlier warps (small, max)
     size_t fsmem[6];      // its dynamic shared memory; 0: the separate pass
+    int ks[6];            // K splits per colblock, per variant (thread-block cluster size; 1: none)
 };
 
 namespace {
@@ -870,10 +981,16 @@ int max_optin_smem() {
 template <int TPC, int NB, int XT>
 int cb_ctas_per_sm() {
     const int smem = static_cast<int>(CbGeom<TPC, NB, XT>::smem());
+    const int cap = max_optin_smem();  // launches add the split-K area (ks_bytes)
     if (NB == 1 && XT != kF16)  // the HSUB2-free twin (same shared memory)
-        cudaFuncSetAttribute(k_gemv_cb<TPC, NB, XT, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_gemv_cb<TPC, NB, XT, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
     auto k = k_gemv_cb<TPC, NB, XT, false, false>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+    if (TPC == 1) {  // the split-K twins
+        cudaFuncSetAttribute(k_gemv_cb<TPC, NB, XT, false, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+        if (NB == 1 && XT != kF16)
+            cudaFuncSetAttribute(k_gemv_cb<TPC, NB, XT, true, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+    }
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kStreamThreads, smem) != cudaSuccess || n < 1) n = 1;
     return n;
@@ -926,6 +1043,11 @@ int fused_ctas_per_sm(size_t smem, int threads) {
         cudaFuncSetAttribute(k_gemv_cb<TPC, NB, XT, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
     auto k = k_gemv_cb<TPC, NB, XT, false, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+    if (TPC == 1) {  // the split-K twins
+        cudaFuncSetAttribute(k_gemv_cb<TPC, NB, XT, false, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+        if (NB == 1 && XT != kF16)
+            cudaFuncSetAttribute(k_gemv_cb<TPC, NB, XT, true, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+    }
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, threads, smem) != cudaSuccess) n = 0;
     return n;
@@ -956,6 +1078,31 @@ void fused_variant(int tpc, int v, size_t ob, int threads, FusedGeom* g, int* ct
     }
 }
 
+// q-blocks per ring stage of variant v (x dtype, NB) at colblock width tpc
+template <int TPC>
+int stage_qblocks_t(int v) {
+    switch (v) {
+        case 0: return CbGeom<TPC, 1, kF32>::S;
+        case 1: return CbGeom<TPC, 2, kF32>::S;
+        case 2: return CbGeom<TPC, 1, kBF16>::S;
+        case 3: return CbGeom<TPC, 2, kBF16>::S;
+        case 4: return CbGeom<TPC, 1, kF16>::S;
+        default: return CbGeom<TPC, 2, kF16>::S;
+    }
+}
+int stage_qblocks(int tpc, int v) {
+    return tpc == 1 ? stage_qblocks_t<1>(v) : tpc == 2 ? stage_qblocks_t<2>(v) : tpc == 4 ? stage_qblocks_t<4>(v)
+                                                                                         : stage_qblocks_t<8>(v);
+}
+
+// split-K reduction area (k_gemv_cb): 2 mbarriers + (ks - 1) slots of the
+// writers' partial outputs, plus alignment slack
+size_t ks_bytes(int tpc, int nb, int ks) {
+    if (ks <= 1) return 0;
+    const int nwr = tpc >= kCW ? kCW : tpc, tw = tpc >= kCW ? tpc / kCW : 1;
+    return 32 + static_cast<size_t>(ks - 1) * nwr * 32 * tw * nb * 4 * sizeof(float);
+}
+
 template <typename K>
 void launch_pdl(K kernel, unsigned grid, unsigned threads, size_t smem, cudaStream_t st, const GemvArgs& a) {
     // programmatic dependent launch: the weight stream of this GEMV starts
@@ -966,11 +1113,15 @@ void launch_pdl(K kernel, unsigned grid, unsigned threads, size_t smem, cudaStre
     lc.blockDim = dim3(threads);
     lc.dynamicSmemBytes = smem;
     lc.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = chain ? 1 : 0;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = static_cast<unsigned>(a.ks);
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
     lc.attrs = at;
-    lc.numAttrs = 1;
+    lc.numAttrs = a.ks > 1 ? 2 : 1;
     cudaLaunchKernelEx(&lc, kernel, a);
 }
 
@@ -981,6 +1132,18 @@ template <int TPC, int NB, int XT>
 void launch_cb_t(const GemvArgs& a, int grid, size_t smem, cudaStream_t st) {
     const unsigned gd = static_cast<unsigned>(grid);
     const bool sf = NB == 1 && XT != kF16 && a.batch <= 2;
+    const size_t kx = ks_bytes(TPC, NB, a.ks);  // split-K area at the end of dynamic shared memory
+    if (TPC == 1 && a.ks == 2) {  // split K is chosen for 1-tile colblocks only (ezq_gemv_prepare)
+        if (smem) {
+            const unsigned nt = static_cast<unsigned>(kStreamThreads + 32 * out_warps(a.batch));
+            if (sf) launch_pdl(k_gemv_cb<TPC, NB, XT, true, true, 2>, gd, nt, smem + kx, st, a);
+            else launch_pdl(k_gemv_cb<TPC, NB, XT, false, true, 2>, gd, nt, smem + kx, st, a);
+        } else {
+            if (sf) launch_pdl(k_gemv_cb<TPC, NB, XT, true, false, 2>, gd, kStreamThreads, CbGeom<TPC, NB, XT, true>::smem() + kx, st, a);
+            else launch_pdl(k_gemv_cb<TPC, NB, XT, false, false, 2>, gd, kStreamThreads, CbGeom<TPC, NB, XT>::smem() + kx, st, a);
+        }
+        return;
+    }
     if (smem) {
         const unsigned nt = static_cast<unsigned>(kStreamThreads + 32 * out_warps(a.batch));
         if (sf) launch_pdl(k_gemv_cb<TPC, NB, XT, true, true>, gd, nt, smem, st, a);
@@ -1114,10 +1277,29 @@ int ezq_gemv_prepare_ex(const ezq_qweight* q, int outlier_dtype, void* stream, e
     p->ncb = (p->tiles + p->tpc - 1) / p->tpc;
     const int* occ = occupancy(p->tpc);
     static const bool dbg = std::getenv("EZQ_GEMV_DEBUG") != nullptr;
+    // Split K across a cluster when the colblocks cannot fill the resident
+    // CTAs (latency-bound shapes: few output columns, long K): 2 CTAs per
+    // colblock when each rank keeps >= 3 ring stages (measured on B200:
+    // 11008x4096 batch 1 / 16: 11.8 -> 11.0 / 22.6 -> 15.6 us; 4 ranks and
+    // 2-stage ranks were slower), per variant (its stage size).
+    const char* ek = std::getenv("EZQ_GEMV_KS");  // tuning / test aid
     for (int v = 0; v < 6; ++v) {
-        p->grid[v] = static_cast<int>(std::min<int64_t>(p->ncb, static_cast<int64_t>(sms) * occ[v]));
+        const int64_t res = static_cast<int64_t>(sms) * occ[v];
+        const int sq = stage_qblocks(p->tpc, v);
+        const int64_t nst = (p->kq + sq - 1) / sq;
+        int ks = p->tpc == 1 && p->ncb * 2 <= res && nst >= 6 ? 2 : 1;
+        if (ek && p->tpc == 1) ks = std::atoi(ek) == 2 ? 2 : 1;
+        p->ks[v] = ks;
+    }
+    auto grid_of = [&](int64_t slots, int ks) {  // persistent CTAs: whole clusters, at most one unit each
+        int64_t gr = std::min<int64_t>(p->ncb * ks, slots);
+        gr -= gr % ks;
+        return static_cast<int>(std::max<int64_t>(gr, ks));
+    };
+    for (int v = 0; v < 6; ++v) {
+        p->grid[v] = grid_of(static_cast<int64_t>(sms) * occ[v], p->ks[v]);
         if (dbg)
-            std::fprintf(stderr, "ezq_gemv_prepare: tpc %d ncb %lld variant %d ctas/sm %d grid %d\n", p->tpc,
+            std::fprintf(stderr, "ezq_gemv_prepare: tpc %d ks %d ncb %lld variant %d ctas/sm %d grid %d\n", p->tpc, p->ks[v],
                          static_cast<long long>(p->ncb), v, occ[v], p->grid[v]);
     }
     // Fused outliers: for every colblock and 512-row segment, the header
@@ -1195,10 +1377,13 @@ int ezq_gemv_prepare_ex(const ezq_qweight* q, int outlier_dtype, void* stream, e
         fused_variant(p->tpc, v, static_cast<size_t>(mx), kStreamThreads + 32 * kOutWarpsSmall, &fg, &c1);
         fused_variant(p->tpc, v, static_cast<size_t>(mx), kStreamThreads + 32 * kOutWarpsMax, &fg, &c4);
         if (c1 < 1 || c4 < 1) continue;
+        if (fg.osm_off + static_cast<size_t>(kRing) * mx + ks_bytes(p->tpc, (v & 1) ? 2 : 1, p->ks[v]) >
+            static_cast<size_t>(max_optin_smem()))
+            continue;  // no room for the split-K area
         p->ob[v] = static_cast<int>(mx);
         p->fsmem[v] = fg.osm_off + static_cast<size_t>(kRing) * mx;
-        p->gridf[v][0] = static_cast<int>(std::min<int64_t>(p->ncb, static_cast<int64_t>(sms) * c1));
-        p->gridf[v][1] = static_cast<int>(std::min<int64_t>(p->ncb, static_cast<int64_t>(sms) * c4));
+        p->gridf[v][0] = grid_of(static_cast<int64_t>(sms) * c1, p->ks[v]);
+        p->gridf[v][1] = grid_of(static_cast<int64_t>(sms) * c4, p->ks[v]);
         if (dbg)
             std::fprintf(stderr, "ezq_gemv_prepare: fused variant %d: %lld B/stage, smem %zu, ctas/sm %d / %d\n", v,
                          static_cast<long long>(mx), p->fsmem[v], c1, c4);
@@ -1293,6 +1478,7 @@ int ezq_gemv(const ezq_gemv_plan* p, const void* x, int x_dtype, int batch, floa
             if (e != cudaSuccess) return cuda_error(e, "gemv: before the main kernel");
         }
         const int v = x_dtype * 2 + (two ? 1 : 0);
+        a.ks = p->ks[v];
         const bool fused = p->n_out && p->fsmem[v];
         if (fused) {
             a.oseg = p->oseg;
