@@ -719,58 +719,7 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
                             }
                         }
             } else {
-            float yv[TW][NB][4];
-#pragma unroll
-            for (int u = 0; u < TW; ++u)
-#pragma unroll
-                for (int n8 = 0; n8 < NB; ++n8)
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int64_t jc = (cb * TPC + tile0 + u * kCW) * kTileCols + g + (q >= 2 ? 8 : 0);
-                        const int n = n8 * 8 + 2 * t + (q & 1);
-                        float v = 0.f;
-                        if (jc < a.cols && n < a.batch) {
-                            v = a.scales[jc] * d[u][n8][q];
-                            if (OUT) v += os[((tile0 + u * kCW) * kTileCols + g + (q >= 2 ? 8 : 0)) * Gm::NBT + n];
-                        }
-                        yv[u][n8][q] = v;
-                    }
-            {  // split K: the ranks' partial outputs meet in rank 0 (DSMEM)
-                const int wl = warp * 32 + lane;  // writers are warps 0 .. NWR - 1
-#define YV(i) yv[(i) / (NB * 4)][((i) / 4) % NB][(i) % 4]
-                if (rank != 0) {
-                    if (it >= 1) bar_wait_cluster(cfree, (it - 1) & 1);  // rank 0 has read the previous colblock
-                    const unsigned la = static_cast<unsigned>(__cvta_generic_to_shared(kbuf + ((rank - 1) * NWR * 32 + wl) * RV));
-                    unsigned ra;
-                    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(ra) : "r"(la));
-#pragma unroll
-                    for (int i = 0; i < RV; ++i)
-                        asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(ra + 4 * i), "f"(YV(i)) : "memory");
-                    named_sync(3, NWR * 32);
-                    if (wl == 0) {
-                        unsigned rb;
-                        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rb) : "r"(cfull));
-                        asm volatile("fence.acq_rel.cluster;\nmbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb)
-                                     : "memory");
-                    }
-                } else {
-                    bar_wait_cluster(cfull, it & 1);
-                    for (int r = 1; r < KS; ++r) {  // fixed rank order: deterministic
-                        const float* src = kbuf + ((r - 1) * NWR * 32 + wl) * RV;
-#pragma unroll
-                        for (int i = 0; i < RV; ++i) YV(i) += src[i];
-                    }
-                    named_sync(3, NWR * 32);  // every writer has read the slots
-                    if (wl == 0 && cb + cbstep < a.ncb)  // (no signal after the last colblock: the ranks may have exited)
-                        for (int r = 1; r < KS; ++r) {
-                            unsigned rb;
-                            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(cfree), "r"(r));
-                            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
-                        }
-                }
-#undef YV
-            }
-            if (rank == 0) {
+                float yv[TW][NB][4];
 #pragma unroll
                 for (int u = 0; u < TW; ++u)
 #pragma unroll
@@ -779,9 +728,60 @@ __global__ void __launch_bounds__(kOutThreads) k_gemv_cb(const GemvArgs a) {
                         for (int q = 0; q < 4; ++q) {
                             const int64_t jc = (cb * TPC + tile0 + u * kCW) * kTileCols + g + (q >= 2 ? 8 : 0);
                             const int n = n8 * 8 + 2 * t + (q & 1);
-                            if (jc < a.cols && n < a.batch) a.y[static_cast<int64_t>(n) * a.cols + jc] = yv[u][n8][q];
+                            float v = 0.f;
+                            if (jc < a.cols && n < a.batch) {
+                                v = a.scales[jc] * d[u][n8][q];
+                                if (OUT) v += os[((tile0 + u * kCW) * kTileCols + g + (q >= 2 ? 8 : 0)) * Gm::NBT + n];
+                            }
+                            yv[u][n8][q] = v;
                         }
-            }
+                {  // split K: the ranks' partial outputs meet in rank 0 (DSMEM)
+                    const int wl = warp * 32 + lane;  // writers are warps 0 .. NWR - 1
+#define YV(i) yv[(i) / (NB * 4)][((i) / 4) % NB][(i) % 4]
+                    if (rank != 0) {
+                        if (it >= 1) bar_wait_cluster(cfree, (it - 1) & 1);  // rank 0 has read the previous colblock
+                        const unsigned la = static_cast<unsigned>(__cvta_generic_to_shared(kbuf + ((rank - 1) * NWR * 32 + wl) * RV));
+                        unsigned ra;
+                        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(ra) : "r"(la));
+#pragma unroll
+                        for (int i = 0; i < RV; ++i)
+                            asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(ra + 4 * i), "f"(YV(i)) : "memory");
+                        named_sync(3, NWR * 32);
+                        if (wl == 0) {
+                            unsigned rb;
+                            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(rb) : "r"(cfull));
+                            asm volatile("fence.acq_rel.cluster;\nmbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb)
+                                         : "memory");
+                        }
+                    } else {
+                        bar_wait_cluster(cfull, it & 1);
+                        for (int r = 1; r < KS; ++r) {  // fixed rank order: deterministic
+                            const float* src = kbuf + ((r - 1) * NWR * 32 + wl) * RV;
+#pragma unroll
+                            for (int i = 0; i < RV; ++i) YV(i) += src[i];
+                        }
+                        named_sync(3, NWR * 32);  // every writer has read the slots
+                        if (wl == 0 && cb + cbstep < a.ncb)  // (no signal after the last colblock: the ranks may have exited)
+                            for (int r = 1; r < KS; ++r) {
+                                unsigned rb;
+                                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(cfree), "r"(r));
+                                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
+                            }
+                    }
+#undef YV
+                }
+                if (rank == 0) {
+#pragma unroll
+                    for (int u = 0; u < TW; ++u)
+#pragma unroll
+                        for (int n8 = 0; n8 < NB; ++n8)
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const int64_t jc = (cb * TPC + tile0 + u * kCW) * kTileCols + g + (q >= 2 ? 8 : 0);
+                                const int n = n8 * 8 + 2 * t + (q & 1);
+                                if (jc < a.cols && n < a.batch) a.y[static_cast<int64_t>(n) * a.cols + jc] = yv[u][n8][q];
+                            }
+                }
             }
         }
         if (OUT) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(rbar0) : "memory");
