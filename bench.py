@@ -281,22 +281,25 @@ def gemv_bench(N, torch, copies=8, batches=(1, 4, 8, 16), reps=20):
             mats = [d.float() for d in dense]
             b = N.quantize_batch(mats, Config(sigma_n=sig[ratio]), "outliers-only", out_mem=N.MEM_DEVICE)
             del mats
-            plans = [N.GemvPlan(b, i) for i in range(copies)]
             n_out = sum(b[i].n_outliers for i in range(copies)) / copies
-            for B in batches:
-                x = torch.randn(B, r, generator=gen, device="cuda").to(torch.bfloat16)
-                y = torch.empty(B, c, device="cuda", dtype=torch.float32)
-                us = timed(lambda: [p(x, y) for p in plans])
-                nbytes = (r * c) / 2 + 4 * c + 6 * n_out + 2 * B * r + 4 * B * c  # 6 B: f32 value + u16 row
-                rec = {"shape": f"{r}x{c}", "batch": B, "outlier_pct": 100 * ratio, "us": us,
-                       "gbps": nbytes / (us * 1e-6) / 1e9, "frac": nbytes / (us * 1e-6) / 1e9 / hbm}
-                if ratio == 0.0:
-                    xh = x.half()
-                    yd = torch.empty(B, c, device="cuda", dtype=torch.float16)
-                    rec["dense_fp16_us"] = timed(lambda: [torch.matmul(xh, d, out=yd) for d in dense])
-                rows_out.append(rec)
-            for p in plans:
-                p.close()
+            # configs[4] names fp16 outlier values; f32 (exact) rows beside them
+            for odt in (("float16", "float32") if ratio else ("float32",)):
+                plans = [N.GemvPlan(b, i, outlier_dtype=odt) for i in range(copies)]
+                vb = 6 if odt == "float32" else 4  # value + u16 row
+                for B in batches:
+                    x = torch.randn(B, r, generator=gen, device="cuda").to(torch.bfloat16)
+                    y = torch.empty(B, c, device="cuda", dtype=torch.float32)
+                    us = timed(lambda: [p(x, y) for p in plans])
+                    nbytes = (r * c) / 2 + 4 * c + vb * n_out + 2 * B * r + 4 * B * c
+                    rec = {"shape": f"{r}x{c}", "batch": B, "outlier_pct": 100 * ratio, "outlier_dtype": odt, "us": us,
+                           "gbps": nbytes / (us * 1e-6) / 1e9, "frac": nbytes / (us * 1e-6) / 1e9 / hbm}
+                    if ratio == 0.0:
+                        xh = x.half()
+                        yd = torch.empty(B, c, device="cuda", dtype=torch.float16)
+                        rec["dense_fp16_us"] = timed(lambda: [torch.matmul(xh, d, out=yd) for d in dense])
+                    rows_out.append(rec)
+                for p in plans:
+                    p.close()
             b.close()
         del dense
     # the paper's practical-latency shape (BLOOM-176B FFN): one 385 MB copy
@@ -323,7 +326,8 @@ def gemv_bench(N, torch, copies=8, batches=(1, 4, 8, 16), reps=20):
     base = {(e["shape"], e["batch"]): e["us"] for e in rows_out if e["outlier_pct"] == 0.0}
     for e in rows_out:
         e["overhead_vs_int4_pct"] = 100.0 * (e["us"] / base[(e["shape"], e["batch"])] - 1.0)
-    b1 = [e for e in rows_out if e["batch"] == 1 and e["outlier_pct"] == 1.0 and e["shape"] != "14336x53746"]
+    b1 = [e for e in rows_out if e["batch"] == 1 and e["outlier_pct"] == 1.0 and e["shape"] != "14336x53746"
+          and e["outlier_dtype"] == "float16"]  # configs[4]: fp16 outliers
     big = {(e["batch"], e["outlier_pct"], e.get("outlier_dtype", "float32")): e for e in rows_out
            if e["shape"] == "14336x53746"}
     return {"metric": "dequant-GEMV HBM GB/s", "unit": "GB/s",

@@ -981,12 +981,12 @@ int max_optin_smem() {
 template <int TPC, int NB, int XT>
 int cb_ctas_per_sm() {
     const int smem = static_cast<int>(CbGeom<TPC, NB, XT>::smem());
-    const int cap = max_optin_smem();  // launches add the split-K area (ks_bytes)
+    const int cap = max_optin_smem();  // split-K launches add their area (ks_bytes)
     if (NB == 1 && XT != kF16)  // the HSUB2-free twin (same shared memory)
-        cudaFuncSetAttribute(k_gemv_cb<TPC, NB, XT, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
+        cudaFuncSetAttribute(k_gemv_cb<TPC, NB, XT, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     auto k = k_gemv_cb<TPC, NB, XT, false, false>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
-    if (TPC == 1) {  // the split-K twins
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if constexpr (TPC == 1) {  // the split-K twins
         cudaFuncSetAttribute(k_gemv_cb<TPC, NB, XT, false, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
         if (NB == 1 && XT != kF16)
             cudaFuncSetAttribute(k_gemv_cb<TPC, NB, XT, true, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
@@ -1043,7 +1043,7 @@ int fused_ctas_per_sm(size_t smem, int threads) {
         cudaFuncSetAttribute(k_gemv_cb<TPC, NB, XT, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
     auto k = k_gemv_cb<TPC, NB, XT, false, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
-    if (TPC == 1) {  // the split-K twins
+    if constexpr (TPC == 1) {  // the split-K twins
         cudaFuncSetAttribute(k_gemv_cb<TPC, NB, XT, false, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
         if (NB == 1 && XT != kF16)
             cudaFuncSetAttribute(k_gemv_cb<TPC, NB, XT, true, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
@@ -1133,7 +1133,7 @@ void launch_cb_t(const GemvArgs& a, int grid, size_t smem, cudaStream_t st) {
     const unsigned gd = static_cast<unsigned>(grid);
     const bool sf = NB == 1 && XT != kF16 && a.batch <= 2;
     const size_t kx = ks_bytes(TPC, NB, a.ks);  // split-K area at the end of dynamic shared memory
-    if (TPC == 1 && a.ks == 2) {  // split K is chosen for 1-tile colblocks only (ezq_gemv_prepare)
+    if constexpr (TPC == 1) if (a.ks == 2) {  // split K is chosen for 1-tile colblocks only (ezq_gemv_prepare)
         if (smem) {
             const unsigned nt = static_cast<unsigned>(kStreamThreads + 32 * out_warps(a.batch));
             if (sf) launch_pdl(k_gemv_cb<TPC, NB, XT, true, true, 2>, gd, nt, smem + kx, st, a);
