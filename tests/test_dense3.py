@@ -136,3 +136,11 @@ def test_dense3_device_batch_and_gemv_gpu(gpu):
     p1.close()
     p2.close()
     b.close()
+
+
+def test_dense3_wrapper_rejects_non_u8_tensors(N):
+    import torch
+    with pytest.raises(ValueError):
+        N.pack_dense3(torch.zeros(16, dtype=torch.int16))
+    with pytest.raises(ValueError):
+        N.unpack_dense3(torch.zeros(6, dtype=torch.uint8)[::2], 4)
