@@ -222,6 +222,7 @@ int ezq_pack_dense3(const uint8_t* levels, int64_t count, uint8_t* out, int mem,
     if (count < 0) return set_error(EZQ_ERR_INVALID_ARGUMENT, "negative level count");
     if (mem != EZQ_MEM_HOST && mem != EZQ_MEM_DEVICE) return set_error(EZQ_ERR_INVALID_ARGUMENT, "unknown memory kind");
     if (count == 0) return clear_error();
+    if (!levels || !out) return set_error(EZQ_ERR_INVALID_ARGUMENT, "null buffer");
     int dev;
     if (int s = bind_device(&dev)) return s;
     cudaStream_t st = pick_stream(stream, dev);
@@ -256,6 +257,7 @@ int ezq_unpack_dense3(const uint8_t* dense, int64_t count, uint8_t* out, int mem
     if (count < 0) return set_error(EZQ_ERR_INVALID_ARGUMENT, "negative level count");
     if (mem != EZQ_MEM_HOST && mem != EZQ_MEM_DEVICE) return set_error(EZQ_ERR_INVALID_ARGUMENT, "unknown memory kind");
     if (count == 0) return clear_error();
+    if (!dense || !out) return set_error(EZQ_ERR_INVALID_ARGUMENT, "null buffer");
     int dev;
     if (int s = bind_device(&dev)) return s;
     cudaStream_t st = pick_stream(stream, dev);
@@ -279,6 +281,7 @@ int ezq_dequantize_dense3(const ezq_qweight* q, const uint8_t* dense, float* out
     if (q->rows <= 0 || q->cols <= 0) return set_error(EZQ_ERR_IO_FORMAT, "quantized tensor has empty shape");
     if (q->bits != 3) return set_error(EZQ_ERR_INVALID_ARGUMENT, "dense 3-bit codes need a 3-bit artifact");
     if (q->reserved) return set_error(EZQ_ERR_IO_FORMAT, "scale count does not match columns");
+    if (!dense || !out || !q->scales) return set_error(EZQ_ERR_INVALID_ARGUMENT, "null buffer");
     const int64_t N = q->rows * q->cols;
     const size_t db = static_cast<size_t>(ezq_dense3_size(N));
     int dev;
@@ -343,6 +346,7 @@ int ezq_gemv_prepare_dense3(const ezq_qweight* q, const uint8_t* dense, int outl
     if (q->mem != EZQ_MEM_DEVICE) return set_error(EZQ_ERR_INVALID_ARGUMENT, "ezq_gemv needs a device-resident artifact");
     if (q->bits != 3) return set_error(EZQ_ERR_INVALID_ARGUMENT, "dense 3-bit codes need a 3-bit artifact");
     if (q->rows <= 0 || q->cols <= 0) return set_error(EZQ_ERR_IO_FORMAT, "quantized tensor has empty shape");
+    if (!dense) return set_error(EZQ_ERR_INVALID_ARGUMENT, "null buffer");
     const int64_t N = q->rows * q->cols;
     int dev;
     if (int s = bind_device(&dev)) return s;

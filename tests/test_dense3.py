@@ -144,3 +144,11 @@ def test_dense3_wrapper_rejects_non_u8_tensors(N):
         N.pack_dense3(torch.zeros(16, dtype=torch.int16))
     with pytest.raises(ValueError):
         N.unpack_dense3(torch.zeros(6, dtype=torch.uint8)[::2], 4)
+
+
+@pytest.mark.gpu
+def test_dense3_null_buffers_gpu(gpu):
+    from paper_2403_02775_b200.native import lib, MEM_DEVICE, MEM_HOST, INVALID_ARGUMENT
+    assert lib().ezq_pack_dense3(None, 10, None, MEM_HOST, None) == INVALID_ARGUMENT
+    assert lib().ezq_unpack_dense3(None, 10, None, MEM_DEVICE, None) == INVALID_ARGUMENT
+    assert lib().ezq_pack_dense3(None, 0, None, MEM_HOST, None) == 0  # empty: no-op
