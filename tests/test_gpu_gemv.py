@@ -241,3 +241,38 @@ def test_gemv_every_colblock_width(gpu, O, monkeypatch, tpc, batch, dtype):
         assert np.abs(y - yref).max() <= 1e-3 * np.abs(yref).max(), (tpc, fused)
         plan.close()
     b.close()
+
+
+@pytest.mark.parametrize("rows,cols", [(2048, 12000), (4096, 4096), (1536, 700)])
+@pytest.mark.parametrize("batch,dtype", [(1, "bfloat16"), (3, "float32"), (16, "bfloat16"), (12, "float16")])
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_gemv_split_k_clusters(gpu, O, monkeypatch, rows, cols, batch, dtype, fused):
+    """Split K over 2-CTA clusters (EZQ_GEMV_KS=2 with 1-tile colblocks):
+    2048x12000 has 750 colblocks, more than the resident clusters, so every
+    cluster loops over several colblocks (rank 0 frees rank 1's slot between
+    them); 1536x700 gives rank 1 the shorter half. Within the 1e-3 gate
+    against dequantize + the fp64 GEMV, within fp32 rounding of the unsplit
+    kernel, and bit-identical across calls (fixed rank order)."""
+    import torch
+    W = O.gaussian(rows, cols, rows * 7 + cols, 0.02)
+    O.plant_outliers(W, max(1, W.size // 100), 0.2, 1.0, 13)
+    b = gpu.quantize_batch([torch.from_numpy(W).cuda()], Config(sigma_n=2.5758, steps=10), out_mem=gpu.MEM_DEVICE)
+    x = torch.randn(batch, rows, generator=torch.Generator(device="cuda").manual_seed(9), device="cuda")
+    x = x.to(getattr(torch, dtype))
+    monkeypatch.setenv("EZQ_GEMV_TPC", "1")
+    monkeypatch.setenv("EZQ_GEMV_FUSED", fused)
+    monkeypatch.setenv("EZQ_GEMV_KS", "1")
+    p1 = gpu.GemvPlan(b, 0)
+    y1 = p1(x).cpu().numpy().astype(np.float64)
+    monkeypatch.setenv("EZQ_GEMV_KS", "2")
+    p2 = gpu.GemvPlan(b, 0)
+    y2 = p2(x).cpu().numpy()
+    yref = O.gemv_f64(gpu.dequantize(b.to_host(0)), x.float().cpu().numpy())
+    scale = np.abs(yref).max()
+    assert np.abs(y2.astype(np.float64) - yref).max() <= 1e-3 * scale
+    assert np.abs(y2.astype(np.float64) - y1).max() <= 1e-5 * scale
+    for _ in range(2):
+        assert np.array_equal(p2(x).cpu().numpy().view(np.uint32), y2.view(np.uint32))
+    p1.close()
+    p2.close()
+    b.close()
