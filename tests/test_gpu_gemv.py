@@ -276,3 +276,34 @@ def test_gemv_split_k_clusters(gpu, O, monkeypatch, rows, cols, batch, dtype, fu
     p1.close()
     p2.close()
     b.close()
+
+
+def test_gemv_bloom_shape_fused_vs_separate(gpu, monkeypatch):
+    """The paper's practical-latency shape (BLOOM-176B FFN, 14336x53746, 1%
+    outliers), which the bench times: the fused outlier term and the separate
+    CSC pass agree to fp32 rounding and both hold the 1e-3 gate against
+    dequantize + an fp64 matmul (batch 1 and 16, bf16 x)."""
+    import torch
+    r, c = 14336, 53746
+    g = torch.Generator(device="cuda").manual_seed(5)
+    W = torch.randn(r, c, generator=g, device="cuda") * 0.02
+    b = gpu.quantize_batch([W], Config(sigma_n=2.5758), "outliers-only", out_mem=gpu.MEM_DEVICE)
+    del W
+    What = torch.empty(r, c, device="cuda")
+    b.dequantize_into(0, What)
+    monkeypatch.setenv("EZQ_GEMV_FUSED", "1")
+    pf = gpu.GemvPlan(b, 0)
+    monkeypatch.setenv("EZQ_GEMV_FUSED", "0")
+    ps = gpu.GemvPlan(b, 0)
+    Wd = What.double()
+    for B in (1, 16):
+        x = torch.randn(B, r, generator=g, device="cuda").to(torch.bfloat16)
+        yf, ys = pf(x).double(), ps(x).double()
+        ref = x.double() @ Wd
+        sc = ref.abs().max().item()
+        assert (yf - ref).abs().max().item() <= 1e-3 * sc
+        assert (ys - ref).abs().max().item() <= 1e-3 * sc
+        assert (yf - ys).abs().max().item() <= 1e-5 * sc
+    pf.close()
+    ps.close()
+    b.close()
